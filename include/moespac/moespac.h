@@ -1,0 +1,284 @@
+/*
+ * moespac.h — C ABI of the B200-native MoE-SpAc verification-step hot path.
+ *
+ * This is the drop-in boundary for the reference's verification-step path
+ * (/root/reference/proj/core — C++ namespace `moesim`). The reference exposes
+ * only a C++ API; every entry point below names the reference routine it
+ * replaces (file:line relative to /root/reference/proj). INTEGRATION.md shows
+ * the binding a maintainer adds on the reference side.
+ *
+ * Conventions:
+ *  - Every function returns moespac_status and never throws. Error classes map
+ *    1:1 onto the reference's exceptions: MOESPAC_E_INVALID <-
+ *    std::invalid_argument, MOESPAC_E_RANGE <- std::out_of_range,
+ *    MOESPAC_E_LOGIC <- std::logic_error, MOESPAC_E_IO <- std::runtime_error;
+ *    plus MOESPAC_E_CUDA / MOESPAC_E_NCCL / MOESPAC_E_NOMEM. The message of the
+ *    last failure on the calling thread is moespac_last_error().
+ *  - Plain pointers and sizes only. "_dev" pointers are device (HBM) memory,
+ *    "_host" pointers host memory. `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - The caller owns I/O buffers; a context owns expert slot pools, copy
+ *    streams, estimator state and scheduler state. One context per device,
+ *    driven by one host thread (not reentrant), mirroring the reference's
+ *    single-mutator rule.
+ *  - There is no CPU fallback: device entry points fail with
+ *    MOESPAC_E_CUDA when no usable sm_100 device is present.
+ */
+#ifndef MOESPAC_MOESPAC_H
+#define MOESPAC_MOESPAC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOESPAC_ABI_VERSION 1
+
+typedef enum moespac_status {
+  MOESPAC_OK = 0,
+  MOESPAC_E_INVALID = 1,
+  MOESPAC_E_RANGE = 2,
+  MOESPAC_E_LOGIC = 3,
+  MOESPAC_E_IO = 4,
+  MOESPAC_E_CUDA = 5,
+  MOESPAC_E_NCCL = 6,
+  MOESPAC_E_NOMEM = 7
+} moespac_status;
+
+const char* moespac_last_error(void);
+int moespac_abi_version(void);
+
+/* ------------------------------------------------------------------ config
+ * moespac_sched_config mirrors moesim::SimConfig (core/include/moesim/
+ * sim_core.hpp:23-36) with TraceConfig, HardwareProfile, EstimatorConfig and
+ * PolicySpec flattened; moespac_default_sched_config() == default_sim_config()
+ * (core/src/config.cpp:11-39). `policy` uses moesim::PolicyKind numbering
+ * (core/include/moesim/policies.hpp:18-27). */
+typedef struct moespac_sched_config {
+  int32_t n_layers, n_experts, top_k, gamma;
+  double alpha, drift_scale, route_noise;
+  int32_t shift_period, _pad0;
+  uint64_t seed;
+  int64_t t_cpu_unit_ns, t_gpu_unit_ns, t_io_unit_ns, t_draft_unit_ns, expert_bytes;
+  int32_t utility_cap, adaptive_boundaries;
+  double forgetting;
+  int32_t init_up, init_down;
+  int32_t policy, fixed_tau, fixed_up, fixed_down;
+  double cache_ratio;
+  int64_t token_budget;
+  int32_t max_steps, warmup_steps;
+  double ratio_smoothing;
+} moespac_sched_config;
+
+void moespac_default_sched_config(moespac_sched_config* out);
+
+/* LayerTiming / StepReport (core/include/moesim/sim_core.hpp:38-61). */
+typedef struct moespac_layer_timing {
+  int64_t t_cpu_ns, t_gpu_ns, t_io_used_ns, stall_ns, bubble_ns, wall_ns;
+  int32_t tau, fallback, n_prefetch, n_loads;
+} moespac_layer_timing;
+
+typedef struct moespac_step_report {
+  int64_t draft_ns, cache_hits, cache_misses, faults_fn, faults_fp, step_wall_ns;
+  double accuracy;
+  int32_t accepted_tokens, n_experts, n_layers, n_loads;
+  /* measured on the device for this step (0 when timing is off) */
+  float gpu_ms_total, gpu_ms_router, gpu_ms_hist, gpu_ms_ffn, gpu_ms_combine, gpu_ms_h2d_loads;
+} moespac_step_report;
+
+/* Realized split of one layer (core/src/sim_core.cpp:233-283), as K2 emits it. */
+typedef struct moespac_layer_outcome {
+  int32_t distinct, distinct_hits, hit_tokens, miss_tokens, agree, faults_fn, faults_fp, n_local_hits;
+} moespac_layer_outcome;
+
+/* ------------------------------------------------------------------ host scheduler
+ * Heterogeneous Workload Balancer + Asynchronous Execution Engine bookkeeping,
+ * host only (no device needed). Replaces the per-layer decision half of
+ * Simulation::run_utility_step (core/src/sim_core.cpp:177-228) and its
+ * accounting half (:229-297). shard_world > 1 runs expert-partitioned
+ * bookkeeping (expert e on shard e % shard_world). */
+typedef struct moespac_sched moespac_sched;
+
+moespac_status moespac_sched_create(const moespac_sched_config* cfg, int shard_world, moespac_sched** out);
+void moespac_sched_destroy(moespac_sched* s);
+/* Phase 1: scores_host [L][N] = estimator snapshot after the previous step. */
+moespac_status moespac_sched_decide(moespac_sched* s, const int32_t* scores_host);
+/* Decision tables of the last decide(): taus [L], resident/loaded bitmaps
+ * [L][ceil(N/32)], slot table [L][N] (slot within the owning shard, -1 if not
+ * resident). Any pointer may be NULL. */
+moespac_status moespac_sched_tables(const moespac_sched* s, int32_t* taus, uint32_t* resident_bits,
+                                    uint32_t* loaded_bits, int32_t* slot_table);
+/* Per-layer ThresholdDecision: [L][5] = tau, fallback, pred_cpu_ns, pred_gpu_ns, n_prefetch. */
+moespac_status moespac_sched_decisions(const moespac_sched* s, int64_t* out);
+/* Ordered loads of the last decide(): [n][4] = layer, expert, shard, slot. Returns n (or -1). */
+int64_t moespac_sched_loads(const moespac_sched* s, int32_t* out, int64_t cap);
+/* Phase 2 with K2 counters [L], or with host frequencies [L][N]. */
+moespac_status moespac_sched_observe(moespac_sched* s, const moespac_layer_outcome* outcomes, int accepted,
+                                     moespac_step_report* rep, moespac_layer_timing* layers);
+moespac_status moespac_sched_observe_freqs(moespac_sched* s, const int32_t* freqs_host, int accepted,
+                                           moespac_step_report* rep, moespac_layer_timing* layers);
+/* SimEvent log (sim_core.hpp:65-73): [n][6] = kind, step, layer, expert, start_ns, duration_ns. */
+int64_t moespac_sched_events(const moespac_sched* s, int64_t* out, int64_t cap);
+int64_t moespac_sched_total_time_ns(const moespac_sched* s);
+moespac_status moespac_sched_ratios(const moespac_sched* s, int layer, double* cpu_ratio, double* gpu_ratio,
+                                    int32_t* b_est);
+
+/* solve_threshold (core/src/workload_balancer.cpp:106-167). resident: [n] bytes.
+ * out[6] = tau, fallback, pred_cpu_ns, pred_gpu_ns, n_prefetch, evals. */
+moespac_status moespac_solve_threshold(const int32_t* scores, int n, const uint8_t* resident, int gamma,
+                                       int top_k, int b_est, const double* cpu_ratio, const double* gpu_ratio,
+                                       int cap, int64_t t_cpu_unit_ns, int64_t t_gpu_unit_ns,
+                                       int64_t t_io_unit_ns, int64_t expert_bytes, int64_t vram_left_bytes,
+                                       int64_t draft_credit_ns, int64_t* out);
+/* update_ratio_estimates (core/src/workload_balancer.cpp:169-199), in place. */
+moespac_status moespac_update_ratio_estimates(double* cpu_ratio, double* gpu_ratio, int cap, int tau_used,
+                                              double observed_rc, double observed_rg, double smoothing);
+/* layer_capacity_experts (core/src/sim_core.cpp:31-34). */
+int moespac_layer_capacity_experts(double cache_ratio, int n_experts);
+
+/* ------------------------------------------------------------------ device kernels (stateless)
+ * K1 — router top-k + gates. Replaces the selection block of
+ * TraceGenerator::next_step (core/src/trace_model.cpp:87-104).
+ * logits_dev [rows][n_experts] fp64 -> ids_dev [rows][top_k] ascending,
+ * gates_dev [rows][top_k] fp32 (may be NULL). gate_mode 0: softmax over the
+ * selected k (Eq. 3); 1: softmax over all N, not renormalised. n_experts <= 1024. */
+moespac_status moespac_router_topk(const double* logits_dev, int rows, int n_experts, int top_k, int gate_mode,
+                                   int32_t* ids_dev, float* gates_dev, void* stream);
+
+/* K2 — per layer: activation histogram (trace_model.cpp:122-130), exclusive
+ * scan, (expert, token, slot)-sorted permutation, LayerEstimator::observe_step
+ * (utility_estimator.cpp:47-72) in place on est_state_dev, and the realized
+ * split / accuracy / fault counters (sim_core.cpp:233-283). One launch for all
+ * layers. */
+typedef struct moespac_k2_args {
+  const int32_t* ids_dev;          /* [L][T][k] */
+  int32_t n_layers, tokens, top_k, n_experts;
+  const uint32_t* resident_bits_dev; /* [L][W] after this step's loads */
+  const uint32_t* loaded_bits_dev;   /* [L][W] loaded this step, or NULL */
+  const int32_t* taus_dev;           /* [L] */
+  int32_t* est_state_dev;            /* [L][N][4] score, up, down, last_freq */
+  int32_t utility_cap, adaptive_boundaries;
+  double forgetting;
+  int32_t shard_rank, shard_world;
+  int32_t* freqs_dev;      /* [L][N] */
+  int32_t* offsets_dev;    /* [L][N+1] */
+  int32_t* perm_dev;       /* [L][T*k] */
+  int32_t* hit_list_dev;   /* [L][N] */
+  int32_t* hit_ord_dev;    /* [L][N] */
+  int32_t* counters_dev;   /* [L][8] = moespac_layer_outcome */
+  int32_t* scores_out_dev; /* [L][N] */
+} moespac_k2_args;
+moespac_status moespac_hist_scan_observe(const moespac_k2_args* a, void* stream);
+
+/* LayerEstimator constructor state (utility_estimator.cpp:23-33) for n experts. */
+moespac_status moespac_estimator_init(int32_t* est_state_dev, int n, int gamma, int init_up, int init_down,
+                                      void* stream);
+
+/* K3 — grouped SwiGLU expert FFN over the resident activated experts of one
+ * layer (replaces the modeled charge at core/src/sim_core.cpp:253-254). */
+typedef struct moespac_ffn_args {
+  const uint16_t* h_dev;       /* [T][d] bf16 */
+  int32_t tokens, d_model, d_ffn, top_k, n_experts;
+  const int32_t* perm_dev, *offsets_dev;
+  const float* gates_dev;      /* [T][k] */
+  const int32_t* hit_list_dev, *counters_dev; /* one layer's K2 outputs */
+  const int32_t* slot_of_dev;  /* [N] */
+  const uint16_t* pool_dev;    /* tiled expert images, one per slot */
+  const uint16_t* shared_dev;  /* tiled shared-expert units */
+  int32_t n_shared_units;
+  float* workspace_dev;        /* moespac_ffn_workspace_bytes() */
+  int32_t grid;                /* 0 = one CTA per SM */
+} moespac_ffn_args;
+size_t moespac_ffn_workspace_bytes(int tokens, int d_model, int n_experts, int n_shared_units, int grid);
+int64_t moespac_expert_image_elems(int d_model, int d_ffn);
+moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream);
+
+/* Combine: y = sum of the K3 partials in fixed order; writes y_dev [T][d] fp32
+ * and/or h_out_dev = bf16(h_in + y + y_extra). ids/hit_ord from K1/K2. */
+typedef struct moespac_combine_args {
+  const uint16_t* h_in_dev;
+  const float* y_extra_dev;
+  int32_t tokens, d_model, d_ffn, top_k;
+  const int32_t* ids_dev, *hit_ord_dev, *counters_dev;
+  int32_t n_shared_units, grid;
+  const float* workspace_dev;
+  float* y_dev;
+  uint16_t* h_out_dev;
+} moespac_combine_args;
+moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream);
+
+/* Standard layouts (w_gate, w_up: [ffn][d]; w_down: [d][ffn]) -> tiled image. */
+moespac_status moespac_pack_expert(const uint16_t* w_gate_dev, const uint16_t* w_up_dev,
+                                   const uint16_t* w_down_dev, int d_model, int d_ffn, uint16_t* image_dev,
+                                   void* stream);
+moespac_status moespac_fill_synthetic(uint16_t* dev, int64_t n_elems, uint64_t seed, float stdv, void* stream);
+
+/* ------------------------------------------------------------------ engine context
+ * The full verification step on one device: K1 -> K2 -> per layer
+ * [wait own loads] K3 -> combine (-> NCCL all-reduce in expert-parallel mode),
+ * with the host scheduler deciding every layer's tau and loads during the
+ * draft window and the Asynchronous Execution Engine issuing each load as a
+ * pinned-host -> HBM cudaMemcpyAsync on a copy stream. Replaces
+ * Simulation::run_utility_step (core/src/sim_core.cpp:157-316). */
+typedef struct moespac_model_desc {
+  int32_t n_layers, n_experts, top_k, gamma;
+  int32_t d_model, d_ffn;
+  int32_t n_shared_units; /* shared experts expressed in units of d_ffn rows */
+  int32_t gate_mode;      /* see moespac_router_topk */
+} moespac_model_desc;
+
+typedef struct moespac_ctx moespac_ctx;
+
+/* expert_bytes in cfg is overridden by the real image size. */
+moespac_status moespac_ctx_create(int device, const moespac_model_desc* model, const moespac_sched_config* cfg,
+                                  int shard_rank, int shard_world, moespac_ctx** out);
+void moespac_ctx_destroy(moespac_ctx* c);
+/* Pinned host master copy: n_images tiled expert images; expert (l, e) is
+ * image (l*N + e) % n_images. Returns the host pointer for the caller to fill. */
+moespac_status moespac_ctx_host_arena(moespac_ctx* c, int64_t n_images, uint16_t** arena_host);
+/* Fill arena images + shared units with synthetic weights (seeded per image). */
+moespac_status moespac_ctx_fill_synthetic(moespac_ctx* c, uint64_t seed, float stdv);
+/* Shared units of layer l from a device buffer [n_shared_units][image]. */
+moespac_status moespac_ctx_set_shared(moespac_ctx* c, int layer, const uint16_t* units_dev);
+/* Upload the warm-fill residents (sim_core.cpp:108-111) from the arena. */
+moespac_status moespac_ctx_finalize(moespac_ctx* c);
+/* Expert-parallel combine over NCCL: 128-byte ncclUniqueId from rank 0. */
+moespac_status moespac_nccl_unique_id(void* out128);
+moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* unique_id128, int nranks, int rank);
+moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
+
+/* One verification step end to end with HOST buffers: H2D logits [L][T][N]
+ * fp64 and h_in [T][d] bf16, run, D2H h_out [T][d] bf16 + the step's
+ * scores/counters. `accepted` = tokens accepted this step (trace record). */
+moespac_status moespac_step(moespac_ctx* c, const double* logits_host, const uint16_t* h_in_host, int accepted,
+                            uint16_t* h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
+/* Same with device-resident inputs/outputs. */
+moespac_status moespac_step_device(moespac_ctx* c, const double* logits_dev, const uint16_t* h_in_dev,
+                                   int accepted, uint16_t* h_out_dev, moespac_step_report* rep,
+                                   moespac_layer_timing* layers);
+
+/* Device views of the last step (for parity checks; pointers owned by ctx). */
+typedef struct moespac_ctx_views {
+  const int32_t* ids_dev;       /* [L][T][k] */
+  const float* gates_dev;       /* [L][T][k] */
+  const int32_t* freqs_dev;     /* [L][N] */
+  const int32_t* offsets_dev;   /* [L][N+1] */
+  const int32_t* perm_dev;      /* [L][T*k] */
+  const int32_t* counters_dev;  /* [L][8] */
+  const int32_t* est_state_dev; /* [L][N][4] */
+  const uint16_t* h_dev;        /* [L+1][T][d] bf16 layer inputs / final output */
+  const float* y_dev;           /* [L][T][d] fp32 MoE outputs (this rank's partial before all-reduce) */
+  const uint16_t* pool_dev;     /* [L][slots][image] */
+  int64_t slots_per_layer, image_elems;
+} moespac_ctx_views;
+moespac_status moespac_ctx_get_views(const moespac_ctx* c, moespac_ctx_views* out);
+/* Host scheduler of the context (read-only use of the moespac_sched_* getters). */
+const moespac_sched* moespac_ctx_sched(const moespac_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOESPAC_MOESPAC_H */

@@ -1,0 +1,321 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes/numpy front-end to the CPU oracle.
+
+Importable only from tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs. The product package never imports it.
+
+Two libraries:
+  * ``_build/liboracle.so`` — plain-C restatement (moespac_oracle.c); always
+    built by ``make -C oracle`` (no reference tree needed);
+  * ``_ref/libmoesim_ref.so`` — the unmodified reference ``moesim_core``
+    compiled from /root/reference/proj/core/src/*.cpp plus ref_shim.cpp.
+    Built only where /root/reference exists; the built file travels to the
+    GPU box with the repo snapshot.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_ORC_PATH = os.path.join(HERE, "_build", "liboracle.so")
+_REF_PATH = os.path.join(HERE, "_ref", "libmoesim_ref.so")
+
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+
+
+def build() -> None:
+    subprocess.check_call(["make", "-s", "-C", HERE])
+
+
+_orc = None
+_ref = None
+
+
+def orc() -> C.CDLL:
+    global _orc
+    if _orc is None:
+        if not os.path.exists(_ORC_PATH):
+            build()
+        lib = C.CDLL(_ORC_PATH)
+        lib.orc_gen_create.restype = C.c_void_p
+        lib.orc_gen_create.argtypes = [C.c_int] * 4 + [C.c_double] * 3 + [C.c_int, C.c_uint64]
+        lib.orc_gen_destroy.argtypes = [C.c_void_p]
+        lib.orc_gen_next.restype = C.c_int
+        lib.orc_gen_next.argtypes = [C.c_void_p, C.c_void_p, _i32p]
+        lib.orc_router_topk.argtypes = [_f64p, C.c_int, C.c_int, C.c_int, C.c_int, _i32p, C.c_void_p]
+        lib.orc_hist_scan.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, _i32p, _i32p, _i32p]
+        lib.orc_estimator_init.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, C.c_int]
+        lib.orc_estimator_observe.argtypes = [_i32p, _i32p, C.c_int, C.c_int, C.c_double, C.c_int]
+        lib.orc_realized_split.argtypes = [_i32p, _i32p, _u8p, C.c_void_p, C.c_int, C.c_int, _i64p]
+        lib.orc_expert_apply.argtypes = [_u16p, C.c_int, C.c_int, _i32p, _f64p, C.c_int,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, _f64p, C.c_int]
+        lib.orc_expert_apply_f32.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, _f32p, C.c_int,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, _f32p, C.c_int]
+        lib.orc_max_threads.restype = C.c_int
+        lib.orc_f32_to_bf16.restype = C.c_uint16
+        lib.orc_f32_to_bf16.argtypes = [C.c_float]
+        _orc = lib
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(_REF_PATH)
+
+
+# --------------------------------------------------------------------------
+# Synthetic workload (restated TraceGenerator, trace_model.cpp:59-109)
+# --------------------------------------------------------------------------
+class Generator:
+    """Restated reference generator that also returns the noisy fp64 logits."""
+
+    def __init__(self, L, N, k, gamma, alpha=0.8, drift=0.02, noise=0.2, shift_period=0, seed=1):
+        self.L, self.N, self.k, self.gamma = L, N, k, gamma
+        self.T = gamma + 1
+        self._lib = orc()
+        self._h = self._lib.orc_gen_create(L, N, k, gamma, alpha, drift, noise, shift_period, seed)
+        if not self._h:
+            raise ValueError("invalid TraceConfig")
+
+    def next_step(self):
+        logits = np.empty((self.L, self.T, self.N), np.float64)
+        ids = np.empty((self.L, self.T, self.k), np.int32)
+        acc = self._lib.orc_gen_next(self._h, logits.ctypes.data, ids)
+        return logits, ids, acc
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.orc_gen_destroy(self._h)
+            self._h = None
+
+
+def router_topk(logits: np.ndarray, k: int, gate_mode: int = 0):
+    logits = np.ascontiguousarray(logits, np.float64)
+    N = logits.shape[-1]
+    rows = logits.size // N
+    ids = np.empty(rows * k, np.int32)
+    gates = np.empty(rows * k, np.float64)
+    orc().orc_router_topk(logits.reshape(-1), rows, N, k, gate_mode, ids, gates.ctypes.data)
+    shp = logits.shape[:-1] + (k,)
+    return ids.reshape(shp), gates.reshape(shp)
+
+
+def hist_scan(ids: np.ndarray, N: int):
+    ids = np.ascontiguousarray(ids, np.int32)
+    T, k = ids.shape
+    freqs = np.empty(N, np.int32)
+    offs = np.empty(N + 1, np.int32)
+    perm = np.empty(T * k, np.int32)
+    orc().orc_hist_scan(ids.reshape(-1), T, k, N, freqs, offs, perm)
+    return freqs, offs, perm
+
+
+def estimator_init(N, gamma, init_up=-1, init_down=-1):
+    st = np.empty((N, 4), np.int32)
+    orc().orc_estimator_init(st.reshape(-1), N, gamma, init_up, init_down)
+    return st
+
+
+def estimator_observe(state: np.ndarray, freqs: np.ndarray, cap: int, lam: float, adaptive=True):
+    st = np.ascontiguousarray(state, np.int32).copy()
+    orc().orc_estimator_observe(st.reshape(-1), np.ascontiguousarray(freqs, np.int32),
+                                st.shape[0], cap, lam, int(adaptive))
+    return st
+
+
+def realized_split(freqs, scores, resident, tau, loaded=None):
+    out = np.zeros(8, np.int64)
+    ld = None if loaded is None else np.ascontiguousarray(loaded, np.uint8)
+    orc().orc_realized_split(np.ascontiguousarray(freqs, np.int32),
+                             np.ascontiguousarray(scores, np.int32),
+                             np.ascontiguousarray(resident, np.uint8),
+                             None if ld is None else ld.ctypes.data, len(freqs), tau, out)
+    return out
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return r
+
+
+def expert_apply(h_bits, tok, gate, wg, wu, wd, y, n_threads=0):
+    """y[tok[i]] += gate[i] * SwiGLU_e(h[tok[i]]) in fp64 (standard layouts)."""
+    d = h_bits.shape[1]
+    ffn = wg.shape[0]
+    tok = np.ascontiguousarray(tok, np.int32)
+    gate = np.ascontiguousarray(gate, np.float64)
+    wg = np.ascontiguousarray(wg, np.uint16)
+    wu = np.ascontiguousarray(wu, np.uint16)
+    wd = np.ascontiguousarray(wd, np.uint16)
+    orc().orc_expert_apply(np.ascontiguousarray(h_bits, np.uint16), d, ffn, tok, gate, len(tok),
+                           wg.ctypes.data, wu.ctypes.data, wd.ctypes.data, y, n_threads)
+
+
+def moe_layer(h_bits, ids, gates, experts, shared=(), n_threads=0):
+    """Eq. 3 MoE layer output y (fp64 [T][d]) over the given experts.
+
+    experts: dict expert_id -> (wg[ffn][d], wu[ffn][d], wd[d][ffn]) bf16 bits;
+             activations whose expert is absent from the dict are skipped
+             (cold / other-shard experts).
+    shared:  sequence of (wg, wu, wd) applied to every token with gate 1.
+    """
+    T, d = h_bits.shape
+    y = np.zeros((T, d), np.float64)
+    k = ids.shape[1]
+    for e in sorted(experts):
+        toks = [t for t in range(T) for j in range(k) if ids[t, j] == e]
+        g = [gates[t, j] for t in range(T) for j in range(k) if ids[t, j] == e]
+        if toks:
+            wg, wu, wd = experts[e]
+            expert_apply(h_bits, toks, g, wg, wu, wd, y, n_threads)
+    for wg, wu, wd in shared:
+        expert_apply(h_bits, list(range(T)), [1.0] * T, wg, wu, wd, y, n_threads)
+    return y
+
+
+# --------------------------------------------------------------------------
+# The compiled reference (oracle/_ref)
+# --------------------------------------------------------------------------
+class RefSimConfig(C.Structure):
+    """Same field layout as moespac_sched_config (include/moespac/moespac.h)."""
+    _fields_ = [
+        ("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
+        ("alpha", C.c_double), ("drift_scale", C.c_double), ("route_noise", C.c_double),
+        ("shift_period", C.c_int32), ("_pad0", C.c_int32), ("seed", C.c_uint64),
+        ("t_cpu_unit_ns", C.c_int64), ("t_gpu_unit_ns", C.c_int64), ("t_io_unit_ns", C.c_int64),
+        ("t_draft_unit_ns", C.c_int64), ("expert_bytes", C.c_int64),
+        ("utility_cap", C.c_int32), ("adaptive_boundaries", C.c_int32), ("forgetting", C.c_double),
+        ("init_up", C.c_int32), ("init_down", C.c_int32),
+        ("policy", C.c_int32), ("fixed_tau", C.c_int32), ("fixed_up", C.c_int32), ("fixed_down", C.c_int32),
+        ("cache_ratio", C.c_double), ("token_budget", C.c_int64),
+        ("max_steps", C.c_int32), ("warmup_steps", C.c_int32), ("ratio_smoothing", C.c_double),
+    ]
+
+
+POLICIES = ["moe_spac", "on_demand_gpu", "lru_cache", "static_split", "ar_mode",
+            "fixed_tau", "fixed_boundaries", "binary_utility"]
+
+
+def default_config(**kw) -> RefSimConfig:
+    """default_sim_config() (proj/core/src/config.cpp:11-39) with overrides."""
+    c = RefSimConfig()
+    c.n_layers, c.n_experts, c.top_k, c.gamma = 48, 128, 8, 8
+    c.alpha, c.drift_scale, c.route_noise = 0.8, 0.02, 0.2
+    c.shift_period, c.seed = 0, 1
+    c.t_cpu_unit_ns, c.t_gpu_unit_ns, c.t_io_unit_ns, c.t_draft_unit_ns = 100_000, 40_000, 400_000, 300_000
+    c.expert_bytes = 25_000_000
+    c.utility_cap, c.adaptive_boundaries, c.forgetting = 4, 1, 0.1
+    c.init_up, c.init_down = -1, -1
+    c.policy, c.fixed_tau, c.fixed_up, c.fixed_down = 0, 2, 3, 1
+    c.cache_ratio, c.token_budget, c.max_steps, c.warmup_steps = 0.17, 512, 0, 32
+    c.ratio_smoothing = 0.3
+    for key, v in kw.items():
+        if key == "policy" and isinstance(v, str):
+            v = POLICIES.index(v)
+        setattr(c, key, v)
+    return c
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not os.path.exists(_REF_PATH):
+            raise FileNotFoundError(f"{_REF_PATH} not built (needs /root/reference; run make -C oracle)")
+        lib = C.CDLL(_REF_PATH)
+        P = C.POINTER(RefSimConfig)
+        lib.ref_last_error.restype = C.c_char_p
+        lib.ref_trace_generate.argtypes = [P, C.c_int, _i32p, _i32p]
+        lib.ref_trace_time_ns.restype = C.c_double
+        lib.ref_trace_time_ns.argtypes = [P, C.c_int]
+        lib.ref_sim_run.argtypes = [P, _i32p, _i32p, C.c_int, _i64p, _i64p, _f64p, _i64p, C.c_int64,
+                                    _i64p, _i64p]
+        lib.ref_sim_time_ns.restype = C.c_double
+        lib.ref_sim_time_ns.argtypes = [P, _i32p, _i32p, C.c_int]
+        lib.ref_estimator_run.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                          C.c_int, _i32p, _i32p, C.c_int]
+        lib.ref_estimator_init.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, _i32p]
+        lib.ref_solve_threshold.argtypes = [_i32p, C.c_int, _u8p, C.c_int, C.c_int, C.c_int, _f64p, _f64p,
+                                            C.c_int] + [C.c_int64] * 6 + [_i64p]
+        lib.ref_update_ratio_estimates.argtypes = [_f64p, _f64p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                                   C.c_double]
+        lib.ref_layer_capacity_experts.argtypes = [C.c_double, C.c_int]
+        _ref = lib
+    return _ref
+
+
+def _check(rc):
+    if rc < 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return rc
+
+
+def ref_trace(cfg: RefSimConfig, n_steps: int):
+    T = cfg.gamma + 1
+    ids = np.empty((n_steps, cfg.n_layers, T, cfg.top_k), np.int32)
+    acc = np.empty(n_steps, np.int32)
+    _check(ref().ref_trace_generate(C.byref(cfg), n_steps, ids.reshape(-1), acc))
+    return ids, acc
+
+
+@dataclass
+class RefRun:
+    layer_rec: np.ndarray  # [S][L][10]
+    step_rec: np.ndarray   # [S][8]
+    accuracy: np.ndarray   # [S]
+    events: np.ndarray     # [E][6] kind, step, layer, expert, start, dur
+    total_time_ns: int
+    steps: int = field(default=0)
+
+
+EV_DRAFT, EV_CPU, EV_GPU, EV_STALL, EV_LOAD, EV_EVICT = range(6)
+
+
+def ref_sim_run(cfg: RefSimConfig, ids: np.ndarray, accepted: np.ndarray) -> RefRun:
+    S = len(accepted)
+    L = cfg.n_layers
+    lr = np.zeros((S, L, 10), np.int64)
+    sr = np.zeros((S, 8), np.int64)
+    acc = np.zeros(S, np.float64)
+    cap = S * (1 + L * (4 + 2 * cfg.n_experts))
+    ev = np.zeros((cap, 6), np.int64)
+    nev = np.zeros(1, np.int64)
+    tot = np.zeros(1, np.int64)
+    steps = _check(ref().ref_sim_run(C.byref(cfg), np.ascontiguousarray(ids, np.int32).reshape(-1),
+                                     np.ascontiguousarray(accepted, np.int32), S, lr.reshape(-1),
+                                     sr.reshape(-1), acc, ev.reshape(-1), cap, nev, tot))
+    n = int(nev[0])
+    assert n <= cap
+    return RefRun(lr[:steps], sr[:steps], acc[:steps], ev[:n], int(tot[0]), steps)
+
+
+def ref_estimator_run(state, freqs_seq, cap, lam, gamma, adaptive=True, init_up=-1, init_down=-1):
+    st = np.ascontiguousarray(state, np.int32).copy()
+    fs = np.ascontiguousarray(freqs_seq, np.int32)
+    _check(ref().ref_estimator_run(st.shape[0], cap, lam, gamma, int(adaptive), init_up, init_down,
+                                   st.reshape(-1), fs.reshape(-1), fs.shape[0]))
+    return st
+
+
+def ref_solve_threshold(scores, resident, gamma, top_k, b_est, rc, rg, t_cpu, t_gpu, t_io,
+                        expert_bytes, vram_left, draft_credit):
+    out = np.zeros(6, np.int64)
+    cap = len(rc)
+    _check(ref().ref_solve_threshold(np.ascontiguousarray(scores, np.int32), len(scores),
+                                     np.ascontiguousarray(resident, np.uint8), gamma, top_k, b_est,
+                                     np.ascontiguousarray(rc, np.float64), np.ascontiguousarray(rg, np.float64),
+                                     cap, t_cpu, t_gpu, t_io, expert_bytes, vram_left, draft_credit, out))
+    return out

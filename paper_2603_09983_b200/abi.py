@@ -1,0 +1,406 @@
+"""ctypes binding of libmoespac.so (include/moespac/moespac.h).
+
+This is the Python face of the C ABI that the reference-side integration
+would bind. It adds no logic: every call goes straight
+to the native library, and device calls take torch CUDA tensors only as
+memory owners (their data_ptr). There is no CPU fallback — if the library or
+an sm_100 device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "_lib", "libmoespac.so")
+HEADER = os.path.join(_ROOT, "include", "moespac", "moespac.h")
+
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_RANGE", 3: "E_LOGIC", 4: "E_IO", 5: "E_CUDA", 6: "E_NCCL", 7: "E_NOMEM"}
+
+
+class MoespacError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.code = STATUS.get(status, str(status))
+        super().__init__(f"moespac {self.code}: {msg}")
+
+
+class SchedConfig(C.Structure):
+    """moespac_sched_config (mirrors moesim::SimConfig)."""
+    _fields_ = [
+        ("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
+        ("alpha", C.c_double), ("drift_scale", C.c_double), ("route_noise", C.c_double),
+        ("shift_period", C.c_int32), ("_pad0", C.c_int32), ("seed", C.c_uint64),
+        ("t_cpu_unit_ns", C.c_int64), ("t_gpu_unit_ns", C.c_int64), ("t_io_unit_ns", C.c_int64),
+        ("t_draft_unit_ns", C.c_int64), ("expert_bytes", C.c_int64),
+        ("utility_cap", C.c_int32), ("adaptive_boundaries", C.c_int32), ("forgetting", C.c_double),
+        ("init_up", C.c_int32), ("init_down", C.c_int32),
+        ("policy", C.c_int32), ("fixed_tau", C.c_int32), ("fixed_up", C.c_int32), ("fixed_down", C.c_int32),
+        ("cache_ratio", C.c_double), ("token_budget", C.c_int64),
+        ("max_steps", C.c_int32), ("warmup_steps", C.c_int32), ("ratio_smoothing", C.c_double),
+    ]
+
+
+class LayerTiming(C.Structure):
+    _fields_ = [("t_cpu_ns", C.c_int64), ("t_gpu_ns", C.c_int64), ("t_io_used_ns", C.c_int64),
+                ("stall_ns", C.c_int64), ("bubble_ns", C.c_int64), ("wall_ns", C.c_int64),
+                ("tau", C.c_int32), ("fallback", C.c_int32), ("n_prefetch", C.c_int32), ("n_loads", C.c_int32)]
+
+
+class StepReport(C.Structure):
+    _fields_ = [("draft_ns", C.c_int64), ("cache_hits", C.c_int64), ("cache_misses", C.c_int64),
+                ("faults_fn", C.c_int64), ("faults_fp", C.c_int64), ("step_wall_ns", C.c_int64),
+                ("accuracy", C.c_double), ("accepted_tokens", C.c_int32), ("n_experts", C.c_int32),
+                ("n_layers", C.c_int32), ("n_loads", C.c_int32),
+                ("gpu_ms_total", C.c_float), ("gpu_ms_router", C.c_float), ("gpu_ms_hist", C.c_float),
+                ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float)]
+
+
+class LayerOutcome(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("distinct", "distinct_hits", "hit_tokens", "miss_tokens", "agree",
+                                         "faults_fn", "faults_fp", "n_local_hits")]
+
+
+class K2Args(C.Structure):
+    _fields_ = [("ids_dev", C.c_void_p), ("n_layers", C.c_int32), ("tokens", C.c_int32), ("top_k", C.c_int32),
+                ("n_experts", C.c_int32), ("resident_bits_dev", C.c_void_p), ("loaded_bits_dev", C.c_void_p),
+                ("taus_dev", C.c_void_p), ("est_state_dev", C.c_void_p), ("utility_cap", C.c_int32),
+                ("adaptive_boundaries", C.c_int32), ("forgetting", C.c_double), ("shard_rank", C.c_int32),
+                ("shard_world", C.c_int32), ("freqs_dev", C.c_void_p), ("offsets_dev", C.c_void_p),
+                ("perm_dev", C.c_void_p), ("hit_list_dev", C.c_void_p), ("hit_ord_dev", C.c_void_p),
+                ("counters_dev", C.c_void_p), ("scores_out_dev", C.c_void_p)]
+
+
+class FfnArgs(C.Structure):
+    _fields_ = [("h_dev", C.c_void_p), ("tokens", C.c_int32), ("d_model", C.c_int32), ("d_ffn", C.c_int32),
+                ("top_k", C.c_int32), ("n_experts", C.c_int32), ("perm_dev", C.c_void_p),
+                ("offsets_dev", C.c_void_p), ("gates_dev", C.c_void_p), ("hit_list_dev", C.c_void_p),
+                ("counters_dev", C.c_void_p), ("slot_of_dev", C.c_void_p), ("pool_dev", C.c_void_p),
+                ("shared_dev", C.c_void_p), ("n_shared_units", C.c_int32), ("workspace_dev", C.c_void_p),
+                ("grid", C.c_int32)]
+
+
+class CombineArgs(C.Structure):
+    _fields_ = [("h_in_dev", C.c_void_p), ("y_extra_dev", C.c_void_p), ("tokens", C.c_int32),
+                ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("top_k", C.c_int32), ("ids_dev", C.c_void_p),
+                ("hit_ord_dev", C.c_void_p), ("counters_dev", C.c_void_p), ("n_shared_units", C.c_int32),
+                ("grid", C.c_int32), ("workspace_dev", C.c_void_p), ("y_dev", C.c_void_p),
+                ("h_out_dev", C.c_void_p)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
+                ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("n_shared_units", C.c_int32),
+                ("gate_mode", C.c_int32)]
+
+
+class CtxViews(C.Structure):
+    _fields_ = [("ids_dev", C.c_void_p), ("gates_dev", C.c_void_p), ("freqs_dev", C.c_void_p),
+                ("offsets_dev", C.c_void_p), ("perm_dev", C.c_void_p), ("counters_dev", C.c_void_p),
+                ("est_state_dev", C.c_void_p), ("h_dev", C.c_void_p), ("y_dev", C.c_void_p),
+                ("pool_dev", C.c_void_p), ("slots_per_layer", C.c_int64), ("image_elems", C.c_int64)]
+
+
+POLICIES = ["moe_spac", "on_demand_gpu", "lru_cache", "static_split", "ar_mode",
+            "fixed_tau", "fixed_boundaries", "binary_utility"]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libmoespac.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing — run paper_2603_09983_b200/build.py (or __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    sig = {
+        "moespac_last_error": (C.c_char_p, []),
+        "moespac_abi_version": (C.c_int, []),
+        "moespac_default_sched_config": (None, [C.POINTER(SchedConfig)]),
+        "moespac_sched_create": (C.c_int, [C.POINTER(SchedConfig), C.c_int, C.POINTER(vp)]),
+        "moespac_sched_destroy": (None, [vp]),
+        "moespac_sched_decide": (C.c_int, [vp, vp]),
+        "moespac_sched_tables": (C.c_int, [vp, vp, vp, vp, vp]),
+        "moespac_sched_decisions": (C.c_int, [vp, vp]),
+        "moespac_sched_loads": (i64, [vp, vp, i64]),
+        "moespac_sched_observe": (C.c_int, [vp, vp, C.c_int, vp, vp]),
+        "moespac_sched_observe_freqs": (C.c_int, [vp, vp, C.c_int, vp, vp]),
+        "moespac_sched_events": (i64, [vp, vp, i64]),
+        "moespac_sched_total_time_ns": (i64, [vp]),
+        "moespac_sched_ratios": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+        "moespac_solve_threshold": (C.c_int, [vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int,
+                                              i64, i64, i64, i64, i64, i64, vp]),
+        "moespac_update_ratio_estimates": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_double, C.c_double,
+                                                     C.c_double]),
+        "moespac_layer_capacity_experts": (C.c_int, [C.c_double, C.c_int]),
+        "moespac_router_topk": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
+        "moespac_hist_scan_observe": (C.c_int, [C.POINTER(K2Args), vp]),
+        "moespac_estimator_init": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]),
+        "moespac_ffn_workspace_bytes": (C.c_size_t, [C.c_int] * 5),
+        "moespac_expert_image_elems": (i64, [C.c_int, C.c_int]),
+        "moespac_expert_ffn": (C.c_int, [C.POINTER(FfnArgs), vp]),
+        "moespac_ffn_combine": (C.c_int, [C.POINTER(CombineArgs), vp]),
+        "moespac_pack_expert": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
+        "moespac_fill_synthetic": (C.c_int, [vp, i64, C.c_uint64, C.c_float, vp]),
+        "moespac_ctx_create": (C.c_int, [C.c_int, C.POINTER(ModelDesc), C.POINTER(SchedConfig), C.c_int, C.c_int,
+                                         C.POINTER(vp)]),
+        "moespac_ctx_destroy": (None, [vp]),
+        "moespac_ctx_host_arena": (C.c_int, [vp, i64, C.POINTER(vp)]),
+        "moespac_ctx_fill_synthetic": (C.c_int, [vp, C.c_uint64, C.c_float]),
+        "moespac_ctx_set_shared": (C.c_int, [vp, C.c_int, vp]),
+        "moespac_ctx_finalize": (C.c_int, [vp]),
+        "moespac_nccl_unique_id": (C.c_int, [vp]),
+        "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
+        "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+        "moespac_step": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
+        "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
+        "moespac_ctx_get_views": (C.c_int, [vp, C.POINTER(CtxViews)]),
+        "moespac_ctx_sched": (vp, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def header_functions() -> list[str]:
+    """Every function the public header declares."""
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(moespac_[a-z0-9_]+)\s*\(", txt)))
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise MoespacError(status, lib().moespac_last_error().decode())
+
+
+def ptr(x) -> int | None:
+    """Address of a torch tensor / numpy array (None passes NULL)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def default_config(**kw) -> SchedConfig:
+    c = SchedConfig()
+    lib().moespac_default_sched_config(C.byref(c))
+    for k, v in kw.items():
+        if k == "policy" and isinstance(v, str):
+            v = POLICIES.index(v)
+        setattr(c, k, v)
+    return c
+
+
+# ---------------------------------------------------------------- scheduler
+class Scheduler:
+    """Host scheduler (HWB + AEE bookkeeping): the decision half of run_utility_step."""
+
+    def __init__(self, cfg: SchedConfig, shard_world: int = 1):
+        self.cfg = cfg
+        self.L, self.N = cfg.n_layers, cfg.n_experts
+        self.W = (self.N + 31) // 32
+        h = C.c_void_p()
+        check(lib().moespac_sched_create(C.byref(cfg), shard_world, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moespac_sched_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def decide(self, scores: np.ndarray) -> None:
+        s = np.ascontiguousarray(scores, np.int32)
+        assert s.size == self.L * self.N
+        check(lib().moespac_sched_decide(self._h, s.ctypes.data))
+
+    def tables(self):
+        taus = np.zeros(self.L, np.int32)
+        rb = np.zeros((self.L, self.W), np.uint32)
+        lb = np.zeros((self.L, self.W), np.uint32)
+        slots = np.zeros((self.L, self.N), np.int32)
+        check(lib().moespac_sched_tables(self._h, taus.ctypes.data, rb.ctypes.data, lb.ctypes.data,
+                                         slots.ctypes.data))
+        return taus, rb, lb, slots
+
+    def decisions(self) -> np.ndarray:
+        out = np.zeros((self.L, 5), np.int64)
+        check(lib().moespac_sched_decisions(self._h, out.ctypes.data))
+        return out
+
+    def loads(self) -> np.ndarray:
+        n = lib().moespac_sched_loads(self._h, None, 0)
+        out = np.zeros((max(n, 1), 4), np.int32)
+        lib().moespac_sched_loads(self._h, out.ctypes.data, n)
+        return out[:n]
+
+    def observe_freqs(self, freqs: np.ndarray, accepted: int):
+        f = np.ascontiguousarray(freqs, np.int32)
+        rep = StepReport()
+        lay = (LayerTiming * self.L)()
+        check(lib().moespac_sched_observe_freqs(self._h, f.ctypes.data, accepted, C.byref(rep), lay))
+        return rep, list(lay)
+
+    def observe(self, outcomes: np.ndarray, accepted: int):
+        o = np.ascontiguousarray(outcomes, np.int32)
+        assert o.shape == (self.L, 8)
+        rep = StepReport()
+        lay = (LayerTiming * self.L)()
+        check(lib().moespac_sched_observe(self._h, o.ctypes.data, accepted, C.byref(rep), lay))
+        return rep, list(lay)
+
+    def events(self) -> np.ndarray:
+        n = lib().moespac_sched_events(self._h, None, 0)
+        out = np.zeros((max(n, 1), 6), np.int64)
+        lib().moespac_sched_events(self._h, out.ctypes.data, n)
+        return out[:n]
+
+    def total_time_ns(self) -> int:
+        return lib().moespac_sched_total_time_ns(self._h)
+
+    def ratios(self, layer: int):
+        K = self.cfg.utility_cap if self.cfg.policy != POLICIES.index("binary_utility") else 1
+        rc = np.zeros(K, np.float64)
+        rg = np.zeros(K, np.float64)
+        b = C.c_int32()
+        check(lib().moespac_sched_ratios(self._h, layer, rc.ctypes.data, rg.ctypes.data, C.byref(b)))
+        return rc, rg, b.value
+
+
+def solve_threshold(scores, resident, gamma, top_k, b_est, rc, rg, t_cpu, t_gpu, t_io, expert_bytes, vram_left,
+                    draft_credit) -> np.ndarray:
+    out = np.zeros(6, np.int64)
+    s = np.ascontiguousarray(scores, np.int32)
+    r = np.ascontiguousarray(resident, np.uint8)
+    rc = np.ascontiguousarray(rc, np.float64)
+    rg = np.ascontiguousarray(rg, np.float64)
+    check(lib().moespac_solve_threshold(s.ctypes.data, len(s), r.ctypes.data, gamma, top_k, b_est, rc.ctypes.data,
+                                        rg.ctypes.data, len(rc), t_cpu, t_gpu, t_io, expert_bytes, vram_left,
+                                        draft_credit, out.ctypes.data))
+    return out
+
+
+# ---------------------------------------------------------------- device kernels
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(stream)
+
+
+def router_topk(logits, k: int, gate_mode: int = 0, stream=None):
+    """K1 on a CUDA fp64 tensor [..., N] -> (ids int32 [..., k], gates fp32 [..., k])."""
+    import torch
+    assert logits.is_cuda and logits.dtype == torch.float64 and logits.is_contiguous()
+    N = logits.shape[-1]
+    rows = logits.numel() // N
+    ids = torch.empty(logits.shape[:-1] + (k,), dtype=torch.int32, device=logits.device)
+    gates = torch.empty(logits.shape[:-1] + (k,), dtype=torch.float32, device=logits.device)
+    check(lib().moespac_router_topk(ptr(logits), rows, N, k, gate_mode, ptr(ids), ptr(gates), _stream(stream)))
+    return ids, gates
+
+
+def expert_image_elems(d: int, ffn: int) -> int:
+    return lib().moespac_expert_image_elems(d, ffn)
+
+
+def pack_expert(wg, wu, wd, stream=None):
+    """Standard-layout bf16 (as torch.bfloat16 or int16/uint16 views) -> tiled image (uint16 view)."""
+    import torch
+    ffn, d = wg.shape
+    out = torch.empty(3 * ffn * d, dtype=torch.int16, device=wg.device)
+    check(lib().moespac_pack_expert(ptr(wg), ptr(wu), ptr(wd), d, ffn, ptr(out), _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------- engine context
+class Context:
+    """moespac_ctx: the full verification step on one device."""
+
+    def __init__(self, device: int, model: ModelDesc, cfg: SchedConfig, rank: int = 0, world: int = 1):
+        self.model, self.cfg, self.rank, self.world = model, cfg, rank, world
+        h = C.c_void_p()
+        check(lib().moespac_ctx_create(device, C.byref(model), C.byref(cfg), rank, world, C.byref(h)))
+        self._h = h
+        self.T = model.gamma + 1
+        self.image_elems = expert_image_elems(model.d_model, model.d_ffn)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moespac_ctx_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def host_arena(self, n_images: int) -> np.ndarray:
+        p = C.c_void_p()
+        check(lib().moespac_ctx_host_arena(self._h, n_images, C.byref(p)))
+        arr = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint16)), shape=(n_images, self.image_elems))
+        return arr
+
+    def fill_synthetic(self, seed: int = 3, stdv: float = 0.02):
+        check(lib().moespac_ctx_fill_synthetic(self._h, seed, stdv))
+
+    def set_shared(self, layer: int, units_dev):
+        check(lib().moespac_ctx_set_shared(self._h, layer, ptr(units_dev)))
+
+    def finalize(self):
+        check(lib().moespac_ctx_finalize(self._h))
+
+    def set_timing(self, on: bool = True):
+        check(lib().moespac_ctx_set_timing(self._h, int(on)))
+
+    def set_nccl(self, uid: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(uid, 128)
+        check(lib().moespac_ctx_set_nccl(self._h, buf, nranks, rank))
+
+    def step(self, logits_host: np.ndarray, h_in_host: np.ndarray, accepted: int, h_out_host: np.ndarray):
+        rep = StepReport()
+        lay = (LayerTiming * self.model.n_layers)()
+        check(lib().moespac_step(self._h, ptr(logits_host), ptr(h_in_host), accepted, ptr(h_out_host),
+                                 C.byref(rep), lay))
+        return rep, list(lay)
+
+    def step_device(self, logits_dev, h_in_dev, accepted: int, h_out_dev):
+        rep = StepReport()
+        lay = (LayerTiming * self.model.n_layers)()
+        check(lib().moespac_step_device(self._h, ptr(logits_dev), ptr(h_in_dev), accepted, ptr(h_out_dev),
+                                        C.byref(rep), lay))
+        return rep, list(lay)
+
+    def views(self) -> CtxViews:
+        v = CtxViews()
+        check(lib().moespac_ctx_get_views(self._h, C.byref(v)))
+        return v
+
+    def sched_events(self) -> np.ndarray:
+        s = lib().moespac_ctx_sched(self._h)
+        n = lib().moespac_sched_events(s, None, 0)
+        out = np.zeros((max(n, 1), 6), np.int64)
+        lib().moespac_sched_events(s, out.ctypes.data, n)
+        return out[:n]
+
+    def sched_decisions(self) -> np.ndarray:
+        s = lib().moespac_ctx_sched(self._h)
+        out = np.zeros((self.model.n_layers, 5), np.int64)
+        check(lib().moespac_sched_decisions(s, out.ctypes.data))
+        return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().moespac_nccl_unique_id(buf))
+    return buf.raw

@@ -1,0 +1,53 @@
+"""The five BASELINE.json workload shapes.
+
+d / ffn / layer counts / shared experts come from the public model configs,
+not from the reference (which has no FFN at all; its "expert" is
+expert_bytes = 25 MB, core/src/config.cpp:27). Gate normalisation per model:
+Mixtral and Qwen3 renormalise over the top-k (Eq. 3, gate_mode 0);
+Qwen1.5-MoE and DeepSeek-V2-Lite take the softmax over all N (gate_mode 1).
+Shared experts are expressed as units of d_ffn rows (Qwen1.5: one 5632-row
+shared expert = 4 units of 1408; DeepSeek-V2-Lite: 2 x 1408 = 2 units).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+
+@dataclass(frozen=True)
+class WorkloadConfig:
+    name: str
+    n_layers: int
+    n_experts: int
+    top_k: int
+    gamma: int
+    d_model: int
+    d_ffn: int
+    n_shared_units: int = 0
+    gate_mode: int = 0
+    cache_ratio: float = 0.17
+    description: str = ""
+
+    @property
+    def tokens(self) -> int:
+        return self.gamma + 1
+
+    @property
+    def expert_bytes(self) -> int:
+        return 3 * self.d_model * self.d_ffn * 2
+
+    def with_(self, **kw) -> "WorkloadConfig":
+        return replace(self, **kw)
+
+
+CONFIGS = {
+    "tiny": WorkloadConfig("tiny", 1, 8, 2, 4, 512, 1024, 0, 0, 0.17,
+                           "tiny synthetic MoE layer: 8 experts top-2, d=512, ffn=1024, draft_len=4"),
+    "mixtral": WorkloadConfig("mixtral", 32, 8, 2, 4, 4096, 14336, 0, 0, 1.0,
+                              "Mixtral-8x7B-shaped MoE layer: 8 experts top-2, d=4096, ffn=14336, draft_len=4, bf16"),
+    "qwen15": WorkloadConfig("qwen15", 24, 60, 4, 6, 2048, 1408, 4, 1, 0.5,
+                             "Qwen1.5-MoE-A2.7B shape: 60 experts top-4 + shared expert, draft_len=6, 50% cache"),
+    "dsv2": WorkloadConfig("dsv2", 27, 64, 6, 8, 2048, 1408, 2, 1, 0.17,
+                           "DeepSeek-V2-Lite shape: 64 routed experts top-6, 27 layers, draft_len=8"),
+    "qwen3": WorkloadConfig("qwen3", 48, 128, 8, 8, 2048, 768, 0, 0, 0.17,
+                            "Qwen3-30B-A3B shape: 128 experts top-8, cache-budget sweep 10-100%"),
+}

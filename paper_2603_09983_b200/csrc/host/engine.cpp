@@ -1,0 +1,497 @@
+// Device engine — the B200 replacement for Simulation::run_utility_step
+// (/root/reference/proj/core/src/sim_core.cpp:157-316). See engine.hpp.
+//
+// Per step, on one device:
+//   host   : StepScheduler::decide() for all L layers (draft window)
+//   copy   : every decided load -> cudaMemcpyAsync(pinned arena -> HBM slot)
+//            in drain order; event load_done[l] after layer l's loads
+//   compute: H2D tables (+ logits, h_in) -> K1 (all layers) -> K2 (all
+//            layers) -> for each layer: wait load_done[l], K3, combine
+//            (expert-parallel: fp32 partial -> ncclAllReduce -> residual)
+//            -> D2H scores + counters (+ h_out)
+//   host   : StepScheduler::observe() with the K2 counters.
+#include "engine.hpp"
+
+#include <dlfcn.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../kernels/launch.hpp"
+
+namespace moespac {
+
+// ---- minimal NCCL surface, resolved at run time -------------------------
+struct NcclApi {
+  void* so = nullptr;
+  int (*get_unique_id)(void*) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  static NcclApi* load() {
+    auto* a = new NcclApi;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((a->so = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!a->so) {
+      delete a;
+      throw NcclError("libnccl.so.2 not loadable");
+    }
+    a->get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(a->so, "ncclGetUniqueId"));
+    a->all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(a->so, "ncclAllReduce"));
+    a->comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(a->so, "ncclCommDestroy"));
+    a->error_string = reinterpret_cast<const char* (*)(int)>(dlsym(a->so, "ncclGetErrorString"));
+    if (!a->get_unique_id || !a->all_reduce || !a->comm_destroy) {
+      delete a;
+      throw NcclError("libnccl missing symbols");
+    }
+    return a;
+  }
+};
+
+struct NcclUid {
+  char internal[128];
+};
+using CommInitFn = int (*)(void**, int, NcclUid, int);
+
+moespac_status nccl_unique_id(void* out) {
+  std::unique_ptr<NcclApi> api(NcclApi::load());
+  return api->get_unique_id(out) == 0 ? MOESPAC_OK : MOESPAC_E_NCCL;
+}
+
+void Engine::check(cudaError_t e, const char* what) const {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_config& c, int rank, int world)
+    : device_(device), rank_(rank), world_(world), m_(m) {
+  if (m.n_layers < 1 || m.n_experts < 1 || m.top_k < 1 || m.top_k > m.n_experts || m.gamma < 1)
+    throw std::invalid_argument("moespac_model_desc: invalid shape");
+  if (m.d_model % 512 != 0 || m.d_ffn % kFfnChunkRows != 0 || m.d_ffn <= 0)
+    throw std::invalid_argument("moespac_model_desc: d_model % 512 == 0 and d_ffn % 16 == 0 required");
+  if (m.gamma + 1 > kFfnMaxTokens) throw std::invalid_argument("moespac_model_desc: gamma + 1 must be <= 16");
+  if (m.n_experts > 1024) throw std::invalid_argument("moespac_model_desc: n_experts must be <= 1024");
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("moespac_ctx: bad shard rank/world");
+  if (m.n_layers != c.n_layers || m.n_experts != c.n_experts || m.top_k != c.top_k || m.gamma != c.gamma)
+    throw std::invalid_argument("moespac_ctx: model desc and sched config disagree on the workload shape");
+  T_ = m.gamma + 1;
+  W_ = (m.n_experts + 31) / 32;
+  image_elems_ = 3LL * m.d_ffn * m.d_model;
+
+  SchedConfig sc;
+  sc.n_layers = c.n_layers;
+  sc.n_experts = c.n_experts;
+  sc.top_k = c.top_k;
+  sc.gamma = c.gamma;
+  sc.profile.t_cpu_unit_ns = c.t_cpu_unit_ns;
+  sc.profile.t_gpu_unit_ns = c.t_gpu_unit_ns;
+  sc.profile.t_io_unit_ns = c.t_io_unit_ns;
+  sc.profile.t_draft_unit_ns = c.t_draft_unit_ns;
+  sc.profile.expert_bytes = image_elems_ * 2;  // real image size (decision-neutral)
+  sc.estimator.utility_cap = c.utility_cap;
+  sc.estimator.forgetting = c.forgetting;
+  sc.estimator.gamma = c.gamma;
+  sc.estimator.adaptive_boundaries = c.adaptive_boundaries != 0;
+  sc.estimator.init_up = c.init_up;
+  sc.estimator.init_down = c.init_down;
+  sc.policy.kind = static_cast<PolicyKind>(c.policy);
+  sc.policy.fixed_tau = c.fixed_tau;
+  sc.policy.fixed_up = c.fixed_up;
+  sc.policy.fixed_down = c.fixed_down;
+  sc.cache_ratio = c.cache_ratio;
+  sc.ratio_smoothing = c.ratio_smoothing;
+  sc.shard_world = world;
+  sched_ = std::make_unique<StepScheduler>(sc);
+  slots_ = sched_->slots_per_layer(rank);
+
+  int ndev = 0;
+  check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) throw CudaError("moespac_ctx: no such CUDA device");
+  check(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10) throw CudaError("moespac requires an sm_100 (B200) device");
+  sms_ = prop.multiProcessorCount;
+  stages_ = ffn_pick_stages(T_, m.d_model, prop.sharedMemPerBlockOptin);
+  if (stages_ == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
+  ffn_smem_ = ffn_smem_bytes(T_, m.d_model, stages_);
+
+  const int L = m.n_layers, N = m.n_experts, k = m.top_k, d = m.d_model;
+  auto dmalloc = [&](void** p, size_t bytes, const char* what) {
+    check(cudaMalloc(p, bytes ? bytes : 16), what);
+  };
+  dmalloc(reinterpret_cast<void**>(&pool_), static_cast<size_t>(L) * slots_ * image_elems_ * 2, "cudaMalloc pool");
+  dmalloc(reinterpret_cast<void**>(&shared_), static_cast<size_t>(L) * m.n_shared_units * image_elems_ * 2,
+          "cudaMalloc shared");
+  if (m.n_shared_units > 0)
+    check(cudaMemset(shared_, 0, static_cast<size_t>(L) * m.n_shared_units * image_elems_ * 2), "memset");
+  dmalloc(reinterpret_cast<void**>(&logits_d_), sizeof(double) * L * T_ * N, "cudaMalloc logits");
+  dmalloc(reinterpret_cast<void**>(&ids_d_), sizeof(int32_t) * L * T_ * k, "cudaMalloc ids");
+  dmalloc(reinterpret_cast<void**>(&gates_d_), sizeof(float) * L * T_ * k, "cudaMalloc gates");
+  dmalloc(reinterpret_cast<void**>(&freqs_d_), sizeof(int32_t) * L * N, "cudaMalloc freqs");
+  dmalloc(reinterpret_cast<void**>(&offsets_d_), sizeof(int32_t) * L * (N + 1), "cudaMalloc offsets");
+  dmalloc(reinterpret_cast<void**>(&perm_d_), sizeof(int32_t) * L * T_ * k, "cudaMalloc perm");
+  dmalloc(reinterpret_cast<void**>(&hit_list_d_), sizeof(int32_t) * L * N, "cudaMalloc hit_list");
+  dmalloc(reinterpret_cast<void**>(&hit_ord_d_), sizeof(int32_t) * L * N, "cudaMalloc hit_ord");
+  dmalloc(reinterpret_cast<void**>(&est_d_), sizeof(int32_t) * L * N * 4, "cudaMalloc est");
+  dmalloc(reinterpret_cast<void**>(&y_d_), sizeof(float) * L * T_ * d, "cudaMalloc y");
+  dmalloc(reinterpret_cast<void**>(&h_d_), sizeof(uint16_t) * (L + 1) * T_ * d, "cudaMalloc h");
+  work_bytes_ = static_cast<size_t>(sms_ + N + m.n_shared_units) * T_ * d * 4;
+  dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
+  tables_bytes_ = sizeof(uint32_t) * 2 * L * W_ + sizeof(int32_t) * L + sizeof(int32_t) * L * N;
+  dmalloc(reinterpret_cast<void**>(&tables_d_), tables_bytes_, "cudaMalloc tables");
+  out_bytes_ = sizeof(int32_t) * (L * N + L * 8);
+  dmalloc(reinterpret_cast<void**>(&out_d_), out_bytes_, "cudaMalloc out");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&tables_h_), tables_bytes_, cudaHostAllocDefault), "cudaHostAlloc");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&out_h_), out_bytes_, cudaHostAllocDefault), "cudaHostAlloc");
+  check(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking), "stream");
+  check(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "stream");
+  load_done_.resize(static_cast<size_t>(L));
+  ffn_beg_.resize(static_cast<size_t>(L));
+  ffn_end_.resize(static_cast<size_t>(L));
+  for (int l = 0; l < L; ++l) {
+    check(cudaEventCreateWithFlags(&load_done_[static_cast<size_t>(l)], cudaEventDisableTiming), "event");
+    check(cudaEventCreate(&ffn_beg_[static_cast<size_t>(l)]), "event");
+    check(cudaEventCreate(&ffn_end_[static_cast<size_t>(l)]), "event");
+  }
+  for (auto& e : ev_) check(cudaEventCreate(&e), "event");
+
+  // LayerEstimator ctor state for every layer (utility_estimator.cpp:23-33)
+  const EstimatorConfig ec = estimator_config_for(sched_->config().policy, sched_->config().estimator);
+  const int init_up = ec.init_up >= 0 ? ec.init_up : ec.gamma / 2;
+  const int init_down = ec.init_down >= 0 ? ec.init_down : ec.gamma / 2;
+  check(launch_estimator_init(est_d_, L * N, init_up, init_down, compute_), "estimator init");
+  check(cudaStreamSynchronize(compute_), "sync");
+  scores_.assign(static_cast<size_t>(L) * N, 0);
+}
+
+Engine::~Engine() {
+  cudaSetDevice(device_);
+  if (compute_) cudaStreamSynchronize(compute_);
+  if (copy_) cudaStreamSynchronize(copy_);
+  if (comm_ && nccl_) nccl_->comm_destroy(comm_);
+  for (void* p : {static_cast<void*>(pool_), static_cast<void*>(shared_), static_cast<void*>(logits_d_),
+                  static_cast<void*>(ids_d_), static_cast<void*>(gates_d_), static_cast<void*>(freqs_d_),
+                  static_cast<void*>(offsets_d_), static_cast<void*>(perm_d_), static_cast<void*>(hit_list_d_),
+                  static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
+                  static_cast<void*>(h_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
+                  static_cast<void*>(out_d_)})
+    if (p) cudaFree(p);
+  if (arena_h_) cudaFreeHost(arena_h_);
+  if (tables_h_) cudaFreeHost(tables_h_);
+  if (out_h_) cudaFreeHost(out_h_);
+  for (auto e : load_done_) cudaEventDestroy(e);
+  for (auto e : ffn_beg_) cudaEventDestroy(e);
+  for (auto e : ffn_end_) cudaEventDestroy(e);
+  for (auto e : ev_)
+    if (e) cudaEventDestroy(e);
+  if (compute_) cudaStreamDestroy(compute_);
+  if (copy_) cudaStreamDestroy(copy_);
+}
+
+uint16_t* Engine::host_arena(int64_t n_images) {
+  if (n_images < 1) throw std::invalid_argument("host arena: n_images >= 1");
+  if (arena_h_) cudaFreeHost(arena_h_);
+  arena_h_ = nullptr;
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  const cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&arena_h_),
+                                      static_cast<size_t>(n_images) * image_elems_ * 2, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    arena_h_ = nullptr;
+    throw std::bad_alloc();
+  }
+  n_images_ = n_images;
+  synthetic_ = false;
+  finalized_ = false;
+  return arena_h_;
+}
+
+static uint64_t image_seed(uint64_t seed, int64_t image) {
+  return seed * 1000003ULL + static_cast<uint64_t>(image) * 0x9E3779B97F4A7C15ULL + 1;
+}
+
+void Engine::fill_synthetic(uint64_t seed, float stdv) {
+  if (!arena_h_) throw std::logic_error("fill_synthetic: allocate the host arena first");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  uint16_t* tmp = nullptr;
+  check(cudaMalloc(&tmp, image_elems_ * 2), "cudaMalloc tmp");
+  for (int64_t i = 0; i < n_images_; ++i) {
+    check(launch_fill_synthetic(tmp, image_elems_, image_seed(seed, i), stdv, compute_), "fill");
+    check(cudaMemcpyAsync(arena_h_ + i * image_elems_, tmp, image_elems_ * 2, cudaMemcpyDeviceToHost, compute_),
+          "D2H arena");
+  }
+  for (int l = 0; l < m_.n_layers; ++l)
+    for (int u = 0; u < m_.n_shared_units; ++u)
+      check(launch_fill_synthetic(shared_ + (static_cast<int64_t>(l) * m_.n_shared_units + u) * image_elems_,
+                                  image_elems_, image_seed(seed ^ 0x5bd1e995ULL, l * 64 + u), stdv, compute_),
+            "fill shared");
+  check(cudaStreamSynchronize(compute_), "sync");
+  cudaFree(tmp);
+  synthetic_ = true;
+  synth_seed_ = seed;
+  synth_std_ = stdv;
+}
+
+void Engine::set_shared(int layer, const uint16_t* units_dev) {
+  if (layer < 0 || layer >= m_.n_layers) throw std::out_of_range("set_shared: layer out of range");
+  check(cudaMemcpyAsync(shared_ + static_cast<int64_t>(layer) * m_.n_shared_units * image_elems_, units_dev,
+                        static_cast<size_t>(m_.n_shared_units) * image_elems_ * 2, cudaMemcpyDeviceToDevice, compute_),
+        "copy shared");
+  check(cudaStreamSynchronize(compute_), "sync");
+}
+
+// Warm fill (sim_core.cpp:108-111): the residents the scheduler placed at
+// construction are uploaded into their slots.
+void Engine::finalize() {
+  if (!arena_h_) throw std::logic_error("finalize: no host arena");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  const std::vector<int32_t>& slot = sched_->slot_table();
+  const int N = m_.n_experts;
+  for (int l = 0; l < m_.n_layers; ++l)
+    for (int e = rank_; e < N; e += world_) {
+      const int s = slot[static_cast<size_t>(l) * N + e];
+      if (s < 0) continue;
+      if (synthetic_)
+        check(launch_fill_synthetic(slot_ptr(l, s), image_elems_, image_seed(synth_seed_, image_of(l, e)), synth_std_,
+                                    compute_),
+              "fill slot");
+      else
+        check(cudaMemcpyAsync(slot_ptr(l, s), arena_h_ + image_of(l, e) * image_elems_, image_elems_ * 2,
+                              cudaMemcpyHostToDevice, compute_),
+              "warm fill");
+    }
+  check(cudaStreamSynchronize(compute_), "sync");
+  finalized_ = true;
+}
+
+void Engine::set_nccl(const void* uid, int nranks, int rank) {
+  if (nranks != world_ || rank != rank_) throw std::invalid_argument("set_nccl: ranks disagree with the shard layout");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  nccl_.reset(NcclApi::load());
+  auto init = reinterpret_cast<CommInitFn>(dlsym(nccl_->so, "ncclCommInitRank"));
+  if (!init) throw NcclError("ncclCommInitRank missing");
+  NcclUid id;
+  std::memcpy(id.internal, uid, 128);
+  const int r = init(&comm_, nranks, id, rank);
+  if (r != 0) throw NcclError(std::string("ncclCommInitRank: ") + (nccl_->error_string ? nccl_->error_string(r) : "?"));
+}
+
+void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
+                  uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers) {
+  if (!finalized_) throw std::logic_error("moespac_step: context not finalized");
+  if (world_ > 1 && !comm_) throw std::logic_error("moespac_step: expert-parallel context needs moespac_ctx_set_nccl");
+  if (accepted < 1 || accepted > T_) throw std::out_of_range("moespac_step: accepted must be in [1, gamma+1]");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  const int L = m_.n_layers, N = m_.n_experts, k = m_.top_k, d = m_.d_model;
+
+  // ---- host: decisions for every layer (the draft window) ----
+  sched_->decide(scores_.data());
+  uint32_t* rb = reinterpret_cast<uint32_t*>(tables_h_);
+  uint32_t* lb = rb + static_cast<size_t>(L) * W_;
+  int32_t* taus = reinterpret_cast<int32_t*>(lb + static_cast<size_t>(L) * W_);
+  int32_t* slots = taus + L;
+  std::memcpy(rb, sched_->resident_bits().data(), sizeof(uint32_t) * L * W_);
+  std::memcpy(lb, sched_->loaded_bits().data(), sizeof(uint32_t) * L * W_);
+  std::memcpy(taus, sched_->taus().data(), sizeof(int32_t) * L);
+  std::memcpy(slots, sched_->slot_table().data(), sizeof(int32_t) * L * N);
+  const uint32_t* rb_d = reinterpret_cast<const uint32_t*>(tables_d_);
+  const uint32_t* lb_d = rb_d + static_cast<size_t>(L) * W_;
+  const int32_t* taus_d = reinterpret_cast<const int32_t*>(lb_d + static_cast<size_t>(L) * W_);
+  const int32_t* slots_d = taus_d + L;
+
+  if (timing_) check(cudaEventRecord(ev_[0], compute_), "event");
+  // ---- copy engine: loads in drain order, one event per layer ----
+  int n_loads = 0;
+  {
+    size_t i = 0;
+    const auto& loads = sched_->loads();
+    for (int l = 0; l < L; ++l) {
+      for (; i < loads.size() && loads[i].layer == l; ++i) {
+        const SlotLoad& ld = loads[i];
+        if (ld.shard != rank_) continue;
+        check(cudaMemcpyAsync(slot_ptr(l, ld.slot), arena_h_ + image_of(l, ld.expert) * image_elems_,
+                              image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
+              "H2D expert load");
+        ++n_loads;
+      }
+      check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
+    }
+  }
+  // ---- compute stream ----
+  check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
+  const double* lg = logits;
+  if (logits_host) {
+    check(cudaMemcpyAsync(logits_d_, logits, sizeof(double) * L * T_ * N, cudaMemcpyHostToDevice, compute_),
+          "H2D logits");
+    lg = logits_d_;
+  }
+  check(cudaMemcpyAsync(h_d_, h_in, sizeof(uint16_t) * T_ * d,
+                        h_in_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, compute_),
+        "h_in");
+  if (timing_) check(cudaEventRecord(ev_[1], compute_), "event");
+  check(launch_router_topk(lg, L * T_, N, k, m_.gate_mode, ids_d_, gates_d_, compute_), "K1 router");
+  if (timing_) check(cudaEventRecord(ev_[2], compute_), "event");
+  dev::K2Args a2{};
+  a2.ids = ids_d_;
+  a2.L = L;
+  a2.T = T_;
+  a2.k = k;
+  a2.N = N;
+  a2.resident_bits = rb_d;
+  a2.loaded_bits = lb_d;
+  a2.taus = taus_d;
+  a2.est_state = est_d_;
+  {
+    const EstimatorConfig ec = estimator_config_for(sched_->config().policy, sched_->config().estimator);
+    a2.utility_cap = ec.utility_cap;
+    a2.adaptive = ec.adaptive_boundaries ? 1 : 0;
+    a2.forgetting = ec.forgetting;
+  }
+  a2.shard_rank = rank_;
+  a2.shard_world = world_;
+  a2.freqs = freqs_d_;
+  a2.offsets = offsets_d_;
+  a2.perm = perm_d_;
+  a2.hit_list = hit_list_d_;
+  a2.hit_ord = hit_ord_d_;
+  int32_t* scores_out_d = out_d_;
+  int32_t* counters_d = out_d_ + static_cast<size_t>(L) * N;
+  a2.counters = counters_d;
+  a2.scores_out = scores_out_d;
+  check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
+  if (timing_) check(cudaEventRecord(ev_[3], compute_), "event");
+
+  for (int l = 0; l < L; ++l) {
+    check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
+    const uint16_t* hl = h_d_ + static_cast<size_t>(l) * T_ * d;
+    uint16_t* hn = h_d_ + static_cast<size_t>(l + 1) * T_ * d;
+    dev::FfnArgs fa{};
+    fa.h = hl;
+    fa.T = T_;
+    fa.d = d;
+    fa.ffn = m_.d_ffn;
+    fa.k = k;
+    fa.N = N;
+    fa.perm = perm_d_ + static_cast<size_t>(l) * T_ * k;
+    fa.offsets = offsets_d_ + static_cast<size_t>(l) * (N + 1);
+    fa.gates = gates_d_ + static_cast<size_t>(l) * T_ * k;
+    fa.hit_list = hit_list_d_ + static_cast<size_t>(l) * N;
+    fa.counters = counters_d + static_cast<size_t>(l) * 8;
+    fa.slot_of = slots_d + static_cast<size_t>(l) * N;
+    fa.pool = pool_ + static_cast<int64_t>(l) * slots_ * image_elems_;
+    fa.shared_w = shared_ + static_cast<int64_t>(l) * m_.n_shared_units * image_elems_;
+    // expert-parallel: shared units are computed once, on rank 0
+    const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
+    fa.n_shared = n_shared_eff;
+    fa.expert_elems = image_elems_;
+    fa.partial = work_d_;
+    fa.n_stages = stages_;
+    if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
+    check(launch_expert_ffn(fa, sms_, ffn_smem_, compute_), "K3 expert FFN");
+    if (timing_) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
+    dev::CombineArgs ca{};
+    ca.h_in = hl;
+    ca.y_extra = nullptr;
+    ca.T = T_;
+    ca.d = d;
+    ca.ffn = m_.d_ffn;
+    ca.k = k;
+    ca.ids = ids_d_ + static_cast<size_t>(l) * T_ * k;
+    ca.hit_ord = hit_ord_d_ + static_cast<size_t>(l) * N;
+    ca.counters = fa.counters;
+    ca.n_shared = n_shared_eff;
+    ca.grid = sms_;
+    ca.partial = work_d_;
+    float* yl = y_d_ + static_cast<size_t>(l) * T_ * d;
+    ca.y_out = yl;
+    ca.h_out = world_ > 1 ? nullptr : hn;
+    check(launch_combine(ca, compute_), "combine");
+    if (world_ > 1) {
+      const int r = nccl_->all_reduce(yl, yl, static_cast<size_t>(T_) * d, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm_,
+                                      compute_);
+      if (r != 0) throw NcclError("ncclAllReduce failed");
+      check(launch_residual(hl, yl, hn, T_ * d, compute_), "residual");
+    }
+  }
+  if (timing_) check(cudaEventRecord(ev_[4], compute_), "event");
+  check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
+  const uint16_t* hfin = h_d_ + static_cast<size_t>(L) * T_ * d;
+  if (h_out)
+    check(cudaMemcpyAsync(h_out, hfin, sizeof(uint16_t) * T_ * d,
+                          h_out_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, compute_),
+          "h_out");
+  if (timing_) check(cudaEventRecord(ev_[5], compute_), "event");
+  check(cudaStreamSynchronize(compute_), "sync compute");
+  check(cudaStreamSynchronize(copy_), "sync copy");
+
+  // ---- host: accounting with the K2 counters ----
+  std::memcpy(scores_.data(), out_h_, sizeof(int32_t) * L * N);
+  const auto* oc = reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N);
+  StepReport sr = sched_->observe(oc, accepted);
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->draft_ns = sr.draft_ns;
+    rep->cache_hits = sr.cache_hits;
+    rep->cache_misses = sr.cache_misses;
+    rep->faults_fn = sr.faults_fn;
+    rep->faults_fp = sr.faults_fp;
+    rep->step_wall_ns = sr.step_wall_ns;
+    rep->accuracy = sr.accuracy;
+    rep->accepted_tokens = sr.accepted_tokens;
+    rep->n_experts = N;
+    rep->n_layers = L;
+    rep->n_loads = n_loads;
+    if (timing_) {
+      auto ms = [](cudaEvent_t a, cudaEvent_t b) {
+        float v = 0.f;
+        cudaEventElapsedTime(&v, a, b);
+        return v;
+      };
+      rep->gpu_ms_total = ms(ev_[0], ev_[5]);
+      rep->gpu_ms_router = ms(ev_[1], ev_[2]);
+      rep->gpu_ms_hist = ms(ev_[2], ev_[3]);
+      float f = 0.f;
+      for (int l = 0; l < L; ++l) f += ms(ffn_beg_[static_cast<size_t>(l)], ffn_end_[static_cast<size_t>(l)]);
+      rep->gpu_ms_ffn = f;
+      rep->gpu_ms_combine = ms(ev_[3], ev_[4]) - f;
+    }
+  }
+  if (layers) {
+    for (int l = 0; l < L; ++l) {
+      const LayerTiming& lt = sr.layers[static_cast<size_t>(l)];
+      moespac_layer_timing& o = layers[l];
+      o.t_cpu_ns = lt.t_cpu_ns;
+      o.t_gpu_ns = lt.t_gpu_ns;
+      o.t_io_used_ns = lt.t_io_used_ns;
+      o.stall_ns = lt.stall_ns;
+      o.bubble_ns = lt.bubble_ns;
+      o.wall_ns = lt.wall_ns;
+      o.tau = lt.tau;
+      o.fallback = lt.fallback;
+      o.n_prefetch = lt.n_prefetch;
+      o.n_loads = 0;
+      for (const SlotLoad& ld : sched_->loads())
+        if (ld.layer == l) ++o.n_loads;
+    }
+  }
+}
+
+void Engine::views(moespac_ctx_views* v) const {
+  const int L = m_.n_layers, N = m_.n_experts;
+  v->ids_dev = ids_d_;
+  v->gates_dev = gates_d_;
+  v->freqs_dev = freqs_d_;
+  v->offsets_dev = offsets_d_;
+  v->perm_dev = perm_d_;
+  v->counters_dev = out_d_ + static_cast<size_t>(L) * N;
+  v->est_state_dev = est_d_;
+  v->h_dev = h_d_;
+  v->y_dev = y_d_;
+  v->pool_dev = pool_;
+  v->slots_per_layer = slots_;
+  v->image_elems = image_elems_;
+}
+
+}  // namespace moespac

@@ -1,0 +1,87 @@
+// Device engine: one verification step of the MoE-SpAc hot path on one B200.
+// See include/moespac/moespac.h (moespac_ctx_*) for the contract and
+// DESIGN.md for the HBM layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <vector>
+
+#include "../../../include/moespac/moespac.h"
+#include "step_scheduler.hpp"
+
+namespace moespac {
+
+struct NcclApi;  // dlopen'ed libnccl (no link-time dependency)
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+moespac_status nccl_unique_id(void* out128);
+
+class Engine {
+ public:
+  Engine(int device, const moespac_model_desc& m, const moespac_sched_config& cfg, int rank, int world);
+  ~Engine();
+
+  uint16_t* host_arena(int64_t n_images);
+  void fill_synthetic(uint64_t seed, float stdv);
+  void set_shared(int layer, const uint16_t* units_dev);
+  void finalize();
+  void set_nccl(const void* uid, int nranks, int rank);
+  void set_timing(bool on) { timing_ = on; }
+  void step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
+            uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
+  void views(moespac_ctx_views* v) const;
+  const StepScheduler& sched() const { return *sched_; }
+
+ private:
+  void check(cudaError_t e, const char* what) const;
+  int64_t image_of(int layer, int expert) const {
+    return (static_cast<int64_t>(layer) * m_.n_experts + expert) % n_images_;
+  }
+  uint16_t* slot_ptr(int layer, int slot) const {
+    return pool_ + (static_cast<int64_t>(layer) * slots_ + slot) * image_elems_;
+  }
+
+  int device_ = 0, rank_ = 0, world_ = 1, sms_ = 148, T_ = 0, W_ = 1, stages_ = 6;
+  size_t ffn_smem_ = 0;
+  moespac_model_desc m_{};
+  std::unique_ptr<StepScheduler> sched_;
+  int64_t image_elems_ = 0, slots_ = 0, n_images_ = 0;
+  bool synthetic_ = false, finalized_ = false, timing_ = false;
+  uint64_t synth_seed_ = 0;
+  float synth_std_ = 0.02f;
+
+  // HBM
+  uint16_t* pool_ = nullptr;    // [L][slots][image]
+  uint16_t* shared_ = nullptr;  // [L][n_shared][image]
+  double* logits_d_ = nullptr;
+  int32_t *ids_d_ = nullptr, *freqs_d_ = nullptr, *offsets_d_ = nullptr, *perm_d_ = nullptr;
+  int32_t *hit_list_d_ = nullptr, *hit_ord_d_ = nullptr, *est_d_ = nullptr;
+  float *gates_d_ = nullptr, *y_d_ = nullptr, *work_d_ = nullptr;
+  uint16_t* h_d_ = nullptr;     // [L+1][T][d]
+  uint8_t* tables_d_ = nullptr; // resident bits | loaded bits | taus | slot table
+  int32_t* out_d_ = nullptr;    // scores_out [L][N] | counters [L][8]
+  size_t tables_bytes_ = 0, out_bytes_ = 0, work_bytes_ = 0;
+  // host
+  uint16_t* arena_h_ = nullptr;
+  uint8_t* tables_h_ = nullptr;
+  int32_t* out_h_ = nullptr;
+  std::vector<int32_t> scores_;  // [L][N] snapshot for the next decide()
+
+  cudaStream_t compute_ = nullptr, copy_ = nullptr;
+  std::vector<cudaEvent_t> load_done_, ffn_beg_, ffn_end_;
+  cudaEvent_t ev_[6] = {};
+  std::unique_ptr<NcclApi> nccl_;
+  void* comm_ = nullptr;
+};
+
+}  // namespace moespac

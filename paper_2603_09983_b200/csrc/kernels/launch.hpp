@@ -1,0 +1,78 @@
+// Kernel argument blocks and host-side launcher declarations.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace moespac {
+namespace dev {
+
+struct K2Args {
+  const int32_t* ids;            // [L][T][k]
+  int L, T, k, N;
+  const uint32_t* resident_bits;  // [L][W] after this step's loads
+  const uint32_t* loaded_bits;    // [L][W] loaded this step (may be null)
+  const int32_t* taus;            // [L]
+  int32_t* est_state;             // [L][N][4] score, up, down, last_freq (in/out)
+  int utility_cap, adaptive;
+  double forgetting;
+  int shard_rank, shard_world;
+  int32_t* freqs;      // [L][N]
+  int32_t* offsets;    // [L][N+1]
+  int32_t* perm;       // [L][T*k]
+  int32_t* hit_list;   // [L][N] local-shard resident activated experts, ascending
+  int32_t* hit_ord;    // [L][N] ordinal in hit_list or -1
+  int32_t* counters;   // [L][8] distinct, hits, hit_tok, miss_tok, agree, fn, fp, n_local_hits
+  int32_t* scores_out; // [L][N] post-update scores (next step's snapshot)
+};
+
+struct FfnArgs {
+  const uint16_t* h;        // [T][d] bf16 layer input
+  int T, d, ffn, k, N;
+  const int32_t* perm;      // [T*k]
+  const int32_t* offsets;   // [N+1]
+  const float* gates;       // [T][k]
+  const int32_t* hit_list;  // [N]
+  const int32_t* counters;  // [8], counters[7] = number of local hits
+  const int32_t* slot_of;   // [N] slot of each expert in `pool` (-1 if absent)
+  const uint16_t* pool;     // tiled expert images, stride expert_elems
+  const uint16_t* shared_w; // tiled shared-expert units, stride expert_elems
+  int n_shared;
+  long long expert_elems;   // 3*ffn*d
+  float* partial;           // [(grid + N + n_shared)][T][d]
+  int n_stages;
+};
+
+struct CombineArgs {
+  const uint16_t* h_in;     // [T][d] bf16 (residual; may be null)
+  const float* y_extra;     // [T][d] fp32 added before rounding (cold path / remote); may be null
+  int T, d, ffn, k;
+  const int32_t* ids;       // [T][k]
+  const int32_t* hit_ord;   // [N]
+  const int32_t* counters;  // counters[7] = local hits
+  int n_shared;
+  int grid;                 // K3 grid size
+  const float* partial;
+  float* y_out;             // [T][d] fp32 (may be null)
+  uint16_t* h_out;          // [T][d] bf16 (may be null)
+};
+
+}  // namespace dev
+
+cudaError_t launch_router_topk(const double* logits, int rows, int N, int k, int gate_mode, int32_t* ids,
+                               float* gates, cudaStream_t stream);
+cudaError_t launch_hist_scan_observe(const dev::K2Args& a, cudaStream_t stream);
+cudaError_t launch_estimator_init(int32_t* st, int n, int up, int down, cudaStream_t stream);
+size_t ffn_smem_bytes(int T, int d, int n_stages);
+int ffn_pick_stages(int T, int d, size_t smem_limit);
+cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream);
+cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream);
+cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, int n, cudaStream_t stream);
+cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
+                               uint16_t* out, cudaStream_t stream);
+cudaError_t launch_fill_synthetic(uint16_t* out, long long n, uint64_t seed, float stdv, cudaStream_t stream);
+
+constexpr int kFfnMaxTokens = 16;
+constexpr int kFfnChunkRows = 16;
+
+}  // namespace moespac
