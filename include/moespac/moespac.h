@@ -86,6 +86,10 @@ typedef struct moespac_step_report {
   int32_t accepted_tokens, n_experts, n_layers, n_loads;
   /* measured on the device for this step (0 when timing is off) */
   float gpu_ms_total, gpu_ms_router, gpu_ms_hist, gpu_ms_ffn, gpu_ms_combine, gpu_ms_h2d_loads;
+  /* algorithmic K3 bytes this step on this rank: (local hit experts + shared
+   * units) x image bytes, summed over layers; and the kernel launches issued */
+  int64_t ffn_bytes, h2d_bytes, d2h_bytes;
+  int32_t kernel_launches, _pad;
 } moespac_step_report;
 
 /* Realized split of one layer (core/src/sim_core.cpp:233-283), as K2 emits it. */
@@ -137,6 +141,16 @@ moespac_status moespac_update_ratio_estimates(double* cpu_ratio, double* gpu_rat
                                               double observed_rc, double observed_rg, double smoothing);
 /* layer_capacity_experts (core/src/sim_core.cpp:31-34). */
 int moespac_layer_capacity_experts(double cache_ratio, int n_experts);
+
+/* ------------------------------------------------------------------ synthetic workload
+ * The host half of TraceGenerator::next_step (core/src/trace_model.cpp:73-109):
+ * the latent random walk and per-token Gumbel noise from the same
+ * mt19937_64 stream, emitted as noisy fp64 logits [L][gamma+1][N] for K1 (the
+ * top-k selection itself runs on the device). Uses the trace fields of cfg. */
+typedef struct moespac_trace_synth moespac_trace_synth;
+moespac_status moespac_trace_synth_create(const moespac_sched_config* cfg, moespac_trace_synth** out);
+moespac_status moespac_trace_synth_next(moespac_trace_synth* s, double* logits_host, int32_t* accepted);
+void moespac_trace_synth_destroy(moespac_trace_synth* s);
 
 /* ------------------------------------------------------------------ device kernels (stateless)
  * K1 — router top-k + gates. Replaces the selection block of
@@ -248,6 +262,9 @@ moespac_status moespac_ctx_finalize(moespac_ctx* c);
 moespac_status moespac_nccl_unique_id(void* out128);
 moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* unique_id128, int nranks, int rank);
 moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
+/* The context's compute stream (cudaStream_t as void*) — every kernel of a
+ * step runs on it, so events recorded there bracket whole steps. */
+void* moespac_ctx_stream(const moespac_ctx* c);
 
 /* One verification step end to end with HOST buffers: H2D logits [L][T][N]
  * fp64 and h_in [T][d] bf16, run, D2H h_out [T][d] bf16 + the step's

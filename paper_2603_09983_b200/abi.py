@@ -57,7 +57,9 @@ class StepReport(C.Structure):
                 ("accuracy", C.c_double), ("accepted_tokens", C.c_int32), ("n_experts", C.c_int32),
                 ("n_layers", C.c_int32), ("n_loads", C.c_int32),
                 ("gpu_ms_total", C.c_float), ("gpu_ms_router", C.c_float), ("gpu_ms_hist", C.c_float),
-                ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float)]
+                ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float),
+                ("ffn_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("kernel_launches", C.c_int32), ("_pad", C.c_int32)]
 
 
 class LayerOutcome(C.Structure):
@@ -163,6 +165,10 @@ def lib() -> C.CDLL:
         "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_ctx_get_views": (C.c_int, [vp, C.POINTER(CtxViews)]),
         "moespac_ctx_sched": (vp, [vp]),
+        "moespac_ctx_stream": (vp, [vp]),
+        "moespac_trace_synth_create": (C.c_int, [C.POINTER(SchedConfig), C.POINTER(vp)]),
+        "moespac_trace_synth_next": (C.c_int, [vp, vp, vp]),
+        "moespac_trace_synth_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -293,6 +299,30 @@ def solve_threshold(scores, resident, gamma, top_k, b_est, rc, rg, t_cpu, t_gpu,
     return out
 
 
+class TraceSynth:
+    """Host half of TraceGenerator::next_step: noisy fp64 logits for K1."""
+
+    def __init__(self, cfg: SchedConfig):
+        self.L, self.N, self.T = cfg.n_layers, cfg.n_experts, cfg.gamma + 1
+        h = C.c_void_p()
+        check(lib().moespac_trace_synth_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    def next(self, out: np.ndarray | None = None):
+        if out is None:
+            out = np.empty((self.L, self.T, self.N), np.float64)
+        acc = C.c_int32()
+        check(lib().moespac_trace_synth_next(self._h, out.ctypes.data, C.byref(acc)))
+        return out, acc.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().moespac_trace_synth_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
 # ---------------------------------------------------------------- device kernels
 def _stream(stream):
     if stream is None:
@@ -381,6 +411,9 @@ class Context:
                                         C.byref(rep), lay))
         return rep, list(lay)
 
+    def stream(self) -> int:
+        return lib().moespac_ctx_stream(self._h) or 0
+
     def views(self) -> CtxViews:
         v = CtxViews()
         check(lib().moespac_ctx_get_views(self._h, C.byref(v)))
@@ -393,11 +426,55 @@ class Context:
         lib().moespac_sched_events(s, out.ctypes.data, n)
         return out[:n]
 
+    def sched_tables(self):
+        s = lib().moespac_ctx_sched(self._h)
+        L, N = self.model.n_layers, self.model.n_experts
+        W = (N + 31) // 32
+        taus = np.zeros(L, np.int32)
+        rb = np.zeros((L, W), np.uint32)
+        lb = np.zeros((L, W), np.uint32)
+        slots = np.zeros((L, N), np.int32)
+        check(lib().moespac_sched_tables(s, taus.ctypes.data, rb.ctypes.data, lb.ctypes.data, slots.ctypes.data))
+        return taus, rb, lb, slots
+
     def sched_decisions(self) -> np.ndarray:
         s = lib().moespac_ctx_sched(self._h)
         out = np.zeros((self.model.n_layers, 5), np.int64)
         check(lib().moespac_sched_decisions(s, out.ctypes.data))
         return out
+
+
+_cudart_lib = None
+
+
+def _cudart() -> C.CDLL:
+    """The process's CUDA runtime (already loaded by torch) — used only to
+    read device views back for checks."""
+    global _cudart_lib
+    if _cudart_lib is None:
+        import torch  # noqa: F401  (ensures libcudart is loaded)
+        for name in ("libcudart.so.12", "libcudart.so"):
+            try:
+                _cudart_lib = C.CDLL(name)
+                break
+            except OSError:
+                continue
+        if _cudart_lib is None:
+            raise ImportError("libcudart not loadable")
+        _cudart_lib.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+        _cudart_lib.cudaDeviceSynchronize.argtypes = []
+    return _cudart_lib
+
+
+def fetch(dev_ptr: int, shape, dtype) -> np.ndarray:
+    """Copy a device buffer into a new numpy array (synchronous)."""
+    out = np.empty(shape, dtype)
+    rt = _cudart()
+    rt.cudaDeviceSynchronize()
+    rc = rt.cudaMemcpy(out.ctypes.data, dev_ptr, out.nbytes, 2)  # cudaMemcpyDeviceToHost
+    if rc != 0:
+        raise RuntimeError(f"cudaMemcpy D2H failed ({rc})")
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -30,11 +30,12 @@ SOURCES = [
     "host/scheduler.cpp",
     "host/step_scheduler.cpp",
     "host/engine.cpp",
+    "host/trace_synth.cpp",
     "abi.cpp",
 ]
 HEADERS = [
     "kernels/common.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
-    "host/engine.hpp",
+    "host/engine.hpp", "host/trace_synth.hpp",
 ]
 
 
@@ -61,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(OBJ_DIR, src.replace("/", "_") + ".o")
         objs.append(obj)
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(sp), hdr_time):
-            flags = COMMON + (CU_FLAGS if src.endswith(".cu") else ["-x", "c++"])
+            flags = COMMON + (CU_FLAGS if src.endswith(".cu") else ["-x", "c++", "-Wno-deprecated-gpu-targets"])
             jobs.append(([nvcc] + flags + ["-c", sp, "-o", obj], src))
 
     def run(job):

@@ -9,6 +9,7 @@
 #include "../../include/moespac/moespac.h"
 #include "host/engine.hpp"
 #include "host/step_scheduler.hpp"
+#include "host/trace_synth.hpp"
 #include "kernels/launch.hpp"
 
 using namespace moespac;
@@ -16,6 +17,10 @@ using namespace moespac;
 struct moespac_sched {
   StepScheduler s;
   explicit moespac_sched(const SchedConfig& c) : s(c) {}
+};
+struct moespac_trace_synth {
+  TraceSynth t;
+  explicit moespac_trace_synth(const TraceSynthConfig& c) : t(c) {}
 };
 struct moespac_ctx {
   Engine e;
@@ -326,6 +331,30 @@ int moespac_layer_capacity_experts(double cache_ratio, int n_experts) {
   return layer_capacity_experts(cache_ratio, n_experts);
 }
 
+// ------------------------------------------------------------ workload
+moespac_status moespac_trace_synth_create(const moespac_sched_config* cfg, moespac_trace_synth** out) {
+  return guard([&] {
+    if (!cfg || !out) throw std::invalid_argument("moespac_trace_synth_create: null argument");
+    TraceSynthConfig c;
+    c.n_layers = cfg->n_layers;
+    c.n_experts = cfg->n_experts;
+    c.top_k = cfg->top_k;
+    c.gamma = cfg->gamma;
+    c.alpha = cfg->alpha;
+    c.drift_scale = cfg->drift_scale;
+    c.route_noise = cfg->route_noise;
+    c.shift_period = cfg->shift_period;
+    c.seed = cfg->seed;
+    *out = new moespac_trace_synth(c);
+  });
+}
+
+moespac_status moespac_trace_synth_next(moespac_trace_synth* s, double* logits, int32_t* accepted) {
+  return guard([&] { *accepted = s->t.next(logits); });
+}
+
+void moespac_trace_synth_destroy(moespac_trace_synth* s) { delete s; }
+
 // ------------------------------------------------------------ kernels
 moespac_status moespac_router_topk(const double* logits, int rows, int n, int k, int gate_mode, int32_t* ids,
                                    float* gates, void* stream) {
@@ -403,8 +432,8 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     int dev = 0, optin = 0;
     cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
     cuda_ok(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
-    const int stages = ffn_pick_stages(a->tokens, a->d_model, static_cast<size_t>(optin));
-    if (!stages) throw std::invalid_argument("moespac_expert_ffn: tokens x d_model too large for shared memory");
+    const FfnPlan plan = ffn_plan(a->tokens, a->d_model, static_cast<size_t>(optin));
+    if (!plan.n_stages) throw std::invalid_argument("moespac_expert_ffn: tokens x d_model too large for shared memory");
     dev::FfnArgs f{};
     f.h = a->h_dev;
     f.T = a->tokens;
@@ -423,9 +452,10 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.n_shared = a->n_shared_units;
     f.expert_elems = 3LL * a->d_model * a->d_ffn;
     f.partial = a->workspace_dev;
-    f.n_stages = stages;
+    f.n_stages = plan.n_stages;
+    f.global_acc = plan.global_acc ? 1 : 0;
     const int grid = a->grid > 0 ? a->grid : device_sms();
-    cuda_ok(launch_expert_ffn(f, grid, ffn_smem_bytes(a->tokens, a->d_model, stages), static_cast<cudaStream_t>(stream)),
+    cuda_ok(launch_expert_ffn(f, grid, plan.smem, static_cast<cudaStream_t>(stream)),
             "expert_ffn");
   });
 }
@@ -510,6 +540,8 @@ moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* uid, int nranks,
 moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_timing(enabled != 0); });
 }
+
+void* moespac_ctx_stream(const moespac_ctx* c) { return c->e.stream(); }
 
 moespac_status moespac_step(moespac_ctx* c, const double* logits, const uint16_t* h_in, int accepted, uint16_t* h_out,
                             moespac_step_report* rep, moespac_layer_timing* layers) {

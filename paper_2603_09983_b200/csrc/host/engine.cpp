@@ -114,9 +114,11 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   if (prop.major != 10) throw CudaError("moespac requires an sm_100 (B200) device");
   sms_ = prop.multiProcessorCount;
-  stages_ = ffn_pick_stages(T_, m.d_model, prop.sharedMemPerBlockOptin);
-  if (stages_ == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
-  ffn_smem_ = ffn_smem_bytes(T_, m.d_model, stages_);
+  const FfnPlan plan = ffn_plan(T_, m.d_model, prop.sharedMemPerBlockOptin);
+  if (plan.n_stages == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
+  stages_ = plan.n_stages;
+  global_acc_ = plan.global_acc;
+  ffn_smem_ = plan.smem;
 
   const int L = m.n_layers, N = m.n_experts, k = m.top_k, d = m.d_model;
   auto dmalloc = [&](void** p, size_t bytes, const char* what) {
@@ -388,6 +390,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.expert_elems = image_elems_;
     fa.partial = work_d_;
     fa.n_stages = stages_;
+    fa.global_acc = global_acc_ ? 1 : 0;
     if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
     check(launch_expert_ffn(fa, sms_, ffn_smem_, compute_), "K3 expert FFN");
     if (timing_) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
@@ -443,6 +446,15 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     rep->n_experts = N;
     rep->n_layers = L;
     rep->n_loads = n_loads;
+    const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
+    int64_t units = 0;
+    for (int l = 0; l < L; ++l) units += oc[l].n_local_hits + n_shared_eff;
+    rep->ffn_bytes = units * image_elems_ * 2;
+    rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads) * image_elems_ * 2 +
+                     (logits_host ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
+                     (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
+    rep->d2h_bytes = static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
+    rep->kernel_launches = 2 + 2 * L + (world_ > 1 ? L : 0);
     if (timing_) {
       auto ms = [](cudaEvent_t a, cudaEvent_t b) {
         float v = 0.f;

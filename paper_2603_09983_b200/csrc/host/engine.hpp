@@ -41,6 +41,7 @@ class Engine {
             uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
   void views(moespac_ctx_views* v) const;
   const StepScheduler& sched() const { return *sched_; }
+  void* stream() const { return compute_; }
 
  private:
   void check(cudaError_t e, const char* what) const;
@@ -56,7 +57,7 @@ class Engine {
   moespac_model_desc m_{};
   std::unique_ptr<StepScheduler> sched_;
   int64_t image_elems_ = 0, slots_ = 0, n_images_ = 0;
-  bool synthetic_ = false, finalized_ = false, timing_ = false;
+  bool synthetic_ = false, finalized_ = false, timing_ = false, global_acc_ = false;
   uint64_t synth_seed_ = 0;
   float synth_std_ = 0.02f;
 

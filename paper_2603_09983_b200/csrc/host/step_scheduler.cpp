@@ -219,6 +219,7 @@ LayerOutcome StepScheduler::split_on_host(int l, const std::int32_t* freqs) cons
 }
 
 StepReport StepScheduler::observe_freqs(const std::int32_t* freqs, int accepted_count) {
+  if (!decided_) throw std::logic_error("StepScheduler: observe() without decide()");
   std::vector<LayerOutcome> out(static_cast<std::size_t>(cfg_.n_layers));
   for (int l = 0; l < cfg_.n_layers; ++l)
     out[static_cast<std::size_t>(l)] = split_on_host(l, freqs + static_cast<std::size_t>(l) * cfg_.n_experts);

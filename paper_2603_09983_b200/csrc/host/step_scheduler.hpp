@@ -75,7 +75,7 @@ std::int64_t recompute_total_time(const std::vector<SimEvent>& log);
 // device or by split_on_host() in host-only mode.
 struct LayerOutcome {
   std::int32_t distinct = 0, distinct_hits = 0, hit_tokens = 0, miss_tokens = 0;
-  std::int32_t agree = 0, faults_fn = 0, faults_fp = 0, reserved = 0;
+  std::int32_t agree = 0, faults_fn = 0, faults_fp = 0, n_local_hits = 0;
 };
 
 struct SlotLoad {

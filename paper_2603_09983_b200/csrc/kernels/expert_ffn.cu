@@ -49,13 +49,17 @@ constexpr int FC = 16;    // ffn rows per chunk
 constexpr int MAX_T = 16;
 
 
+// NT bucket used by dispatch_chunk (padding rows need ysum storage).
+__host__ __device__ __forceinline__ int token_bucket(int t) { return t <= 9 ? t : (t <= 12 ? 12 : 16); }
+
 struct Geo {
-  int d, cpe, gu_tiles, dn_tiles, DW, DR, nsub, rows_per_tile_group;
+  int d, cpe, gu_tiles, dn_tiles, DW, DR, nsub, rows_per_tile_group, tp;
   long long chunk_elems;
 };
 
-__device__ __forceinline__ Geo make_geo(int d, int ffn) {
+__device__ __forceinline__ Geo make_geo(int d, int ffn, int T) {
   Geo g;
+  g.tp = token_bucket(T);
   g.d = d;
   g.cpe = ffn / FC;
   g.gu_tiles = d / 256;
@@ -97,7 +101,8 @@ struct Smem {
   uint64_t* full;
   uint64_t* empty;
   uint16_t* h;     // [T][d]
-  float* ysum;     // [nsub][T][d]
+  float* ysum;     // [nsub][TP][d], TP = token_bucket(T); unused in global mode
+  float* yglob;    // global-accumulation mode: this CTA's partial block for the current entry
   float* a;        // [MAX_T][FC]
   int* tok;        // [MAX_T]
   float* gate;     // [MAX_T]
@@ -171,7 +176,11 @@ __device__ __forceinline__ void chunk_compute(const Geo& g, const Smem& s, Pipe&
   // ---------------- down ----------------
   const int cg = tid % (g.DW / 4);
   const int rsub = tid / (g.DW / 4);
-  float* ys = s.ysum + static_cast<size_t>(rsub) * MAX_T * g.d;
+  float* yrow[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+    yrow[t] = s.yglob ? s.yglob + static_cast<size_t>(s.tok[t]) * g.d
+                      : s.ysum + (static_cast<size_t>(rsub) * g.tp + t) * g.d;
   for (int ct2 = 0; ct2 < g.d / g.DW; ++ct2) {
     float acc2[NT][4];
 #pragma unroll
@@ -204,7 +213,7 @@ __device__ __forceinline__ void chunk_compute(const Geo& g, const Smem& s, Pipe&
     const int col = ct2 * g.DW + cg * 4;
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      float4* dst = reinterpret_cast<float4*>(ys + static_cast<size_t>(t) * g.d + col);
+      float4* dst = reinterpret_cast<float4*>(yrow[t] + col);
       float4 v = *dst;
       v.x += acc2[t][0];
       v.y += acc2[t][1];
@@ -242,9 +251,11 @@ __device__ __forceinline__ const uint16_t* entry_weights(const FfnArgs& a, int o
 
 __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const Geo g = make_geo(a.d, a.ffn);
+  const Geo g = make_geo(a.d, a.ffn, a.T);
   const int ns = a.n_stages;
+  const bool global_acc = a.global_acc != 0;
   Smem s;
+  s.yglob = nullptr;
   uint8_t* ptr = smem_raw;
   s.ring = ptr;
   ptr += static_cast<size_t>(ns) * TILE_BYTES;
@@ -253,7 +264,7 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
   s.empty = reinterpret_cast<uint64_t*>(ptr);
   ptr += 8 * ns;
   s.ysum = reinterpret_cast<float*>(ptr);
-  ptr += static_cast<size_t>(g.nsub) * MAX_T * a.d * 4;
+  if (!global_acc) ptr += static_cast<size_t>(g.nsub) * g.tp * a.d * 4;
   s.a = reinterpret_cast<float*>(ptr);
   ptr += MAX_T * FC * 4;
   s.gate = reinterpret_cast<float*>(ptr);
@@ -287,7 +298,7 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
     const int n4 = a.T * a.d / 8;
     for (int i = tid; i < n4; i += FFN_THREADS) dst[i] = src[i];
     float4* ys = reinterpret_cast<float4*>(s.ysum);
-    const int ny = g.nsub * MAX_T * a.d / 4;
+    const int ny = global_acc ? 0 : g.nsub * g.tp * a.d / 4;
     for (int i = tid; i < ny; i += FFN_THREADS) ys[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncthreads();
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
   int cur = -1;
   auto flush = [&](int o) {
     named_bar_sync(1, FFN_CONSUMERS);
+    if (global_acc) return;  // already accumulated in place
     const int nt = *s.ntok;
     float* P = a.partial + static_cast<long long>(b + o) * a.T * a.d;
     for (int t = 0; t < nt; ++t) {
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
         float4 v = *reinterpret_cast<float4*>(s.ysum + static_cast<size_t>(t) * a.d + c);
         *reinterpret_cast<float4*>(s.ysum + static_cast<size_t>(t) * a.d + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int r = 1; r < g.nsub; ++r) {
-          float* y2 = s.ysum + (static_cast<size_t>(r) * MAX_T + t) * a.d + c;
+          float* y2 = s.ysum + (static_cast<size_t>(r) * g.tp + t) * a.d + c;
           const float4 u = *reinterpret_cast<float4*>(y2);
           *reinterpret_cast<float4*>(y2) = make_float4(0.f, 0.f, 0.f, 0.f);
           v.x += u.x;
@@ -371,6 +383,16 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
         if (tid == 0) *s.ntok = nt;
       }
       named_bar_sync(1, FFN_CONSUMERS);
+      if (global_acc) {
+        // zero this entry's rows of the CTA-exclusive partial block
+        s.yglob = a.partial + static_cast<long long>(b + o) * a.T * a.d;
+        const int nt = *s.ntok;
+        for (int t = 0; t < nt; ++t)
+          for (int c = tid * 4; c < a.d; c += FFN_CONSUMERS * 4)
+            *reinterpret_cast<float4*>(s.yglob + static_cast<size_t>(s.tok[t]) * a.d + c) =
+                make_float4(0.f, 0.f, 0.f, 0.f);
+        named_bar_sync(1, FFN_CONSUMERS);
+      }
       cur = o;
     }
     dispatch_chunk(*s.ntok, g, s, p, ns, warp, lane, tid);
@@ -392,6 +414,8 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
     const long long lo = owner_of(static_cast<long long>(o) * cpe, n, a.grid);
     const long long hi = owner_of(static_cast<long long>(o + 1) * cpe - 1, n, a.grid);
     for (long long b = lo; b <= hi; ++b) {
+      // with fewer chunks than CTAs some CTAs own nothing and wrote no block
+      if ((b * n) / a.grid == ((b + 1) * n) / a.grid) continue;
       const float4 v =
           *reinterpret_cast<const float4*>(a.partial + ((b + o) * a.T + t) * static_cast<long long>(a.d) + c);
       acc.x += v.x;
@@ -499,18 +523,26 @@ __global__ void fill_synthetic_kernel(uint16_t* out, long long n, uint64_t seed,
 }  // namespace dev
 
 // ---------------------------------------------------------------- launchers
-size_t ffn_smem_bytes(int T, int d, int n_stages) {
+size_t ffn_smem_bytes(int T, int d, int n_stages, bool global_acc) {
   const int DW = d < 1024 ? d : 1024;
   const int nsub = dev::FFN_CONSUMERS / (DW / 4);
   return static_cast<size_t>(n_stages) * dev::TILE_BYTES + 16ull * n_stages +
-         static_cast<size_t>(nsub) * dev::MAX_T * d * 4 + dev::MAX_T * dev::FC * 4 + dev::MAX_T * 8 + 16 +
+         (global_acc ? 0 : static_cast<size_t>(nsub) * dev::token_bucket(T) * d * 4) + dev::MAX_T * dev::FC * 4 + dev::MAX_T * 8 + 16 +
          static_cast<size_t>(T) * d * 2;
 }
 
-int ffn_pick_stages(int T, int d, size_t smem_limit) {
-  for (int ns = 6; ns >= 2; --ns)
-    if (ffn_smem_bytes(T, d, ns) <= smem_limit) return ns;
-  return 0;
+FfnPlan ffn_plan(int T, int d, size_t smem_limit) {
+  // Prefer the shared-memory accumulator with a >= 4-deep ring; otherwise
+  // accumulate in the CTA's exclusive partial block (L2-resident) and keep
+  // the deep ring. Global mode needs one accumulator copy (d >= 1024).
+  for (int ns = 6; ns >= 4; --ns)
+    if (ffn_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_smem_bytes(T, d, ns, false)};
+  if (d >= 1024)
+    for (int ns = 6; ns >= 2; --ns)
+      if (ffn_smem_bytes(T, d, ns, true) <= smem_limit) return {ns, true, ffn_smem_bytes(T, d, ns, true)};
+  for (int ns = 3; ns >= 2; --ns)
+    if (ffn_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_smem_bytes(T, d, ns, false)};
+  return {0, false, 0};
 }
 
 cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream) {

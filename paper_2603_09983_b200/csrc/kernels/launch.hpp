@@ -41,6 +41,7 @@ struct FfnArgs {
   long long expert_elems;   // 3*ffn*d
   float* partial;           // [(grid + N + n_shared)][T][d]
   int n_stages;
+  int global_acc;           // 1: accumulate down-proj partials in `partial` (large T*d)
 };
 
 struct CombineArgs {
@@ -63,8 +64,13 @@ cudaError_t launch_router_topk(const double* logits, int rows, int N, int k, int
                                float* gates, cudaStream_t stream);
 cudaError_t launch_hist_scan_observe(const dev::K2Args& a, cudaStream_t stream);
 cudaError_t launch_estimator_init(int32_t* st, int n, int up, int down, cudaStream_t stream);
-size_t ffn_smem_bytes(int T, int d, int n_stages);
-int ffn_pick_stages(int T, int d, size_t smem_limit);
+struct FfnPlan {
+  int n_stages;
+  bool global_acc;
+  size_t smem;
+};
+size_t ffn_smem_bytes(int T, int d, int n_stages, bool global_acc);
+FfnPlan ffn_plan(int T, int d, size_t smem_limit);
 cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream);
 cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream);
 cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, int n, cudaStream_t stream);

@@ -1,0 +1,160 @@
+"""End-to-end verification step on the GPU through the C ABI (moespac_step).
+
+Checks, step after step with real expert loads (cache < 100%):
+  * the engine's scheduling record (SimEvent log: ordered evict/load ids,
+    taus, timings) equals the compiled reference Simulation on the same trace;
+  * K1 ids equal the reference trace; K2 counters equal the reference split;
+  * every layer's fp32 MoE output matches the fp64 oracle over exactly the
+    experts resident after this step's loads (rel-L2 <= 1e-5), and the bf16
+    residual chain h_{l+1} = bf16(h_l + y_l) is within 1 bf16 ulp;
+  * host-buffer (moespac_step) and device-buffer (moespac_step_device) paths
+    are bitwise identical.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import ref_or_skip
+from paper_2603_09983_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _experts(rng, L, N, d, ffn, units):
+    std = {}
+    for l in range(L):
+        for e in range(N):
+            std[(l, e)] = tuple(O.f32_to_bf16_bits(rng.normal(0, 0.03, s).astype(np.float32))
+                                for s in ((ffn, d), (ffn, d), (d, ffn)))
+    shared = {l: [tuple(O.f32_to_bf16_bits(rng.normal(0, 0.03, s).astype(np.float32))
+                        for s in ((ffn, d), (ffn, d), (d, ffn))) for _ in range(units)] for l in range(L)}
+    return std, shared
+
+
+def _pack(w):
+    return abi.pack_expert(*[torch.from_numpy(x.view(np.int16)).cuda() for x in w])
+
+
+def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared):
+    cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache)
+    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, gate_mode), cfg)
+    arena = ctx.host_arena(L * N)
+    for (l, e), w in std.items():
+        arena[l * N + e] = _pack(w).cpu().numpy().view(np.uint16)
+    for l in range(L):
+        if units:
+            ctx.set_shared(l, torch.stack([_pack(w) for w in shared[l]]))
+    ctx.finalize()
+    return ctx, cfg
+
+
+def _resident(rb, l, N):
+    return [e for e in range(N) if (int(rb[l, e >> 5]) >> (e & 31)) & 1]
+
+
+@pytest.mark.parametrize("L,N,k,g,d,ffn,units,gate_mode,cache", [
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25),
+    (2, 8, 2, 4, 512, 128, 0, 0, 0.17),
+    (2, 32, 8, 8, 2048, 48, 0, 0, 0.5),
+])
+def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache):
+    ref_or_skip()
+    rng = np.random.default_rng(L * 100 + N)
+    std, shared = _experts(rng, L, N, d, ffn, units)
+    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared)
+    T = g + 1
+    steps = 10
+    gen = O.Generator(L, N, k, g, seed=1)
+    rcfg = O.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache, token_budget=0)
+    ids_ref, acc_ref = O.ref_trace(rcfg, steps)
+    run = O.ref_sim_run(rcfg, ids_ref, acc_ref)
+    total_loads = 0
+    for s in range(steps):
+        logits, ids, acc = gen.next_step()
+        assert np.array_equal(ids, ids_ref[s]) and acc == acc_ref[s]
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        h_out = np.zeros_like(h0)
+        rep, lay = ctx.step(logits, h0, acc, h_out)
+        total_loads += rep.n_loads
+        v = ctx.views()
+        got_ids = abi.fetch(v.ids_dev, (L, T, k), np.int32)
+        assert np.array_equal(got_ids, ids)
+        hs = abi.fetch(v.h_dev, (L + 1, T, d), np.uint16)
+        ys = abi.fetch(v.y_dev, (L, T, d), np.float32)
+        assert np.array_equal(hs[0], h0) and np.array_equal(hs[L], h_out)
+        _, rb, _, _ = ctx.sched_tables()
+        for l in range(L):
+            _, gates = O.router_topk(logits[l], k, gate_mode)
+            res = _resident(rb, l, N)
+            y_ref = O.moe_layer(hs[l], ids[l], gates, {e: std[(l, e)] for e in res}, shared[l])
+            rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
+            assert rel <= 1e-5, (s, l, rel)
+            exact = O.bf16_bits_to_f32(hs[l]).astype(np.float64) + y_ref
+            got = O.bf16_bits_to_f32(hs[l + 1]).astype(np.float64)
+            assert np.all(np.abs(got - exact) <= np.abs(exact) * 2.0 ** -8 + 1e-5 * np.abs(y_ref).max())
+            r = run.layer_rec[s, l]
+            assert [lay[l].tau, lay[l].fallback, lay[l].n_prefetch, lay[l].t_cpu_ns, lay[l].t_gpu_ns] == list(r[:5])
+        sr = run.step_rec[s]
+        assert [rep.cache_hits, rep.cache_misses, rep.faults_fn, rep.faults_fp] == list(sr[1:5])
+    assert np.array_equal(ctx.sched_events(), run.events)
+    if cache < 1.0:
+        assert total_loads > 0, "the test must exercise real expert loads"
+    ctx.close()
+
+
+def test_host_and_device_paths_bitwise_equal():
+    L, N, k, g, d, ffn = 2, 16, 4, 6, 1024, 64
+    rng = np.random.default_rng(5)
+    std, shared = _experts(rng, L, N, d, ffn, 1)
+    outs = []
+    for mode in ("host", "device"):
+        ctx, cfg = _make_ctx(L, N, k, g, d, ffn, 1, 0, 0.5, std, shared)
+        gen = O.Generator(L, N, k, g, seed=4)
+        hrng = np.random.default_rng(9)
+        res = []
+        for s in range(5):
+            logits, _, acc = gen.next_step()
+            h0 = O.f32_to_bf16_bits(hrng.normal(0, 1, (g + 1, d)).astype(np.float32))
+            if mode == "host":
+                h_out = np.zeros_like(h0)
+                ctx.step(logits, h0, acc, h_out)
+            else:
+                lg = torch.from_numpy(logits).cuda()
+                hd = torch.from_numpy(h0.view(np.int16)).cuda()
+                ho = torch.zeros_like(hd)
+                ctx.step_device(lg, hd, acc, ho)
+                torch.cuda.synchronize()
+                h_out = ho.cpu().numpy().view(np.uint16)
+            res.append(h_out)
+        outs.append(res)
+        ctx.close()
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_step_argument_errors():
+    L, N, k, g, d, ffn = 1, 8, 2, 4, 512, 32
+    cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=1.0)
+    with pytest.raises(abi.MoespacError) as ei:
+        abi.Context(0, abi.ModelDesc(L, N, k, g, 500, ffn, 0, 0), cfg)  # d % 512
+    assert ei.value.code == "E_INVALID"
+    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, 0, 0), cfg)
+    logits = np.zeros((L, g + 1, N))
+    h = np.zeros((g + 1, d), np.uint16)
+    with pytest.raises(abi.MoespacError) as ei:
+        ctx.step(logits, h, 1, h.copy())  # not finalized
+    assert ei.value.code == "E_LOGIC"
+    ctx.host_arena(N)
+    ctx.finalize()
+    with pytest.raises(abi.MoespacError) as ei:
+        ctx.step(logits, h, g + 2, h.copy())
+    assert ei.value.code == "E_RANGE"
+    ctx.close()

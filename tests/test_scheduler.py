@@ -1,0 +1,262 @@
+"""Decision parity of the product host scheduler (C++ via the C ABI) — CPU only.
+
+The two-phase StepScheduler (decide before routing is known, observe after)
+must reproduce the reference Simulation::run_utility_step
+(core/src/sim_core.cpp:157-316) record for record: every LayerTiming field,
+every StepReport field and the complete SimEvent log (ordered evict / load
+ids, timestamps), on the committed golden fixtures made by the reference.
+Also the reference's own balancer tests (workload_balancer_test.cpp) and the
+expert-parallel (sharded) bookkeeping invariants.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import ref_or_skip
+from paper_2603_09983_b200 import abi
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def replay(cfg, ids, accepted, shard_world=1, cap=None):
+    """Drive the product scheduler over a trace with oracle freqs/estimator."""
+    L, N, k, g = cfg.n_layers, cfg.n_experts, cfg.top_k, cfg.gamma
+    pol = abi.POLICIES[cfg.policy]
+    K = 1 if pol == "binary_utility" else (cap or cfg.utility_cap)
+    init_up, init_down = (cfg.fixed_up, cfg.fixed_down) if pol == "fixed_boundaries" else (-1, -1)
+    s = abi.Scheduler(cfg, shard_world)
+    est = [O.estimator_init(N, g, init_up, init_down) for _ in range(L)]
+    scores = np.zeros((L, N), np.int32)
+    recs, steps = [], []
+    for st in range(len(accepted)):
+        s.decide(scores)
+        freqs = np.stack([O.hist_scan(ids[st, l], N)[0] for l in range(L)])
+        rep, lay = s.observe_freqs(freqs, int(accepted[st]))
+        recs.append([[x.tau, x.fallback, x.n_prefetch, x.t_cpu_ns, x.t_gpu_ns, x.t_io_used_ns, x.stall_ns,
+                      x.wall_ns, x.bubble_ns] for x in lay])
+        steps.append(rep)
+        for l in range(L):
+            est[l] = O.estimator_observe(est[l], freqs[l], K, cfg.forgetting, pol != "fixed_boundaries")
+            scores[l] = est[l][:, 0]
+    return s, np.array(recs, np.int64), steps
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "sim_*.npz"))),
+                         ids=lambda p: os.path.basename(p)[4:-4])
+def test_scheduler_matches_reference_simulation(path):
+    z = np.load(path)
+    cfg = abi.default_config(n_layers=int(z["L"]), n_experts=int(z["N"]), top_k=int(z["k"]),
+                             gamma=int(z["gamma"]), cache_ratio=float(z["cache_ratio"]), policy=int(z["policy"]))
+    s, recs, steps = replay(cfg, z["ids"], z["accepted"])
+    assert np.array_equal(recs, z["layer_rec"][:, :, :9])
+    for i, rep in enumerate(steps):
+        sr = z["step_rec"][i]
+        assert [rep.accepted_tokens, rep.cache_hits, rep.cache_misses, rep.faults_fn, rep.faults_fp,
+                rep.step_wall_ns, rep.draft_ns] == list(sr[:7])
+        assert rep.accuracy == z["accuracy"][i]
+    assert np.array_equal(s.events(), z["events"])
+    assert s.total_time_ns() == int(z["total_time_ns"])
+
+
+def test_time_conservation_and_full_cache():
+    # sim_core_test.cpp:117-130 — a full cache never misses; clock == sum of walls
+    cfg = abi.default_config(n_layers=2, n_experts=32, cache_ratio=1.0)
+    gen = O.Generator(2, 32, 8, 8, seed=1)
+    trace = [gen.next_step() for _ in range(12)]
+    ids = np.stack([t[1] for t in trace])
+    acc = np.array([t[2] for t in trace])
+    s, recs, steps = replay(cfg, ids, acc)
+    assert all(r.cache_misses == 0 for r in steps)
+    assert sum(r.step_wall_ns for r in steps) == s.total_time_ns()
+    ev = s.events()
+    total = ev[ev[:, 0] == O.EV_DRAFT, 5].sum()
+    for st in range(len(steps)):
+        for l in range(2):
+            m = (ev[:, 1] == st) & (ev[:, 2] == l)
+            cpu = ev[m & (ev[:, 0] == O.EV_CPU), 5].sum()
+            gpu = ev[m & (ev[:, 0] == O.EV_GPU), 5].sum()
+            stall = ev[m & (ev[:, 0] == O.EV_STALL), 5].sum()
+            total += max(cpu, gpu) + stall
+    assert total == s.total_time_ns()
+
+
+def test_hand_checked_two_step_timeline():
+    # sim_core_test.cpp:65-115 (tiny_config + two_phase_trace)
+    cfg = abi.default_config(n_layers=1, n_experts=4, top_k=2, gamma=2, t_cpu_unit_ns=1000, t_gpu_unit_ns=100,
+                             t_io_unit_ns=500, t_draft_unit_ns=1000, expert_bytes=100, utility_cap=2,
+                             cache_ratio=0.5)
+    ids = np.array([[[[0, 1], [0, 1], [0, 1]]], [[[2, 3], [2, 3], [2, 3]]]], np.int32)
+    s, recs, steps = replay(cfg, ids, np.array([2, 3]), cap=2)
+    r1, r2 = steps
+    assert recs[0, 0, :3].tolist() == [1, 0, 0] and recs[0, 0, 3:5].tolist() == [0, 200]
+    assert r1.step_wall_ns == 2200 and r1.cache_hits == 6 and abs(r1.accuracy - 0.5) < 1e-12
+    assert r1.faults_fn == 2 and r1.faults_fp == 0
+    assert recs[1, 0, 3] == 6000 and r2.step_wall_ns == 8000 and r2.cache_misses == 6 and r2.accuracy == 0.0
+    assert s.total_time_ns() == 10200
+
+
+def _solver_rows():
+    z = np.load(os.path.join(GOLDEN, "solver.npz"))
+    ro = so = 0
+    for i in range(len(z["cap"])):
+        cap, n = int(z["cap"][i]), int(z["n"][i])
+        yield (z["scores"][so:so + n], z["res"][so:so + n], z["gkb"][i], z["rc"][ro:ro + cap],
+               z["rg"][ro:ro + cap], z["t"][i], z["out"][i])
+        ro += cap
+        so += n
+
+
+def test_solver_matches_reference_golden():
+    n = 0
+    for scores, res, (g, k, b), rc, rg, t, out in _solver_rows():
+        got = abi.solve_threshold(scores, res, int(g), int(k), int(b), rc, rg, *[int(x) for x in t])
+        assert np.array_equal(got, out)
+        n += 1
+    assert n == 1000
+
+
+def test_solver_brute_force_and_eval_budget():
+    # workload_balancer_test.cpp:166-231: objective == brute force; fallback iff infeasible
+    fb = feas = 0
+    for scores, res, (g, k, b), rc, rg, t, out in _solver_rows():
+        t_cpu, t_gpu, t_io, eb, vram, credit = [int(x) for x in t]
+        got = abi.solve_threshold(scores, res, int(g), int(k), int(b), rc, rg, t_cpu, t_gpu, t_io, eb, vram, credit)
+        best = None
+        for tau in range(1, len(rc) + 1):
+            cpu = int(np.round(rc[tau - 1] * g * k * t_cpu + 0.0)) if False else None  # placeholder (see below)
+        # recompute with the same llround semantics as the reference
+        objs = []
+        for tau in range(1, len(rc) + 1):
+            c = np.float64(rc[tau - 1]) * g * k * np.float64(t_cpu)
+            p = np.float64(rg[tau - 1]) * b * np.float64(t_gpu)
+            cpu = int(np.floor(abs(c) + 0.5)) * (1 if c >= 0 else -1)
+            gpu = int(np.floor(abs(p) + 0.5)) * (1 if p >= 0 else -1)
+            n = int(np.sum((scores >= tau) & (res == 0)))
+            ok = t_io * n <= max(cpu, gpu) + credit and eb * n <= vram
+            objs.append(abs(cpu - gpu) if ok else None)
+            if ok and (best is None or abs(cpu - gpu) < best):
+                best = abs(cpu - gpu)
+        if best is None:
+            assert got[1] == 1 and got[0] == len(rc)
+            fb += 1
+        else:
+            assert got[1] == 0 and objs[got[0] - 1] == best
+            feas += 1
+        assert got[5] <= 2 * int(np.ceil(np.log2(len(rc)))) + 8
+    assert feas > 100 and fb > 10
+
+
+def test_solver_kats():
+    # workload_balancer_test.cpp:96-164
+    t = (1_000_000,) * 4
+    got = abi.solve_threshold(np.zeros(8, np.int32), np.zeros(8, np.uint8), 2, 2, 4, [0.25, 0.5, 0.75, 1.0],
+                              [1.0, 0.75, 0.5, 0.25], *t, 10**9, 0)
+    assert got[:5].tolist() == [2, 0, 2_000_000, 3_000_000, 0]  # tie (1 ms, 1 ms) -> smaller tau
+    got = abi.solve_threshold(np.zeros(4, np.int32), np.zeros(4, np.uint8), 2, 2, 4, [0.0, 0.75, 1.0],
+                              [1.0, 0.75, 0.5], *t, 10**9, 0)
+    assert got[0] == 2 and got[2] == got[3]
+    got = abi.solve_threshold(np.full(8, 4, np.int32), np.zeros(8, np.uint8), 2, 2, 4, [0.5] * 4, [0.5] * 4, *t, 0, 0)
+    assert got[1] == 1 and got[0] == 4
+
+
+def test_ratio_update_kats_and_errors():
+    rc, rg = np.array([0.1, 0.2, 0.3]), np.array([0.9, 0.8, 0.7])
+    abi.check(abi.lib().moespac_update_ratio_estimates(rc.ctypes.data, rg.ctypes.data, 3, 2, 0.9, 0.1, 1.0))
+    np.testing.assert_allclose(rc, [0.1, 0.9, 0.9])
+    np.testing.assert_allclose(rg, [0.9, 0.1, 0.1])
+    rc, rg = np.array([0.2, 0.4]), np.array([0.8, 0.6])
+    abi.check(abi.lib().moespac_update_ratio_estimates(rc.ctypes.data, rg.ctypes.data, 2, 1, 1.0, 0.0, 0.5))
+    np.testing.assert_allclose(rc, [0.6, 0.6])
+    np.testing.assert_allclose(rg, [0.4, 0.4])
+    for args, code in [((0, 0.5, 0.5, 0.5), "E_RANGE"), ((1, 1.5, 0.5, 0.5), "E_INVALID"),
+                       ((1, 0.5, 0.5, 1.5), "E_INVALID")]:
+        with pytest.raises(abi.MoespacError) as ei:
+            abi.check(abi.lib().moespac_update_ratio_estimates(rc.ctypes.data, rg.ctypes.data, 2, *args))
+        assert ei.value.code == code
+
+
+def test_config_errors_map_to_reference_exceptions():
+    with pytest.raises(abi.MoespacError) as ei:
+        abi.Scheduler(abi.default_config(cache_ratio=0.0))
+    assert ei.value.code == "E_INVALID"
+    with pytest.raises(abi.MoespacError) as ei:
+        abi.Scheduler(abi.default_config(utility_cap=9, gamma=8))  # K <= gamma
+    assert ei.value.code == "E_INVALID"
+    with pytest.raises(abi.MoespacError) as ei:
+        abi.Scheduler(abi.default_config(policy="lru_cache"))
+    assert ei.value.code == "E_INVALID"
+    s = abi.Scheduler(abi.default_config(n_layers=1, n_experts=8, top_k=2, gamma=4))
+    with pytest.raises(abi.MoespacError) as ei:
+        s.observe_freqs(np.zeros((1, 8), np.int32), 1)  # observe without decide
+    assert ei.value.code == "E_LOGIC"
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_bookkeeping_invariants(world):
+    """Expert-parallel mode: every shard keeps <= min(|shard|, C1) residents of
+    its own experts; tau is global; G == 1 reduces to the reference."""
+    L, N, k, g = 6, 64, 6, 8
+    cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=0.17)
+    gen = O.Generator(L, N, k, g, seed=1)
+    trace = [gen.next_step() for _ in range(30)]
+    ids = np.stack([t[1] for t in trace])
+    acc = np.array([t[2] for t in trace])
+    c1 = abi.lib().moespac_layer_capacity_experts(0.17, N)
+    s = abi.Scheduler(cfg, world)
+    est = [O.estimator_init(N, g) for _ in range(L)]
+    scores = np.zeros((L, N), np.int32)
+    for st in range(len(acc)):
+        s.decide(scores)
+        taus, rb, lb, slots = s.tables()
+        for l in range(L):
+            resident = [e for e in range(N) if (rb[l, e >> 5] >> (e & 31)) & 1]
+            for r in range(world):
+                mine = [e for e in resident if e % world == r]
+                cap_r = min(len(range(r, N, world)), c1)
+                assert len(mine) <= cap_r
+                sl = sorted(slots[l, mine].tolist())
+                assert len(set(sl)) == len(sl) and all(0 <= x < cap_r for x in sl)
+            assert all(slots[l, e] == -1 for e in range(N) if e not in resident)
+        loads = s.loads()
+        for (l, e, sh, slot) in loads:
+            assert e % world == sh and slots[l, e] == slot
+        freqs = np.stack([O.hist_scan(ids[st, l], N)[0] for l in range(L)])
+        s.observe_freqs(freqs, int(acc[st]))
+        for l in range(L):
+            est[l] = O.estimator_observe(est[l], freqs[l], 4, 0.1)
+            scores[l] = est[l][:, 0]
+
+
+@pytest.mark.ref
+def test_scheduler_vs_live_reference_fuzz():
+    """Random shapes/profiles/policies against the live reference Simulation."""
+    ref_or_skip()
+    rng = np.random.default_rng(2026)
+    for trial in range(25):
+        L = int(rng.integers(1, 6))
+        N = int(rng.integers(2, 70))
+        k = int(rng.integers(1, min(N, 9) + 1))
+        g = int(rng.integers(1, 10))
+        K = int(rng.integers(1, g + 1))
+        pol = ["moe_spac", "fixed_tau", "fixed_boundaries", "binary_utility"][trial % 4]
+        kw = dict(n_layers=L, n_experts=N, top_k=k, gamma=g, utility_cap=K, policy=pol,
+                  cache_ratio=float(rng.choice([0.1, 0.17, 0.3, 0.5, 1.0])),
+                  t_cpu_unit_ns=int(rng.integers(1, 200_000)), t_gpu_unit_ns=int(rng.integers(1, 100_000)),
+                  t_io_unit_ns=int(rng.integers(1, 800_000)), t_draft_unit_ns=int(rng.integers(1, 500_000)),
+                  forgetting=float(rng.integers(0, 11)) / 10, fixed_tau=int(rng.integers(1, K + 1)),
+                  ratio_smoothing=float(rng.random()))
+        rcfg = O.default_config(token_budget=0, **kw)
+        if O.layer_cap(rcfg) if hasattr(O, "layer_cap") else False:
+            pass
+        ids, acc = O.ref_trace(rcfg, 25)
+        try:
+            run = O.ref_sim_run(rcfg, ids, acc)
+        except RuntimeError:
+            continue
+        cfg = abi.default_config(**kw)
+        s, recs, _ = replay(cfg, ids, acc, cap=K)
+        assert np.array_equal(recs, run.layer_rec[:, :, :9]), (trial, kw)
+        assert np.array_equal(s.events(), run.events), (trial, kw)
