@@ -55,6 +55,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--trace-steps", type=int, default=64)
+    ap.add_argument("--ffn-kernel", type=int, default=0, help="0 auto (tcgen05), 1 CUDA-core GEMV, 2 tcgen05")
     return ap.parse_args()
 
 
@@ -210,7 +211,7 @@ def run_ours(args, w, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=w.cache_ratio)
-    model = abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode)
+    model = abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode, args.ffn_kernel)
     ctx = abi.Context(local_rank, model, cfg, rank, world)
     n_images = min(L * N, max(N, 8))
     ctx.host_arena(n_images)
@@ -239,7 +240,6 @@ def run_ours(args, w, rank, world, local_rank):
     h_out_d = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
     torch.cuda.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream())
-    ctx.set_timing(True)
 
     def barrier():
         if world > 1:
@@ -270,23 +270,34 @@ def run_ours(args, w, rank, world, local_rank):
     for i in range(args.warmup):
         dev_step(i % S)
     with ClockSampler(local_rank) as clk:
+        # (1) headline: whole steps, no per-kernel events (layer kernels use
+        #     programmatic dependent launch)
+        ctx.set_timing(False)
         ms, reps = timed(dev_step, args.steps, args.warmup)
         for i in range(max(1, args.warmup // 2)):
             host_step(i % S)
         ms_e2e, reps_e2e = timed(host_step, args.steps, args.warmup)
+        # (2) roofline: the same steps with a CUDA-event pair around every K3
+        #     launch (PDL off so each pair brackets exactly one kernel)
+        ctx.set_timing(True)
+        ms_t, reps_t = timed(dev_step, args.steps, args.warmup)
+    reps_tok = reps
+    reps = reps_t
     tokens = float(sum(accepted[(args.warmup + i) % S] for i in range(args.steps)))
     ffn_ms = sum(r.gpu_ms_ffn for r in reps)
     ffn_bytes = sum(r.ffn_bytes for r in reps)
-    launches = sum(r.kernel_launches for r in reps)
+    launches = sum(r.kernel_launches for r in reps_tok)
     hits = sum(r.cache_hits for r in reps)
     misses = sum(r.cache_misses for r in reps)
     loads = sum(r.n_loads for r in reps)
     out = {
-        "ms": ms, "ms_e2e": ms_e2e, "tokens": tokens, "ffn_ms": ffn_ms, "ffn_bytes": ffn_bytes,
+        "ms": ms, "ms_e2e": ms_e2e, "ms_timed": ms_t, "tokens": tokens, "ffn_ms": ffn_ms, "ffn_bytes": ffn_bytes,
         "ffn_launches": args.steps * L, "launches": launches, "hits": hits, "misses": misses, "loads": loads,
         "h2d": float(np.mean([r.h2d_bytes for r in reps_e2e])), "d2h": float(np.mean([r.d2h_bytes for r in reps_e2e])),
         "router_ms": float(np.mean([r.gpu_ms_router for r in reps])),
         "hist_ms": float(np.mean([r.gpu_ms_hist for r in reps])),
+        "gpu_step_ms": float(np.mean([r.gpu_ms_total for r in reps])),
+        "layers_other_ms": float(np.mean([r.gpu_ms_combine for r in reps])),
         "clocks": clk.summary(),
     }
     if world > 1:
@@ -369,8 +380,10 @@ def main():
     line["gpu_launches"] = int(r["launches"])
     line["clocks"] = r["clocks"]
     line["detail"] = {"hit_rate": r["hits"] / max(1, r["hits"] + r["misses"]), "loads_per_step": r["loads"] / args.steps,
-                      "router_ms": r["router_ms"], "hist_ms": r["hist_ms"],
-                      "ffn_ms_per_step": r["ffn_ms"] / args.steps, "tokens_per_step": r["tokens"] / args.steps}
+                      "router_ms": r["router_ms"], "hist_ms": r["hist_ms"], "gpu_step_ms": r["gpu_step_ms"],
+                      "layers_non_ffn_ms": r["layers_other_ms"],
+                      "ffn_ms_per_step": r["ffn_ms"] / args.steps, "tokens_per_step": r["tokens"] / args.steps,
+                      "ms_per_step_with_kernel_events": r["ms_timed"] / args.steps}
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_path_sample(w, args.cpu_budget_s, use_ref_sched=True)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}

@@ -191,7 +191,17 @@ moespac_status moespac_estimator_init(int32_t* est_state_dev, int n, int gamma, 
                                       void* stream);
 
 /* K3 — grouped SwiGLU expert FFN over the resident activated experts of one
- * layer (replaces the modeled charge at core/src/sim_core.cpp:253-254). */
+ * layer (replaces the modeled charge at core/src/sim_core.cpp:253-254).
+ * Two kernels, one contract: MOESPAC_FFN_TENSOR (tcgen05.mma, TMEM
+ * accumulators; needs d % 128 == 0, ffn % 64 == 0) and MOESPAC_FFN_CUDACORE
+ * (weight-streaming GEMV on the CUDA cores; d % 512 == 0, ffn % 16 == 0).
+ * Expert images must be packed for the kernel that reads them. */
+#define MOESPAC_FFN_AUTO 0
+#define MOESPAC_FFN_CUDACORE 1
+#define MOESPAC_FFN_TENSOR 2
+int moespac_ffn_resolve(int kernel, int d_model, int d_ffn);
+/* h [T][d] bf16 -> h^T UMMA operand image (16 * d bf16) for the tensor kernel. */
+moespac_status moespac_build_hT(const uint16_t* h_dev, int tokens, int d_model, uint16_t* hT_dev, void* stream);
 typedef struct moespac_ffn_args {
   const uint16_t* h_dev;       /* [T][d] bf16 */
   int32_t tokens, d_model, d_ffn, top_k, n_experts;
@@ -204,6 +214,8 @@ typedef struct moespac_ffn_args {
   int32_t n_shared_units;
   float* workspace_dev;        /* moespac_ffn_workspace_bytes() */
   int32_t grid;                /* 0 = one CTA per SM */
+  int32_t kernel;              /* MOESPAC_FFN_* (image layout must match) */
+  const uint16_t* hT_dev;      /* tensor-core kernel: moespac_build_hT(h) image */
 } moespac_ffn_args;
 size_t moespac_ffn_workspace_bytes(int tokens, int d_model, int n_experts, int n_shared_units, int grid);
 int64_t moespac_expert_image_elems(int d_model, int d_ffn);
@@ -225,8 +237,8 @@ moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream);
 
 /* Standard layouts (w_gate, w_up: [ffn][d]; w_down: [d][ffn]) -> tiled image. */
 moespac_status moespac_pack_expert(const uint16_t* w_gate_dev, const uint16_t* w_up_dev,
-                                   const uint16_t* w_down_dev, int d_model, int d_ffn, uint16_t* image_dev,
-                                   void* stream);
+                                   const uint16_t* w_down_dev, int d_model, int d_ffn, int kernel,
+                                   uint16_t* image_dev, void* stream);
 moespac_status moespac_fill_synthetic(uint16_t* dev, int64_t n_elems, uint64_t seed, float stdv, void* stream);
 
 /* ------------------------------------------------------------------ engine context
@@ -241,6 +253,7 @@ typedef struct moespac_model_desc {
   int32_t d_model, d_ffn;
   int32_t n_shared_units; /* shared experts expressed in units of d_ffn rows */
   int32_t gate_mode;      /* see moespac_router_topk */
+  int32_t ffn_kernel;     /* MOESPAC_FFN_*; expert images use its layout */
 } moespac_model_desc;
 
 typedef struct moespac_ctx moespac_ctx;
@@ -261,7 +274,12 @@ moespac_status moespac_ctx_finalize(moespac_ctx* c);
 /* Expert-parallel combine over NCCL: 128-byte ncclUniqueId from rank 0. */
 moespac_status moespac_nccl_unique_id(void* out128);
 moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* unique_id128, int nranks, int rank);
+/* Per-kernel CUDA-event timing in moespac_step_report (off by default). While
+ * timing is on, layer kernels are launched without programmatic dependent
+ * launch so each K3 event pair brackets exactly that kernel. */
 moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
+/* Programmatic dependent launch between layer kernels (on by default). */
+moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a
  * step runs on it, so events recorded there bracket whole steps. */
 void* moespac_ctx_stream(const moespac_ctx* c);
@@ -291,6 +309,11 @@ typedef struct moespac_ctx_views {
   int64_t slots_per_layer, image_elems;
 } moespac_ctx_views;
 moespac_status moespac_ctx_get_views(const moespac_ctx* c, moespac_ctx_views* out);
+/* Decision tables the last executed step ran with (the context's scheduler
+ * already holds the next step's decisions, made while that step's layers
+ * ran). Same layouts as moespac_sched_tables. */
+moespac_status moespac_ctx_step_tables(const moespac_ctx* c, int32_t* taus, uint32_t* resident_bits,
+                                       uint32_t* loaded_bits, int32_t* slot_table);
 /* Host scheduler of the context (read-only use of the moespac_sched_* getters). */
 const moespac_sched* moespac_ctx_sched(const moespac_ctx* c);
 

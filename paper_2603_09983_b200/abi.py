@@ -83,7 +83,7 @@ class FfnArgs(C.Structure):
                 ("offsets_dev", C.c_void_p), ("gates_dev", C.c_void_p), ("hit_list_dev", C.c_void_p),
                 ("counters_dev", C.c_void_p), ("slot_of_dev", C.c_void_p), ("pool_dev", C.c_void_p),
                 ("shared_dev", C.c_void_p), ("n_shared_units", C.c_int32), ("workspace_dev", C.c_void_p),
-                ("grid", C.c_int32)]
+                ("grid", C.c_int32), ("kernel", C.c_int32), ("hT_dev", C.c_void_p)]
 
 
 class CombineArgs(C.Structure):
@@ -97,7 +97,7 @@ class CombineArgs(C.Structure):
 class ModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("n_shared_units", C.c_int32),
-                ("gate_mode", C.c_int32)]
+                ("gate_mode", C.c_int32), ("ffn_kernel", C.c_int32)]
 
 
 class CtxViews(C.Structure):
@@ -149,7 +149,9 @@ def lib() -> C.CDLL:
         "moespac_expert_image_elems": (i64, [C.c_int, C.c_int]),
         "moespac_expert_ffn": (C.c_int, [C.POINTER(FfnArgs), vp]),
         "moespac_ffn_combine": (C.c_int, [C.POINTER(CombineArgs), vp]),
-        "moespac_pack_expert": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, vp]),
+        "moespac_pack_expert": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, vp]),
+        "moespac_ffn_resolve": (C.c_int, [C.c_int, C.c_int, C.c_int]),
+        "moespac_build_hT": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
         "moespac_fill_synthetic": (C.c_int, [vp, i64, C.c_uint64, C.c_float, vp]),
         "moespac_ctx_create": (C.c_int, [C.c_int, C.POINTER(ModelDesc), C.POINTER(SchedConfig), C.c_int, C.c_int,
                                          C.POINTER(vp)]),
@@ -161,11 +163,13 @@ def lib() -> C.CDLL:
         "moespac_nccl_unique_id": (C.c_int, [vp]),
         "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
         "moespac_step": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_ctx_get_views": (C.c_int, [vp, C.POINTER(CtxViews)]),
         "moespac_ctx_sched": (vp, [vp]),
         "moespac_ctx_stream": (vp, [vp]),
+        "moespac_ctx_step_tables": (C.c_int, [vp, vp, vp, vp, vp]),
         "moespac_trace_synth_create": (C.c_int, [C.POINTER(SchedConfig), C.POINTER(vp)]),
         "moespac_trace_synth_next": (C.c_int, [vp, vp, vp]),
         "moespac_trace_synth_destroy": (None, [vp]),
@@ -347,12 +351,28 @@ def expert_image_elems(d: int, ffn: int) -> int:
     return lib().moespac_expert_image_elems(d, ffn)
 
 
-def pack_expert(wg, wu, wd, stream=None):
-    """Standard-layout bf16 (as torch.bfloat16 or int16/uint16 views) -> tiled image (uint16 view)."""
+FFN_AUTO, FFN_CUDACORE, FFN_TENSOR = 0, 1, 2
+
+
+def ffn_resolve(kernel: int, d: int, ffn: int) -> int:
+    return lib().moespac_ffn_resolve(kernel, d, ffn)
+
+
+def pack_expert(wg, wu, wd, kernel: int = FFN_AUTO, stream=None):
+    """Standard-layout bf16 (int16 views) -> tiled image for `kernel` (int16 view)."""
     import torch
     ffn, d = wg.shape
     out = torch.empty(3 * ffn * d, dtype=torch.int16, device=wg.device)
-    check(lib().moespac_pack_expert(ptr(wg), ptr(wu), ptr(wd), d, ffn, ptr(out), _stream(stream)))
+    check(lib().moespac_pack_expert(ptr(wg), ptr(wu), ptr(wd), d, ffn, kernel, ptr(out), _stream(stream)))
+    return out
+
+
+def build_hT(h, stream=None):
+    """[T][d] bf16 (int16 view) -> h^T UMMA image for the tensor-core K3."""
+    import torch
+    T, d = h.shape
+    out = torch.empty(16 * d, dtype=torch.int16, device=h.device)
+    check(lib().moespac_build_hT(ptr(h), T, d, ptr(out), _stream(stream)))
     return out
 
 
@@ -393,6 +413,9 @@ class Context:
     def set_timing(self, on: bool = True):
         check(lib().moespac_ctx_set_timing(self._h, int(on)))
 
+    def set_pdl(self, on: bool = True):
+        check(lib().moespac_ctx_set_pdl(self._h, int(on)))
+
     def set_nccl(self, uid: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(uid, 128)
         check(lib().moespac_ctx_set_nccl(self._h, buf, nranks, rank))
@@ -426,15 +449,16 @@ class Context:
         lib().moespac_sched_events(s, out.ctypes.data, n)
         return out[:n]
 
-    def sched_tables(self):
-        s = lib().moespac_ctx_sched(self._h)
+    def step_tables(self):
+        """Decision tables the last executed step ran with."""
         L, N = self.model.n_layers, self.model.n_experts
         W = (N + 31) // 32
         taus = np.zeros(L, np.int32)
         rb = np.zeros((L, W), np.uint32)
         lb = np.zeros((L, W), np.uint32)
         slots = np.zeros((L, N), np.int32)
-        check(lib().moespac_sched_tables(s, taus.ctypes.data, rb.ctypes.data, lb.ctypes.data, slots.ctypes.data))
+        check(lib().moespac_ctx_step_tables(self._h, taus.ctypes.data, rb.ctypes.data, lb.ctypes.data,
+                                            slots.ctypes.data))
         return taus, rb, lb, slots
 
     def sched_decisions(self) -> np.ndarray:

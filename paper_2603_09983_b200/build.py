@@ -27,6 +27,7 @@ CU_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 SOURCES = [
     "kernels/router_hist.cu",
     "kernels/expert_ffn.cu",
+    "kernels/expert_ffn_tc.cu",
     "host/scheduler.cpp",
     "host/step_scheduler.cpp",
     "host/engine.cpp",

@@ -424,15 +424,28 @@ static int device_sms() {
   return sms;
 }
 
+int moespac_ffn_resolve(int kernel, int d, int ffn) { return ffn_resolve(kernel, d, ffn); }
+
+moespac_status moespac_build_hT(const uint16_t* h, int tokens, int d, uint16_t* hT, void* stream) {
+  return guard([&] {
+    if (tokens < 1 || tokens > kFfnMaxTokens || d % 64) throw std::invalid_argument("moespac_build_hT: shape");
+    require_device();
+    cuda_ok(launch_build_hT(h, tokens, d, hT, static_cast<cudaStream_t>(stream)), "build_hT");
+  });
+}
+
 moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
   return guard([&] {
-    if (a->d_model % 512 || a->d_ffn % kFfnChunkRows || a->tokens < 1 || a->tokens > kFfnMaxTokens)
-      throw std::invalid_argument("moespac_expert_ffn: d_model % 512, d_ffn % 16, 1 <= tokens <= 16");
+    const int kern = ffn_resolve(a->kernel, a->d_model, a->d_ffn);
+    if (!ffn_shape_ok(kern, a->d_model, a->d_ffn) || a->tokens < 1 || a->tokens > kFfnMaxTokens)
+      throw std::invalid_argument("moespac_expert_ffn: unsupported shape for this kernel (1 <= tokens <= 16)");
+    if (kern == kFfnTensorCore && !a->hT_dev) throw std::invalid_argument("moespac_expert_ffn: hT_dev required");
     require_device();
     int dev = 0, optin = 0;
     cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
     cuda_ok(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
-    const FfnPlan plan = ffn_plan(a->tokens, a->d_model, static_cast<size_t>(optin));
+    const FfnPlan plan = kern == kFfnTensorCore ? ffn_tc_plan(a->tokens, a->d_model, static_cast<size_t>(optin))
+                                                : ffn_plan(a->tokens, a->d_model, static_cast<size_t>(optin));
     if (!plan.n_stages) throw std::invalid_argument("moespac_expert_ffn: tokens x d_model too large for shared memory");
     dev::FfnArgs f{};
     f.h = a->h_dev;
@@ -454,8 +467,10 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.partial = a->workspace_dev;
     f.n_stages = plan.n_stages;
     f.global_acc = plan.global_acc ? 1 : 0;
+    f.hT = a->hT_dev;
     const int grid = a->grid > 0 ? a->grid : device_sms();
-    cuda_ok(launch_expert_ffn(f, grid, plan.smem, static_cast<cudaStream_t>(stream)),
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_ok(kern == kFfnTensorCore ? launch_expert_ffn_tc(f, grid, plan.smem, st) : launch_expert_ffn(f, grid, plan.smem, st),
             "expert_ffn");
   });
 }
@@ -484,11 +499,15 @@ moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream) 
 }
 
 moespac_status moespac_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
-                                   uint16_t* out, void* stream) {
+                                   int kernel, uint16_t* out, void* stream) {
   return guard([&] {
-    if (d % 512 || ffn % kFfnChunkRows || ffn <= 0) throw std::invalid_argument("moespac_pack_expert: shape");
+    const int kern = ffn_resolve(kernel, d, ffn);
+    if (!ffn_shape_ok(kern, d, ffn)) throw std::invalid_argument("moespac_pack_expert: shape");
     require_device();
-    cuda_ok(launch_pack_expert(wg, wu, wd, d, ffn, out, static_cast<cudaStream_t>(stream)), "pack_expert");
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_ok(kern == kFfnTensorCore ? launch_pack_expert_tc(wg, wu, wd, d, ffn, out, st)
+                                   : launch_pack_expert(wg, wu, wd, d, ffn, out, st),
+            "pack_expert");
   });
 }
 
@@ -541,6 +560,10 @@ moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_timing(enabled != 0); });
 }
 
+moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
+  return guard([&] { c->e.set_pdl(enabled != 0); });
+}
+
 void* moespac_ctx_stream(const moespac_ctx* c) { return c->e.stream(); }
 
 moespac_status moespac_step(moespac_ctx* c, const double* logits, const uint16_t* h_in, int accepted, uint16_t* h_out,
@@ -551,6 +574,11 @@ moespac_status moespac_step(moespac_ctx* c, const double* logits, const uint16_t
 moespac_status moespac_step_device(moespac_ctx* c, const double* logits, const uint16_t* h_in, int accepted,
                                    uint16_t* h_out, moespac_step_report* rep, moespac_layer_timing* layers) {
   return guard([&] { c->e.step(logits, false, h_in, false, accepted, h_out, false, rep, layers); });
+}
+
+moespac_status moespac_ctx_step_tables(const moespac_ctx* c, int32_t* taus, uint32_t* rb, uint32_t* lb,
+                                      int32_t* slots) {
+  return guard([&] { c->e.step_tables(taus, rb, lb, slots); });
 }
 
 moespac_status moespac_ctx_get_views(const moespac_ctx* c, moespac_ctx_views* out) {

@@ -69,8 +69,12 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
     : device_(device), rank_(rank), world_(world), m_(m) {
   if (m.n_layers < 1 || m.n_experts < 1 || m.top_k < 1 || m.top_k > m.n_experts || m.gamma < 1)
     throw std::invalid_argument("moespac_model_desc: invalid shape");
-  if (m.d_model % 512 != 0 || m.d_ffn % kFfnChunkRows != 0 || m.d_ffn <= 0)
-    throw std::invalid_argument("moespac_model_desc: d_model % 512 == 0 and d_ffn % 16 == 0 required");
+  kernel_ = ffn_resolve(m.ffn_kernel, m.d_model, m.d_ffn);
+  if (kernel_ != kFfnCudaCore && kernel_ != kFfnTensorCore) throw std::invalid_argument("moespac_model_desc: ffn_kernel");
+  if (!ffn_shape_ok(kernel_, m.d_model, m.d_ffn))
+    throw std::invalid_argument(kernel_ == kFfnTensorCore
+                                    ? "moespac_model_desc: tensor-core FFN needs d_model % 128 == 0, d_ffn % 64 == 0"
+                                    : "moespac_model_desc: d_model % 512 == 0 and d_ffn % 16 == 0 required");
   if (m.gamma + 1 > kFfnMaxTokens) throw std::invalid_argument("moespac_model_desc: gamma + 1 must be <= 16");
   if (m.n_experts > 1024) throw std::invalid_argument("moespac_model_desc: n_experts must be <= 1024");
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("moespac_ctx: bad shard rank/world");
@@ -114,7 +118,8 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   if (prop.major != 10) throw CudaError("moespac requires an sm_100 (B200) device");
   sms_ = prop.multiProcessorCount;
-  const FfnPlan plan = ffn_plan(T_, m.d_model, prop.sharedMemPerBlockOptin);
+  const FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, prop.sharedMemPerBlockOptin)
+                                                 : ffn_plan(T_, m.d_model, prop.sharedMemPerBlockOptin);
   if (plan.n_stages == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
   stages_ = plan.n_stages;
   global_acc_ = plan.global_acc;
@@ -140,6 +145,8 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   dmalloc(reinterpret_cast<void**>(&est_d_), sizeof(int32_t) * L * N * 4, "cudaMalloc est");
   dmalloc(reinterpret_cast<void**>(&y_d_), sizeof(float) * L * T_ * d, "cudaMalloc y");
   dmalloc(reinterpret_cast<void**>(&h_d_), sizeof(uint16_t) * (L + 1) * T_ * d, "cudaMalloc h");
+  dmalloc(reinterpret_cast<void**>(&hT_d_), sizeof(uint16_t) * 2 * 16 * d, "cudaMalloc hT");
+  check(cudaMemset(hT_d_, 0, sizeof(uint16_t) * 2 * 16 * d), "memset hT");  // token pad rows stay zero
   work_bytes_ = static_cast<size_t>(sms_ + N + m.n_shared_units) * T_ * d * 4;
   dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
   tables_bytes_ = sizeof(uint32_t) * 2 * L * W_ + sizeof(int32_t) * L + sizeof(int32_t) * L * N;
@@ -159,6 +166,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
     check(cudaEventCreate(&ffn_end_[static_cast<size_t>(l)]), "event");
   }
   for (auto& e : ev_) check(cudaEventCreate(&e), "event");
+  check(cudaEventCreateWithFlags(&k2_done_, cudaEventDisableTiming | cudaEventBlockingSync), "event");
 
   // LayerEstimator ctor state for every layer (utility_estimator.cpp:23-33)
   const EstimatorConfig ec = estimator_config_for(sched_->config().policy, sched_->config().estimator);
@@ -178,7 +186,7 @@ Engine::~Engine() {
                   static_cast<void*>(ids_d_), static_cast<void*>(gates_d_), static_cast<void*>(freqs_d_),
                   static_cast<void*>(offsets_d_), static_cast<void*>(perm_d_), static_cast<void*>(hit_list_d_),
                   static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
-                  static_cast<void*>(h_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
+                  static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
                   static_cast<void*>(out_d_)})
     if (p) cudaFree(p);
   if (arena_h_) cudaFreeHost(arena_h_);
@@ -189,6 +197,7 @@ Engine::~Engine() {
   for (auto e : ffn_end_) cudaEventDestroy(e);
   for (auto e : ev_)
     if (e) cudaEventDestroy(e);
+  if (k2_done_) cudaEventDestroy(k2_done_);
   if (compute_) cudaStreamDestroy(compute_);
   if (copy_) cudaStreamDestroy(copy_);
 }
@@ -266,6 +275,7 @@ void Engine::finalize() {
     }
   check(cudaStreamSynchronize(compute_), "sync");
   finalized_ = true;
+  decided_ = false;
 }
 
 void Engine::set_nccl(const void* uid, int nranks, int rank) {
@@ -288,8 +298,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   check(cudaSetDevice(device_), "cudaSetDevice");
   const int L = m_.n_layers, N = m_.n_experts, k = m_.top_k, d = m_.d_model;
 
-  // ---- host: decisions for every layer (the draft window) ----
-  sched_->decide(scores_.data());
+  // ---- host: this step's decisions. They were made during the previous
+  // step's FFN phase (decide() needs only the K2 scores of that step); the
+  // very first step decides here.
+  if (!decided_) {
+    sched_->decide(scores_.data());
+    decided_ = true;
+  }
   uint32_t* rb = reinterpret_cast<uint32_t*>(tables_h_);
   uint32_t* lb = rb + static_cast<size_t>(L) * W_;
   int32_t* taus = reinterpret_cast<int32_t*>(lb + static_cast<size_t>(L) * W_);
@@ -302,9 +317,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   const uint32_t* lb_d = rb_d + static_cast<size_t>(L) * W_;
   const int32_t* taus_d = reinterpret_cast<const int32_t*>(lb_d + static_cast<size_t>(L) * W_);
   const int32_t* slots_d = taus_d + L;
+  std::vector<int> layer_loads(static_cast<size_t>(L), 0), layer_loads_local(static_cast<size_t>(L), 0);
 
   if (timing_) check(cudaEventRecord(ev_[0], compute_), "event");
-  // ---- copy engine: loads in drain order, one event per layer ----
+  // ---- copy engine: this step's loads in drain order, one event per layer.
+  // The previous step fully completed before this call returned, so no slot
+  // being overwritten is still read by an in-flight FFN (the device-side
+  // meaning of the reference's frozen score, execution_engine.cpp:111-118).
   int n_loads = 0;
   {
     size_t i = 0;
@@ -312,7 +331,9 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     for (int l = 0; l < L; ++l) {
       for (; i < loads.size() && loads[i].layer == l; ++i) {
         const SlotLoad& ld = loads[i];
+        ++layer_loads[static_cast<size_t>(l)];
         if (ld.shard != rank_) continue;
+        ++layer_loads_local[static_cast<size_t>(l)];
         check(cudaMemcpyAsync(slot_ptr(l, ld.slot), arena_h_ + image_of(l, ld.expert) * image_elems_,
                               image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
               "H2D expert load");
@@ -321,7 +342,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
     }
   }
-  // ---- compute stream ----
+  // ---- compute stream
   check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
   if (logits_host) {
@@ -364,9 +385,22 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   a2.scores_out = scores_out_d;
   check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
   if (timing_) check(cudaEventRecord(ev_[3], compute_), "event");
+  // scores + counters back to the host right away: the host scheduler works
+  // on them while the device runs the layers below
+  check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
+  check(cudaEventRecord(k2_done_, compute_), "event");
 
+  const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
+  const bool tc = kernel_ == kFfnTensorCore;
+  uint16_t* hT[2] = {hT_d_, hT_d_ + static_cast<size_t>(16) * d};
+  if (tc) check(launch_build_hT(h_d_, T_, d, hT[0], compute_), "build_hT");
   for (int l = 0; l < L; ++l) {
-    check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
+    // Only a layer with this-rank loads needs the copy-stream event; every
+    // other K3 is launched programmatically-dependent on the previous kernel
+    // so its prologue and first weight copies overlap that kernel's tail.
+    const bool has_loads = layer_loads_local[static_cast<size_t>(l)] > 0;
+    if (has_loads) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
+    const bool pdl = pdl_ && !has_loads && !timing_;
     const uint16_t* hl = h_d_ + static_cast<size_t>(l) * T_ * d;
     uint16_t* hn = h_d_ + static_cast<size_t>(l + 1) * T_ * d;
     dev::FfnArgs fa{};
@@ -385,14 +419,16 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.pool = pool_ + static_cast<int64_t>(l) * slots_ * image_elems_;
     fa.shared_w = shared_ + static_cast<int64_t>(l) * m_.n_shared_units * image_elems_;
     // expert-parallel: shared units are computed once, on rank 0
-    const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
     fa.n_shared = n_shared_eff;
     fa.expert_elems = image_elems_;
     fa.partial = work_d_;
     fa.n_stages = stages_;
     fa.global_acc = global_acc_ ? 1 : 0;
+    fa.hT = hT[l & 1];
     if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
-    check(launch_expert_ffn(fa, sms_, ffn_smem_, compute_), "K3 expert FFN");
+    check(tc ? launch_expert_ffn_tc(fa, sms_, ffn_smem_, compute_, pdl)
+             : launch_expert_ffn(fa, sms_, ffn_smem_, compute_, pdl),
+          "K3 expert FFN");
     if (timing_) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
     dev::CombineArgs ca{};
     ca.h_in = hl;
@@ -410,29 +446,36 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     float* yl = y_d_ + static_cast<size_t>(l) * T_ * d;
     ca.y_out = yl;
     ca.h_out = world_ > 1 ? nullptr : hn;
-    check(launch_combine(ca, compute_), "combine");
+    ca.hT_out = (world_ == 1 && tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr;
+    check(launch_combine(ca, compute_, pdl_ && !timing_), "combine");
     if (world_ > 1) {
       const int r = nccl_->all_reduce(yl, yl, static_cast<size_t>(T_) * d, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm_,
                                       compute_);
       if (r != 0) throw NcclError("ncclAllReduce failed");
-      check(launch_residual(hl, yl, hn, T_ * d, compute_), "residual");
+      check(launch_residual(hl, yl, hn, (tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr, d, T_ * d, compute_),
+            "residual");
     }
   }
   if (timing_) check(cudaEventRecord(ev_[4], compute_), "event");
-  check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
   const uint16_t* hfin = h_d_ + static_cast<size_t>(L) * T_ * d;
   if (h_out)
     check(cudaMemcpyAsync(h_out, hfin, sizeof(uint16_t) * T_ * d,
                           h_out_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, compute_),
           "h_out");
   if (timing_) check(cudaEventRecord(ev_[5], compute_), "event");
+
+  // ---- host, overlapped with the layers: account this step with the K2
+  // counters, then decide the next step (needs only the new scores).
+  check(cudaEventSynchronize(k2_done_), "sync K2");
+  std::memcpy(scores_.data(), out_h_, sizeof(int32_t) * L * N);
+  std::vector<LayerOutcome> oc(reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N),
+                               reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N) + L);
+  StepReport sr = sched_->observe(oc.data(), accepted);
+  sched_->decide(scores_.data());
+
   check(cudaStreamSynchronize(compute_), "sync compute");
   check(cudaStreamSynchronize(copy_), "sync copy");
 
-  // ---- host: accounting with the K2 counters ----
-  std::memcpy(scores_.data(), out_h_, sizeof(int32_t) * L * N);
-  const auto* oc = reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N);
-  StepReport sr = sched_->observe(oc, accepted);
   if (rep) {
     std::memset(rep, 0, sizeof(*rep));
     rep->draft_ns = sr.draft_ns;
@@ -446,15 +489,15 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     rep->n_experts = N;
     rep->n_layers = L;
     rep->n_loads = n_loads;
-    const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
     int64_t units = 0;
-    for (int l = 0; l < L; ++l) units += oc[l].n_local_hits + n_shared_eff;
+    for (int l = 0; l < L; ++l) units += oc[static_cast<size_t>(l)].n_local_hits + n_shared_eff;
     rep->ffn_bytes = units * image_elems_ * 2;
     rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads) * image_elems_ * 2 +
                      (logits_host ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
                      (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
-    rep->d2h_bytes = static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
-    rep->kernel_launches = 2 + 2 * L + (world_ > 1 ? L : 0);
+    rep->d2h_bytes =
+        static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
+    rep->kernel_launches = 2 + 2 * L + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
     if (timing_) {
       auto ms = [](cudaEvent_t a, cudaEvent_t b) {
         float v = 0.f;
@@ -483,11 +526,21 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       o.tau = lt.tau;
       o.fallback = lt.fallback;
       o.n_prefetch = lt.n_prefetch;
-      o.n_loads = 0;
-      for (const SlotLoad& ld : sched_->loads())
-        if (ld.layer == l) ++o.n_loads;
+      o.n_loads = layer_loads[static_cast<size_t>(l)];
     }
   }
+}
+
+void Engine::step_tables(int32_t* taus, uint32_t* rb, uint32_t* lb, int32_t* slots) const {
+  const int L = m_.n_layers, N = m_.n_experts;
+  const uint32_t* srb = reinterpret_cast<const uint32_t*>(tables_h_);
+  const uint32_t* slb = srb + static_cast<size_t>(L) * W_;
+  const int32_t* staus = reinterpret_cast<const int32_t*>(slb + static_cast<size_t>(L) * W_);
+  const int32_t* sslots = staus + L;
+  if (taus) std::memcpy(taus, staus, sizeof(int32_t) * L);
+  if (rb) std::memcpy(rb, srb, sizeof(uint32_t) * L * W_);
+  if (lb) std::memcpy(lb, slb, sizeof(uint32_t) * L * W_);
+  if (slots) std::memcpy(slots, sslots, sizeof(int32_t) * L * N);
 }
 
 void Engine::views(moespac_ctx_views* v) const {

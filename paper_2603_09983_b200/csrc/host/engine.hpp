@@ -37,9 +37,13 @@ class Engine {
   void finalize();
   void set_nccl(const void* uid, int nranks, int rank);
   void set_timing(bool on) { timing_ = on; }
+  void set_pdl(bool on) { pdl_ = on; }
   void step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
             uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
   void views(moespac_ctx_views* v) const;
+  // decision tables the last executed step ran with
+  void step_tables(int32_t* taus, uint32_t* rb, uint32_t* lb, int32_t* slots) const;
+  int ffn_kernel() const { return kernel_; }
   const StepScheduler& sched() const { return *sched_; }
   void* stream() const { return compute_; }
 
@@ -52,6 +56,7 @@ class Engine {
     return pool_ + (static_cast<int64_t>(layer) * slots_ + slot) * image_elems_;
   }
 
+  int kernel_ = 0;
   int device_ = 0, rank_ = 0, world_ = 1, sms_ = 148, T_ = 0, W_ = 1, stages_ = 6;
   size_t ffn_smem_ = 0;
   moespac_model_desc m_{};
@@ -69,6 +74,7 @@ class Engine {
   int32_t *hit_list_d_ = nullptr, *hit_ord_d_ = nullptr, *est_d_ = nullptr;
   float *gates_d_ = nullptr, *y_d_ = nullptr, *work_d_ = nullptr;
   uint16_t* h_d_ = nullptr;     // [L+1][T][d]
+  uint16_t* hT_d_ = nullptr;    // h^T UMMA image of the current layer input (tensor-core K3)
   uint8_t* tables_d_ = nullptr; // resident bits | loaded bits | taus | slot table
   int32_t* out_d_ = nullptr;    // scores_out [L][N] | counters [L][8]
   size_t tables_bytes_ = 0, out_bytes_ = 0, work_bytes_ = 0;
@@ -81,6 +87,9 @@ class Engine {
   cudaStream_t compute_ = nullptr, copy_ = nullptr;
   std::vector<cudaEvent_t> load_done_, ffn_beg_, ffn_end_;
   cudaEvent_t ev_[6] = {};
+  cudaEvent_t k2_done_ = nullptr;
+  bool decided_ = false;  // next step's decisions already made
+  bool pdl_ = true;       // programmatic dependent launch between layer kernels
   std::unique_ptr<NcclApi> nccl_;
   void* comm_ = nullptr;
 };

@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
       mbar_init(&s.empty[i], FFN_CONSUMER_WARPS);
     }
     fence_mbar_init();
+    pdl_trigger();
   }
+  pdl_wait();  // h and the partial workspace come from the previous kernel
   // hidden states of all T tokens -> smem (bf16), ysum <- 0
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.h);
@@ -402,34 +404,54 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
 
 // ---------------------------------------------------------------- combine
 
+// One CTA per (token, 128-column slice); the partial rows of the token (its
+// experts in ascending id, each over the CTAs that covered it in ascending
+// order) are dealt round-robin to the 8 warps, then the 8 warp sums are added
+// in warp order — a fixed summation tree, so the result is deterministic.
 __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
+  __shared__ float4 red[8][32];
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();  // partials of the K3 launch just before
   const int t = blockIdx.x;
-  const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
-  if (c >= a.d) return;
-  const int cpe = a.ffn / FC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.y * 128 + lane * 4;
+  const int qpe = a.ffn / FC;
   const int n_hits = a.counters[7];
-  const long long n = static_cast<long long>(n_hits + a.n_shared) * cpe;
+  const int n = (n_hits + a.n_shared) * qpe;
+  const int G = a.grid;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  auto add_entry = [&](int o) {
-    const long long lo = owner_of(static_cast<long long>(o) * cpe, n, a.grid);
-    const long long hi = owner_of(static_cast<long long>(o + 1) * cpe - 1, n, a.grid);
-    for (long long b = lo; b <= hi; ++b) {
-      // with fewer chunks than CTAs some CTAs own nothing and wrote no block
-      if ((b * n) / a.grid == ((b + 1) * n) / a.grid) continue;
-      const float4 v =
-          *reinterpret_cast<const float4*>(a.partial + ((b + o) * a.T + t) * static_cast<long long>(a.d) + c);
-      acc.x += v.x;
-      acc.y += v.y;
-      acc.z += v.z;
-      acc.w += v.w;
-    }
-  };
-  if (n > 0) {
+  if (n > 0 && c < a.d) {
+    int idx = 0;
+    auto add_entry = [&](int o) {
+      const int lo = ((o * qpe + 1) * G - 1) / n;
+      const int hi = (((o + 1) * qpe) * G - 1) / n;
+      for (int b = lo; b <= hi; ++b) {
+        // with fewer work units than CTAs some CTAs own nothing
+        if ((b * n) / G == ((b + 1) * n) / G) continue;
+        if ((idx++ & 7) != warp) continue;
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(
+            a.partial + (static_cast<long long>(b + o) * a.T + t) * static_cast<long long>(a.d) + c));
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+    };
     for (int j = 0; j < a.k; ++j) {
       const int o = a.hit_ord[a.ids[t * a.k + j]];
       if (o >= 0) add_entry(o);
     }
     for (int sidx = 0; sidx < a.n_shared; ++sidx) add_entry(n_hits + sidx);
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp != 0 || c >= a.d) return;
+  for (int w = 1; w < 8; ++w) {
+    const float4 v = red[w][lane];
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
   }
   const size_t off = static_cast<size_t>(t) * a.d + c;
   if (a.y_out) *reinterpret_cast<float4*>(a.y_out + off) = acc;
@@ -453,17 +475,32 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
     o.x = static_cast<uint32_t>(f32_to_bf16_rn(r.x)) | (static_cast<uint32_t>(f32_to_bf16_rn(r.y)) << 16);
     o.y = static_cast<uint32_t>(f32_to_bf16_rn(r.z)) | (static_cast<uint32_t>(f32_to_bf16_rn(r.w)) << 16);
     *reinterpret_cast<uint2*>(a.h_out + off) = o;
+    if (a.hT_out) {
+      // the next layer's h^T UMMA image (tensor-core K3): 4 consecutive k of
+      // token t share one 8-byte run (k % 8 in {0..3} or {4..7})
+      const int kt = c >> 6, j = (c >> 3) & 7, e = c & 7;
+      const int w = kt * 1024 + (t >> 3) * 512 + j * 64 + (t & 7) * 8 + e;
+      *reinterpret_cast<uint2*>(a.hT_out + w) = o;
+    }
   }
 }
 
 // h_out = bf16(h_in + y) — residual after an expert-parallel all-reduce.
-__global__ void residual_kernel(const uint16_t* h_in, const float* y, uint16_t* h_out, int n) {
+__global__ void residual_kernel(const uint16_t* h_in, const float* y, uint16_t* h_out, uint16_t* hT_out, int d,
+                                int n) {
+  pdl_wait();
+  pdl_trigger();
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
   if (i >= n) return;
   const uint32_t hv = *reinterpret_cast<const uint32_t*>(h_in + i);
   const float a = bf_lo(hv) + y[i], b = bf_hi(hv) + y[i + 1];
-  *reinterpret_cast<uint32_t*>(h_out + i) =
-      static_cast<uint32_t>(f32_to_bf16_rn(a)) | (static_cast<uint32_t>(f32_to_bf16_rn(b)) << 16);
+  const uint32_t o = static_cast<uint32_t>(f32_to_bf16_rn(a)) | (static_cast<uint32_t>(f32_to_bf16_rn(b)) << 16);
+  *reinterpret_cast<uint32_t*>(h_out + i) = o;
+  if (hT_out) {
+    const int t = i / d, c = i % d;
+    const int kt = c >> 6, j = (c >> 3) & 7, e = c & 7;
+    *reinterpret_cast<uint32_t*>(hT_out + kt * 1024 + (t >> 3) * 512 + j * 64 + (t & 7) * 8 + e) = o;
+  }
 }
 
 // ---------------------------------------------------------------- packing
@@ -545,26 +582,24 @@ FfnPlan ffn_plan(int T, int d, size_t smem_limit) {
   return {0, false, 0};
 }
 
-cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream) {
+cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(dev::expert_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dev::expert_ffn_kernel<<<grid, dev::FFN_THREADS, smem, stream>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(dev::expert_ffn_kernel, dim3(grid), dim3(dev::FFN_THREADS), smem, stream, pdl, a);
 }
 
-cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream) {
-  const dim3 grid(a.T, (a.d / 4 + 255) / 256);
-  dev::combine_kernel<<<grid, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream, bool pdl) {
+  return launch_pdl(dev::combine_kernel, dim3(a.T, (a.d + 127) / 128), dim3(256), 0, stream, pdl, a);
 }
 
-cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, int n, cudaStream_t stream) {
-  dev::residual_kernel<<<(n / 2 + 255) / 256, 256, 0, stream>>>(h_in, y, h_out, n);
-  return cudaGetLastError();
+cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, uint16_t* hT_out, int d, int n,
+                            cudaStream_t stream, bool pdl) {
+  return launch_pdl(dev::residual_kernel, dim3((n / 2 + 255) / 256), dim3(256), 0, stream, pdl, h_in, y, h_out,
+                    hT_out, d, n);
 }
 
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,

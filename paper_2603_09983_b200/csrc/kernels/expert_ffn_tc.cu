@@ -1,0 +1,595 @@
+// K3 (tensor-core variant) — grouped SwiGLU expert FFN on the 5th-gen tensor
+// cores: TMA bulk copies -> shared-memory UMMA operands -> tcgen05.mma ->
+// TMEM accumulators -> tcgen05.ld epilogue.
+//
+// Same contract and partial-block protocol as the CUDA-core kernel in
+// expert_ffn.cu (the combine kernel is shared); what changes is where the
+// multiply-adds run. At verification batches (T <= 16) the contraction is a
+// GEMV, so the tensor cores are idle most of the time either way — the point
+// of this variant is that the SMs no longer unpack bf16 and issue FFMA for
+// every weight element, which is what bounded the CUDA-core kernel (ncu:
+// issue-bound at ~58% of HBM). Here an SM issues ~10 instructions per 16 KiB
+// of weights and the kernel is bounded by the TMA weight stream.
+//
+// Tiled expert image (v2), per chunk of 64 ffn rows (ffn % 64 == 0):
+//   d/64 gate|up K-tiles, each [128 rows][64 k] bf16 in UMMA K-major
+//     core-matrix order (8 rows x 16 B core matrices; row-group outer:
+//     byte = g*1024 + j*128 + r*16 + e*2, rows 0-63 gate, 64-127 up);
+//   d/128 down M-tiles, each [128 out rows][64 f] of W_down, core matrices
+//     k-chunk outer (byte = j*2048 + g*128 + r*16 + e*2) so that a 16-row
+//     quarter of the chunk (k-chunks 2q, 2q+1) is one contiguous 4 KiB run.
+// Work unit = 16 ffn rows (a "quarter"), as in the CUDA-core kernel; a CTA
+// covering part of a chunk loads only its quarters' rows (2 gate/up copies +
+// 1 down copy per tile) and skips the down k-steps it does not own.
+//
+// Operands per MMA (cta_group::1, kind::f16, M=128, N=16, K=16):
+//   gate/up: A = weight tile (smem), B = h^T for all T tokens (zero-padded
+//            to 16; a 2 KiB slice per K-tile, streamed with the weights from
+//            an L2-resident image built per layer), D1 = TMEM [128][16].
+//   down:    A = W_down tile (smem), B = a^T split into bf16 hi + lo parts
+//            (a = silu(g) * u * gate_t; two MMAs keep ~16 mantissa bits),
+//            D2 = TMEM [128][16] per M-tile, 8 M-tiles per pass, 2 passes
+//            in flight.
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (+ TMEM owner), 2-5 = epilogue
+// (TMEM lane quarters 2,3,0,1).
+#include <cstdint>
+
+#include "common.cuh"
+#include "launch.hpp"
+
+namespace moespac {
+namespace dev {
+namespace tc {
+
+constexpr int THREADS = 192;
+constexpr int EPI_THREADS = 128;
+constexpr int A_BYTES = 16384;
+constexpr int B_BYTES = 2048;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int FCH = 64;  // ffn rows per chunk
+constexpr int QROWS = 16;
+constexpr int TMEM_COLS = 512;
+constexpr int D2_COL0 = 256;
+constexpr int PASS_TILES = 8;
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Phase {
+  uint32_t bit = 0;
+  __device__ __forceinline__ void flip() { bit ^= 1u; }
+};
+
+struct Ring {
+  int stage = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void advance(int ns) {
+    if (++stage == ns) {
+      stage = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// Iterates the CTA's work as segments (entry, chunk, quarter range).
+struct Seg {
+  int o, c, qa, qb;  // quarters [qa, qb) of chunk c of entry o
+};
+
+struct SegIter {
+  long long q, q1;
+  int qpe;  // quarters per entry = ffn / 16
+  __device__ __forceinline__ bool next(Seg& s) {
+    if (q >= q1) return false;
+    const int o = static_cast<int>(q / qpe);
+    const int qi = static_cast<int>(q % qpe);
+    const int c = qi / 4;
+    const int qa = qi % 4;
+    const long long chunk_end = static_cast<long long>(o) * qpe + (c + 1) * 4;
+    const long long end = chunk_end < q1 ? chunk_end : q1;
+    s = {o, c, qa, qa + static_cast<int>(end - q)};
+    q = end;
+    return true;
+  }
+};
+
+__device__ __forceinline__ const uint16_t* entry_weights(const FfnArgs& a, int o, int n_hits) {
+  if (o < n_hits) return a.pool + static_cast<long long>(a.slot_of[a.hit_list[o]]) * a.expert_elems;
+  return a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int ns = a.n_stages;
+  const int d = a.d, T = a.T;
+  const int ktiles = d / 64, mtiles = d / 128;
+  const int passes = (mtiles + PASS_TILES - 1) / PASS_TILES;
+  const long long chunk_elems = 3LL * FCH * d;
+  const int qpe = a.ffn / QROWS;
+
+  uint8_t* p = smem_raw;
+  uint8_t* ring = p;
+  p += static_cast<size_t>(ns) * STAGE_BYTES;
+  uint8_t* aT = p;  // [2 buf][2 part][4096]
+  p += 2 * 2 * 4096;
+  float* u_s = reinterpret_cast<float*>(p);  // [64][17] (padded: conflict-free column writes)
+  p += 64 * 17 * 4;
+  float* ysum = reinterpret_cast<float*>(p);  // [T][d] (unless global_acc)
+  if (!a.global_acc) p += static_cast<size_t>(T) * d * 4;
+  float* gate_s = reinterpret_cast<float*>(p);  // [2 slots][16] per-token gate of the entry
+  p += 2 * 16 * 4;
+  int* tok_s = reinterpret_cast<int*>(p);  // [2 slots][16] token list of the entry (for flush)
+  p += 2 * 16 * 4;
+  int* misc = reinterpret_cast<int*>(p);  // [1] tmem base, [2..3] ntok per slot
+  p += 16;
+  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
+  uint64_t* full = bars;
+  uint64_t* empty = full + ns;
+  uint64_t* d1_full = empty + ns;   // [2]
+  uint64_t* d1_empty = d1_full + 2; // [2]
+  uint64_t* at_full = d1_empty + 2; // [2]
+  uint64_t* at_empty = at_full + 2; // [2]
+  uint64_t* d2_full = at_empty + 2; // [2]
+  uint64_t* d2_empty = d2_full + 2; // [2]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_hits = a.counters[7];
+  const long long n = static_cast<long long>(n_hits + a.n_shared) * qpe;
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long q0 = n > 0 ? (b * n) / G : 0;
+  const long long q1 = n > 0 ? ((b + 1) * n) / G : 0;
+  if (q0 >= q1) return;
+
+  if (tid == 0) {
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d1_full[i], 1);
+      mbar_init(&d1_empty[i], 4);
+      mbar_init(&at_full[i], 1);
+      mbar_init(&at_empty[i], 1);
+      mbar_init(&d2_full[i], 1);
+      mbar_init(&d2_empty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[1])),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (!a.global_acc) {
+    float4* ys = reinterpret_cast<float4*>(ysum);
+    for (int i = tid; i < T * d / 4; i += THREADS) ys[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = static_cast<uint32_t>(misc[1]);
+  if (tid == 0) pdl_trigger();  // the combine may launch and park on its own wait
+  // Everything below except the producer's first weight copies depends on
+  // the previous kernel (h^T image, partial workspace): wait for it.
+  if (warp != 0) pdl_wait();
+
+  // All three roles walk the same software-pipelined sequence of segments:
+  //   GU(0), GU(1), DN(0), GU(2), DN(1), ..., DN(last)
+  // so the tensor core streams chunk i+1's gate/up tiles while the epilogue
+  // turns chunk i's D1 into a^T; DN(i) then finds a^T(i) ready.
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy();
+      Ring r;
+      SegIter it{q0, q1, qpe};
+      Seg cur, prev;
+      bool more = it.next(cur), has_prev = false;
+      // Weights do not depend on the previous kernel: put the first ring's
+      // worth of gate/up weight copies in flight, then wait, then add their
+      // h^T slices.
+      int kt0 = 0;
+      {
+        const uint8_t* base =
+            reinterpret_cast<const uint8_t*>(entry_weights(a, cur.o, n_hits) + cur.c * chunk_elems);
+        const uint32_t gseg = static_cast<uint32_t>(cur.qb - cur.qa) * 2048u;
+        kt0 = min(ns, ktiles);
+        for (int kt = 0; kt < kt0; ++kt) {
+          uint8_t* st = ring + static_cast<size_t>(kt) * STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[kt], 2 * gseg + B_BYTES);
+          const uint8_t* tile = base + static_cast<size_t>(kt) * A_BYTES;
+          bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[kt], pol);
+          bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[kt], pol);
+        }
+        pdl_wait();
+        for (int kt = 0; kt < kt0; ++kt)
+          bulk_g2s(ring + static_cast<size_t>(kt) * STAGE_BYTES + A_BYTES,
+                   reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES, B_BYTES, &full[kt],
+                   pol);
+        for (int kt = 0; kt < kt0; ++kt) r.advance(ns);
+      }
+      while (more || has_prev) {
+        if (more) {
+          const uint8_t* base =
+              reinterpret_cast<const uint8_t*>(entry_weights(a, cur.o, n_hits) + cur.c * chunk_elems);
+          const uint32_t gseg = static_cast<uint32_t>(cur.qb - cur.qa) * 2048u;
+          for (int kt = kt0; kt < ktiles; ++kt) {
+            mbar_wait(&empty[r.stage], r.ph ^ 1u);
+            uint8_t* st = ring + static_cast<size_t>(r.stage) * STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[r.stage], 2 * gseg + B_BYTES);
+            const uint8_t* tile = base + static_cast<size_t>(kt) * A_BYTES;
+            bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[r.stage], pol);
+            bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[r.stage], pol);
+            bulk_g2s(st + A_BYTES, reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES,
+                     B_BYTES, &full[r.stage], pol);
+            r.advance(ns);
+          }
+          kt0 = 0;
+        }
+        if (has_prev) {
+          const uint8_t* base =
+              reinterpret_cast<const uint8_t*>(entry_weights(a, prev.o, n_hits) + prev.c * chunk_elems);
+          const uint32_t dseg = static_cast<uint32_t>(prev.qb - prev.qa) * 4096u;
+          for (int mt = 0; mt < mtiles; ++mt) {
+            mbar_wait(&empty[r.stage], r.ph ^ 1u);
+            uint8_t* st = ring + static_cast<size_t>(r.stage) * STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[r.stage], dseg);
+            const uint8_t* tile = base + static_cast<size_t>(ktiles + mt) * A_BYTES;
+            bulk_g2s(st + prev.qa * 4096, tile + prev.qa * 4096, dseg, &full[r.stage], pol);
+            r.advance(ns);
+          }
+        }
+        has_prev = more;
+        prev = cur;
+        if (more) more = it.next(cur);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      Ring r;
+      Phase d1e[2], ate[2], d2e[2];
+      int c3 = 0;  // D2 pass buffer counter
+      SegIter it{q0, q1, qpe};
+      Seg cur, prev;
+      bool more = it.next(cur), has_prev = false;
+      int i = 0;
+      const uint32_t ring_addr = smem_u32(ring);
+      const uint32_t at_addr = smem_u32(aT);
+      while (more || has_prev) {
+        if (more) {  // GU(i): D1[i & 1] = W_gu x h^T
+          const int b1 = i & 1;
+          mbar_wait(&d1_empty[b1], d1e[b1].bit ^ 1u);
+          d1e[b1].flip();
+          fence_after();
+          const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
+          for (int kt = 0; kt < ktiles; ++kt) {
+            mbar_wait(&full[r.stage], r.ph);
+            fence_after();
+            const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_bf16(d1, smem_desc(sa + k * 256, 128, 1024), smem_desc(sa + A_BYTES + k * 256, 128, 1024),
+                       (kt | k) != 0);
+            mma_commit(&empty[r.stage]);
+            r.advance(ns);
+          }
+          mma_commit(&d1_full[b1]);
+        }
+        if (has_prev) {  // DN(i-1): D2 = W_down x a^T(i-1), hi + lo
+          const int ab = (i - 1) & 1;
+          mbar_wait(&at_full[ab], ate[ab].bit);
+          ate[ab].flip();
+          fence_after();
+          const uint32_t ahi = at_addr + static_cast<uint32_t>(ab) * 8192u;
+          const uint32_t alo = ahi + 4096u;
+          for (int ps = 0; ps < passes; ++ps) {
+            const int pb = c3 & 1;
+            mbar_wait(&d2_empty[pb], d2e[pb].bit ^ 1u);
+            d2e[pb].flip();
+            fence_after();
+            const int mt_end = min(mtiles, (ps + 1) * PASS_TILES);
+            for (int mt = ps * PASS_TILES; mt < mt_end; ++mt) {
+              mbar_wait(&full[r.stage], r.ph);
+              fence_after();
+              const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
+              const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>(pb * 128 + (mt - ps * PASS_TILES) * 16);
+              bool first = true;
+              for (int k = prev.qa; k < prev.qb; ++k) {
+                const uint64_t ad = smem_desc(sa + k * 4096, 2048, 128);
+                mma_bf16(d2, ad, smem_desc(ahi + k * 512, 256, 128), first ? 0u : 1u);
+                mma_bf16(d2, ad, smem_desc(alo + k * 512, 256, 128), 1u);
+                first = false;
+              }
+              mma_commit(&empty[r.stage]);
+              r.advance(ns);
+            }
+            mma_commit(&d2_full[pb]);
+            ++c3;
+          }
+          mma_commit(&at_empty[ab]);
+        }
+        has_prev = more;
+        prev = cur;
+        if (more) more = it.next(cur);
+        ++i;
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (4 warps)
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = tid - 64; // 0..127
+    Phase d1f[2], atf[2], d2f[2];
+    int c3 = 0;
+    int cur_entry = -1, eslot = 1;
+    int seg_slot[2] = {0, 0};
+    // per-entry token data, two slots (entry being drained / entry being fed)
+    auto load_entry = [&](int o, int slot) {
+      named_bar_sync(2, EPI_THREADS);
+      if (et < 16) {
+        gate_s[slot * 16 + et] = 0.f;
+        tok_s[slot * 16 + et] = 0;
+      }
+      named_bar_sync(2, EPI_THREADS);
+      if (et == 0) {
+        int nt = 0;
+        if (o < n_hits) {
+          const int e = a.hit_list[o];
+          const int p0 = a.offsets[e];
+          nt = a.offsets[e + 1] - p0;
+          for (int i = 0; i < nt; ++i) {
+            const int idx = a.perm[p0 + i];
+            tok_s[slot * 16 + i] = idx / a.k;
+            gate_s[slot * 16 + idx / a.k] = a.gates[idx];
+          }
+        } else {
+          nt = T;
+          for (int i = 0; i < T; ++i) {
+            tok_s[slot * 16 + i] = i;
+            gate_s[slot * 16 + i] = 1.f;
+          }
+        }
+        misc[2 + slot] = nt;
+      }
+      named_bar_sync(2, EPI_THREADS);
+      if (a.global_acc) {  // zero this entry's rows of the CTA-exclusive partial block
+        float* P = a.partial + static_cast<long long>(b + o) * T * d;
+        const int nt = misc[2 + slot];
+        for (int t = 0; t < nt; ++t)
+          for (int c = et * 4; c < d; c += EPI_THREADS * 4)
+            *reinterpret_cast<float4*>(P + static_cast<long long>(tok_s[slot * 16 + t]) * d + c) =
+                make_float4(0.f, 0.f, 0.f, 0.f);
+        named_bar_sync(2, EPI_THREADS);
+      }
+    };
+    auto flush = [&](int o, int slot) {
+      named_bar_sync(2, EPI_THREADS);
+      if (!a.global_acc) {
+        const int nt = misc[2 + slot];
+        float* P = a.partial + static_cast<long long>(b + o) * T * d;
+        for (int t = 0; t < nt; ++t) {
+          const int tg = tok_s[slot * 16 + t];
+          for (int c = et * 4; c < d; c += EPI_THREADS * 4) {
+            float4* src = reinterpret_cast<float4*>(ysum + static_cast<size_t>(tg) * d + c);
+            *reinterpret_cast<float4*>(P + static_cast<long long>(tg) * d + c) = *src;
+            *src = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      }
+      named_bar_sync(2, EPI_THREADS);
+    };
+    SegIter it{q0, q1, qpe};
+    Seg cur, prev;
+    bool more = it.next(cur), has_prev = false;
+    int i = 0;
+    while (more || has_prev) {
+      if (more) {
+        // ---- A(i): D1 -> a^T (bf16 hi/lo) for DN(i)
+        if (cur.o != cur_entry) {
+          eslot ^= 1;
+          load_entry(cur.o, eslot);
+          cur_entry = cur.o;
+        }
+        seg_slot[i & 1] = eslot;
+        const float* gs = gate_s + eslot * 16;
+        const int b1 = i & 1;
+        mbar_wait(&d1_full[b1], d1f[b1].bit);
+        d1f[b1].flip();
+        fence_after();
+        float v[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b1 * 16), v);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d1_empty[b1]);
+        const int row = 32 * q + lane;  // D1 row: < 64 gate, >= 64 up
+        if (row >= 64) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) u_s[(row - 64) * 17 + t] = v[t];
+        }
+        const int ab = i & 1;
+        // a^T buffer ab is free once DN(i-2) completed
+        mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);
+        atf[ab].flip();
+        named_bar_sync(2, EPI_THREADS);
+        if (row < 64) {
+          const int f = row;
+          const bool mine = f >= cur.qa * QROWS && f < cur.qb * QROWS;
+          uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
+          uint16_t* lo = hi + 2048;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            float av = 0.f;
+            if (mine) {
+              const float g = v[t];
+              av = g / (1.f + __expf(-g)) * u_s[f * 17 + t] * gs[t];
+            }
+            const uint16_t h16 = f32_to_bf16_rn(av);
+            const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
+            // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
+            const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
+            hi[off] = h16;
+            lo[off] = f32_to_bf16_rn(rem);
+          }
+        }
+        fence_proxy_async();
+        named_bar_sync(2, EPI_THREADS);
+        if (et == 0) mbar_arrive(&at_full[ab]);
+      }
+      if (has_prev) {
+        // ---- D(i-1): D2 passes -> per-expert fp32 accumulator
+        for (int ps = 0; ps < passes; ++ps) {
+          const int pb = c3 & 1;
+          mbar_wait(&d2_full[pb], d2f[pb].bit);
+          d2f[pb].flip();
+          fence_after();
+          const int mt0 = ps * PASS_TILES, mt_end = min(mtiles, mt0 + PASS_TILES);
+          for (int mt = mt0; mt < mt_end; ++mt) {
+            float y[16];
+            tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) +
+                          static_cast<uint32_t>(D2_COL0 + pb * 128 + (mt - mt0) * 16),
+                      y);
+            const int orow = mt * 128 + 32 * q + lane;
+            if (a.global_acc) {
+              float* P = a.partial + static_cast<long long>(b + prev.o) * T * d;
+              for (int t = 0; t < T; ++t) P[static_cast<long long>(t) * d + orow] += y[t];
+            } else {
+#pragma unroll
+              for (int t = 0; t < 16; ++t)
+                if (t < T) ysum[static_cast<size_t>(t) * d + orow] += y[t];
+            }
+          }
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d2_empty[pb]);
+          ++c3;
+        }
+        if (!more || cur.o != prev.o) flush(prev.o, seg_slot[(i - 1) & 1]);
+      }
+      has_prev = more;
+      prev = cur;
+      if (more) more = it.next(cur);
+      ++i;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// h [T][d] bf16 -> h^T image: per K-tile of 64, [tg 2][j 8][r 8][e 8] bf16
+// (token = 8 tg + r, k = 64 kt + 8 j + e), tokens >= T zero.
+__global__ void build_hT_kernel(const uint16_t* __restrict__ h, int T, int d, uint16_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int total = (d / 64) * 1024;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int kt = i >> 10, w = i & 1023;
+    const int tg = w >> 9, j = (w >> 6) & 7, r = (w >> 3) & 7, e = w & 7;
+    const int t = tg * 8 + r, k = kt * 64 + j * 8 + e;
+    out[i] = t < T ? h[static_cast<size_t>(t) * d + k] : static_cast<uint16_t>(0);
+  }
+}
+
+// Standard layouts -> v2 tiled image (see file header).
+__global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uint16_t* __restrict__ wu,
+                                      const uint16_t* __restrict__ wd, int d, int ffn, uint16_t* __restrict__ out) {
+  const long long total = 3LL * ffn * d;
+  const long long chunk = 3LL * FCH * d;
+  const long long gu = 2LL * FCH * d;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = idx / chunk, r0 = idx % chunk;
+    uint16_t v;
+    if (r0 < gu) {
+      const long long kt = r0 / 8192;
+      const int w = static_cast<int>(r0 % 8192);
+      const int g = w >> 9, j = (w >> 6) & 7, r = (w >> 3) & 7, e = w & 7;
+      const int row = g * 8 + r;
+      const long long k = kt * 64 + j * 8 + e;
+      v = row < FCH ? wg[(c * FCH + row) * d + k] : wu[(c * FCH + row - FCH) * d + k];
+    } else {
+      const long long r2 = r0 - gu;
+      const long long mt = r2 / 8192;
+      const int w = static_cast<int>(r2 % 8192);
+      const int j = w >> 10, g = (w >> 6) & 15, r = (w >> 3) & 7, e = w & 7;
+      const long long orow = mt * 128 + g * 8 + r;
+      const long long f = c * FCH + j * 8 + e;
+      v = wd[orow * ffn + f];
+    }
+    out[idx] = v;
+  }
+}
+
+}  // namespace tc
+}  // namespace dev
+
+size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc) {
+  return static_cast<size_t>(n_stages) * dev::tc::STAGE_BYTES + 2 * 2 * 4096 + 64 * 17 * 4 +
+         (global_acc ? 0 : static_cast<size_t>(T) * d * 4) + 2 * 16 * 4 * 2 + 16 + 8 + 8 * (2 * n_stages + 12);
+}
+
+FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit) {
+  for (int ns = 8; ns >= 4; --ns)
+    if (ffn_tc_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_tc_smem_bytes(T, d, ns, false)};
+  for (int ns = 8; ns >= 2; --ns)
+    if (ffn_tc_smem_bytes(T, d, ns, true) <= smem_limit) return {ns, true, ffn_tc_smem_bytes(T, d, ns, true)};
+  return {0, false, 0};
+}
+
+cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(dev::tc::expert_ffn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  return launch_pdl(dev::tc::expert_ffn_tc_kernel, dim3(grid), dim3(dev::tc::THREADS), smem, stream, pdl, a);
+}
+
+cudaError_t launch_build_hT(const uint16_t* h, int T, int d, uint16_t* out, cudaStream_t stream, bool pdl) {
+  return launch_pdl(dev::tc::build_hT_kernel, dim3((d / 64 * 1024 + 255) / 256), dim3(256), 0, stream, pdl, h, T, d,
+                    out);
+}
+
+cudaError_t launch_pack_expert_tc(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
+                                  uint16_t* out, cudaStream_t stream) {
+  dev::tc::pack_expert_tc_kernel<<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, out);
+  return cudaGetLastError();
+}
+
+}  // namespace moespac

@@ -42,6 +42,7 @@ struct FfnArgs {
   float* partial;           // [(grid + N + n_shared)][T][d]
   int n_stages;
   int global_acc;           // 1: accumulate down-proj partials in `partial` (large T*d)
+  const uint16_t* hT;       // tcgen05 variant: h^T UMMA image [d/64][16 tok][64] (build_hT)
 };
 
 struct CombineArgs {
@@ -56,6 +57,7 @@ struct CombineArgs {
   const float* partial;
   float* y_out;             // [T][d] fp32 (may be null)
   uint16_t* h_out;          // [T][d] bf16 (may be null)
+  uint16_t* hT_out;         // optional h^T UMMA image of h_out (next layer's tensor-core K3 operand)
 };
 
 }  // namespace dev
@@ -71,14 +73,34 @@ struct FfnPlan {
 };
 size_t ffn_smem_bytes(int T, int d, int n_stages, bool global_acc);
 FfnPlan ffn_plan(int T, int d, size_t smem_limit);
-cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream);
-cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream);
-cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, int n, cudaStream_t stream);
+cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
+size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc);
+FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit);
+cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
+cudaError_t launch_build_hT(const uint16_t* h, int T, int d, uint16_t* out, cudaStream_t stream, bool pdl = false);
+cudaError_t launch_pack_expert_tc(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
+                                  uint16_t* out, cudaStream_t stream);
+cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream, bool pdl = false);
+cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, uint16_t* hT_out, int d, int n,
+                            cudaStream_t stream, bool pdl = false);
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream);
 cudaError_t launch_fill_synthetic(uint16_t* out, long long n, uint64_t seed, float stdv, cudaStream_t stream);
 
 constexpr int kFfnMaxTokens = 16;
 constexpr int kFfnChunkRows = 16;
+
+// K3 variants: the tensor-core kernel (tcgen05/TMEM, image layout v2:
+// d % 128 == 0, ffn % 64 == 0) and the CUDA-core GEMV (layout v1:
+// d % 512 == 0, ffn % 16 == 0). 0 picks tcgen05 when the shape allows.
+enum FfnKernel { kFfnAuto = 0, kFfnCudaCore = 1, kFfnTensorCore = 2 };
+inline int ffn_resolve(int kernel, int d, int ffn) {
+  if (kernel == kFfnAuto) return (d % 128 == 0 && ffn % 64 == 0) ? kFfnTensorCore : kFfnCudaCore;
+  return kernel;
+}
+inline bool ffn_shape_ok(int kernel, int d, int ffn) {
+  return kernel == kFfnTensorCore ? (d % 128 == 0 && ffn % 64 == 0 && d >= 128)
+                                  : (d % 512 == 0 && ffn % 16 == 0 && ffn > 0);
+}
 
 }  // namespace moespac

@@ -39,19 +39,20 @@ def _experts(rng, L, N, d, ffn, units):
     return std, shared
 
 
-def _pack(w):
-    return abi.pack_expert(*[torch.from_numpy(x.view(np.int16)).cuda() for x in w])
+def _pack(w, kernel):
+    return abi.pack_expert(*[torch.from_numpy(x.view(np.int16)).cuda() for x in w], kernel=kernel)
 
 
-def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared):
+def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel=abi.FFN_AUTO):
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache)
-    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, gate_mode), cfg)
+    kernel = abi.ffn_resolve(kernel, d, ffn)
+    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, gate_mode, kernel), cfg)
     arena = ctx.host_arena(L * N)
     for (l, e), w in std.items():
-        arena[l * N + e] = _pack(w).cpu().numpy().view(np.uint16)
+        arena[l * N + e] = _pack(w, kernel).cpu().numpy().view(np.uint16)
     for l in range(L):
         if units:
-            ctx.set_shared(l, torch.stack([_pack(w) for w in shared[l]]))
+            ctx.set_shared(l, torch.stack([_pack(w, kernel) for w in shared[l]]))
     ctx.finalize()
     return ctx, cfg
 
@@ -60,16 +61,18 @@ def _resident(rb, l, N):
     return [e for e in range(N) if (int(rb[l, e >> 5]) >> (e & 31)) & 1]
 
 
-@pytest.mark.parametrize("L,N,k,g,d,ffn,units,gate_mode,cache", [
-    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25),
-    (2, 8, 2, 4, 512, 128, 0, 0, 0.17),
-    (2, 32, 8, 8, 2048, 48, 0, 0, 0.5),
+@pytest.mark.parametrize("L,N,k,g,d,ffn,units,gate_mode,cache,kernel", [
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_CUDACORE),
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_TENSOR),
+    (2, 8, 2, 4, 512, 128, 0, 0, 0.17, abi.FFN_TENSOR),
+    (2, 32, 8, 8, 2048, 48, 0, 0, 0.5, abi.FFN_CUDACORE),
+    (2, 32, 8, 8, 2048, 128, 0, 0, 0.5, abi.FFN_TENSOR),
 ])
-def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache):
+def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache, kernel):
     ref_or_skip()
     rng = np.random.default_rng(L * 100 + N)
     std, shared = _experts(rng, L, N, d, ffn, units)
-    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared)
+    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel)
     T = g + 1
     steps = 10
     gen = O.Generator(L, N, k, g, seed=1)
@@ -90,7 +93,7 @@ def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate
         hs = abi.fetch(v.h_dev, (L + 1, T, d), np.uint16)
         ys = abi.fetch(v.y_dev, (L, T, d), np.float32)
         assert np.array_equal(hs[0], h0) and np.array_equal(hs[L], h_out)
-        _, rb, _, _ = ctx.sched_tables()
+        _, rb, _, _ = ctx.step_tables()
         for l in range(L):
             _, gates = O.router_topk(logits[l], k, gate_mode)
             res = _resident(rb, l, N)
@@ -144,9 +147,9 @@ def test_step_argument_errors():
     L, N, k, g, d, ffn = 1, 8, 2, 4, 512, 32
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=1.0)
     with pytest.raises(abi.MoespacError) as ei:
-        abi.Context(0, abi.ModelDesc(L, N, k, g, 500, ffn, 0, 0), cfg)  # d % 512
+        abi.Context(0, abi.ModelDesc(L, N, k, g, 500, ffn, 0, 0, abi.FFN_CUDACORE), cfg)  # d % 512
     assert ei.value.code == "E_INVALID"
-    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, 0, 0), cfg)
+    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, 0, 0, abi.FFN_CUDACORE), cfg)
     logits = np.zeros((L, g + 1, N))
     h = np.zeros((g + 1, d), np.uint16)
     with pytest.raises(abi.MoespacError) as ei:

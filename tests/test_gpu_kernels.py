@@ -132,12 +132,21 @@ def _rand_experts(rng, n, d, ffn, std=0.02):
     return out
 
 
-def _pack(experts):
+def _pack(experts, kernel=abi.FFN_AUTO):
     imgs = []
     for wg, wu, wd in experts:
         t = [torch.from_numpy(x.view(np.int16)).cuda() for x in (wg, wu, wd)]
-        imgs.append(abi.pack_expert(*t))
+        imgs.append(abi.pack_expert(*t, kernel=kernel))
     return torch.stack(imgs)
+
+
+def _kernels(d, ffn):
+    ks = []
+    if d % 512 == 0 and ffn % 16 == 0:
+        ks.append(abi.FFN_CUDACORE)
+    if d % 128 == 0 and ffn % 64 == 0:
+        ks.append(abi.FFN_TENSOR)
+    return ks
 
 
 @pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
@@ -154,8 +163,15 @@ def _pack(experts):
     (8, 2, 5, 4096, 128, 0, 0, 1.0),      # Mixtral d
     (60, 4, 7, 2048, 1408, 4, 1, 0.5),    # Qwen1.5 shape
     (128, 8, 9, 2048, 768, 0, 0, 0.6),    # Qwen3 shape
+    (8, 2, 5, 4096, 256, 0, 0, 1.0),      # Mixtral d, tensor-core eligible
+    (16, 4, 16, 1024, 128, 1, 0, 0.7),    # T = 16 (N fully used)
+    (16, 4, 9, 128, 64, 0, 0, 1.0),       # smallest tensor-core shape
+    (64, 6, 9, 2048, 1408, 2, 1, 0.3),    # DeepSeek-V2-Lite shape
 ])
-def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_frac):
+@pytest.mark.parametrize("kernel", [abi.FFN_CUDACORE, abi.FFN_TENSOR], ids=["cudacore", "tensor"])
+def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel):
+    if kernel not in _kernels(d, ffn):
+        pytest.skip("shape not supported by this kernel variant")
     rng = np.random.default_rng(N * 7 + T)
     experts = _rand_experts(rng, N, d, ffn)
     shared = _rand_experts(rng, n_shared, d, ffn)
@@ -166,8 +182,8 @@ def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_f
     # device inputs
     lg = torch.from_numpy(logits).cuda()
     ids, gates = abi.router_topk(lg, k, gate_mode)
-    pool = _pack(experts)
-    shared_t = _pack(shared) if n_shared else torch.zeros(1, dtype=torch.int16, device="cuda")
+    pool = _pack(experts, kernel)
+    shared_t = _pack(shared, kernel) if n_shared else torch.zeros(1, dtype=torch.int16, device="cuda")
     slot_of = torch.arange(N, dtype=torch.int32, device="cuda")
     W = (N + 31) // 32
     rb = torch.from_numpy(_bits(resident[None]).view(np.int32)).cuda()
@@ -185,9 +201,10 @@ def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_f
     ws = torch.empty(abi.lib().moespac_ffn_workspace_bytes(T, d, N, n_shared, grid) // 4, dtype=torch.float32,
                      device="cuda")
     h_t = torch.from_numpy(h.view(np.int16)).cuda()
+    hT = abi.build_hT(h_t)
     fa = abi.FfnArgs(abi.ptr(h_t), T, d, ffn, k, N, abi.ptr(bufs["perm"]), abi.ptr(bufs["offsets"]), abi.ptr(gates),
                      abi.ptr(bufs["hl"]), abi.ptr(bufs["cnt"]), abi.ptr(slot_of), abi.ptr(pool), abi.ptr(shared_t),
-                     n_shared, abi.ptr(ws), grid)
+                     n_shared, abi.ptr(ws), grid, kernel, abi.ptr(hT))
     abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), s0))
     y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
     h_out = torch.zeros((T, d), dtype=torch.int16, device="cuda")
@@ -203,11 +220,12 @@ def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_f
     _check_bf16_residual(h, y_ref, h_out.cpu().numpy().view(np.uint16))
 
 
-def test_expert_ffn_deterministic():
+@pytest.mark.parametrize("kernel", [abi.FFN_CUDACORE, abi.FFN_TENSOR], ids=["cudacore", "tensor"])
+def test_expert_ffn_deterministic(kernel):
     import ctypes
     rng = np.random.default_rng(11)
     N, k, T, d, ffn = 16, 4, 9, 2048, 128
-    pool = _pack(_rand_experts(rng, N, d, ffn))
+    pool = _pack(_rand_experts(rng, N, d, ffn), kernel)
     ids, gates = abi.router_topk(torch.from_numpy(rng.normal(0, 1, (T, N))).cuda(), k, 0)
     h_t = torch.from_numpy(O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32)).view(np.int16)).cuda()
     slot_of = torch.arange(N, dtype=torch.int32, device="cuda")
@@ -223,9 +241,10 @@ def test_expert_ffn_deterministic():
                         abi.ptr(bufs["hl"]), abi.ptr(bufs["ho"]), abi.ptr(bufs["cnt"]), abi.ptr(bufs["sc"]))
         abi.check(abi.lib().moespac_hist_scan_observe(ctypes.byref(a2), abi._stream(None)))
         ws = torch.full((abi.lib().moespac_ffn_workspace_bytes(T, d, N, 0, 148) // 4,), float("nan"), device="cuda")
+        hT = abi.build_hT(h_t)
         fa = abi.FfnArgs(abi.ptr(h_t), T, d, ffn, k, N, abi.ptr(bufs["perm"]), abi.ptr(bufs["offsets"]),
                          abi.ptr(gates), abi.ptr(bufs["hl"]), abi.ptr(bufs["cnt"]), abi.ptr(slot_of), abi.ptr(pool),
-                         None, 0, abi.ptr(ws), 148)
+                         None, 0, abi.ptr(ws), 148, kernel, abi.ptr(hT))
         abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
         y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
         ca = abi.CombineArgs(None, None, T, d, ffn, k, abi.ptr(ids), abi.ptr(bufs["ho"]), abi.ptr(bufs["cnt"]), 0,
