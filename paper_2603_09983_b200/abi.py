@@ -83,7 +83,7 @@ class FfnArgs(C.Structure):
                 ("offsets_dev", C.c_void_p), ("gates_dev", C.c_void_p), ("hit_list_dev", C.c_void_p),
                 ("counters_dev", C.c_void_p), ("slot_of_dev", C.c_void_p), ("pool_dev", C.c_void_p),
                 ("shared_dev", C.c_void_p), ("n_shared_units", C.c_int32), ("workspace_dev", C.c_void_p),
-                ("grid", C.c_int32), ("kernel", C.c_int32), ("hT_dev", C.c_void_p)]
+                ("grid", C.c_int32), ("kernel", C.c_int32), ("hT_dev", C.c_void_p), ("debug_ts_dev", C.c_void_p)]
 
 
 class CombineArgs(C.Structure):
@@ -186,7 +186,7 @@ def header_functions() -> list[str]:
     """Every function the public header declares."""
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(moespac_[a-z0-9_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(moespac_[A-Za-z0-9_]+)\s*\(", txt)))
 
 
 def check(status: int) -> None:

@@ -468,6 +468,7 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.n_stages = plan.n_stages;
     f.global_acc = plan.global_acc ? 1 : 0;
     f.hT = a->hT_dev;
+    f.dbg = reinterpret_cast<unsigned long long*>(a->debug_ts_dev);
     const int grid = a->grid > 0 ? a->grid : device_sms();
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_ok(kern == kFfnTensorCore ? launch_expert_ffn_tc(f, grid, plan.smem, st) : launch_expert_ffn(f, grid, plan.smem, st),

@@ -124,6 +124,14 @@ struct SegIter {
   }
 };
 
+__device__ __forceinline__ void stamp(const FfnArgs& a, int slot) {
+  if (a.dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[blockIdx.x * 8 + slot] = t;
+  }
+}
+
 __device__ __forceinline__ const uint16_t* entry_weights(const FfnArgs& a, int o, int n_hits) {
   if (o < n_hits) return a.pool + static_cast<long long>(a.slot_of[a.hit_list[o]]) * a.expert_elems;
   return a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
@@ -164,6 +172,10 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   uint64_t* d2_empty = d2_full + 2; // [2]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    stamp(a, 0);
+    if (a.dbg) a.dbg[blockIdx.x * 8 + 7] = static_cast<unsigned long long>(clock64());
+  }
   const int n_hits = a.counters[7];
   const long long n = static_cast<long long>(n_hits + a.n_shared) * qpe;
   const int G = gridDim.x, b = blockIdx.x;
@@ -199,7 +211,10 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   __syncthreads();
   fence_after();
   const uint32_t tmem = static_cast<uint32_t>(misc[1]);
-  if (tid == 0) pdl_trigger();  // the combine may launch and park on its own wait
+  if (tid == 0) {
+    pdl_trigger();  // the combine may launch and park on its own wait
+    stamp(a, 1);
+  }
   // Everything below except the producer's first weight copies depends on
   // the previous kernel (h^T image, partial workspace): wait for it.
   if (warp != 0) pdl_wait();
@@ -296,6 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
           for (int kt = 0; kt < ktiles; ++kt) {
             mbar_wait(&full[r.stage], r.ph);
+            if (i == 0 && kt == 0) stamp(a, 2);
             fence_after();
             const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
 #pragma unroll
@@ -306,6 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
             r.advance(ns);
           }
           mma_commit(&d1_full[b1]);
+          if (i == 0) stamp(a, 3);
         }
         if (has_prev) {  // DN(i-1): D2 = W_down x a^T(i-1), hi + lo
           const int ab = (i - 1) & 1;
@@ -464,7 +481,10 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         }
         fence_proxy_async();
         named_bar_sync(2, EPI_THREADS);
-        if (et == 0) mbar_arrive(&at_full[ab]);
+        if (et == 0) {
+          mbar_arrive(&at_full[ab]);
+          if (i == 0) stamp(a, 4);
+        }
       }
       if (has_prev) {
         // ---- D(i-1): D2 passes -> per-expert fp32 accumulator
@@ -502,8 +522,13 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
       ++i;
     }
   }
+  if (tid == 64) stamp(a, 5);  // epilogue finished (all flushes written)
   fence_before();
   __syncthreads();
+  if (tid == 0) {
+    stamp(a, 6);
+    if (a.dbg) a.dbg[blockIdx.x * 8 + 7] = static_cast<unsigned long long>(clock64()) - a.dbg[blockIdx.x * 8 + 7];
+  }
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));

@@ -43,6 +43,7 @@ struct FfnArgs {
   int n_stages;
   int global_acc;           // 1: accumulate down-proj partials in `partial` (large T*d)
   const uint16_t* hT;       // tcgen05 variant: h^T UMMA image [d/64][16 tok][64] (build_hT)
+  unsigned long long* dbg;  // optional per-CTA %globaltimer stamps [grid][8] (profiling)
 };
 
 struct CombineArgs {

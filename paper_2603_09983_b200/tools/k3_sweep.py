@@ -1,0 +1,101 @@
+"""K3 microbenchmark: time vs number of activated resident experts.
+
+Separates the per-launch fixed cost from the streaming bandwidth of the
+expert-FFN kernels (both variants) through the stateless C ABI:
+    python -m paper_2603_09983_b200.tools.k3_sweep --d 2048 --ffn 768 --T 9
+Prints one JSON line per (kernel, n_experts).
+"""
+import argparse
+import ctypes
+import json
+
+import torch
+
+from paper_2603_09983_b200 import abi
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--d", type=int, default=2048)
+    ap.add_argument("--ffn", type=int, default=768)
+    ap.add_argument("--T", type=int, default=9)
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--N", type=int, default=128)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--experts", default="1,2,4,8,16,32,64,128")
+    ap.add_argument("--kernels", default="2,1")
+    ap.add_argument("--stamps", action="store_true", help="dump per-CTA timeline (tensor-core kernel)")
+    args = ap.parse_args()
+    d, ffn, T, k, N = args.d, args.ffn, args.T, args.k, args.N
+    dev = torch.device("cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    img = 3 * d * ffn
+    pool = torch.empty(N * img, dtype=torch.int16, device=dev)
+    abi.check(abi.lib().moespac_fill_synthetic(abi.ptr(pool), pool.numel(), 7, 0.02, abi._stream(None)))
+    h = (torch.randn(T, d, device=dev) * 1.0).to(torch.bfloat16).view(torch.int16)
+    hT = abi.build_hT(h)
+    ws = torch.empty(abi.lib().moespac_ffn_workspace_bytes(T, d, N, 0, sms) // 4, device=dev)
+    slot_of = torch.arange(N, dtype=torch.int32, device=dev)
+    for kern in [int(x) for x in args.kernels.split(",")]:
+        if abi.ffn_resolve(kern, d, ffn) != kern:
+            continue
+        for ne in [int(x) for x in args.experts.split(",")]:
+            ne = min(ne, N)
+            # routing: token t picks experts (t*k + j) % ne -> min(ne, T*k) distinct
+            ids = torch.tensor([sorted({(t * k + j) % ne for j in range(k)}) for t in range(T)], dtype=torch.int32)
+            kk = ids.shape[1]
+            ids = ids.to(dev)
+            gates = torch.full((T, kk), 1.0 / kk, device=dev)
+            bufs = {n: torch.zeros(s, dtype=torch.int32, device=dev) for n, s in
+                    [("freqs", N), ("offsets", N + 1), ("perm", T * kk), ("hl", N), ("ho", N), ("cnt", 8), ("sc", N)]}
+            rb = torch.full(((N + 31) // 32,), -1, dtype=torch.int32, device=dev)
+            taus = torch.ones(1, dtype=torch.int32, device=dev)
+            st = torch.zeros((N, 4), dtype=torch.int32, device=dev)
+            a2 = abi.K2Args(abi.ptr(ids), 1, T, kk, N, abi.ptr(rb), None, abi.ptr(taus), abi.ptr(st), 4, 1, 0.1, 0, 1,
+                            abi.ptr(bufs["freqs"]), abi.ptr(bufs["offsets"]), abi.ptr(bufs["perm"]),
+                            abi.ptr(bufs["hl"]), abi.ptr(bufs["ho"]), abi.ptr(bufs["cnt"]), abi.ptr(bufs["sc"]))
+            abi.check(abi.lib().moespac_hist_scan_observe(ctypes.byref(a2), abi._stream(None)))
+            torch.cuda.synchronize()
+            n_hit = int(bufs["cnt"][7].item())
+            fa = abi.FfnArgs(abi.ptr(h), T, d, ffn, kk, N, abi.ptr(bufs["perm"]), abi.ptr(bufs["offsets"]),
+                             abi.ptr(gates), abi.ptr(bufs["hl"]), abi.ptr(bufs["cnt"]), abi.ptr(slot_of),
+                             abi.ptr(pool), None, 0, abi.ptr(ws), sms, kern, abi.ptr(hT))
+            for _ in range(3):
+                abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # back-to-back launches (as in the engine): host-side call overhead
+            # overlaps device execution and drops out of the average
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(args.iters):
+                abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / args.iters
+            byts = n_hit * img * 2
+            if args.stamps and kern == 2:
+                dbg = torch.zeros((sms, 8), dtype=torch.int64, device=dev)
+                fa.debug_ts_dev = abi.ptr(dbg)
+                abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
+                torch.cuda.synchronize()
+                fa.debug_ts_dev = None
+                t = dbg.cpu().numpy().astype("float64")
+                act = t[:, 1] > 0
+                t0 = t[act, 0].min()
+                rel = (t[act] - t0) / 1e3
+                rel[t[act] == 0] = float("nan")
+                rel = rel[:, :7]
+                import numpy as np
+                names = ["entry", "prologue", "first_data", "gu0_issued", "a0_ready", "epi_done", "end"]
+                summ = {nm: [round(float(np.nanmin(rel[:, j])), 2), round(float(np.nanmedian(rel[:, j])), 2),
+                             round(float(np.nanmax(rel[:, j])), 2)] for j, nm in enumerate(names)}
+                cyc = t[act, 7]
+                print(json.dumps({"stamps_us_min_med_max": summ, "active_ctas": int(act.sum()),
+                                  "cta_clock64_cycles_med_max": [float(np.median(cyc)), float(cyc.max())],
+                                  "entry_spread_us": round(float(np.nanmax(rel[:, 0])), 2)}), flush=True)
+            print(json.dumps({"kernel": kern, "experts": n_hit, "tokens": T, "d": d, "ffn": ffn, "us": round(us, 2),
+                              "MB": round(byts / 1e6, 1), "GBps": round(byts / us / 1e3, 1)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

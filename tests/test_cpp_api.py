@@ -1,0 +1,18 @@
+"""The reference's unit-test scenarios for the scheduling primitives, run
+against the B200 build's C++ operator API (tests/cpp/test_operator_api.cpp).
+CPU only: compiles with g++ against csrc/host/scheduler.{hpp,cpp}."""
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HOST = os.path.join(ROOT, "paper_2603_09983_b200", "csrc", "host")
+
+
+def test_operator_api_scenarios(tmp_path):
+    exe = tmp_path / "test_operator_api"
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-ffp-contract=off", "-I", HOST,
+                           os.path.join(ROOT, "tests", "cpp", "test_operator_api.cpp"),
+                           os.path.join(HOST, "scheduler.cpp"), "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failures" in r.stdout
