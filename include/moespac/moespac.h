@@ -89,7 +89,11 @@ typedef struct moespac_step_report {
   /* algorithmic K3 bytes this step on this rank: (local hit experts + shared
    * units) x image bytes, summed over layers; and the kernel launches issued */
   int64_t ffn_bytes, h2d_bytes, d2h_bytes;
-  int32_t kernel_launches, _pad;
+  int32_t kernel_launches;
+  /* cold path: (layer, expert) misses computed on the host cores this step
+   * and the host time spent on them */
+  int32_t cold_experts;
+  float cpu_ms_cold, _pad;
 } moespac_step_report;
 
 /* Realized split of one layer (core/src/sim_core.cpp:233-283), as K2 emits it. */
@@ -279,6 +283,11 @@ moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* unique_id128, in
  * timing is on, layer kernels are launched without programmatic dependent
  * launch so each K3 event pair brackets exactly that kernel. */
 moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
+/* Host threads for the cold-expert path (activations whose expert is not
+ * resident are computed on the CPU from the pinned arena, in parallel with
+ * the device, and added by the combine): -1 = all cores (default), 0 = off
+ * (misses are counted but not computed). Takes effect at moespac_ctx_finalize. */
+moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
 /* Programmatic dependent launch between layer kernels (on by default). */
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a

@@ -59,7 +59,8 @@ class StepReport(C.Structure):
                 ("gpu_ms_total", C.c_float), ("gpu_ms_router", C.c_float), ("gpu_ms_hist", C.c_float),
                 ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float),
                 ("ffn_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("kernel_launches", C.c_int32), ("_pad", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("cold_experts", C.c_int32), ("cpu_ms_cold", C.c_float),
+                ("_pad", C.c_float)]
 
 
 class LayerOutcome(C.Structure):
@@ -164,6 +165,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
         "moespac_step": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_ctx_get_views": (C.c_int, [vp, C.POINTER(CtxViews)]),
@@ -412,6 +414,9 @@ class Context:
 
     def set_timing(self, on: bool = True):
         check(lib().moespac_ctx_set_timing(self._h, int(on)))
+
+    def set_cold_threads(self, n: int = -1):
+        check(lib().moespac_ctx_set_cold_threads(self._h, n))
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))

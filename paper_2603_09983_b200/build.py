@@ -32,11 +32,12 @@ SOURCES = [
     "host/step_scheduler.cpp",
     "host/engine.cpp",
     "host/trace_synth.cpp",
+    "host/cold_executor.cpp",
     "abi.cpp",
 ]
 HEADERS = [
     "kernels/common.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
-    "host/engine.hpp", "host/trace_synth.hpp",
+    "host/engine.hpp", "host/trace_synth.hpp", "host/cold_executor.hpp",
 ]
 
 
@@ -64,6 +65,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(sp), hdr_time):
             flags = COMMON + (CU_FLAGS if src.endswith(".cu") else ["-x", "c++", "-Wno-deprecated-gpu-targets"])
+            if src.endswith("cold_executor.cpp"):  # host fp32 SwiGLU loops: let them vectorise
+                flags = flags + ["-Xcompiler", "-mavx2,-mfma,-fno-math-errno,-fassociative-math,-fno-signed-zeros,-fno-trapping-math"]
             jobs.append(([nvcc] + flags + ["-c", sp, "-o", obj], src))
 
     def run(job):

@@ -561,6 +561,10 @@ moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_timing(enabled != 0); });
 }
 
+moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads) {
+  return guard([&] { c->e.set_cold_threads(threads); });
+}
+
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_pdl(enabled != 0); });
 }

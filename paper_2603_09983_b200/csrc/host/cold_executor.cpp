@@ -1,0 +1,177 @@
+// Cold-expert executor — see cold_executor.hpp. Compiled with
+// -O3 -mavx2 -mfma (build.py) so the fp32 dot/axpy loops vectorise; reads
+// the expert images in their device tile order (no host-side relayout), so
+// a miss costs exactly one pass over the expert's bytes in host DRAM.
+#include "cold_executor.hpp"
+
+#include <cmath>
+#include <cstring>
+
+namespace moespac {
+
+namespace {
+
+inline float bf(uint16_t b) {
+  uint32_t u = static_cast<uint32_t>(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+inline float silu(float x) { return x / (1.f + std::exp(-x)); }
+
+}  // namespace
+
+ColdExecutor::ColdExecutor(int threads, int layout, int d, int ffn, int T)
+    : layout_(layout), d_(d), ffn_(ffn), T_(T), rows_(layout == 2 ? 64 : 16) {
+  if (threads < 1) threads = 1;
+  part_.assign(static_cast<size_t>(threads), std::vector<float>(static_cast<size_t>(T) * d));
+  scratch_.assign(static_cast<size_t>(threads), std::vector<float>());
+  hf_.assign(static_cast<size_t>(T) * d, 0.f);
+  for (int w = 1; w < threads; ++w) workers_.emplace_back([this, w] {
+      int seen = 0;
+      for (;;) {
+        {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+          if (stop_) return;
+          seen = gen_;
+        }
+        work(w);
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_cv_.notify_all();
+      }
+    });
+}
+
+ColdExecutor::~ColdExecutor() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  for (auto& t : workers_) t.join();
+}
+
+// One chunk of one expert: gate/up rows -> a = silu(g) * u * gate -> down.
+void ColdExecutor::chunk(const ColdItem& it, int c, const float* hf, float* y, std::vector<float>& scr) const {
+  const int d = d_, R = rows_, n = it.n_tok;
+  scr.resize(static_cast<size_t>(2 * R) * 16 + static_cast<size_t>(d));
+  float* acc = scr.data();        // [2R][16] gate rows then up rows, per token
+  float* wrow = acc + 2 * R * 16;  // one unpacked row [d] (or [64] for layout 2 runs)
+  std::memset(acc, 0, sizeof(float) * 2 * R * 16);
+  const uint16_t* base = it.image + static_cast<size_t>(c) * 3 * R * d;
+  if (layout_ == 2) {
+    // gate|up K-tiles [128 rows][64 k]: element (row, kk) at
+    // (row>>3)*512 + (kk>>3)*64 + (row&7)*8 + (kk&7)
+    for (int kt = 0; kt < d / 64; ++kt) {
+      const uint16_t* tile = base + static_cast<size_t>(kt) * 8192;
+      for (int row = 0; row < 128; ++row) {
+        float w[64];
+        const uint16_t* rp = tile + (row >> 3) * 512 + (row & 7) * 8;
+        for (int j = 0; j < 8; ++j)
+          for (int e = 0; e < 8; ++e) w[j * 8 + e] = bf(rp[j * 64 + e]);
+        float* ar = acc + row * 16;
+        for (int i = 0; i < n; ++i) {
+          const float* hv = hf + static_cast<size_t>(it.tok[i]) * d + kt * 64;
+          float s = 0.f;
+          for (int k = 0; k < 64; ++k) s += w[k] * hv[k];
+          ar[i] += s;
+        }
+      }
+    }
+  } else {
+    // gate|up tiles [32 rows][256 cols] row-major: rows 0-15 gate, 16-31 up
+    for (int ct = 0; ct < d / 256; ++ct) {
+      const uint16_t* tile = base + static_cast<size_t>(ct) * 8192;
+      for (int row = 0; row < 32; ++row) {
+        float w[256];
+        for (int k = 0; k < 256; ++k) w[k] = bf(tile[row * 256 + k]);
+        float* ar = acc + row * 16;
+        for (int i = 0; i < n; ++i) {
+          const float* hv = hf + static_cast<size_t>(it.tok[i]) * d + ct * 256;
+          float s = 0.f;
+          for (int k = 0; k < 256; ++k) s += w[k] * hv[k];
+          ar[i] += s;
+        }
+      }
+    }
+  }
+  // a[f][i] (stored over the gate accumulators)
+  for (int f = 0; f < R; ++f)
+    for (int i = 0; i < n; ++i) acc[f * 16 + i] = silu(acc[f * 16 + i]) * acc[(R + f) * 16 + i] * it.gate[i];
+  if (layout_ == 2) {
+    // down M-tiles [128 out][64 f]: element (o, f) at (f>>3)*1024 + (o>>3)*64 + (o&7)*8 + (f&7)
+    const uint16_t* dbase = base + static_cast<size_t>(d / 64) * 8192;
+    for (int mt = 0; mt < d / 128; ++mt) {
+      const uint16_t* tile = dbase + static_cast<size_t>(mt) * 8192;
+      for (int o = 0; o < 128; ++o) {
+        float w[64];
+        const uint16_t* rp = tile + (o >> 3) * 64 + (o & 7) * 8;
+        for (int j = 0; j < 8; ++j)
+          for (int e = 0; e < 8; ++e) w[j * 8 + e] = bf(rp[j * 1024 + e]);
+        const int orow = mt * 128 + o;
+        for (int i = 0; i < n; ++i) {
+          float s = 0.f;
+          for (int f = 0; f < 64; ++f) s += w[f] * acc[f * 16 + i];
+          y[static_cast<size_t>(it.tok[i]) * d + orow] += s;
+        }
+      }
+    }
+  } else {
+    // down tiles of W_down^T: [DR f-rows][DW out cols]
+    const int DW = d < 1024 ? d : 1024, DR = 8192 / DW, nrg = 16 / DR;
+    const uint16_t* dbase = base + static_cast<size_t>(d / 256) * 8192;
+    for (int t2 = 0; t2 < d / 512; ++t2) {
+      const uint16_t* tile = dbase + static_cast<size_t>(t2) * 8192;
+      const int ct2 = t2 / nrg, fg = t2 % nrg;
+      for (int row = 0; row < DR; ++row) {
+        const int f = fg * DR + row;
+        for (int col = 0; col < DW; ++col) wrow[col] = bf(tile[row * DW + col]);
+        for (int i = 0; i < n; ++i) {
+          const float av = acc[f * 16 + i];
+          float* yr = y + static_cast<size_t>(it.tok[i]) * d + ct2 * DW;
+          for (int col = 0; col < DW; ++col) yr[col] += wrow[col] * av;
+        }
+      }
+    }
+  }
+}
+
+void ColdExecutor::work(int w) {
+  std::vector<float>& part = part_[static_cast<size_t>(w)];
+  std::fill(part.begin(), part.end(), 0.f);
+  const int W = threads();
+  for (size_t u = static_cast<size_t>(w); u < units_.size(); u += static_cast<size_t>(W))
+    chunk((*items_)[static_cast<size_t>(units_[u].first)], units_[u].second, hf_.data(), part.data(),
+          scratch_[static_cast<size_t>(w)]);
+}
+
+void ColdExecutor::run(const std::vector<ColdItem>& items, const uint16_t* h, float* y) {
+  const size_t TD = static_cast<size_t>(T_) * d_;
+  for (size_t i = 0; i < TD; ++i) hf_[i] = bf(h[i]);
+  units_.clear();
+  const int cpe = ffn_ / rows_;
+  for (size_t i = 0; i < items.size(); ++i)
+    for (int c = 0; c < cpe; ++c) units_.emplace_back(static_cast<int>(i), c);
+  items_ = &items;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    pending_ = static_cast<int>(workers_.size());
+    ++gen_;
+  }
+  cv_.notify_all();
+  work(0);
+  {
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+  }
+  // fixed-order reduction over workers
+  std::memcpy(y, part_[0].data(), sizeof(float) * TD);
+  for (size_t w = 1; w < part_.size(); ++w) {
+    const float* p = part_[w].data();
+    for (size_t i = 0; i < TD; ++i) y[i] += p[i];
+  }
+}
+
+}  // namespace moespac

@@ -1,0 +1,54 @@
+// Cold-expert executor: the CPU side of the Heterogeneous Workload
+// Balancer's split (§3.3, Eq. 7: T_cpu = r_c(τ)·γ·k·T_cpu_unit;
+// the reference models it as miss_tokens·t_cpu_unit, sim_core.cpp:253).
+// Activations whose expert is not HBM-resident this step are computed here,
+// on all host cores, straight from the pinned master-copy image (the same
+// tiled image the copy engine would upload), while the GPU runs the
+// resident experts of the same layer; the fp32 result is added to the
+// layer output by the combine kernel (y_extra).
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace moespac {
+
+struct ColdItem {
+  const uint16_t* image;  // tiled expert image (host)
+  int n_tok;
+  int tok[16];
+  float gate[16];
+};
+
+class ColdExecutor {
+ public:
+  // layout: 1 = CUDA-core image (16-row chunks), 2 = tensor-core image (64-row chunks)
+  ColdExecutor(int threads, int layout, int d, int ffn, int T);
+  ~ColdExecutor();
+  // y[T][d] = sum over items of gate * SwiGLU(h[tok]); h: bf16 [T][d].
+  // Deterministic: fixed work partition, fixed reduction order.
+  void run(const std::vector<ColdItem>& items, const uint16_t* h, float* y);
+  int threads() const { return static_cast<int>(workers_.size()) + 1; }
+
+ private:
+  void work(int w);
+  void chunk(const ColdItem& it, int c, const float* hf, float* y, std::vector<float>& scratch) const;
+  int layout_, d_, ffn_, T_, rows_;
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  int gen_ = 0, pending_ = 0;
+  bool stop_ = false;
+  // current job
+  const std::vector<ColdItem>* items_ = nullptr;
+  std::vector<float> hf_;                 // [T][d] fp32
+  std::vector<std::vector<float>> part_;  // per worker [T][d]
+  std::vector<std::vector<float>> scratch_;
+  std::vector<std::pair<int, int>> units_;  // (item, chunk)
+};
+
+}  // namespace moespac

@@ -14,11 +14,14 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "../kernels/launch.hpp"
+#include "cold_executor.hpp"
 
 namespace moespac {
 
@@ -149,6 +152,16 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaMemset(hT_d_, 0, sizeof(uint16_t) * 2 * 16 * d), "memset hT");  // token pad rows stay zero
   work_bytes_ = static_cast<size_t>(sms_ + N + m.n_shared_units) * T_ * d * 4;
   dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
+  dmalloc(reinterpret_cast<void**>(&ycold_d_), sizeof(float) * L * T_ * d, "cudaMalloc ycold");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocDefault),
+        "cudaHostAlloc");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&hcold_h_), sizeof(uint16_t) * (L + 1) * T_ * d, cudaHostAllocDefault),
+        "cudaHostAlloc");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&route_h_), (sizeof(int32_t) + sizeof(float)) * L * T_ * k,
+                      cudaHostAllocDefault),
+        "cudaHostAlloc");
+  h_ready_.resize(static_cast<size_t>(L + 1));
+  for (auto& ev : h_ready_) check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync), "event");
   tables_bytes_ = sizeof(uint32_t) * 2 * L * W_ + sizeof(int32_t) * L + sizeof(int32_t) * L * N;
   dmalloc(reinterpret_cast<void**>(&tables_d_), tables_bytes_, "cudaMalloc tables");
   out_bytes_ = sizeof(int32_t) * (L * N + L * 8);
@@ -189,7 +202,13 @@ Engine::~Engine() {
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
                   static_cast<void*>(out_d_)})
     if (p) cudaFree(p);
+  cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
+  if (ycold_h_) cudaFreeHost(ycold_h_);
+  if (hcold_h_) cudaFreeHost(hcold_h_);
+  if (route_h_) cudaFreeHost(route_h_);
+  if (ycold_d_) cudaFree(ycold_d_);
+  for (auto ev : h_ready_) cudaEventDestroy(ev);
   if (tables_h_) cudaFreeHost(tables_h_);
   if (out_h_) cudaFreeHost(out_h_);
   for (auto e : load_done_) cudaEventDestroy(e);
@@ -276,6 +295,15 @@ void Engine::finalize() {
   check(cudaStreamSynchronize(compute_), "sync");
   finalized_ = true;
   decided_ = false;
+  // Misses are possible when a shard holds fewer slots than experts: start
+  // the host cold-expert executor (the CPU side of the HWB split).
+  const int shard_size = (m_.n_experts - rank_ + world_ - 1) / world_;
+  const int threads = cold_threads_ < 0 ? static_cast<int>(std::max(1u, std::thread::hardware_concurrency()))
+                                        : cold_threads_;
+  if (threads > 0 && slots_ < shard_size)
+    cold_ = std::make_unique<ColdExecutor>(threads, kernel_, m_.d_model, m_.d_ffn, T_);
+  else
+    cold_.reset();
 }
 
 void Engine::set_nccl(const void* uid, int nranks, int rank) {
@@ -385,26 +413,35 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   a2.scores_out = scores_out_d;
   check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
   if (timing_) check(cudaEventRecord(ev_[3], compute_), "event");
-  // scores + counters back to the host right away: the host scheduler works
-  // on them while the device runs the layers below
+  // scores + counters (+ routing for the cold path) back to the host right
+  // away: the host scheduler works on them while the device runs the layers
   check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
+  const bool cold = static_cast<bool>(cold_);
+  int32_t* ids_h = reinterpret_cast<int32_t*>(route_h_);
+  float* gates_h = reinterpret_cast<float*>(route_h_ + sizeof(int32_t) * L * T_ * k);
+  if (cold) {
+    check(cudaMemcpyAsync(ids_h, ids_d_, sizeof(int32_t) * L * T_ * k, cudaMemcpyDeviceToHost, compute_), "D2H ids");
+    check(cudaMemcpyAsync(gates_h, gates_d_, sizeof(float) * L * T_ * k, cudaMemcpyDeviceToHost, compute_),
+          "D2H gates");
+    if (!h_in_host)
+      check(cudaMemcpyAsync(hcold_h_, h_d_, sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_), "D2H h0");
+  }
   check(cudaEventRecord(k2_done_, compute_), "event");
 
   const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
   const bool tc = kernel_ == kFfnTensorCore;
   uint16_t* hT[2] = {hT_d_, hT_d_ + static_cast<size_t>(16) * d};
   if (tc) check(launch_build_hT(h_d_, T_, d, hT[0], compute_), "build_hT");
-  for (int l = 0; l < L; ++l) {
+
+  auto launch_ffn = [&](int l) {
     // Only a layer with this-rank loads needs the copy-stream event; every
     // other K3 is launched programmatically-dependent on the previous kernel
     // so its prologue and first weight copies overlap that kernel's tail.
     const bool has_loads = layer_loads_local[static_cast<size_t>(l)] > 0;
     if (has_loads) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
     const bool pdl = pdl_ && !has_loads && !timing_;
-    const uint16_t* hl = h_d_ + static_cast<size_t>(l) * T_ * d;
-    uint16_t* hn = h_d_ + static_cast<size_t>(l + 1) * T_ * d;
     dev::FfnArgs fa{};
-    fa.h = hl;
+    fa.h = h_d_ + static_cast<size_t>(l) * T_ * d;
     fa.T = T_;
     fa.d = d;
     fa.ffn = m_.d_ffn;
@@ -418,8 +455,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.slot_of = slots_d + static_cast<size_t>(l) * N;
     fa.pool = pool_ + static_cast<int64_t>(l) * slots_ * image_elems_;
     fa.shared_w = shared_ + static_cast<int64_t>(l) * m_.n_shared_units * image_elems_;
-    // expert-parallel: shared units are computed once, on rank 0
-    fa.n_shared = n_shared_eff;
+    fa.n_shared = n_shared_eff;  // expert-parallel: shared units are computed once, on rank 0
     fa.expert_elems = image_elems_;
     fa.partial = work_d_;
     fa.n_stages = stages_;
@@ -430,16 +466,20 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
              : launch_expert_ffn(fa, sms_, ffn_smem_, compute_, pdl),
           "K3 expert FFN");
     if (timing_) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
+  };
+  auto launch_combine_layer = [&](int l, const float* y_extra) {
+    const uint16_t* hl = h_d_ + static_cast<size_t>(l) * T_ * d;
+    uint16_t* hn = h_d_ + static_cast<size_t>(l + 1) * T_ * d;
     dev::CombineArgs ca{};
     ca.h_in = hl;
-    ca.y_extra = nullptr;
+    ca.y_extra = y_extra;
     ca.T = T_;
     ca.d = d;
     ca.ffn = m_.d_ffn;
     ca.k = k;
     ca.ids = ids_d_ + static_cast<size_t>(l) * T_ * k;
     ca.hit_ord = hit_ord_d_ + static_cast<size_t>(l) * N;
-    ca.counters = fa.counters;
+    ca.counters = counters_d + static_cast<size_t>(l) * 8;
     ca.n_shared = n_shared_eff;
     ca.grid = sms_;
     ca.partial = work_d_;
@@ -447,7 +487,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.y_out = yl;
     ca.h_out = world_ > 1 ? nullptr : hn;
     ca.hT_out = (world_ == 1 && tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr;
-    check(launch_combine(ca, compute_, pdl_ && !timing_), "combine");
+    check(launch_combine(ca, compute_, pdl_ && !timing_ && !y_extra), "combine");
     if (world_ > 1) {
       const int r = nccl_->all_reduce(yl, yl, static_cast<size_t>(T_) * d, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm_,
                                       compute_);
@@ -455,6 +495,80 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       check(launch_residual(hl, yl, hn, (tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr, d, T_ * d, compute_),
             "residual");
     }
+  };
+
+  StepReport sr;
+  std::vector<LayerOutcome> oc;
+  auto host_account = [&]() {
+    // account this step with the K2 counters, then decide the next step
+    // (needs only the new scores)
+    std::memcpy(scores_.data(), out_h_, sizeof(int32_t) * L * N);
+    oc.assign(reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N),
+              reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N) + L);
+    sr = sched_->observe(oc.data(), accepted);
+    sched_->decide(scores_.data());
+  };
+  float cpu_ms_cold = 0.f;
+  int cold_experts = 0;
+
+  if (!cold) {
+    // ---- all layers on the device back to back; host accounting overlaps
+    for (int l = 0; l < L; ++l) {
+      launch_ffn(l);
+      launch_combine_layer(l, nullptr);
+    }
+    check(cudaEventSynchronize(k2_done_), "sync K2");
+    host_account();
+  } else {
+    // ---- heterogeneous split: per layer, the device runs the resident
+    // experts while the host cores run the missed ones on the same h_l.
+    launch_ffn(0);
+    check(cudaEventSynchronize(k2_done_), "sync K2");
+    std::vector<std::vector<ColdItem>> items(static_cast<size_t>(L));
+    for (int l = 0; l < L; ++l) {
+      const uint32_t* res = rb + static_cast<size_t>(l) * W_;
+      const int32_t* il = ids_h + static_cast<size_t>(l) * T_ * k;
+      const float* gl = gates_h + static_cast<size_t>(l) * T_ * k;
+      for (int e = rank_; e < N; e += world_) {  // this rank's shard of the misses
+        if ((res[e >> 5] >> (e & 31)) & 1u) continue;
+        ColdItem it{};
+        it.image = arena_h_ + image_of(l, e) * image_elems_;
+        for (int t = 0; t < T_; ++t)
+          for (int j = 0; j < k; ++j)
+            if (il[t * k + j] == e) {
+              it.tok[it.n_tok] = t;
+              it.gate[it.n_tok] = gl[t * k + j];
+              ++it.n_tok;
+            }
+        if (it.n_tok) items[static_cast<size_t>(l)].push_back(it);
+      }
+      cold_experts += static_cast<int>(items[static_cast<size_t>(l)].size());
+    }
+    if (h_in_host) std::memcpy(hcold_h_, h_in, sizeof(uint16_t) * T_ * d);
+    for (int l = 0; l < L; ++l) {
+      const float* y_extra = nullptr;
+      if (!items[static_cast<size_t>(l)].empty()) {
+        if (l > 0) check(cudaEventSynchronize(h_ready_[static_cast<size_t>(l)]), "sync h_l");
+        const auto c0 = std::chrono::steady_clock::now();
+        float* yh = ycold_h_ + static_cast<size_t>(l) * T_ * d;
+        cold_->run(items[static_cast<size_t>(l)], hcold_h_ + static_cast<size_t>(l) * T_ * d, yh);
+        cpu_ms_cold += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        float* yd = ycold_d_ + static_cast<size_t>(l) * T_ * d;
+        check(cudaMemcpyAsync(yd, yh, sizeof(float) * T_ * d, cudaMemcpyHostToDevice, compute_), "H2D cold y");
+        y_extra = yd;
+      }
+      launch_combine_layer(l, y_extra);
+      if (l + 1 < L) {
+        if (!items[static_cast<size_t>(l + 1)].empty()) {
+          check(cudaMemcpyAsync(hcold_h_ + static_cast<size_t>(l + 1) * T_ * d, h_d_ + static_cast<size_t>(l + 1) * T_ * d,
+                                sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_),
+                "D2H h_l");
+          check(cudaEventRecord(h_ready_[static_cast<size_t>(l + 1)], compute_), "event");
+        }
+        launch_ffn(l + 1);
+      }
+    }
+    host_account();
   }
   if (timing_) check(cudaEventRecord(ev_[4], compute_), "event");
   const uint16_t* hfin = h_d_ + static_cast<size_t>(L) * T_ * d;
@@ -463,16 +577,6 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
                           h_out_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, compute_),
           "h_out");
   if (timing_) check(cudaEventRecord(ev_[5], compute_), "event");
-
-  // ---- host, overlapped with the layers: account this step with the K2
-  // counters, then decide the next step (needs only the new scores).
-  check(cudaEventSynchronize(k2_done_), "sync K2");
-  std::memcpy(scores_.data(), out_h_, sizeof(int32_t) * L * N);
-  std::vector<LayerOutcome> oc(reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N),
-                               reinterpret_cast<const LayerOutcome*>(out_h_ + static_cast<size_t>(L) * N) + L);
-  StepReport sr = sched_->observe(oc.data(), accepted);
-  sched_->decide(scores_.data());
-
   check(cudaStreamSynchronize(compute_), "sync compute");
   check(cudaStreamSynchronize(copy_), "sync copy");
 
@@ -498,6 +602,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     rep->d2h_bytes =
         static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
     rep->kernel_launches = 2 + 2 * L + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
+    rep->cold_experts = cold_experts;
+    rep->cpu_ms_cold = cpu_ms_cold;
     if (timing_) {
       auto ms = [](cudaEvent_t a, cudaEvent_t b) {
         float v = 0.f;

@@ -16,6 +16,7 @@
 namespace moespac {
 
 struct NcclApi;  // dlopen'ed libnccl (no link-time dependency)
+class ColdExecutor;
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -30,6 +31,8 @@ class Engine {
  public:
   Engine(int device, const moespac_model_desc& m, const moespac_sched_config& cfg, int rank, int world);
   ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
 
   uint16_t* host_arena(int64_t n_images);
   void fill_synthetic(uint64_t seed, float stdv);
@@ -38,6 +41,9 @@ class Engine {
   void set_nccl(const void* uid, int nranks, int rank);
   void set_timing(bool on) { timing_ = on; }
   void set_pdl(bool on) { pdl_ = on; }
+  // host threads for cold (non-resident) experts: -1 auto, 0 = off (misses
+  // are then counted but not computed); takes effect at finalize()
+  void set_cold_threads(int n) { cold_threads_ = n; }
   void step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
             uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
   void views(moespac_ctx_views* v) const;
@@ -90,6 +96,13 @@ class Engine {
   cudaEvent_t k2_done_ = nullptr;
   bool decided_ = false;  // next step's decisions already made
   bool pdl_ = true;       // programmatic dependent launch between layer kernels
+  int cold_threads_ = -1;
+  std::unique_ptr<ColdExecutor> cold_;
+  float* ycold_d_ = nullptr;   // [L][T][d] host-computed cold-expert outputs
+  float* ycold_h_ = nullptr;   // pinned staging of the same
+  uint16_t* hcold_h_ = nullptr;  // pinned [L+1][T][d] layer inputs for the cold path
+  uint8_t* route_h_ = nullptr;   // pinned ids [L][T][k] | gates [L][T][k]
+  std::vector<cudaEvent_t> h_ready_;
   std::unique_ptr<NcclApi> nccl_;
   void* comm_ = nullptr;
 };

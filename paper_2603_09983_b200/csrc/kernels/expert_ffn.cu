@@ -454,16 +454,16 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
     acc.w += v.w;
   }
   const size_t off = static_cast<size_t>(t) * a.d + c;
+  if (a.y_extra) {  // cold experts computed on the host (added after the fixed-order device sum)
+    const float4 e = *reinterpret_cast<const float4*>(a.y_extra + off);
+    acc.x += e.x;
+    acc.y += e.y;
+    acc.z += e.z;
+    acc.w += e.w;
+  }
   if (a.y_out) *reinterpret_cast<float4*>(a.y_out + off) = acc;
   if (a.h_out) {
     float4 r = acc;
-    if (a.y_extra) {
-      const float4 e = *reinterpret_cast<const float4*>(a.y_extra + off);
-      r.x += e.x;
-      r.y += e.y;
-      r.z += e.z;
-      r.w += e.w;
-    }
     if (a.h_in) {
       const uint2 hv = *reinterpret_cast<const uint2*>(a.h_in + off);
       r.x += bf_lo(hv.x);

@@ -43,10 +43,11 @@ def _pack(w, kernel):
     return abi.pack_expert(*[torch.from_numpy(x.view(np.int16)).cuda() for x in w], kernel=kernel)
 
 
-def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel=abi.FFN_AUTO):
+def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel=abi.FFN_AUTO, cold=-1):
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache)
     kernel = abi.ffn_resolve(kernel, d, ffn)
     ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, gate_mode, kernel), cfg)
+    ctx.set_cold_threads(cold)
     arena = ctx.host_arena(L * N)
     for (l, e), w in std.items():
         arena[l * N + e] = _pack(w, kernel).cpu().numpy().view(np.uint16)
@@ -61,18 +62,20 @@ def _resident(rb, l, N):
     return [e for e in range(N) if (int(rb[l, e >> 5]) >> (e & 31)) & 1]
 
 
-@pytest.mark.parametrize("L,N,k,g,d,ffn,units,gate_mode,cache,kernel", [
-    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_CUDACORE),
-    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_TENSOR),
-    (2, 8, 2, 4, 512, 128, 0, 0, 0.17, abi.FFN_TENSOR),
-    (2, 32, 8, 8, 2048, 48, 0, 0, 0.5, abi.FFN_CUDACORE),
-    (2, 32, 8, 8, 2048, 128, 0, 0, 0.5, abi.FFN_TENSOR),
+@pytest.mark.parametrize("L,N,k,g,d,ffn,units,gate_mode,cache,kernel,cold", [
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_CUDACORE, -1),
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_TENSOR, -1),
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_TENSOR, 0),
+    (2, 8, 2, 4, 512, 128, 0, 0, 0.17, abi.FFN_TENSOR, 3),
+    (2, 32, 8, 8, 2048, 48, 0, 0, 0.5, abi.FFN_CUDACORE, 2),
+    (2, 32, 8, 8, 2048, 128, 0, 0, 0.5, abi.FFN_TENSOR, -1),
+    (2, 32, 8, 8, 2048, 128, 0, 0, 1.0, abi.FFN_TENSOR, -1),
 ])
-def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache, kernel):
+def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, cold):
     ref_or_skip()
     rng = np.random.default_rng(L * 100 + N)
     std, shared = _experts(rng, L, N, d, ffn, units)
-    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel)
+    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel, cold)
     T = g + 1
     steps = 10
     gen = O.Generator(L, N, k, g, seed=1)
@@ -96,7 +99,8 @@ def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate
         _, rb, _, _ = ctx.step_tables()
         for l in range(L):
             _, gates = O.router_topk(logits[l], k, gate_mode)
-            res = _resident(rb, l, N)
+            # cold path on: misses run on the host cores -> the full Eq. 3 output
+            res = range(N) if cold != 0 else _resident(rb, l, N)
             y_ref = O.moe_layer(hs[l], ids[l], gates, {e: std[(l, e)] for e in res}, shared[l])
             rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
             assert rel <= 1e-5, (s, l, rel)
@@ -107,6 +111,11 @@ def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate
             assert [lay[l].tau, lay[l].fallback, lay[l].n_prefetch, lay[l].t_cpu_ns, lay[l].t_gpu_ns] == list(r[:5])
         sr = run.step_rec[s]
         assert [rep.cache_hits, rep.cache_misses, rep.faults_fn, rep.faults_fp] == list(sr[1:5])
+        if cold != 0 and cache < 1.0:
+            _, rb, _, _ = ctx.step_tables()
+            n_miss = sum(1 for l in range(L) for e in range(N)
+                         if e in set(ids[l].ravel()) and not (int(rb[l, e >> 5]) >> (e & 31)) & 1)
+            assert rep.cold_experts == n_miss
     assert np.array_equal(ctx.sched_events(), run.events)
     if cache < 1.0:
         assert total_loads > 0, "the test must exercise real expert loads"
