@@ -221,6 +221,8 @@ typedef struct moespac_ffn_args {
   int32_t kernel;              /* MOESPAC_FFN_* (image layout must match) */
   const uint16_t* hT_dev;      /* tensor-core kernel: moespac_build_hT(h) image */
   uint64_t* debug_ts_dev;      /* optional [grid][8] per-CTA %globaltimer stamps (profiling), or NULL */
+  int32_t accum;               /* tensor-core kernel: 0 auto, 1 shared-memory, 2 L2 (partial-block) accumulator */
+  int32_t l2_policy;           /* weight stream L2 policy: 0 evict_first (default), 1 evict_normal */
 } moespac_ffn_args;
 size_t moespac_ffn_workspace_bytes(int tokens, int d_model, int n_experts, int n_shared_units, int grid);
 int64_t moespac_expert_image_elems(int d_model, int d_ffn);

@@ -84,7 +84,8 @@ class FfnArgs(C.Structure):
                 ("offsets_dev", C.c_void_p), ("gates_dev", C.c_void_p), ("hit_list_dev", C.c_void_p),
                 ("counters_dev", C.c_void_p), ("slot_of_dev", C.c_void_p), ("pool_dev", C.c_void_p),
                 ("shared_dev", C.c_void_p), ("n_shared_units", C.c_int32), ("workspace_dev", C.c_void_p),
-                ("grid", C.c_int32), ("kernel", C.c_int32), ("hT_dev", C.c_void_p), ("debug_ts_dev", C.c_void_p)]
+                ("grid", C.c_int32), ("kernel", C.c_int32), ("hT_dev", C.c_void_p), ("debug_ts_dev", C.c_void_p),
+                ("accum", C.c_int32), ("l2_policy", C.c_int32)]
 
 
 class CombineArgs(C.Structure):

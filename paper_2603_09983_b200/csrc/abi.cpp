@@ -444,7 +444,7 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     int dev = 0, optin = 0;
     cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
     cuda_ok(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
-    const FfnPlan plan = kern == kFfnTensorCore ? ffn_tc_plan(a->tokens, a->d_model, static_cast<size_t>(optin))
+    const FfnPlan plan = kern == kFfnTensorCore ? ffn_tc_plan(a->tokens, a->d_model, static_cast<size_t>(optin), a->accum)
                                                 : ffn_plan(a->tokens, a->d_model, static_cast<size_t>(optin));
     if (!plan.n_stages) throw std::invalid_argument("moespac_expert_ffn: tokens x d_model too large for shared memory");
     dev::FfnArgs f{};
@@ -469,6 +469,7 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.global_acc = plan.global_acc ? 1 : 0;
     f.hT = a->hT_dev;
     f.dbg = reinterpret_cast<unsigned long long*>(a->debug_ts_dev);
+    f.l2_policy = a->l2_policy;
     const int grid = a->grid > 0 ? a->grid : device_sms();
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_ok(kern == kFfnTensorCore ? launch_expert_ffn_tc(f, grid, plan.smem, st) : launch_expert_ffn(f, grid, plan.smem, st),

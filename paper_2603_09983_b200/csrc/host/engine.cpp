@@ -121,7 +121,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   if (prop.major != 10) throw CudaError("moespac requires an sm_100 (B200) device");
   sms_ = prop.multiProcessorCount;
-  const FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, prop.sharedMemPerBlockOptin)
+  const FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, prop.sharedMemPerBlockOptin, ffn_accum_)
                                                  : ffn_plan(T_, m.d_model, prop.sharedMemPerBlockOptin);
   if (plan.n_stages == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
   stages_ = plan.n_stages;

@@ -97,6 +97,7 @@ class Engine {
   bool decided_ = false;  // next step's decisions already made
   bool pdl_ = true;       // programmatic dependent launch between layer kernels
   int cold_threads_ = -1;
+  int ffn_accum_ = 0;
   std::unique_ptr<ColdExecutor> cold_;
   float* ycold_d_ = nullptr;   // [L][T][d] host-computed cold-expert outputs
   float* ycold_h_ = nullptr;   // pinned staging of the same

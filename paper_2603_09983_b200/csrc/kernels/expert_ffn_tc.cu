@@ -65,6 +65,12 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(IDESC), "r"(acc));
 }
 
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
+  return p != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -124,11 +130,25 @@ struct SegIter {
   }
 };
 
+constexpr int DBG = 16;  // debug slots per CTA
+
 __device__ __forceinline__ void stamp(const FfnArgs& a, int slot) {
   if (a.dbg) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.dbg[blockIdx.x * 8 + slot] = t;
+    a.dbg[blockIdx.x * DBG + slot] = t;
+  }
+}
+
+// mbarrier wait that, in profiling mode, accumulates the cycles spent
+// blocked into debug slot `slot` (slots 8..15: per-role wait counters)
+__device__ __forceinline__ void wait_acc(const FfnArgs& a, uint64_t* bar, uint32_t parity, long long& acc) {
+  if (a.dbg) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
   }
 }
 
@@ -174,7 +194,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     stamp(a, 0);
-    if (a.dbg) a.dbg[blockIdx.x * 8 + 7] = static_cast<unsigned long long>(clock64());
+    if (a.dbg) a.dbg[blockIdx.x * DBG + 7] = static_cast<unsigned long long>(clock64());
   }
   const int n_hits = a.counters[7];
   const long long n = static_cast<long long>(n_hits + a.n_shared) * qpe;
@@ -225,8 +245,12 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   // turns chunk i's D1 into a^T; DN(i) then finds a^T(i) ready.
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy();
+    // The whole warp walks the loop in convergent flow (addresses stay in
+    // uniform registers); one elected lane issues each copy.
+    {
+      const bool leader = elect_one();
+      long long w_empty = 0;
+      const uint64_t pol = a.l2_policy == 1 ? l2_evict_normal_policy() : l2_evict_first_policy();
       Ring r;
       SegIter it{q0, q1, qpe};
       Seg cur, prev;
@@ -242,14 +266,18 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         kt0 = min(ns, ktiles);
         for (int kt = 0; kt < kt0; ++kt) {
           uint8_t* st = ring + static_cast<size_t>(kt) * STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[kt], 2 * gseg + B_BYTES);
+          if (leader) mbar_arrive_expect_tx(&full[kt], 2 * gseg + B_BYTES);
           const uint8_t* tile = base + static_cast<size_t>(kt) * A_BYTES;
-          bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[kt], pol);
-          bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[kt], pol);
+          if (gseg == 8192u) {
+            if (leader) bulk_g2s(st, tile, A_BYTES, &full[kt], pol);
+          } else {
+            if (leader) bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[kt], pol);
+            if (leader) bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[kt], pol);
+          }
         }
         pdl_wait();
         for (int kt = 0; kt < kt0; ++kt)
-          bulk_g2s(ring + static_cast<size_t>(kt) * STAGE_BYTES + A_BYTES,
+          if (leader) bulk_g2s(ring + static_cast<size_t>(kt) * STAGE_BYTES + A_BYTES,
                    reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES, B_BYTES, &full[kt],
                    pol);
         for (int kt = 0; kt < kt0; ++kt) r.advance(ns);
@@ -260,13 +288,17 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
               reinterpret_cast<const uint8_t*>(entry_weights(a, cur.o, n_hits) + cur.c * chunk_elems);
           const uint32_t gseg = static_cast<uint32_t>(cur.qb - cur.qa) * 2048u;
           for (int kt = kt0; kt < ktiles; ++kt) {
-            mbar_wait(&empty[r.stage], r.ph ^ 1u);
+            wait_acc(a, &empty[r.stage], r.ph ^ 1u, w_empty);
             uint8_t* st = ring + static_cast<size_t>(r.stage) * STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[r.stage], 2 * gseg + B_BYTES);
+            if (leader) mbar_arrive_expect_tx(&full[r.stage], 2 * gseg + B_BYTES);
             const uint8_t* tile = base + static_cast<size_t>(kt) * A_BYTES;
-            bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[r.stage], pol);
-            bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[r.stage], pol);
-            bulk_g2s(st + A_BYTES, reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES,
+            if (gseg == 8192u) {
+              if (leader) bulk_g2s(st, tile, A_BYTES, &full[r.stage], pol);
+            } else {
+              if (leader) bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[r.stage], pol);
+              if (leader) bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[r.stage], pol);
+            }
+            if (leader) bulk_g2s(st + A_BYTES, reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES,
                      B_BYTES, &full[r.stage], pol);
             r.advance(ns);
           }
@@ -277,11 +309,11 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
               reinterpret_cast<const uint8_t*>(entry_weights(a, prev.o, n_hits) + prev.c * chunk_elems);
           const uint32_t dseg = static_cast<uint32_t>(prev.qb - prev.qa) * 4096u;
           for (int mt = 0; mt < mtiles; ++mt) {
-            mbar_wait(&empty[r.stage], r.ph ^ 1u);
+            wait_acc(a, &empty[r.stage], r.ph ^ 1u, w_empty);
             uint8_t* st = ring + static_cast<size_t>(r.stage) * STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[r.stage], dseg);
+            if (leader) mbar_arrive_expect_tx(&full[r.stage], dseg);
             const uint8_t* tile = base + static_cast<size_t>(ktiles + mt) * A_BYTES;
-            bulk_g2s(st + prev.qa * 4096, tile + prev.qa * 4096, dseg, &full[r.stage], pol);
+            if (leader) bulk_g2s(st + prev.qa * 4096, tile + prev.qa * 4096, dseg, &full[r.stage], pol);
             r.advance(ns);
           }
         }
@@ -289,10 +321,15 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         prev = cur;
         if (more) more = it.next(cur);
       }
+      if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // Whole warp in convergent flow so descriptors are warp-uniform (no
+    // per-MMA R2UR waterfall); one elected lane issues MMAs and commits.
+    {
+      const bool leader = elect_one();
+      long long w_full = 0, w_at = 0, w_d2e = 0, w_d1e = 0;
       Ring r;
       Phase d1e[2], ate[2], d2e[2];
       int c3 = 0;  // D2 pass buffer counter
@@ -305,62 +342,75 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
       while (more || has_prev) {
         if (more) {  // GU(i): D1[i & 1] = W_gu x h^T
           const int b1 = i & 1;
-          mbar_wait(&d1_empty[b1], d1e[b1].bit ^ 1u);
+          wait_acc(a, &d1_empty[b1], d1e[b1].bit ^ 1u, w_d1e);
           d1e[b1].flip();
           fence_after();
           const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
           for (int kt = 0; kt < ktiles; ++kt) {
-            mbar_wait(&full[r.stage], r.ph);
-            if (i == 0 && kt == 0) stamp(a, 2);
+            wait_acc(a, &full[r.stage], r.ph, w_full);
+            if (i == 0 && kt == 0 && leader) stamp(a, 2);
             fence_after();
             const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
+            const uint64_t adesc = smem_desc(sa, 128, 1024), bdesc = smem_desc(sa + A_BYTES, 128, 1024);
+            if (leader) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_bf16(d1, smem_desc(sa + k * 256, 128, 1024), smem_desc(sa + A_BYTES + k * 256, 128, 1024),
-                       (kt | k) != 0);
-            mma_commit(&empty[r.stage]);
+              for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
+                mma_bf16(d1, adesc + 16 * k, bdesc + 16 * k, (kt | k) != 0);
+              mma_commit(&empty[r.stage]);
+            }
+            __syncwarp();
             r.advance(ns);
           }
-          mma_commit(&d1_full[b1]);
-          if (i == 0) stamp(a, 3);
+          if (leader) mma_commit(&d1_full[b1]);
+          __syncwarp();
+          if (i == 0 && leader) stamp(a, 3);
         }
         if (has_prev) {  // DN(i-1): D2 = W_down x a^T(i-1), hi + lo
           const int ab = (i - 1) & 1;
-          mbar_wait(&at_full[ab], ate[ab].bit);
+          wait_acc(a, &at_full[ab], ate[ab].bit, w_at);
           ate[ab].flip();
           fence_after();
           const uint32_t ahi = at_addr + static_cast<uint32_t>(ab) * 8192u;
-          const uint32_t alo = ahi + 4096u;
+          const uint64_t bhi = smem_desc(ahi, 256, 128), blo = smem_desc(ahi + 4096u, 256, 128);
           for (int ps = 0; ps < passes; ++ps) {
             const int pb = c3 & 1;
-            mbar_wait(&d2_empty[pb], d2e[pb].bit ^ 1u);
+            wait_acc(a, &d2_empty[pb], d2e[pb].bit ^ 1u, w_d2e);
             d2e[pb].flip();
             fence_after();
             const int mt_end = min(mtiles, (ps + 1) * PASS_TILES);
             for (int mt = ps * PASS_TILES; mt < mt_end; ++mt) {
-              mbar_wait(&full[r.stage], r.ph);
+              wait_acc(a, &full[r.stage], r.ph, w_full);
               fence_after();
               const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
               const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>(pb * 128 + (mt - ps * PASS_TILES) * 16);
-              bool first = true;
-              for (int k = prev.qa; k < prev.qb; ++k) {
-                const uint64_t ad = smem_desc(sa + k * 4096, 2048, 128);
-                mma_bf16(d2, ad, smem_desc(ahi + k * 512, 256, 128), first ? 0u : 1u);
-                mma_bf16(d2, ad, smem_desc(alo + k * 512, 256, 128), 1u);
-                first = false;
+              const uint64_t adn = smem_desc(sa, 2048, 128);
+              if (leader) {
+                for (int k = prev.qa; k < prev.qb; ++k) {  // +4096 B (A) / +512 B (a^T) per K=16 step
+                  mma_bf16(d2, adn + 256 * k, bhi + 32 * k, k == prev.qa ? 0u : 1u);
+                  mma_bf16(d2, adn + 256 * k, blo + 32 * k, 1u);
+                }
+                mma_commit(&empty[r.stage]);
               }
-              mma_commit(&empty[r.stage]);
+              __syncwarp();
               r.advance(ns);
             }
-            mma_commit(&d2_full[pb]);
+            if (leader) mma_commit(&d2_full[pb]);
+            __syncwarp();
             ++c3;
           }
-          mma_commit(&at_empty[ab]);
+          if (leader) mma_commit(&at_empty[ab]);
+          __syncwarp();
         }
         has_prev = more;
         prev = cur;
         if (more) more = it.next(cur);
         ++i;
+      }
+      if (a.dbg && leader) {
+        a.dbg[blockIdx.x * DBG + 9] = static_cast<unsigned long long>(w_full);
+        a.dbg[blockIdx.x * DBG + 10] = static_cast<unsigned long long>(w_at);
+        a.dbg[blockIdx.x * DBG + 11] = static_cast<unsigned long long>(w_d2e);
+        a.dbg[blockIdx.x * DBG + 12] = static_cast<unsigned long long>(w_d1e);
       }
     }
   } else {
@@ -368,6 +418,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = tid - 64; // 0..127
     Phase d1f[2], atf[2], d2f[2];
+    long long w_d1f = 0, w_d2f = 0;
     int c3 = 0;
     int cur_entry = -1, eslot = 1;
     int seg_slot[2] = {0, 0};
@@ -441,7 +492,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         seg_slot[i & 1] = eslot;
         const float* gs = gate_s + eslot * 16;
         const int b1 = i & 1;
-        mbar_wait(&d1_full[b1], d1f[b1].bit);
+        wait_acc(a, &d1_full[b1], d1f[b1].bit, w_d1f);
         d1f[b1].flip();
         fence_after();
         float v[16];
@@ -490,7 +541,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         // ---- D(i-1): D2 passes -> per-expert fp32 accumulator
         for (int ps = 0; ps < passes; ++ps) {
           const int pb = c3 & 1;
-          mbar_wait(&d2_full[pb], d2f[pb].bit);
+          wait_acc(a, &d2_full[pb], d2f[pb].bit, w_d2f);
           d2f[pb].flip();
           fence_after();
           const int mt0 = ps * PASS_TILES, mt_end = min(mtiles, mt0 + PASS_TILES);
@@ -502,7 +553,10 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
             const int orow = mt * 128 + 32 * q + lane;
             if (a.global_acc) {
               float* P = a.partial + static_cast<long long>(b + prev.o) * T * d;
-              for (int t = 0; t < T; ++t) P[static_cast<long long>(t) * d + orow] += y[t];
+              const float* gsl = gate_s + seg_slot[(i - 1) & 1] * 16;
+#pragma unroll
+              for (int t = 0; t < 16; ++t)
+                if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += y[t];
             } else {
 #pragma unroll
               for (int t = 0; t < 16; ++t)
@@ -521,13 +575,19 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
       if (more) more = it.next(cur);
       ++i;
     }
+    if (a.dbg && tid == 64) {
+      a.dbg[blockIdx.x * DBG + 13] = static_cast<unsigned long long>(w_d1f);
+      a.dbg[blockIdx.x * DBG + 14] = static_cast<unsigned long long>(w_d2f);
+    }
   }
-  if (tid == 64) stamp(a, 5);  // epilogue finished (all flushes written)
+  if (tid == 64) {
+    stamp(a, 5);  // epilogue finished (all flushes written)
+  }
   fence_before();
   __syncthreads();
   if (tid == 0) {
     stamp(a, 6);
-    if (a.dbg) a.dbg[blockIdx.x * 8 + 7] = static_cast<unsigned long long>(clock64()) - a.dbg[blockIdx.x * 8 + 7];
+    if (a.dbg) a.dbg[blockIdx.x * DBG + 7] = static_cast<unsigned long long>(clock64()) - a.dbg[blockIdx.x * DBG + 7];
   }
   if (warp == 1) {
     fence_after();
@@ -587,10 +647,15 @@ size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc) {
          (global_acc ? 0 : static_cast<size_t>(T) * d * 4) + 2 * 16 * 4 * 2 + 16 + 8 + 8 * (2 * n_stages + 12);
 }
 
-FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit) {
-  for (int ns = 8; ns >= 4; --ns)
-    if (ffn_tc_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_tc_smem_bytes(T, d, ns, false)};
-  for (int ns = 8; ns >= 2; --ns)
+// accum: 0 auto (shared memory when it leaves a >= 4-deep ring), 1 shared-memory
+// accumulator, 2 global (L2) accumulator. Measured: the L2 accumulator puts
+// dependent global read-modify-writes on the drain's critical path and loses
+// ~30% even with a deeper ring, so it is only the fallback for large T x d.
+FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
+  if (accum != 2)
+    for (int ns = 12; ns >= (accum == 1 ? 2 : 4); --ns)
+      if (ffn_tc_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_tc_smem_bytes(T, d, ns, false)};
+  for (int ns = 12; ns >= 2; --ns)
     if (ffn_tc_smem_bytes(T, d, ns, true) <= smem_limit) return {ns, true, ffn_tc_smem_bytes(T, d, ns, true)};
   return {0, false, 0};
 }

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--experts", default="1,2,4,8,16,32,64,128")
     ap.add_argument("--kernels", default="2,1")
+    ap.add_argument("--accum", type=int, default=0)
+    ap.add_argument("--l2", type=int, default=0)
     ap.add_argument("--stamps", action="store_true", help="dump per-CTA timeline (tensor-core kernel)")
     args = ap.parse_args()
     d, ffn, T, k, N = args.d, args.ffn, args.T, args.k, args.N
@@ -59,7 +61,7 @@ def main():
             n_hit = int(bufs["cnt"][7].item())
             fa = abi.FfnArgs(abi.ptr(h), T, d, ffn, kk, N, abi.ptr(bufs["perm"]), abi.ptr(bufs["offsets"]),
                              abi.ptr(gates), abi.ptr(bufs["hl"]), abi.ptr(bufs["cnt"]), abi.ptr(slot_of),
-                             abi.ptr(pool), None, 0, abi.ptr(ws), sms, kern, abi.ptr(hT))
+                             abi.ptr(pool), None, 0, abi.ptr(ws), sms, kern, abi.ptr(hT), None, args.accum, args.l2)
             for _ in range(3):
                 abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -74,7 +76,7 @@ def main():
             us = e0.elapsed_time(e1) * 1e3 / args.iters
             byts = n_hit * img * 2
             if args.stamps and kern == 2:
-                dbg = torch.zeros((sms, 8), dtype=torch.int64, device=dev)
+                dbg = torch.zeros((sms, 16), dtype=torch.int64, device=dev)
                 fa.debug_ts_dev = abi.ptr(dbg)
                 abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
                 torch.cuda.synchronize()
@@ -90,10 +92,14 @@ def main():
                 summ = {nm: [round(float(np.nanmin(rel[:, j])), 2), round(float(np.nanmedian(rel[:, j])), 2),
                              round(float(np.nanmax(rel[:, j])), 2)] for j, nm in enumerate(names)}
                 cyc = t[act, 7]
+                waits = {nm: round(float(np.median(t[act, j] / np.maximum(cyc, 1))), 3) for j, nm in
+                         [(8, "prod_empty"), (9, "mma_full"), (10, "mma_at_full"), (11, "mma_d2_empty"),
+                          (12, "mma_d1_empty"), (13, "epi_d1_full"), (14, "epi_d2_full")]}
+                print(json.dumps({"wait_frac_of_cta_cycles": waits}), flush=True)
                 print(json.dumps({"stamps_us_min_med_max": summ, "active_ctas": int(act.sum()),
                                   "cta_clock64_cycles_med_max": [float(np.median(cyc)), float(cyc.max())],
                                   "entry_spread_us": round(float(np.nanmax(rel[:, 0])), 2)}), flush=True)
-            print(json.dumps({"kernel": kern, "experts": n_hit, "tokens": T, "d": d, "ffn": ffn, "us": round(us, 2),
+            print(json.dumps({"kernel": kern, "accum": args.accum, "l2": args.l2, "experts": n_hit, "tokens": T, "d": d, "ffn": ffn, "us": round(us, 2),
                               "MB": round(byts / 1e6, 1), "GBps": round(byts / us / 1e3, 1)}), flush=True)
 
 
