@@ -406,10 +406,12 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
 
 // One CTA per (token, 128-column slice); the partial rows of the token (its
 // experts in ascending id, each over the CTAs that covered it in ascending
-// order) are dealt round-robin to the 8 warps, then the 8 warp sums are added
-// in warp order — a fixed summation tree, so the result is deterministic.
-__global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
-  __shared__ float4 red[8][32];
+// order) are dealt round-robin to the warps, then the warp sums are added in
+// warp order — a fixed summation tree, so the result is deterministic.
+constexpr int COMBINE_WARPS = 4;  // small footprint: must co-reside with a K3 CTA (PDL)
+
+__global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs a) {
+  __shared__ float4 red[COMBINE_WARPS][32];
   if (threadIdx.x == 0) pdl_trigger();
   pdl_wait();  // partials of the K3 launch just before
   const int t = blockIdx.x;
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
       for (int b = lo; b <= hi; ++b) {
         // with fewer work units than CTAs some CTAs own nothing
         if ((b * n) / G == ((b + 1) * n) / G) continue;
-        if ((idx++ & 7) != warp) continue;
+        if ((idx++ % COMBINE_WARPS) != warp) continue;
         const float4 v = __ldcg(reinterpret_cast<const float4*>(
             a.partial + (static_cast<long long>(b + o) * a.T + t) * static_cast<long long>(a.d) + c));
         acc.x += v.x;
@@ -446,7 +448,7 @@ __global__ void __launch_bounds__(256) combine_kernel(CombineArgs a) {
   red[warp][lane] = acc;
   __syncthreads();
   if (warp != 0 || c >= a.d) return;
-  for (int w = 1; w < 8; ++w) {
+  for (int w = 1; w < COMBINE_WARPS; ++w) {
     const float4 v = red[w][lane];
     acc.x += v.x;
     acc.y += v.y;
@@ -593,7 +595,8 @@ cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cuda
 }
 
 cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream, bool pdl) {
-  return launch_pdl(dev::combine_kernel, dim3(a.T, (a.d + 127) / 128), dim3(256), 0, stream, pdl, a);
+  return launch_pdl(dev::combine_kernel, dim3(a.T, (a.d + 127) / 128), dim3(dev::COMBINE_WARPS * 32), 0, stream, pdl,
+                    a);
 }
 
 cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, uint16_t* hT_out, int d, int n,

@@ -51,6 +51,7 @@ constexpr int QROWS = 16;
 constexpr int TMEM_COLS = 512;
 constexpr int D2_COL0 = 256;
 constexpr int PASS_TILES = 8;
+constexpr int ENT_PRE = 8;  // entries whose routing is staged in the prologue
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -91,6 +92,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct Phase {
   uint32_t bit = 0;
@@ -171,7 +186,9 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   p += static_cast<size_t>(ns) * STAGE_BYTES;
   uint8_t* aT = p;  // [2 buf][2 part][4096]
   p += 2 * 2 * 4096;
-  float* u_s = reinterpret_cast<float*>(p);  // [64][17] (padded: conflict-free column writes)
+  float* u_s = reinterpret_cast<float*>(p);  // [64][17] up rows of D1 (padded: conflict-free)
+  p += 64 * 17 * 4;
+  float* g_s = reinterpret_cast<float*>(p);  // [64][17] gate rows of D1
   p += 64 * 17 * 4;
   float* ysum = reinterpret_cast<float*>(p);  // [T][d] (unless global_acc)
   if (!a.global_acc) p += static_cast<size_t>(T) * d * 4;
@@ -181,6 +198,13 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   p += 2 * 16 * 4;
   int* misc = reinterpret_cast<int*>(p);  // [1] tmem base, [2..3] ntok per slot
   p += 16;
+  // routing of this CTA's first ENT_PRE entries, read once in the prologue
+  float* ent_gate = reinterpret_cast<float*>(p);  // [ENT_PRE][16]
+  p += ENT_PRE * 16 * 4;
+  int* ent_tok = reinterpret_cast<int*>(p);  // [ENT_PRE][16]
+  p += ENT_PRE * 16 * 4;
+  int* ent_n = reinterpret_cast<int*>(p);  // [ENT_PRE]
+  p += ENT_PRE * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
   uint64_t* full = bars;
   uint64_t* empty = full + ns;
@@ -226,6 +250,43 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   if (!a.global_acc) {
     float4* ys = reinterpret_cast<float4*>(ysum);
     for (int i = tid; i < T * d / 4; i += THREADS) ys[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  {  // a^T columns of tokens >= T stay zero for the whole launch
+    uint4* z = reinterpret_cast<uint4*>(aT);
+    for (int i = tid; i < 2 * 2 * 4096 / 16; i += THREADS) z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  {
+    // Stage the routing (token list, per-token gate) of the first ENT_PRE
+    // entries of this CTA's range, one thread per entry, so that expert
+    // switches in the epilogue are shared-memory lookups. K2 wrote these
+    // several kernels ago, so no programmatic-dependency wait is needed.
+    const int o0 = static_cast<int>(q0 / qpe);
+    const int e = tid - 64;
+    const int o = o0 + e;
+    if (e >= 0 && e < ENT_PRE && static_cast<long long>(o) * qpe < q1) {
+      for (int t = 0; t < 16; ++t) {
+        ent_gate[e * 16 + t] = 0.f;
+        ent_tok[e * 16 + t] = 0;
+      }
+      int nt;
+      if (o < n_hits) {
+        const int ex = a.hit_list[o];
+        const int p0 = a.offsets[ex];
+        nt = a.offsets[ex + 1] - p0;
+        for (int j = 0; j < nt; ++j) {
+          const int idx = a.perm[p0 + j];
+          ent_tok[e * 16 + j] = idx / a.k;
+          ent_gate[e * 16 + idx / a.k] = a.gates[idx];
+        }
+      } else {
+        nt = T;
+        for (int j = 0; j < T; ++j) {
+          ent_tok[e * 16 + j] = j;
+          ent_gate[e * 16 + j] = 1.f;
+        }
+      }
+      ent_n[e] = nt;
+    }
   }
   fence_before();
   __syncthreads();
@@ -423,8 +484,28 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
     int cur_entry = -1, eslot = 1;
     int seg_slot[2] = {0, 0};
     // per-entry token data, two slots (entry being drained / entry being fed)
+    const int o_first = static_cast<int>(q0 / qpe);
     auto load_entry = [&](int o, int slot) {
       named_bar_sync(2, EPI_THREADS);
+      const int pre = o - o_first;
+      if (pre < ENT_PRE) {
+        if (et < 16) {
+          gate_s[slot * 16 + et] = ent_gate[pre * 16 + et];
+          tok_s[slot * 16 + et] = ent_tok[pre * 16 + et];
+        }
+        if (et == 0) misc[2 + slot] = ent_n[pre];
+        named_bar_sync(2, EPI_THREADS);
+        if (a.global_acc) {
+          float* P = a.partial + static_cast<long long>(b + o) * T * d;
+          const int nt = misc[2 + slot];
+          for (int t = 0; t < nt; ++t)
+            for (int c = et * 4; c < d; c += EPI_THREADS * 4)
+              *reinterpret_cast<float4*>(P + static_cast<long long>(tok_s[slot * 16 + t]) * d + c) =
+                  make_float4(0.f, 0.f, 0.f, 0.f);
+          named_bar_sync(2, EPI_THREADS);
+        }
+        return;
+      }
       if (et < 16) {
         gate_s[slot * 16 + et] = 0.f;
         tok_s[slot * 16 + et] = 0;
@@ -501,33 +582,34 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&d1_empty[b1]);
         const int row = 32 * q + lane;  // D1 row: < 64 gate, >= 64 up
-        if (row >= 64) {
+        {
+          float* dst = row < 64 ? g_s + row * 17 : u_s + (row - 64) * 17;
 #pragma unroll
-          for (int t = 0; t < 16; ++t) u_s[(row - 64) * 17 + t] = v[t];
+          for (int t = 0; t < 16; ++t)
+            if (t < T) dst[t] = v[t];
         }
         const int ab = i & 1;
         // a^T buffer ab is free once DN(i-2) completed
         mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);
         atf[ab].flip();
         named_bar_sync(2, EPI_THREADS);
-        if (row < 64) {
-          const int f = row;
-          const bool mine = f >= cur.qa * QROWS && f < cur.qb * QROWS;
-          uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
-          uint16_t* lo = hi + 2048;
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            float av = 0.f;
-            if (mine) {
-              const float g = v[t];
-              av = g / (1.f + __expf(-g)) * u_s[f * 17 + t] * gs[t];
+        {
+          // all 128 epilogue threads: row f of the segment's quarters, every
+          // other real token (a = silu(g) * u * gate_t, split into bf16 hi+lo)
+          const int f = et & 63;
+          if (f >= cur.qa * QROWS && f < cur.qb * QROWS) {
+            uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
+            uint16_t* lo = hi + 2048;
+            for (int t = et >> 6; t < T; t += 2) {
+              const float g = g_s[f * 17 + t];
+              const float av = g / (1.f + __expf(-g)) * u_s[f * 17 + t] * gs[t];
+              const uint16_t h16 = f32_to_bf16_rn(av);
+              const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
+              // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
+              const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
+              hi[off] = h16;
+              lo[off] = f32_to_bf16_rn(rem);
             }
-            const uint16_t h16 = f32_to_bf16_rn(av);
-            const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
-            // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
-            const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
-            hi[off] = h16;
-            lo[off] = f32_to_bf16_rn(rem);
           }
         }
         fence_proxy_async();
@@ -545,22 +627,33 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           d2f[pb].flip();
           fence_after();
           const int mt0 = ps * PASS_TILES, mt_end = min(mtiles, mt0 + PASS_TILES);
-          for (int mt = mt0; mt < mt_end; ++mt) {
-            float y[16];
-            tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) +
-                          static_cast<uint32_t>(D2_COL0 + pb * 128 + (mt - mt0) * 16),
-                      y);
-            const int orow = mt * 128 + 32 * q + lane;
-            if (a.global_acc) {
-              float* P = a.partial + static_cast<long long>(b + prev.o) * T * d;
-              const float* gsl = gate_s + seg_slot[(i - 1) & 1] * 16;
-#pragma unroll
-              for (int t = 0; t < 16; ++t)
-                if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += y[t];
+          const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0 + pb * 128);
+          float* P = a.partial + static_cast<long long>(b + prev.o) * T * d;
+          const float* gsl = gate_s + seg_slot[(i - 1) & 1] * 16;
+          for (int mt = mt0; mt < mt_end; mt += 2) {
+            // two M-tiles per wait; only the first T token columns matter
+            uint32_t y0[16], y1[16];
+            const bool two = mt + 1 < mt_end;
+            if (T <= 8) {
+              tmem_ld8_nw(tbase + static_cast<uint32_t>((mt - mt0) * 16), y0);
+              if (two) tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + 1 - mt0) * 16), y1);
             } else {
+              tmem_ld16_nw(tbase + static_cast<uint32_t>((mt - mt0) * 16), y0);
+              if (two) tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + 1 - mt0) * 16), y1);
+            }
+            tmem_wait_ld();
+            for (int h = 0; h < (two ? 2 : 1); ++h) {
+              const uint32_t* yy = h ? y1 : y0;
+              const int orow = (mt + h) * 128 + 32 * q + lane;
+              if (a.global_acc) {
 #pragma unroll
-              for (int t = 0; t < 16; ++t)
-                if (t < T) ysum[static_cast<size_t>(t) * d + orow] += y[t];
+                for (int t = 0; t < 16; ++t)
+                  if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += __uint_as_float(yy[t]);
+              } else {
+#pragma unroll
+                for (int t = 0; t < 16; ++t)
+                  if (t < T) ysum[static_cast<size_t>(t) * d + orow] += __uint_as_float(yy[t]);
+              }
             }
           }
           fence_before();
@@ -643,7 +736,8 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
 }  // namespace dev
 
 size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc) {
-  return static_cast<size_t>(n_stages) * dev::tc::STAGE_BYTES + 2 * 2 * 4096 + 64 * 17 * 4 +
+  return static_cast<size_t>(n_stages) * dev::tc::STAGE_BYTES + 2 * 2 * 4096 + 2 * 64 * 17 * 4 +
+         dev::tc::ENT_PRE * (16 * 8 + 4) +
          (global_acc ? 0 : static_cast<size_t>(T) * d * 4) + 2 * 16 * 4 * 2 + 16 + 8 + 8 * (2 * n_stages + 12);
 }
 
@@ -652,6 +746,11 @@ size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc) {
 // dependent global read-modify-writes on the drain's critical path and loses
 // ~30% even with a deeper ring, so it is only the fallback for large T x d.
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
+  // Leave room on the SM for one combine CTA (2 KiB static + 1 KiB reserve)
+  // next to the K3 CTA (+1 KiB reserve) of 228 KiB: programmatic dependent
+  // launch only overlaps the two kernels when they can co-reside.
+  constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 2048 + 1024;
+  if (smem_limit > kSmPerSm - kReserve - kCombine) smem_limit = kSmPerSm - kReserve - kCombine;
   if (accum != 2)
     for (int ns = 12; ns >= (accum == 1 ? 2 : 4); --ns)
       if (ffn_tc_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_tc_smem_bytes(T, d, ns, false)};
