@@ -16,7 +16,7 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "_lib", "libmoespac.so")
+LIB_PATH = os.environ.get("MOESPAC_LIB") or os.path.join(_PKG, "_lib", "libmoespac.so")  # override: A/B builds
 HEADER = os.path.join(_ROOT, "include", "moespac", "moespac.h")
 
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_RANGE", 3: "E_LOGIC", 4: "E_IO", 5: "E_CUDA", 6: "E_NCCL", 7: "E_NOMEM"}

@@ -22,7 +22,7 @@ LIB = os.path.join(OUT_DIR, "libmoespac.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++20", "-O3", "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall", "-I", os.path.join(ROOT, "include")]
-CU_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+CU_FLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"] + os.environ.get("MOESPAC_NVCC_EXTRA", "").split()
 
 SOURCES = [
     "kernels/router_hist.cu",

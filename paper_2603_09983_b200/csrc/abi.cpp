@@ -466,6 +466,7 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.expert_elems = 3LL * a->d_model * a->d_ffn;
     f.partial = a->workspace_dev;
     f.n_stages = plan.n_stages;
+    f.ring_bytes = plan.n_stages * 1024;
     f.global_acc = plan.global_acc ? 1 : 0;
     f.hT = a->hT_dev;
     f.dbg = reinterpret_cast<unsigned long long*>(a->debug_ts_dev);

@@ -63,7 +63,7 @@ void ColdExecutor::chunk(const ColdItem& it, int c, const float* hf, float* y, s
   const uint16_t* base = it.image + static_cast<size_t>(c) * 3 * R * d;
   if (layout_ == 2) {
     // gate|up K-tiles [128 rows][64 k]: element (row, kk) at
-    // (row>>3)*512 + (kk>>3)*64 + (row&7)*8 + (kk&7)
+    // (row>>3)*512 + (kk>>3)*64 + (row&7)*8 + (kk&7); rows ordered by quarter
     for (int kt = 0; kt < d / 64; ++kt) {
       const uint16_t* tile = base + static_cast<size_t>(kt) * 8192;
       for (int row = 0; row < 128; ++row) {
@@ -71,7 +71,9 @@ void ColdExecutor::chunk(const ColdItem& it, int c, const float* hf, float* y, s
         const uint16_t* rp = tile + (row >> 3) * 512 + (row & 7) * 8;
         for (int j = 0; j < 8; ++j)
           for (int e = 0; e < 8; ++e) w[j * 8 + e] = bf(rp[j * 64 + e]);
-        float* ar = acc + row * 16;
+        // 16-row quarter q = row / 32: 16 gate rows then 16 up rows
+        const int qq = row >> 5, s = row & 31;
+        float* ar = acc + (s < 16 ? qq * 16 + s : R + qq * 16 + (s - 16)) * 16;
         for (int i = 0; i < n; ++i) {
           const float* hv = hf + static_cast<size_t>(it.tok[i]) * d + kt * 64;
           float s = 0.f;

@@ -459,6 +459,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.expert_elems = image_elems_;
     fa.partial = work_d_;
     fa.n_stages = stages_;
+    fa.ring_bytes = stages_ * 1024;
     fa.global_acc = global_acc_ ? 1 : 0;
     fa.hT = hT[l & 1];
     if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");

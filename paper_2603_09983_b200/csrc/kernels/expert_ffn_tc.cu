@@ -45,7 +45,8 @@ constexpr int THREADS = 192;
 constexpr int EPI_THREADS = 128;
 constexpr int A_BYTES = 16384;
 constexpr int B_BYTES = 2048;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int QBYTES = 4096;     // one 16-row quarter of a 128-row tile (gate|up or down)
+constexpr int NSLOT = 32;        // ring entries in flight (mbarrier pairs)
 constexpr int FCH = 64;  // ffn rows per chunk
 constexpr int QROWS = 16;
 constexpr int TMEM_COLS = 512;
@@ -145,6 +146,45 @@ struct SegIter {
   }
 };
 
+// Ring entries. One entry carries m consecutive K-tiles (gate/up: A parts
+// of the segment's quarters + the matching h^T slices) or m consecutive
+// M-tiles (down) of one segment, so the per-entry bookkeeping of the
+// producer and MMA warps (~500 cycles of dependent single-warp work) is
+// amortised over >= 24 KiB whatever the segment's width: m grows as the
+// segment narrows.
+__device__ __forceinline__ int pow2_divisor(int x, int cap) {
+  int m = 1;
+  while (m < cap && x % (2 * m) == 0) m *= 2;
+  return m;
+}
+__device__ __forceinline__ int tiles_per_entry(int nq, int cap) {
+  const int t = nq >= 3 ? 2 : (nq == 2 ? 4 : 8);
+  return t < cap ? t : cap;
+}
+struct Geom {  // one entry: bytes, tiles, read window (bytes from the entry start)
+  uint32_t size, win;
+  int m;
+};
+__device__ __forceinline__ Geom gu_geom(int nq, int cap) {
+  const int m = tiles_per_entry(nq, cap);
+  const uint32_t a = static_cast<uint32_t>(nq) * 4096u;
+  const uint32_t size = static_cast<uint32_t>(m) * (a + 2048u);
+  // tile j's A descriptor reads the 16 KiB window at j*a - qa*4096
+  const uint32_t w = static_cast<uint32_t>(m - 1) * a + 16384u;
+  return {size, size > w ? size : w, m};
+}
+__device__ __forceinline__ Geom dn_geom(int nq, int cap) {
+  const int m = tiles_per_entry(nq, cap);
+  const uint32_t size = static_cast<uint32_t>(m) * static_cast<uint32_t>(nq) * 4096u;
+  return {size, size, m};
+}
+__device__ __forceinline__ uint32_t ring_place(uint32_t& head, const Geom& g, uint32_t rb) {
+  uint32_t e = head;
+  if (e + g.win > rb) e = 0;
+  head = e + ((g.size + 1023u) & ~1023u);
+  return e;
+}
+
 constexpr int DBG = 16;  // debug slots per CTA
 
 __device__ __forceinline__ void stamp(const FfnArgs& a, int slot) {
@@ -174,22 +214,21 @@ __device__ __forceinline__ const uint16_t* entry_weights(const FfnArgs& a, int o
 
 __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int ns = a.n_stages;
   const int d = a.d, T = a.T;
   const int ktiles = d / 64, mtiles = d / 128;
   const int passes = (mtiles + PASS_TILES - 1) / PASS_TILES;
   const long long chunk_elems = 3LL * FCH * d;
   const int qpe = a.ffn / QROWS;
 
+  // [a^T 16 KiB][ring][ysum][small]: the a^T buffers sit right before the
+  // ring so that a shifted A descriptor of a partial entry (up to 12 KiB
+  // before the entry) still addresses this CTA's shared memory.
+  const uint32_t RB = static_cast<uint32_t>(a.ring_bytes);
   uint8_t* p = smem_raw;
-  uint8_t* ring = p;
-  p += static_cast<size_t>(ns) * STAGE_BYTES;
   uint8_t* aT = p;  // [2 buf][2 part][4096]
   p += 2 * 2 * 4096;
-  float* u_s = reinterpret_cast<float*>(p);  // [64][17] up rows of D1 (padded: conflict-free)
-  p += 64 * 17 * 4;
-  float* g_s = reinterpret_cast<float*>(p);  // [64][17] gate rows of D1
-  p += 64 * 17 * 4;
+  uint8_t* ring = p;
+  p += RB;
   float* ysum = reinterpret_cast<float*>(p);  // [T][d] (unless global_acc)
   if (!a.global_acc) p += static_cast<size_t>(T) * d * 4;
   float* gate_s = reinterpret_cast<float*>(p);  // [2 slots][16] per-token gate of the entry
@@ -207,8 +246,8 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   p += ENT_PRE * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
   uint64_t* full = bars;
-  uint64_t* empty = full + ns;
-  uint64_t* d1_full = empty + ns;   // [2]
+  uint64_t* empty = full + NSLOT;
+  uint64_t* d1_full = empty + NSLOT; // [2]
   uint64_t* d1_empty = d1_full + 2; // [2]
   uint64_t* at_full = d1_empty + 2; // [2]
   uint64_t* at_empty = at_full + 2; // [2]
@@ -228,7 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   if (q0 >= q1) return;
 
   if (tid == 0) {
-    for (int i = 0; i < ns; ++i) {
+    for (int i = 0; i < NSLOT; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -304,83 +343,131 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   //   GU(0), GU(1), DN(0), GU(2), DN(1), ..., DN(last)
   // so the tensor core streams chunk i+1's gate/up tiles while the epilogue
   // turns chunk i's D1 into a^T; DN(i) then finds a^T(i) ready.
+  // tiles per ring entry are powers of two dividing the tile counts (and
+  // the D2 pass, so a down entry never straddles two passes)
+  const int kcap = pow2_divisor(ktiles, 8), mcap = pow2_divisor(mtiles, PASS_TILES);
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     // The whole warp walks the loop in convergent flow (addresses stay in
-    // uniform registers); one elected lane issues each copy.
+    // uniform registers); one elected lane issues each copy. Entries are
+    // allocated back to back in a byte ring (a partial segment's tiles cost
+    // only its quarters' bytes) and released in order by the MMA commits.
     {
       const bool leader = elect_one();
       long long w_empty = 0;
       const uint64_t pol = a.l2_policy == 1 ? l2_evict_normal_policy() : l2_evict_first_policy();
-      Ring r;
+      const uint8_t* hTb = reinterpret_cast<const uint8_t*>(a.hT);
+      uint32_t head = 0, idx = 0, tail = 0;
+      // In-flight entry table, one ring slot per lane (NSLOT == 32): lane s
+      // holds the offset / size / sequence number of the entry in slot s,
+      // so "does the new entry overlap any in-flight one" is one warp vote
+      // (no shared-memory FIFO: the producer's shared-memory loads would
+      // queue behind the epilogue's shared-memory traffic).
+      uint32_t my_off = 0, my_size = 0, my_idx = 0xFFFFFFFFu;
+      // place an entry; waits (oldest first) for the MMA to release what it
+      // would overwrite. Returns false (nothing placed) if it would wait and
+      // !may_wait.
+      auto reserve = [&](const Geom& g, bool may_wait, uint32_t& e) -> bool {
+        e = head;
+        if (e + g.win > RB) e = 0;
+        for (;;) {
+          const bool mine = my_idx != 0xFFFFFFFFu && my_idx >= tail && my_off < e + g.size && e < my_off + my_size;
+          const bool over = idx - tail >= static_cast<uint32_t>(NSLOT) || __any_sync(0xffffffffu, mine);
+          if (!over) break;
+          if (!may_wait) return false;
+          wait_acc(a, &empty[tail % NSLOT], (tail / NSLOT) & 1u, w_empty);
+          ++tail;
+        }
+        if (lane == static_cast<int>(idx % NSLOT)) {
+          my_off = e;
+          my_size = g.size;
+          my_idx = idx;
+        }
+        head = e + ((g.size + 1023u) & ~1023u);
+        return true;
+      };
+      // A parts of tiles [t0, t0 + m) of a segment: one copy when the
+      // segment is a whole chunk (tiles are contiguous), else one per tile
+      auto copy_tiles = [&](const uint8_t* base, int t0, int m, int qa, int nq, uint32_t e, uint64_t* bar) {
+        if (!leader) return;
+        if (nq == 4) {
+          bulk_g2s(ring + e, base + static_cast<size_t>(t0) * A_BYTES, static_cast<uint32_t>(m) * A_BYTES, bar, pol);
+        } else {
+          const uint32_t ab = static_cast<uint32_t>(nq) * QBYTES;
+          for (int j = 0; j < m; ++j)
+            bulk_g2s(ring + e + j * ab, base + static_cast<size_t>(t0 + j) * A_BYTES + qa * QBYTES, ab, bar, pol);
+        }
+      };
+      auto seg_base = [&](const Seg& s) {
+        return reinterpret_cast<const uint8_t*>(entry_weights(a, s.o, n_hits) + s.c * chunk_elems);
+      };
       SegIter it{q0, q1, qpe};
       Seg cur, prev;
       bool more = it.next(cur), has_prev = false;
-      // Weights do not depend on the previous kernel: put the first ring's
-      // worth of gate/up weight copies in flight, then wait, then add their
-      // h^T slices.
+      const uint8_t* cur_base = seg_base(cur);
+      const uint8_t* prev_base = cur_base;
+      // Weights do not depend on the previous kernel: put as many of the
+      // first segment's gate/up weight copies in flight as fit without
+      // waiting, then wait for the predecessor, then add their h^T slices.
       int kt0 = 0;
       {
-        const uint8_t* base =
-            reinterpret_cast<const uint8_t*>(entry_weights(a, cur.o, n_hits) + cur.c * chunk_elems);
-        const uint32_t gseg = static_cast<uint32_t>(cur.qb - cur.qa) * 2048u;
-        kt0 = min(ns, ktiles);
-        for (int kt = 0; kt < kt0; ++kt) {
-          uint8_t* st = ring + static_cast<size_t>(kt) * STAGE_BYTES;
-          if (leader) mbar_arrive_expect_tx(&full[kt], 2 * gseg + B_BYTES);
-          const uint8_t* tile = base + static_cast<size_t>(kt) * A_BYTES;
-          if (gseg == 8192u) {
-            if (leader) bulk_g2s(st, tile, A_BYTES, &full[kt], pol);
-          } else {
-            if (leader) bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[kt], pol);
-            if (leader) bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[kt], pol);
-          }
+        const int nq = cur.qb - cur.qa;
+        const Geom g = gu_geom(nq, kcap);
+        int np = 0;
+        uint32_t e;
+        while (kt0 < ktiles && reserve(g, false, e)) {
+          if (leader) mbar_arrive_expect_tx(&full[idx % NSLOT], g.size);
+          copy_tiles(cur_base, kt0, g.m, cur.qa, nq, e, &full[idx % NSLOT]);
+          ++idx;
+          ++np;
+          kt0 += g.m;
         }
         pdl_wait();
-        for (int kt = 0; kt < kt0; ++kt)
-          if (leader) bulk_g2s(ring + static_cast<size_t>(kt) * STAGE_BYTES + A_BYTES,
-                   reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES, B_BYTES, &full[kt],
-                   pol);
-        for (int kt = 0; kt < kt0; ++kt) r.advance(ns);
+        // the prefetched entries lie back to back from offset 0 (no wrap)
+        const uint32_t span = (g.size + 1023u) & ~1023u, ab = static_cast<uint32_t>(g.m * nq) * QBYTES;
+        for (int j = 0; j < np; ++j)
+          if (leader)
+            bulk_g2s(ring + j * span + ab, hTb + static_cast<size_t>(j * g.m) * B_BYTES,
+                     static_cast<uint32_t>(g.m) * B_BYTES, &full[j], pol);
       }
       while (more || has_prev) {
         if (more) {
-          const uint8_t* base =
-              reinterpret_cast<const uint8_t*>(entry_weights(a, cur.o, n_hits) + cur.c * chunk_elems);
-          const uint32_t gseg = static_cast<uint32_t>(cur.qb - cur.qa) * 2048u;
-          for (int kt = kt0; kt < ktiles; ++kt) {
-            wait_acc(a, &empty[r.stage], r.ph ^ 1u, w_empty);
-            uint8_t* st = ring + static_cast<size_t>(r.stage) * STAGE_BYTES;
-            if (leader) mbar_arrive_expect_tx(&full[r.stage], 2 * gseg + B_BYTES);
-            const uint8_t* tile = base + static_cast<size_t>(kt) * A_BYTES;
-            if (gseg == 8192u) {
-              if (leader) bulk_g2s(st, tile, A_BYTES, &full[r.stage], pol);
-            } else {
-              if (leader) bulk_g2s(st + cur.qa * 2048, tile + cur.qa * 2048, gseg, &full[r.stage], pol);
-              if (leader) bulk_g2s(st + 8192 + cur.qa * 2048, tile + 8192 + cur.qa * 2048, gseg, &full[r.stage], pol);
-            }
-            if (leader) bulk_g2s(st + A_BYTES, reinterpret_cast<const uint8_t*>(a.hT) + static_cast<size_t>(kt) * B_BYTES,
-                     B_BYTES, &full[r.stage], pol);
-            r.advance(ns);
+          const int nq = cur.qb - cur.qa;
+          const Geom g = gu_geom(nq, kcap);
+          const uint32_t ab = static_cast<uint32_t>(g.m * nq) * QBYTES;
+          for (int kt = kt0; kt < ktiles; kt += g.m) {
+            uint32_t e;
+            reserve(g, true, e);
+            uint64_t* bar = &full[idx % NSLOT];
+            if (leader) mbar_arrive_expect_tx(bar, g.size);
+            copy_tiles(cur_base, kt, g.m, cur.qa, nq, e, bar);
+            if (leader)
+              bulk_g2s(ring + e + ab, hTb + static_cast<size_t>(kt) * B_BYTES, static_cast<uint32_t>(g.m) * B_BYTES,
+                       bar, pol);
+            ++idx;
           }
           kt0 = 0;
         }
         if (has_prev) {
-          const uint8_t* base =
-              reinterpret_cast<const uint8_t*>(entry_weights(a, prev.o, n_hits) + prev.c * chunk_elems);
-          const uint32_t dseg = static_cast<uint32_t>(prev.qb - prev.qa) * 4096u;
-          for (int mt = 0; mt < mtiles; ++mt) {
-            wait_acc(a, &empty[r.stage], r.ph ^ 1u, w_empty);
-            uint8_t* st = ring + static_cast<size_t>(r.stage) * STAGE_BYTES;
-            if (leader) mbar_arrive_expect_tx(&full[r.stage], dseg);
-            const uint8_t* tile = base + static_cast<size_t>(ktiles + mt) * A_BYTES;
-            if (leader) bulk_g2s(st + prev.qa * 4096, tile + prev.qa * 4096, dseg, &full[r.stage], pol);
-            r.advance(ns);
+          const int nq = prev.qb - prev.qa;
+          const Geom g = dn_geom(nq, mcap);
+          const uint8_t* dbase = prev_base + static_cast<size_t>(ktiles) * A_BYTES;
+          for (int mt = 0; mt < mtiles; mt += g.m) {
+            uint32_t e;
+            reserve(g, true, e);
+            uint64_t* bar = &full[idx % NSLOT];
+            if (leader) mbar_arrive_expect_tx(bar, g.size);
+            copy_tiles(dbase, mt, g.m, prev.qa, nq, e, bar);
+            ++idx;
           }
         }
         has_prev = more;
         prev = cur;
-        if (more) more = it.next(cur);
+        prev_base = cur_base;
+        if (more) {
+          more = it.next(cur);
+          if (more) cur_base = seg_base(cur);
+        }
       }
       if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
     }
@@ -388,12 +475,13 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
     // ------------------------------------------------ MMA issuer
     // Whole warp in convergent flow so descriptors are warp-uniform (no
     // per-MMA R2UR waterfall); one elected lane issues MMAs and commits.
+    // Entry offsets follow the producer's allocation rule.
     {
       const bool leader = elect_one();
       long long w_full = 0, w_at = 0, w_d2e = 0, w_d1e = 0;
-      Ring r;
       Phase d1e[2], ate[2], d2e[2];
       int c3 = 0;  // D2 pass buffer counter
+      uint32_t head = 0, idx = 0;
       SegIter it{q0, q1, qpe};
       Seg cur, prev;
       bool more = it.next(cur), has_prev = false;
@@ -407,59 +495,74 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           d1e[b1].flip();
           fence_after();
           const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
-          for (int kt = 0; kt < ktiles; ++kt) {
-            wait_acc(a, &full[r.stage], r.ph, w_full);
+          const int nq = cur.qb - cur.qa;
+          const Geom g = gu_geom(nq, kcap);
+          const uint32_t ab = static_cast<uint32_t>(nq) * QBYTES;
+          for (int kt = 0; kt < ktiles; kt += g.m) {
+            const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
+            wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
+            ++idx;
             if (i == 0 && kt == 0 && leader) stamp(a, 2);
             fence_after();
-            const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
-            const uint64_t adesc = smem_desc(sa, 128, 1024), bdesc = smem_desc(sa + A_BYTES, 128, 1024);
+            // shifted base: rows of quarter qa of tile j land at off + j*ab
+            const uint32_t va = ring_addr + off - static_cast<uint32_t>(cur.qa) * QBYTES;
+            const uint32_t vb = ring_addr + off + static_cast<uint32_t>(g.m) * ab;
             if (leader) {
+              for (int j = 0; j < g.m; ++j) {
+                const uint64_t adesc = smem_desc(va + j * ab, 128, 1024), bdesc = smem_desc(vb + j * B_BYTES, 128, 1024);
 #pragma unroll
-              for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
-                mma_bf16(d1, adesc + 16 * k, bdesc + 16 * k, (kt | k) != 0);
-              mma_commit(&empty[r.stage]);
+                for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
+                  mma_bf16(d1, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0);
+              }
+              mma_commit(&empty[slot]);
             }
             __syncwarp();
-            r.advance(ns);
           }
           if (leader) mma_commit(&d1_full[b1]);
           __syncwarp();
           if (i == 0 && leader) stamp(a, 3);
         }
         if (has_prev) {  // DN(i-1): D2 = W_down x a^T(i-1), hi + lo
-          const int ab = (i - 1) & 1;
-          wait_acc(a, &at_full[ab], ate[ab].bit, w_at);
-          ate[ab].flip();
+          const int ab_ = (i - 1) & 1;
+          wait_acc(a, &at_full[ab_], ate[ab_].bit, w_at);
+          ate[ab_].flip();
           fence_after();
-          const uint32_t ahi = at_addr + static_cast<uint32_t>(ab) * 8192u;
+          const uint32_t ahi = at_addr + static_cast<uint32_t>(ab_) * 8192u;
           const uint64_t bhi = smem_desc(ahi, 256, 128), blo = smem_desc(ahi + 4096u, 256, 128);
+          const int nq = prev.qb - prev.qa;
+          const Geom g = dn_geom(nq, mcap);
+          const uint32_t tb = static_cast<uint32_t>(nq) * QBYTES;
           for (int ps = 0; ps < passes; ++ps) {
             const int pb = c3 & 1;
             wait_acc(a, &d2_empty[pb], d2e[pb].bit ^ 1u, w_d2e);
             d2e[pb].flip();
             fence_after();
             const int mt_end = min(mtiles, (ps + 1) * PASS_TILES);
-            for (int mt = ps * PASS_TILES; mt < mt_end; ++mt) {
-              wait_acc(a, &full[r.stage], r.ph, w_full);
+            for (int mt = ps * PASS_TILES; mt < mt_end; mt += g.m) {
+              const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
+              wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
+              ++idx;
               fence_after();
-              const uint32_t sa = ring_addr + static_cast<uint32_t>(r.stage) * STAGE_BYTES;
-              const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>(pb * 128 + (mt - ps * PASS_TILES) * 16);
-              const uint64_t adn = smem_desc(sa, 2048, 128);
+              const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * QBYTES;
               if (leader) {
-                for (int k = prev.qa; k < prev.qb; ++k) {  // +4096 B (A) / +512 B (a^T) per K=16 step
-                  mma_bf16(d2, adn + 256 * k, bhi + 32 * k, k == prev.qa ? 0u : 1u);
-                  mma_bf16(d2, adn + 256 * k, blo + 32 * k, 1u);
+                for (int j = 0; j < g.m; ++j) {
+                  const uint32_t d2 =
+                      tmem + D2_COL0 + static_cast<uint32_t>(pb * 128 + (mt + j - ps * PASS_TILES) * 16);
+                  const uint64_t adn = smem_desc(va + j * tb, 2048, 128);
+                  for (int k = prev.qa; k < prev.qb; ++k) {  // +4096 B (A) / +512 B (a^T) per K=16 step
+                    mma_bf16(d2, adn + 256 * k, bhi + 32 * k, k == prev.qa ? 0u : 1u);
+                    mma_bf16(d2, adn + 256 * k, blo + 32 * k, 1u);
+                  }
                 }
-                mma_commit(&empty[r.stage]);
+                mma_commit(&empty[slot]);
               }
               __syncwarp();
-              r.advance(ns);
             }
             if (leader) mma_commit(&d2_full[pb]);
             __syncwarp();
             ++c3;
           }
-          if (leader) mma_commit(&at_empty[ab]);
+          if (leader) mma_commit(&at_empty[ab_]);
           __syncwarp();
         }
         has_prev = more;
@@ -581,34 +684,31 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d1_empty[b1]);
-        const int row = 32 * q + lane;  // D1 row: < 64 gate, >= 64 up
-        {
-          float* dst = row < 64 ? g_s + row * 17 : u_s + (row - 64) * 17;
-#pragma unroll
-          for (int t = 0; t < 16; ++t)
-            if (t < T) dst[t] = v[t];
-        }
         const int ab = i & 1;
         // a^T buffer ab is free once DN(i-2) completed
         mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);
         atf[ab].flip();
-        named_bar_sync(2, EPI_THREADS);
-        {
-          // all 128 epilogue threads: row f of the segment's quarters, every
-          // other real token (a = silu(g) * u * gate_t, split into bf16 hi+lo)
-          const int f = et & 63;
-          if (f >= cur.qa * QROWS && f < cur.qb * QROWS) {
-            uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
-            uint16_t* lo = hi + 2048;
-            for (int t = et >> 6; t < T; t += 2) {
-              const float g = g_s[f * 17 + t];
-              const float av = g / (1.f + __expf(-g)) * u_s[f * 17 + t] * gs[t];
-              const uint16_t h16 = f32_to_bf16_rn(av);
-              const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
-              // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
-              const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
-              hi[off] = h16;
-              lo[off] = f32_to_bf16_rn(rem);
+        // This warp's TMEM lanes are chunk quarter q: lanes 0-15 hold the
+        // gate rows f = 16q + s, lanes 16-31 the up rows of the same f.
+        if (q >= cur.qa && q < cur.qb) {
+          const int s = lane & 15, f = 16 * q + s;
+          uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
+          uint16_t* lo = hi + 2048;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            if (t < T) {
+              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 16);
+              if ((t & 1) == (lane >> 4)) {  // lanes 0-15 even tokens, 16-31 odd tokens
+                const float g = lane < 16 ? v[t] : pv;
+                const float u = lane < 16 ? pv : v[t];
+                const float av = g / (1.f + __expf(-g)) * u * gs[t];
+                const uint16_t h16 = f32_to_bf16_rn(av);
+                const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
+                // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
+                const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
+                hi[off] = h16;
+                lo[off] = f32_to_bf16_rn(rem);
+              }
             }
           }
         }
@@ -716,9 +816,11 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
       const long long kt = r0 / 8192;
       const int w = static_cast<int>(r0 % 8192);
       const int g = w >> 9, j = (w >> 6) & 7, r = (w >> 3) & 7, e = w & 7;
-      const int row = g * 8 + r;
+      const int row = g * 8 + r;            // quarter q = row / 32: 16 gate rows then 16 up rows
+      const int qq = row >> 5, s = row & 31;
+      const long long f = c * FCH + qq * 16 + (s & 15);
       const long long k = kt * 64 + j * 8 + e;
-      v = row < FCH ? wg[(c * FCH + row) * d + k] : wu[(c * FCH + row - FCH) * d + k];
+      v = s < 16 ? wg[f * d + k] : wu[f * d + k];
     } else {
       const long long r2 = r0 - gu;
       const long long mt = r2 / 8192;
@@ -735,27 +837,34 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
 }  // namespace tc
 }  // namespace dev
 
-size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc) {
-  return static_cast<size_t>(n_stages) * dev::tc::STAGE_BYTES + 2 * 2 * 4096 + 2 * 64 * 17 * 4 +
-         dev::tc::ENT_PRE * (16 * 8 + 4) +
-         (global_acc ? 0 : static_cast<size_t>(T) * d * 4) + 2 * 16 * 4 * 2 + 16 + 8 + 8 * (2 * n_stages + 12);
+size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, bool global_acc) {
+  return 2 * 2 * 4096 + static_cast<size_t>(ring_bytes) + (global_acc ? 0 : static_cast<size_t>(T) * d * 4) +
+         2 * 16 * 4 * 2 + 16 + dev::tc::ENT_PRE * (16 * 8 + 4) + 8 +
+         8 * (2 * dev::tc::NSLOT + 12);
 }
 
-// accum: 0 auto (shared memory when it leaves a >= 4-deep ring), 1 shared-memory
+// accum: 0 auto (shared memory when it leaves a >= 64 KiB ring), 1 shared-memory
 // accumulator, 2 global (L2) accumulator. Measured: the L2 accumulator puts
 // dependent global read-modify-writes on the drain's critical path and loses
 // ~30% even with a deeper ring, so it is only the fallback for large T x d.
+// FfnPlan::n_stages reports the ring size in KiB.
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
   // Leave room on the SM for one combine CTA (2 KiB static + 1 KiB reserve)
   // next to the K3 CTA (+1 KiB reserve) of 228 KiB: programmatic dependent
   // launch only overlaps the two kernels when they can co-reside.
   constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 2048 + 1024;
   if (smem_limit > kSmPerSm - kReserve - kCombine) smem_limit = kSmPerSm - kReserve - kCombine;
-  if (accum != 2)
-    for (int ns = 12; ns >= (accum == 1 ? 2 : 4); --ns)
-      if (ffn_tc_smem_bytes(T, d, ns, false) <= smem_limit) return {ns, false, ffn_tc_smem_bytes(T, d, ns, false)};
-  for (int ns = 12; ns >= 2; --ns)
-    if (ffn_tc_smem_bytes(T, d, ns, true) <= smem_limit) return {ns, true, ffn_tc_smem_bytes(T, d, ns, true)};
+  auto ring_for = [&](bool g) -> int {
+    const size_t fixed = ffn_tc_smem_bytes(T, d, 0, g);
+    if (fixed + 32768 > smem_limit) return 0;
+    return static_cast<int>(((smem_limit - fixed) / 1024) * 1024);
+  };
+  if (accum != 2) {
+    const int rb = ring_for(false);
+    if (rb >= (accum == 1 ? 32768 : 65536)) return {rb / 1024, false, ffn_tc_smem_bytes(T, d, rb, false)};
+  }
+  const int rb = ring_for(true);
+  if (rb >= 32768) return {rb / 1024, true, ffn_tc_smem_bytes(T, d, rb, true)};
   return {0, false, 0};
 }
 

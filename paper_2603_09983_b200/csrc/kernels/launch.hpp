@@ -40,7 +40,8 @@ struct FfnArgs {
   int n_shared;
   long long expert_elems;   // 3*ffn*d
   float* partial;           // [(grid + N + n_shared)][T][d]
-  int n_stages;
+  int n_stages;             // CUDA-core kernel: ring stages
+  int ring_bytes;           // tensor-core kernel: byte-ring size
   int global_acc;           // 1: accumulate down-proj partials in `partial` (large T*d)
   const uint16_t* hT;       // tcgen05 variant: h^T UMMA image [d/64][16 tok][64] (build_hT)
   unsigned long long* dbg;  // optional per-CTA %globaltimer stamps [grid][8] (profiling)
@@ -76,7 +77,7 @@ struct FfnPlan {
 size_t ffn_smem_bytes(int T, int d, int n_stages, bool global_acc);
 FfnPlan ffn_plan(int T, int d, size_t smem_limit);
 cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
-size_t ffn_tc_smem_bytes(int T, int d, int n_stages, bool global_acc);
+size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, bool global_acc);
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum = 0);
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
 cudaError_t launch_build_hT(const uint16_t* h, int T, int d, uint16_t* out, cudaStream_t stream, bool pdl = false);
