@@ -220,7 +220,7 @@ typedef struct moespac_ffn_args {
   int32_t grid;                /* 0 = one CTA per SM */
   int32_t kernel;              /* MOESPAC_FFN_* (image layout must match) */
   const uint16_t* hT_dev;      /* tensor-core kernel: moespac_build_hT(h) image */
-  uint64_t* debug_ts_dev;      /* optional [grid][8] per-CTA %globaltimer stamps (profiling), or NULL */
+  uint64_t* debug_ts_dev;      /* optional [grid][32] per-CTA profiling record (%globaltimer stamps, wait counters), or NULL */
   int32_t accum;               /* tensor-core kernel: 0 auto, 1 shared-memory, 2 L2 (partial-block) accumulator */
   int32_t l2_policy;           /* weight stream L2 policy: 0 evict_first (default), 1 evict_normal */
 } moespac_ffn_args;
@@ -292,6 +292,10 @@ moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
 moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
 /* Programmatic dependent launch between layer kernels (on by default). */
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
+/* Profiling hook: device buffer of [n_layers][grid][32] uint64 that every
+ * following step's tensor-core K3 launches fill with per-CTA %globaltimer
+ * stamps and wait counters (layer l at offset l*grid*32), or NULL to stop. */
+moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a
  * step runs on it, so events recorded there bracket whole steps. */
 void* moespac_ctx_stream(const moespac_ctx* c);

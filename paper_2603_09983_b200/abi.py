@@ -166,6 +166,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
         "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
         "moespac_step": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
@@ -421,6 +422,10 @@ class Context:
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))
+
+    def set_k3_trace(self, buf_ptr):
+        """Profiling: per-CTA K3 stamps into a device buffer [L][grid][32] int64 (None: off)."""
+        check(lib().moespac_ctx_set_k3_trace(self._h, buf_ptr))
 
     def set_nccl(self, uid: bytes, nranks: int, rank: int):
         buf = C.create_string_buffer(uid, 128)

@@ -462,6 +462,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.ring_bytes = stages_ * 1024;
     fa.global_acc = global_acc_ ? 1 : 0;
     fa.hT = hT[l & 1];
+    if (k3_trace_) fa.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
     if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
     check(tc ? launch_expert_ffn_tc(fa, sms_, ffn_smem_, compute_, pdl)
              : launch_expert_ffn(fa, sms_, ffn_smem_, compute_, pdl),

@@ -41,6 +41,7 @@ class Engine {
   void set_nccl(const void* uid, int nranks, int rank);
   void set_timing(bool on) { timing_ = on; }
   void set_pdl(bool on) { pdl_ = on; }
+  void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
   // host threads for cold (non-resident) experts: -1 auto, 0 = off (misses
   // are then counted but not computed); takes effect at finalize()
   void set_cold_threads(int n) { cold_threads_ = n; }
@@ -95,7 +96,8 @@ class Engine {
   cudaEvent_t ev_[6] = {};
   cudaEvent_t k2_done_ = nullptr;
   bool decided_ = false;  // next step's decisions already made
-  bool pdl_ = true;       // programmatic dependent launch between layer kernels
+  bool pdl_ = true;                         // programmatic dependent launch between layer kernels
+  unsigned long long* k3_trace_ = nullptr;  // profiling: [L][grid][32]
   int cold_threads_ = -1;
   int ffn_accum_ = 0;
   std::unique_ptr<ColdExecutor> cold_;

@@ -409,42 +409,88 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
 // order) are dealt round-robin to the warps, then the warp sums are added in
 // warp order — a fixed summation tree, so the result is deterministic.
 constexpr int COMBINE_WARPS = 4;  // small footprint: must co-reside with a K3 CTA (PDL)
+constexpr int COMBINE_BATCH = 16;  // partial rows in flight per warp
+constexpr int COMBINE_LIST = 48;  // per-warp row list capacity (else streamed)
 
 __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs a) {
   __shared__ float4 red[COMBINE_WARPS][32];
+  __shared__ int rows[COMBINE_WARPS][COMBINE_LIST];
   if (threadIdx.x == 0) pdl_trigger();
-  pdl_wait();  // partials of the K3 launch just before
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.y * 128 + lane * 4;
   const int qpe = a.ffn / FC;
+  // The routing (K2 outputs: counters, ids, hit order) was final several
+  // kernels ago, so the row list is built before waiting for the K3 launch
+  // whose partials it sums: only the partial loads sit on the critical path.
   const int n_hits = a.counters[7];
   const int n = (n_hits + a.n_shared) * qpe;
   const int G = a.grid;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (n > 0 && c < a.d) {
-    int idx = 0;
-    auto add_entry = [&](int o) {
+    // 1) this warp's partial rows, in the fixed order (experts ascending,
+    //    covering CTAs ascending, dealt round-robin to the warps)
+    int idx = 0, my_n = 0;
+    auto list_entry = [&](int o) {
       const int lo = ((o * qpe + 1) * G - 1) / n;
       const int hi = (((o + 1) * qpe) * G - 1) / n;
       for (int b = lo; b <= hi; ++b) {
         // with fewer work units than CTAs some CTAs own nothing
         if ((b * n) / G == ((b + 1) * n) / G) continue;
         if ((idx++ % COMBINE_WARPS) != warp) continue;
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(
-            a.partial + (static_cast<long long>(b + o) * a.T + t) * static_cast<long long>(a.d) + c));
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
+        if (lane == 0 && my_n < COMBINE_LIST) rows[warp][my_n] = b + o;
+        ++my_n;
       }
     };
     for (int j = 0; j < a.k; ++j) {
       const int o = a.hit_ord[a.ids[t * a.k + j]];
-      if (o >= 0) add_entry(o);
+      if (o >= 0) list_entry(o);
     }
-    for (int sidx = 0; sidx < a.n_shared; ++sidx) add_entry(n_hits + sidx);
+    for (int sidx = 0; sidx < a.n_shared; ++sidx) list_entry(n_hits + sidx);
+    __syncwarp();
+    pdl_wait();  // partials of the K3 launch just before
+    auto row_ptr = [&](int r) {
+      return reinterpret_cast<const float4*>(a.partial + (static_cast<long long>(r) * a.T + t) * a.d + c);
+    };
+    if (my_n <= COMBINE_LIST) {
+      // 2) COMBINE_BATCH independent loads in flight, summed in list order
+      for (int base = 0; base < my_n; base += COMBINE_BATCH) {
+        float4 v[COMBINE_BATCH];
+#pragma unroll
+        for (int u = 0; u < COMBINE_BATCH; ++u)
+          if (base + u < my_n) v[u] = __ldcg(row_ptr(rows[warp][base + u]));
+#pragma unroll
+        for (int u = 0; u < COMBINE_BATCH; ++u)
+          if (base + u < my_n) {
+            acc.x += v[u].x;
+            acc.y += v[u].y;
+            acc.z += v[u].z;
+            acc.w += v[u].w;
+          }
+      }
+    } else {  // long lists: same order, one row at a time
+      idx = 0;
+      auto add_entry = [&](int o) {
+        const int lo = ((o * qpe + 1) * G - 1) / n;
+        const int hi = (((o + 1) * qpe) * G - 1) / n;
+        for (int b = lo; b <= hi; ++b) {
+          if ((b * n) / G == ((b + 1) * n) / G) continue;
+          if ((idx++ % COMBINE_WARPS) != warp) continue;
+          const float4 v = __ldcg(row_ptr(b + o));
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
+        }
+      };
+      for (int j = 0; j < a.k; ++j) {
+        const int o = a.hit_ord[a.ids[t * a.k + j]];
+        if (o >= 0) add_entry(o);
+      }
+      for (int sidx = 0; sidx < a.n_shared; ++sidx) add_entry(n_hits + sidx);
+    }
   }
+  if (!(n > 0 && c < a.d)) pdl_wait();  // (no partials to read; still order after K3)
   red[warp][lane] = acc;
   __syncthreads();
   if (warp != 0 || c >= a.d) return;

@@ -185,7 +185,7 @@ __device__ __forceinline__ uint32_t ring_place(uint32_t& head, const Geom& g, ui
   return e;
 }
 
-constexpr int DBG = 16;  // debug slots per CTA
+constexpr int DBG = 32;  // debug slots per CTA
 
 __device__ __forceinline__ void stamp(const FfnArgs& a, int slot) {
   if (a.dbg) {
@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   // Everything below except the producer's first weight copies depends on
   // the previous kernel (h^T image, partial workspace): wait for it.
   if (warp != 0) pdl_wait();
+  if (tid == 32) stamp(a, 22);  // predecessor complete (PDL) as seen by this CTA
 
   // All three roles walk the same software-pipelined sequence of segments:
   //   GU(0), GU(1), DN(0), GU(2), DN(1), ..., DN(last)
@@ -542,6 +543,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
               const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
               wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
               ++idx;
+              if (i == 1 && mt == 0 && leader) stamp(a, 16);
               fence_after();
               const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * QBYTES;
               if (leader) {
@@ -564,6 +566,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           }
           if (leader) mma_commit(&at_empty[ab_]);
           __syncwarp();
+          if (i == 1 && leader) stamp(a, 17);
         }
         has_prev = more;
         prev = cur;
@@ -701,7 +704,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
               if ((t & 1) == (lane >> 4)) {  // lanes 0-15 even tokens, 16-31 odd tokens
                 const float g = lane < 16 ? v[t] : pv;
                 const float u = lane < 16 ? pv : v[t];
-                const float av = g / (1.f + __expf(-g)) * u * gs[t];
+                const float av = __fdividef(g, 1.f + __expf(-g)) * u * gs[t];
                 const uint16_t h16 = f32_to_bf16_rn(av);
                 const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
                 // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
@@ -725,6 +728,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           const int pb = c3 & 1;
           wait_acc(a, &d2_full[pb], d2f[pb].bit, w_d2f);
           d2f[pb].flip();
+          if (i == 1 && et == 0) stamp(a, 18 + (ps == 0 ? 0 : 1));
           fence_after();
           const int mt0 = ps * PASS_TILES, mt_end = min(mtiles, mt0 + PASS_TILES);
           const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0 + pb * 128);
@@ -749,11 +753,25 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
 #pragma unroll
                 for (int t = 0; t < 16; ++t)
                   if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += __uint_as_float(yy[t]);
-              } else {
-#pragma unroll
-                for (int t = 0; t < 16; ++t)
-                  if (t < T) ysum[static_cast<size_t>(t) * d + orow] += __uint_as_float(yy[t]);
               }
+            }
+            if (!a.global_acc) {
+              // all loads, then all stores: the T read-modify-writes of a row
+              // are independent (a += chain would serialise on each LDS)
+              float* r0 = ysum + mt * 128 + 32 * q + lane;
+              float o0[16], o1[16];
+#pragma unroll
+              for (int t = 0; t < 16; ++t)
+                if (t < T) {
+                  o0[t] = r0[static_cast<size_t>(t) * d];
+                  if (two) o1[t] = r0[static_cast<size_t>(t) * d + 128];
+                }
+#pragma unroll
+              for (int t = 0; t < 16; ++t)
+                if (t < T) {
+                  r0[static_cast<size_t>(t) * d] = o0[t] + __uint_as_float(y0[t]);
+                  if (two) r0[static_cast<size_t>(t) * d + 128] = o1[t] + __uint_as_float(y1[t]);
+                }
             }
           }
           fence_before();
@@ -761,7 +779,9 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           if (lane == 0) mbar_arrive(&d2_empty[pb]);
           ++c3;
         }
+        if (i == 1 && et == 0) stamp(a, 20);
         if (!more || cur.o != prev.o) flush(prev.o, seg_slot[(i - 1) & 1]);
+        if (i == 1 && et == 0) stamp(a, 21);
       }
       has_prev = more;
       prev = cur;
@@ -849,10 +869,10 @@ size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, bool global_acc) {
 // ~30% even with a deeper ring, so it is only the fallback for large T x d.
 // FfnPlan::n_stages reports the ring size in KiB.
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
-  // Leave room on the SM for one combine CTA (2 KiB static + 1 KiB reserve)
+  // Leave room on the SM for one combine CTA (3 KiB static + 1 KiB reserve)
   // next to the K3 CTA (+1 KiB reserve) of 228 KiB: programmatic dependent
   // launch only overlaps the two kernels when they can co-reside.
-  constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 2048 + 1024;
+  constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 3072 + 1024;
   if (smem_limit > kSmPerSm - kReserve - kCombine) smem_limit = kSmPerSm - kReserve - kCombine;
   auto ring_for = [&](bool g) -> int {
     const size_t fixed = ffn_tc_smem_bytes(T, d, 0, g);

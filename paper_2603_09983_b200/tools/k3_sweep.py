@@ -9,6 +9,8 @@ import argparse
 import ctypes
 import json
 
+import numpy as np
+
 import torch
 
 from paper_2603_09983_b200 import abi
@@ -76,7 +78,7 @@ def main():
             us = e0.elapsed_time(e1) * 1e3 / args.iters
             byts = n_hit * img * 2
             if args.stamps and kern == 2:
-                dbg = torch.zeros((sms, 16), dtype=torch.int64, device=dev)
+                dbg = torch.zeros((sms, 32), dtype=torch.int64, device=dev)
                 fa.debug_ts_dev = abi.ptr(dbg)
                 abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
                 torch.cuda.synchronize()
@@ -86,9 +88,9 @@ def main():
                 t0 = t[act, 0].min()
                 rel = (t[act] - t0) / 1e3
                 rel[t[act] == 0] = float("nan")
-                rel = rel[:, :7]
-                import numpy as np
-                names = ["entry", "prologue", "first_data", "gu0_issued", "a0_ready", "epi_done", "end"]
+                rel = np.concatenate([rel[:, :7], rel[:, 16:22]], axis=1)
+                names = ["entry", "prologue", "first_data", "gu0_issued", "a0_ready", "epi_done", "end",
+                         "dn0_data", "dn0_issued", "d2_pass0", "d2_pass1", "dn0_drained", "dn0_flushed"]
                 summ = {nm: [round(float(np.nanmin(rel[:, j])), 2), round(float(np.nanmedian(rel[:, j])), 2),
                              round(float(np.nanmax(rel[:, j])), 2)] for j, nm in enumerate(names)}
                 cyc = t[act, 7]
@@ -96,6 +98,24 @@ def main():
                          [(8, "prod_empty"), (9, "mma_full"), (10, "mma_at_full"), (11, "mma_d2_empty"),
                           (12, "mma_d1_empty"), (13, "epi_d1_full"), (14, "epi_d2_full")]}
                 print(json.dumps({"wait_frac_of_cta_cycles": waits}), flush=True)
+                # end time vs the CTA's number of segments (chunk pieces)
+                qpe = ffn // 16
+                n_q = n_hit * qpe
+                by = {}
+                ends = (t[:, 6] - t0) / 1e3
+                for b in range(sms):
+                    q0, q1 = b * n_q // sms, (b + 1) * n_q // sms
+                    if q0 >= q1 or t[b, 6] == 0:
+                        continue
+                    nseg, q = 0, q0
+                    while q < q1:
+                        q = min((q // 4 + 1) * 4, q1)
+                        nseg += 1
+                    key = f"{nseg}seg_{q1 - q0}q"
+                    by.setdefault(key, []).append(float(ends[b]))
+                print(json.dumps({"end_us_by_cta_shape": {k: [len(v), round(float(np.median(v)), 2), round(max(v), 2)]
+                                                           for k, v in sorted(by.items())}}), flush=True)
+
                 print(json.dumps({"stamps_us_min_med_max": summ, "active_ctas": int(act.sum()),
                                   "cta_clock64_cycles_med_max": [float(np.median(cyc)), float(cyc.max())],
                                   "entry_spread_us": round(float(np.nanmax(rel[:, 0])), 2)}), flush=True)

@@ -1,0 +1,80 @@
+"""Per-layer timeline of one verification step (profiling).
+
+Runs a workload like bench.py (same synthetic model and routing), then one
+device step with the K3 trace hook on, and prints per layer: when K3's CTAs
+saw their predecessor (the previous combine) complete, the K3 span, and the
+gap to the next layer:
+    python -m paper_2603_09983_b200.tools.step_trace --config qwen3
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from paper_2603_09983_b200 import abi, configs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="mixtral")
+    ap.add_argument("--cache-ratio", type=float, default=1.0)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--pdl", type=int, default=1)
+    args = ap.parse_args()
+    w = configs.CONFIGS[args.config]
+    L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
+    cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=args.cache_ratio)
+    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode, 0), cfg, 0, 1)
+    ctx.host_arena(min(L * N, max(N, 8)))
+    ctx.fill_synthetic(seed=3, stdv=0.02)
+    ctx.finalize()
+    ctx.set_pdl(bool(args.pdl))
+    synth = abi.TraceSynth(cfg)
+    S = args.warmup + 1
+    logits = torch.empty((S, L, T, N), dtype=torch.float64)
+    acc = [synth.next(logits[s].numpy())[1] for s in range(S)]
+    logits = logits.cuda()
+    h = torch.randn((S, T, d)).to(torch.bfloat16).cuda()
+    h_out = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
+    for s in range(args.warmup):
+        ctx.step_device(logits[s], h[s], acc[s], h_out)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    buf = torch.zeros((L, sms, 32), dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.set_k3_trace(abi.ptr(buf))
+    ctx.step_device(logits[S - 1], h[S - 1], acc[S - 1], h_out)
+    torch.cuda.synchronize()
+    ctx.set_k3_trace(None)
+    t = buf.cpu().numpy().astype(np.float64)
+    t0 = t[0, :, 0][t[0, :, 0] > 0].min()
+    rows = []
+    for l in range(L):
+        x = t[l]
+        act = x[:, 0] > 0
+        if not act.any():
+            rows.append({"layer": l, "ctas": 0})
+            continue
+        ent = (x[act, 0] - t0) / 1e3
+        pdl = (x[act, 22] - t0) / 1e3
+        end = (x[act, 6] - t0) / 1e3
+        rows.append({"layer": l, "ctas": int(act.sum()), "entry_min": round(ent.min(), 2),
+                     "pred_done": round(float(np.median(pdl)), 2), "end_med": round(float(np.median(end)), 2),
+                     "end_max": round(end.max(), 2)})
+    for i, r in enumerate(rows):
+        if i + 1 < L and "end_max" in r and "pred_done" in rows[i + 1]:
+            r["gap_to_next_us"] = round(rows[i + 1]["pred_done"] - r["end_max"], 2)
+            r["k3_span_us"] = round(r["end_max"] - r["pred_done"], 2)
+        print(json.dumps(r))
+    gaps = [r["gap_to_next_us"] for r in rows if "gap_to_next_us" in r]
+    spans = [r["k3_span_us"] for r in rows if "k3_span_us" in r]
+    print(json.dumps({"config": args.config, "median_gap_us": float(np.median(gaps)),
+                      "median_k3_span_us": float(np.median(spans)),
+                      "step_us": round(rows[-1]["end_max"] - rows[0]["pred_done"], 2)}))
+
+
+if __name__ == "__main__":
+    main()
