@@ -221,7 +221,7 @@ typedef struct moespac_ffn_args {
   int32_t kernel;              /* MOESPAC_FFN_* (image layout must match) */
   const uint16_t* hT_dev;      /* tensor-core kernel: moespac_build_hT(h) image */
   uint64_t* debug_ts_dev;      /* optional [grid][32] per-CTA profiling record (%globaltimer stamps, wait counters), or NULL */
-  int32_t accum;               /* tensor-core kernel: 0 auto, 1 shared-memory, 2 L2 (partial-block) accumulator */
+  int32_t accum;               /* tensor-core kernel: 0 auto, 1 shared-memory, 2 L2 (partial-block), 3 TMEM accumulator (d <= 2048) */
   int32_t l2_policy;           /* weight stream L2 policy: 0 evict_first (default), 1 evict_normal */
 } moespac_ffn_args;
 size_t moespac_ffn_workspace_bytes(int tokens, int d_model, int n_experts, int n_shared_units, int grid);
@@ -296,6 +296,11 @@ moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
  * following step's tensor-core K3 launches fill with per-CTA %globaltimer
  * stamps and wait counters (layer l at offset l*grid*32), or NULL to stop. */
 moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf);
+/* Cross-layer L2 prefetch budget per K3 CTA in bytes (tensor-core K3; 0 = off,
+ * default 384 KiB): after its last weight copy, each CTA prefetches into L2
+ * the start of its next-layer work so HBM stays busy through the launch tail
+ * and the layer handoff. */
+moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a
  * step runs on it, so events recorded there bracket whole steps. */
 void* moespac_ctx_stream(const moespac_ctx* c);

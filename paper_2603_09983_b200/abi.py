@@ -167,6 +167,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
+        "moespac_ctx_set_l2_prefetch": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
         "moespac_step": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
@@ -422,6 +423,10 @@ class Context:
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))
+
+    def set_l2_prefetch(self, nbytes: int):
+        """Per-CTA cross-layer L2 prefetch budget of the tensor-core K3 (0 = off)."""
+        check(lib().moespac_ctx_set_l2_prefetch(self._h, int(nbytes)))
 
     def set_k3_trace(self, buf_ptr):
         """Profiling: per-CTA K3 stamps into a device buffer [L][grid][32] int64 (None: off)."""

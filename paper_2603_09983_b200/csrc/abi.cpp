@@ -468,6 +468,7 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.n_stages = plan.n_stages;
     f.ring_bytes = plan.n_stages * 1024;
     f.global_acc = plan.global_acc ? 1 : 0;
+    f.acc_mode = plan.acc_mode;
     f.hT = a->hT_dev;
     f.dbg = reinterpret_cast<unsigned long long*>(a->debug_ts_dev);
     f.l2_policy = a->l2_policy;
@@ -569,6 +570,13 @@ moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads) {
 
 moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf) {
   return guard([&] { c->e.set_k3_trace(static_cast<unsigned long long*>(dev_buf)); });
+}
+
+moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes) {
+  return guard([&] {
+    if (bytes < 0) throw std::invalid_argument("moespac_ctx_set_l2_prefetch: bytes must be >= 0");
+    c->e.set_l2_prefetch(bytes);
+  });
 }
 
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {

@@ -126,6 +126,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   if (plan.n_stages == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
   stages_ = plan.n_stages;
   global_acc_ = plan.global_acc;
+  acc_mode_ = plan.acc_mode;
   ffn_smem_ = plan.smem;
 
   const int L = m.n_layers, N = m.n_experts, k = m.top_k, d = m.d_model;
@@ -461,8 +462,17 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.n_stages = stages_;
     fa.ring_bytes = stages_ * 1024;
     fa.global_acc = global_acc_ ? 1 : 0;
+    fa.acc_mode = acc_mode_;
     fa.hT = hT[l & 1];
     if (k3_trace_) fa.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
+    if (tc && l + 1 < L && l2_prefetch_ > 0) {
+      fa.nx_counters = counters_d + static_cast<size_t>(l + 1) * 8;
+      fa.nx_hit_list = hit_list_d_ + static_cast<size_t>(l + 1) * N;
+      fa.nx_slot_of = slots_d + static_cast<size_t>(l + 1) * N;
+      fa.nx_pool = pool_ + static_cast<int64_t>(l + 1) * slots_ * image_elems_;
+      fa.nx_shared_w = shared_ + static_cast<int64_t>(l + 1) * m_.n_shared_units * image_elems_;
+      fa.pf_bytes = l2_prefetch_;
+    }
     if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
     check(tc ? launch_expert_ffn_tc(fa, sms_, ffn_smem_, compute_, pdl)
              : launch_expert_ffn(fa, sms_, ffn_smem_, compute_, pdl),

@@ -42,6 +42,7 @@ class Engine {
   void set_timing(bool on) { timing_ = on; }
   void set_pdl(bool on) { pdl_ = on; }
   void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
+  void set_l2_prefetch(int bytes) { l2_prefetch_ = bytes; }
   // host threads for cold (non-resident) experts: -1 auto, 0 = off (misses
   // are then counted but not computed); takes effect at finalize()
   void set_cold_threads(int n) { cold_threads_ = n; }
@@ -98,8 +99,10 @@ class Engine {
   bool decided_ = false;  // next step's decisions already made
   bool pdl_ = true;                         // programmatic dependent launch between layer kernels
   unsigned long long* k3_trace_ = nullptr;  // profiling: [L][grid][32]
+  int l2_prefetch_ = 384 * 1024;            // per-CTA next-layer L2 prefetch (bytes)
   int cold_threads_ = -1;
   int ffn_accum_ = 0;
+  int acc_mode_ = 0;
   std::unique_ptr<ColdExecutor> cold_;
   float* ycold_d_ = nullptr;   // [L][T][d] host-computed cold-expert outputs
   float* ycold_h_ = nullptr;   // pinned staging of the same

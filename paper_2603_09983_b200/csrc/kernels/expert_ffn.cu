@@ -412,6 +412,7 @@ constexpr int COMBINE_WARPS = 4;  // small footprint: must co-reside with a K3 C
 constexpr int COMBINE_BATCH = 16;  // partial rows in flight per warp
 constexpr int COMBINE_LIST = 48;  // per-warp row list capacity (else streamed)
 
+// (<= 112 registers: see expert_ffn_tc_kernel)
 __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs a) {
   __shared__ float4 red[COMBINE_WARPS][32];
   __shared__ int rows[COMBINE_WARPS][COMBINE_LIST];

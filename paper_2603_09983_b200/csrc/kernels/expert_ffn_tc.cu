@@ -51,6 +51,8 @@ constexpr int FCH = 64;  // ffn rows per chunk
 constexpr int QROWS = 16;
 constexpr int TMEM_COLS = 512;
 constexpr int D2_COL0 = 256;
+constexpr int ACC_SMEM = 0, ACC_GLOBAL = 1, ACC_TMEM = 2;  // FfnArgs::acc_mode
+constexpr int TMEM_ACC_MAX_D = (512 - D2_COL0) / 16 * 128;  // TMEM mode: D2 for all M-tiles fits
 constexpr int PASS_TILES = 8;
 constexpr int ENT_PRE = 8;  // entries whose routing is staged in the prologue
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
@@ -212,7 +214,10 @@ __device__ __forceinline__ const uint16_t* entry_weights(const FfnArgs& a, int o
   return a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
 }
 
-__global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
+// <= 200 registers: with 2 of its warps on one SM sub-partition (16K registers)
+// a 4-warp combine CTA (<= 112 regs) must still fit next to it, or PDL cannot
+// overlap the combine with this kernel's tail (measured: +3 us per layer).
+__global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int d = a.d, T = a.T;
   const int ktiles = d / 64, mtiles = d / 128;
@@ -229,8 +234,11 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   p += 2 * 2 * 4096;
   uint8_t* ring = p;
   p += RB;
-  float* ysum = reinterpret_cast<float*>(p);  // [T][d] (unless global_acc)
-  if (!a.global_acc) p += static_cast<size_t>(T) * d * 4;
+  // down-projection accumulator across the segments of an entry:
+  // shared memory (ysum), the partial block in global memory, or TMEM
+  const int mode = a.acc_mode;
+  float* ysum = reinterpret_cast<float*>(p);  // [T][d] (shared-memory mode)
+  if (mode == ACC_SMEM) p += static_cast<size_t>(T) * d * 4;
   float* gate_s = reinterpret_cast<float*>(p);  // [2 slots][16] per-token gate of the entry
   p += 2 * 16 * 4;
   int* tok_s = reinterpret_cast<int*>(p);  // [2 slots][16] token list of the entry (for flush)
@@ -286,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (!a.global_acc) {
+  if (mode == ACC_SMEM) {
     float4* ys = reinterpret_cast<float4*>(ysum);
     for (int i = tid; i < T * d / 4; i += THREADS) ys[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -338,7 +346,14 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
   // Everything below except the producer's first weight copies depends on
   // the previous kernel (h^T image, partial workspace): wait for it.
   if (warp != 0) pdl_wait();
-  if (tid == 32) stamp(a, 22);  // predecessor complete (PDL) as seen by this CTA
+  if (tid == 32) {
+    stamp(a, 22);  // predecessor complete (PDL) as seen by this CTA
+    if (a.dbg) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.dbg[blockIdx.x * DBG + 24] = smid;
+    }
+  }
 
   // All three roles walk the same software-pipelined sequence of segments:
   //   GU(0), GU(1), DN(0), GU(2), DN(1), ..., DN(last)
@@ -470,6 +485,35 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           if (more) cur_base = seg_base(cur);
         }
       }
+      if (a.nx_counters && a.pf_bytes > 0) {
+        // ---- cross-layer L2 prefetch (see FfnArgs::pf_bytes): the next
+        // layer's routing is final (K2 ran for all layers), so walk this CTA
+        // index's next-layer segments in stream order and prefetch their
+        // gate/up runs, then their down runs, up to the byte budget.
+        const int nh = a.nx_counters[7];
+        const long long nn = static_cast<long long>(nh + a.n_shared) * qpe;
+        const long long p0 = nn > 0 ? (static_cast<long long>(blockIdx.x) * nn) / gridDim.x : 0;
+        const long long p1 = nn > 0 ? (static_cast<long long>(blockIdx.x + 1) * nn) / gridDim.x : 0;
+        SegIter pit{p0, p1, qpe};
+        Seg s;
+        long long budget = a.pf_bytes;
+        while (budget > 0 && pit.next(s)) {
+          const uint16_t* w = s.o < nh ? a.nx_pool + static_cast<long long>(a.nx_slot_of[a.nx_hit_list[s.o]]) *
+                                                          a.expert_elems
+                                       : a.nx_shared_w + static_cast<long long>(s.o - nh) * a.expert_elems;
+          const uint8_t* base = reinterpret_cast<const uint8_t*>(w + s.c * chunk_elems);
+          const int nq = s.qb - s.qa;
+          const uint32_t run = static_cast<uint32_t>(nq) * QBYTES;
+          for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
+            if (leader)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * A_BYTES +
+                                                                              s.qa * QBYTES),
+                           "r"(run)
+                           : "memory");
+            budget -= run;
+          }
+        }
+      }
       if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
     }
   } else if (warp == 1) {
@@ -482,6 +526,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
       long long w_full = 0, w_at = 0, w_d2e = 0, w_d1e = 0;
       Phase d1e[2], ate[2], d2e[2];
       int c3 = 0;  // D2 pass buffer counter
+      int ent_done = 0, last_dn_o = -1;  // TMEM mode: entries committed, entry of the last DN
       uint32_t head = 0, idx = 0;
       SegIter it{q0, q1, qpe};
       Seg cur, prev;
@@ -533,7 +578,43 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           const int nq = prev.qb - prev.qa;
           const Geom g = dn_geom(nq, mcap);
           const uint32_t tb = static_cast<uint32_t>(nq) * QBYTES;
-          for (int ps = 0; ps < passes; ++ps) {
+          if (mode == ACC_TMEM) {
+            // D2[mt] accumulates the whole entry's down projection in TMEM
+            // (all M-tiles resident); drained once, at the entry's last
+            // segment in this CTA
+            const bool first = prev.o != last_dn_o, last = !more || cur.o != prev.o;
+            if (first && ent_done > 0) {
+              wait_acc(a, &d2_empty[0], static_cast<uint32_t>(ent_done - 1) & 1u, w_d2e);
+              fence_after();
+            }
+            for (int mt = 0; mt < mtiles; mt += g.m) {
+              const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
+              wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
+              ++idx;
+              if (i == 1 && mt == 0 && leader) stamp(a, 16);
+              fence_after();
+              const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * QBYTES;
+              if (leader) {
+                for (int j = 0; j < g.m; ++j) {
+                  const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>((mt + j) * 16);
+                  const uint64_t adn = smem_desc(va + j * tb, 2048, 128);
+                  for (int k = prev.qa; k < prev.qb; ++k) {
+                    mma_bf16(d2, adn + 256 * k, bhi + 32 * k, (first && k == prev.qa) ? 0u : 1u);
+                    mma_bf16(d2, adn + 256 * k, blo + 32 * k, 1u);
+                  }
+                }
+                mma_commit(&empty[slot]);
+              }
+              __syncwarp();
+            }
+            if (last) {
+              if (leader) mma_commit(&d2_full[0]);
+              __syncwarp();
+              ++ent_done;
+            }
+            last_dn_o = prev.o;
+          }
+          for (int ps = 0; ps < (mode == ACC_TMEM ? 0 : passes); ++ps) {
             const int pb = c3 & 1;
             wait_acc(a, &d2_empty[pb], d2e[pb].bit ^ 1u, w_d2e);
             d2e[pb].flip();
@@ -586,7 +667,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
     const int et = tid - 64; // 0..127
     Phase d1f[2], atf[2], d2f[2];
     long long w_d1f = 0, w_d2f = 0;
-    int c3 = 0;
+    int c3 = 0, ent_e = 0;  // ent_e: TMEM mode, entries drained
     int cur_entry = -1, eslot = 1;
     int seg_slot[2] = {0, 0};
     // per-entry token data, two slots (entry being drained / entry being fed)
@@ -601,7 +682,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         }
         if (et == 0) misc[2 + slot] = ent_n[pre];
         named_bar_sync(2, EPI_THREADS);
-        if (a.global_acc) {
+        if (mode == ACC_GLOBAL) {
           float* P = a.partial + static_cast<long long>(b + o) * T * d;
           const int nt = misc[2 + slot];
           for (int t = 0; t < nt; ++t)
@@ -638,7 +719,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
         misc[2 + slot] = nt;
       }
       named_bar_sync(2, EPI_THREADS);
-      if (a.global_acc) {  // zero this entry's rows of the CTA-exclusive partial block
+      if (mode == ACC_GLOBAL) {  // zero this entry's rows of the CTA-exclusive partial block
         float* P = a.partial + static_cast<long long>(b + o) * T * d;
         const int nt = misc[2 + slot];
         for (int t = 0; t < nt; ++t)
@@ -650,7 +731,7 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
     };
     auto flush = [&](int o, int slot) {
       named_bar_sync(2, EPI_THREADS);
-      if (!a.global_acc) {
+      if (mode == ACC_SMEM) {
         const int nt = misc[2 + slot];
         float* P = a.partial + static_cast<long long>(b + o) * T * d;
         for (int t = 0; t < nt; ++t) {
@@ -722,7 +803,44 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           if (i == 0) stamp(a, 4);
         }
       }
-      if (has_prev) {
+      if (has_prev && mode == ACC_TMEM) {
+        // ---- D(i-1), TMEM mode: at the entry's last segment here, drain
+        // D2 (all M-tiles) straight into this CTA's partial block
+        if (!more || cur.o != prev.o) {
+          wait_acc(a, &d2_full[0], static_cast<uint32_t>(ent_e) & 1u, w_d2f);
+          if (i == 1 && et == 0) stamp(a, 18);
+          fence_after();
+          const int slot = seg_slot[(i - 1) & 1];
+          uint32_t tmask = 0;  // tokens of this entry
+          for (int tt = 0; tt < misc[2 + slot]; ++tt) tmask |= 1u << tok_s[slot * 16 + tt];
+          float* P = a.partial + static_cast<long long>(b + prev.o) * T * d + 32 * q + lane;
+          const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0);
+          for (int mt = 0; mt < mtiles; mt += 2) {  // two M-tiles per TMEM wait
+            uint32_t y0[16], y1[16];
+            const bool two = mt + 1 < mtiles;
+            if (T <= 8) {
+              tmem_ld8_nw(tbase + static_cast<uint32_t>(mt * 16), y0);
+              if (two) tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + 1) * 16), y1);
+            } else {
+              tmem_ld16_nw(tbase + static_cast<uint32_t>(mt * 16), y0);
+              if (two) tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + 1) * 16), y1);
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+              if (t < T && ((tmask >> t) & 1u)) {
+                __stcg(P + static_cast<long long>(t) * d + mt * 128, __uint_as_float(y0[t]));
+                if (two) __stcg(P + static_cast<long long>(t) * d + mt * 128 + 128, __uint_as_float(y1[t]));
+              }
+          }
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&d2_empty[0]);
+          ++ent_e;
+          if (i == 1 && et == 0) stamp(a, 20);
+        }
+      }
+      if (has_prev && mode != ACC_TMEM) {
         // ---- D(i-1): D2 passes -> per-expert fp32 accumulator
         for (int ps = 0; ps < passes; ++ps) {
           const int pb = c3 & 1;
@@ -734,44 +852,30 @@ __global__ void __launch_bounds__(THREADS, 1) expert_ffn_tc_kernel(FfnArgs a) {
           const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0 + pb * 128);
           float* P = a.partial + static_cast<long long>(b + prev.o) * T * d;
           const float* gsl = gate_s + seg_slot[(i - 1) & 1] * 16;
-          for (int mt = mt0; mt < mt_end; mt += 2) {
-            // two M-tiles per wait; only the first T token columns matter
-            uint32_t y0[16], y1[16];
-            const bool two = mt + 1 < mt_end;
-            if (T <= 8) {
+          for (int mt = mt0; mt < mt_end; ++mt) {
+            // only the first T token columns matter
+            uint32_t y0[16];
+            if (T <= 8)
               tmem_ld8_nw(tbase + static_cast<uint32_t>((mt - mt0) * 16), y0);
-              if (two) tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + 1 - mt0) * 16), y1);
-            } else {
+            else
               tmem_ld16_nw(tbase + static_cast<uint32_t>((mt - mt0) * 16), y0);
-              if (two) tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + 1 - mt0) * 16), y1);
-            }
             tmem_wait_ld();
-            for (int h = 0; h < (two ? 2 : 1); ++h) {
-              const uint32_t* yy = h ? y1 : y0;
-              const int orow = (mt + h) * 128 + 32 * q + lane;
-              if (a.global_acc) {
+            const int orow = mt * 128 + 32 * q + lane;
+            if (mode == ACC_GLOBAL) {
 #pragma unroll
-                for (int t = 0; t < 16; ++t)
-                  if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += __uint_as_float(yy[t]);
-              }
-            }
-            if (!a.global_acc) {
+              for (int t = 0; t < 16; ++t)
+                if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += __uint_as_float(y0[t]);
+            } else {
               // all loads, then all stores: the T read-modify-writes of a row
               // are independent (a += chain would serialise on each LDS)
-              float* r0 = ysum + mt * 128 + 32 * q + lane;
-              float o0[16], o1[16];
+              float* r0 = ysum + orow;
+              float o0[16];
 #pragma unroll
               for (int t = 0; t < 16; ++t)
-                if (t < T) {
-                  o0[t] = r0[static_cast<size_t>(t) * d];
-                  if (two) o1[t] = r0[static_cast<size_t>(t) * d + 128];
-                }
+                if (t < T) o0[t] = r0[static_cast<size_t>(t) * d];
 #pragma unroll
               for (int t = 0; t < 16; ++t)
-                if (t < T) {
-                  r0[static_cast<size_t>(t) * d] = o0[t] + __uint_as_float(y0[t]);
-                  if (two) r0[static_cast<size_t>(t) * d + 128] = o1[t] + __uint_as_float(y1[t]);
-                }
+                if (t < T) r0[static_cast<size_t>(t) * d] = o0[t] + __uint_as_float(y0[t]);
             }
           }
           fence_before();
@@ -857,34 +961,48 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
 }  // namespace tc
 }  // namespace dev
 
-size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, bool global_acc) {
-  return 2 * 2 * 4096 + static_cast<size_t>(ring_bytes) + (global_acc ? 0 : static_cast<size_t>(T) * d * 4) +
-         2 * 16 * 4 * 2 + 16 + dev::tc::ENT_PRE * (16 * 8 + 4) + 8 +
-         8 * (2 * dev::tc::NSLOT + 12);
+size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, int acc_mode) {
+  return 2 * 2 * 4096 + static_cast<size_t>(ring_bytes) +
+         (acc_mode == dev::tc::ACC_SMEM ? static_cast<size_t>(T) * d * 4 : 0) + 2 * 16 * 4 * 2 + 16 +
+         dev::tc::ENT_PRE * (16 * 8 + 4) + 8 + 8 * (2 * dev::tc::NSLOT + 12);
 }
 
-// accum: 0 auto (shared memory when it leaves a >= 64 KiB ring), 1 shared-memory
-// accumulator, 2 global (L2) accumulator. Measured: the L2 accumulator puts
+// accum: 0 auto, 1 shared-memory accumulator, 2 global (L2) accumulator,
+// 3 TMEM accumulator. Auto: TMEM when D2 for every M-tile fits next to the
+// D1 buffers (d <= 2048) — no per-segment accumulate pass at all and the
+// whole remaining shared memory for the ring; else shared memory when it
+// leaves a >= 64 KiB ring; else global. Measured: the L2 accumulator puts
 // dependent global read-modify-writes on the drain's critical path and loses
 // ~30% even with a deeper ring, so it is only the fallback for large T x d.
-// FfnPlan::n_stages reports the ring size in KiB.
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
   // Leave room on the SM for one combine CTA (3 KiB static + 1 KiB reserve)
   // next to the K3 CTA (+1 KiB reserve) of 228 KiB: programmatic dependent
   // launch only overlaps the two kernels when they can co-reside.
   constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 3072 + 1024;
   if (smem_limit > kSmPerSm - kReserve - kCombine) smem_limit = kSmPerSm - kReserve - kCombine;
-  auto ring_for = [&](bool g) -> int {
-    const size_t fixed = ffn_tc_smem_bytes(T, d, 0, g);
+  auto ring_for = [&](int mode) -> int {
+    const size_t fixed = ffn_tc_smem_bytes(T, d, 0, mode);
     if (fixed + 32768 > smem_limit) return 0;
     return static_cast<int>(((smem_limit - fixed) / 1024) * 1024);
   };
-  if (accum != 2) {
-    const int rb = ring_for(false);
-    if (rb >= (accum == 1 ? 32768 : 65536)) return {rb / 1024, false, ffn_tc_smem_bytes(T, d, rb, false)};
+  auto plan = [&](int mode, int rb) {
+    FfnPlan p{rb / 1024, mode == dev::tc::ACC_GLOBAL, ffn_tc_smem_bytes(T, d, rb, mode)};
+    p.acc_mode = mode;
+    return p;
+  };
+  const bool tmem_ok = d <= dev::tc::TMEM_ACC_MAX_D;
+  if (accum == 3 || (accum == 0 && tmem_ok)) {
+    if (!tmem_ok) return {0, false, 0};
+    const int rb = ring_for(dev::tc::ACC_TMEM);
+    if (rb >= 32768) return plan(dev::tc::ACC_TMEM, rb);
+    return {0, false, 0};
   }
-  const int rb = ring_for(true);
-  if (rb >= 32768) return {rb / 1024, true, ffn_tc_smem_bytes(T, d, rb, true)};
+  if (accum != 2) {
+    const int rb = ring_for(dev::tc::ACC_SMEM);
+    if (rb >= (accum == 1 ? 32768 : 65536)) return plan(dev::tc::ACC_SMEM, rb);
+  }
+  const int rb = ring_for(dev::tc::ACC_GLOBAL);
+  if (rb >= 32768) return plan(dev::tc::ACC_GLOBAL, rb);
   return {0, false, 0};
 }
 

@@ -43,9 +43,20 @@ struct FfnArgs {
   int n_stages;             // CUDA-core kernel: ring stages
   int ring_bytes;           // tensor-core kernel: byte-ring size
   int global_acc;           // 1: accumulate down-proj partials in `partial` (large T*d)
+  int acc_mode;             // tensor-core kernel: 0 shared-memory, 1 global (L2), 2 TMEM accumulator
   const uint16_t* hT;       // tcgen05 variant: h^T UMMA image [d/64][16 tok][64] (build_hT)
-  unsigned long long* dbg;  // optional per-CTA %globaltimer stamps [grid][8] (profiling)
+  unsigned long long* dbg;  // optional per-CTA profiling record [grid][32]
   int l2_policy;            // weight stream L2 policy: 0 evict_first, 1 evict_normal
+  // Next layer (tensor-core kernel): once a CTA has issued its last weight
+  // copy it prefetches into L2 the first pf_bytes of what the same CTA
+  // index will stream in the next layer, so HBM keeps working through this
+  // launch's tail and the layer-to-layer handoff. nx_counters == null: off.
+  const int32_t* nx_counters;
+  const int32_t* nx_hit_list;
+  const int32_t* nx_slot_of;
+  const uint16_t* nx_pool;
+  const uint16_t* nx_shared_w;
+  int pf_bytes;
 };
 
 struct CombineArgs {
@@ -70,14 +81,15 @@ cudaError_t launch_router_topk(const double* logits, int rows, int N, int k, int
 cudaError_t launch_hist_scan_observe(const dev::K2Args& a, cudaStream_t stream);
 cudaError_t launch_estimator_init(int32_t* st, int n, int up, int down, cudaStream_t stream);
 struct FfnPlan {
-  int n_stages;
+  int n_stages;     // CUDA-core: ring stages; tensor-core: ring KiB
   bool global_acc;
   size_t smem;
+  int acc_mode = 0; // tensor-core: 0 shared-memory, 1 global (L2), 2 TMEM accumulator
 };
 size_t ffn_smem_bytes(int T, int d, int n_stages, bool global_acc);
 FfnPlan ffn_plan(int T, int d, size_t smem_limit);
 cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
-size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, bool global_acc);
+size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, int acc_mode);
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum = 0);
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
 cudaError_t launch_build_hT(const uint16_t* h, int T, int d, uint16_t* out, cudaStream_t stream, bool pdl = false);

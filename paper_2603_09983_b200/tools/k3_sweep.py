@@ -97,7 +97,9 @@ def main():
                 waits = {nm: round(float(np.median(t[act, j] / np.maximum(cyc, 1))), 3) for j, nm in
                          [(8, "prod_empty"), (9, "mma_full"), (10, "mma_at_full"), (11, "mma_d2_empty"),
                           (12, "mma_d1_empty"), (13, "epi_d1_full"), (14, "epi_d2_full")]}
-                print(json.dumps({"wait_frac_of_cta_cycles": waits}), flush=True)
+                print(json.dumps({"wait_frac_of_cta_cycles": waits,
+                                  "drain_cycles_med": {nm: float(np.median(t[act, j])) for j, nm in
+                                                       [(25, "tmem_ld"), (26, "lds"), (27, "sts")]}}), flush=True)
                 # end time vs the CTA's number of segments (chunk pieces)
                 qpe = ffn // 16
                 n_q = n_hit * qpe

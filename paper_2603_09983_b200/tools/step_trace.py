@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--cache-ratio", type=float, default=1.0)
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--pf", type=int, default=-1, help="L2 prefetch bytes per CTA (-1: library default)")
+    ap.add_argument("--steps", type=int, default=10, help="timed steps (whole-step events)")
     args = ap.parse_args()
     w = configs.CONFIGS[args.config]
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
@@ -33,6 +35,8 @@ def main():
     ctx.fill_synthetic(seed=3, stdv=0.02)
     ctx.finalize()
     ctx.set_pdl(bool(args.pdl))
+    if args.pf >= 0:
+        ctx.set_l2_prefetch(args.pf)
     synth = abi.TraceSynth(cfg)
     S = args.warmup + 1
     logits = torch.empty((S, L, T, N), dtype=torch.float64)
@@ -42,6 +46,15 @@ def main():
     h_out = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
     for s in range(args.warmup):
         ctx.step_device(logits[s], h[s], acc[s], h_out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.ExternalStream(ctx.stream())
+    e0.record(st)
+    for i in range(args.steps):
+        ctx.step_device(logits[i % args.warmup], h[i % args.warmup], acc[i % args.warmup], h_out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1) / args.steps
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     buf = torch.zeros((L, sms, 32), dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
@@ -69,9 +82,41 @@ def main():
             r["gap_to_next_us"] = round(rows[i + 1]["pred_done"] - r["end_max"], 2)
             r["k3_span_us"] = round(r["end_max"] - r["pred_done"], 2)
         print(json.dumps(r))
+    # K3 tail: per-CTA end (relative to the layer's predecessor-done) vs the
+    # CTA's work shape and SM, for a middle layer
+    lm = L // 2
+    x = t[lm]
+    n_hit_l = None
+    qpe = ffn // 16
+    base = np.median(x[:, 22])
+    ends = (x[:, 6] - base) / 1e3
+    first = (x[:, 2] - base) / 1e3
+    sm = x[:, 24].astype(int)
+    print(json.dumps({"layer": lm, "end_pct_us": [round(float(np.percentile(ends, p)), 2) for p in (0, 10, 50, 90, 100)],
+                      "first_data_pct_us": [round(float(np.percentile(first, p)), 2) for p in (0, 50, 100)],
+                      "slowest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(-ends)[:8]],
+                      "fastest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(ends)[:8]]}))
+    # per-SM lateness across layers: is the tail a property of the SM?
+    late = {}
+    for l in range(L):
+        x = t[l]
+        if not (x[:, 0] > 0).all():
+            continue
+        e = (x[:, 6] - np.median(x[:, 22])) / 1e3
+        rel = e / np.median(e) - 1.0
+        for b in range(x.shape[0]):
+            late.setdefault(int(x[b, 24]), []).append(float(rel[b]))
+    sm_mean = {s_: float(np.mean(v)) for s_, v in late.items()}
+    order = sorted(sm_mean, key=lambda s_: -sm_mean[s_])
+    allv = np.concatenate([np.array(v) for v in late.values()])
+    print(json.dumps({"per_sm_lateness": {"std_all": round(float(allv.std()), 4),
+                                          "std_of_sm_means": round(float(np.std(list(sm_mean.values()))), 4),
+                                          "latest_sms": [[s_, round(sm_mean[s_], 4)] for s_ in order[:10]],
+                                          "earliest_sms": [[s_, round(sm_mean[s_], 4)] for s_ in order[-10:]]}}))
     gaps = [r["gap_to_next_us"] for r in rows if "gap_to_next_us" in r]
     spans = [r["k3_span_us"] for r in rows if "k3_span_us" in r]
-    print(json.dumps({"config": args.config, "median_gap_us": float(np.median(gaps)),
+    print(json.dumps({"config": args.config, "pf": args.pf, "timed_step_ms": round(step_ms, 4),
+                      "median_gap_us": float(np.median(gaps)),
                       "median_k3_span_us": float(np.median(spans)),
                       "step_us": round(rows[-1]["end_max"] - rows[0]["pred_done"], 2)}))
 

@@ -172,6 +172,25 @@ def _kernels(d, ffn):
 def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel):
     if kernel not in _kernels(d, ffn):
         pytest.skip("shape not supported by this kernel variant")
+    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, 0)
+
+
+@pytest.mark.parametrize("accum", [1, 2, 3], ids=["smem", "global", "tmem"])
+@pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
+    (128, 8, 9, 2048, 768, 0, 0, 0.6),     # Qwen3 shape
+    (16, 4, 16, 1024, 128, 1, 0, 0.7),     # T = 16 + shared unit
+    (16, 4, 9, 128, 64, 0, 0, 1.0),        # smallest shape (one M-tile)
+    (60, 4, 7, 2048, 1408, 4, 1, 0.5),     # Qwen1.5 shape
+])
+def test_expert_ffn_tc_accumulator_modes(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, accum):
+    """Every down-projection accumulator of the tensor-core K3 (shared memory,
+    global partial block, TMEM) against the fp64 oracle."""
+    if abi.FFN_TENSOR not in _kernels(d, ffn):
+        pytest.skip("shape not supported by the tensor-core kernel")
+    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, accum)
+
+
+def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum):
     rng = np.random.default_rng(N * 7 + T)
     experts = _rand_experts(rng, N, d, ffn)
     shared = _rand_experts(rng, n_shared, d, ffn)
@@ -204,7 +223,7 @@ def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_f
     hT = abi.build_hT(h_t)
     fa = abi.FfnArgs(abi.ptr(h_t), T, d, ffn, k, N, abi.ptr(bufs["perm"]), abi.ptr(bufs["offsets"]), abi.ptr(gates),
                      abi.ptr(bufs["hl"]), abi.ptr(bufs["cnt"]), abi.ptr(slot_of), abi.ptr(pool), abi.ptr(shared_t),
-                     n_shared, abi.ptr(ws), grid, kernel, abi.ptr(hT))
+                     n_shared, abi.ptr(ws), grid, kernel, abi.ptr(hT), None, accum)
     abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), s0))
     y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
     h_out = torch.zeros((T, d), dtype=torch.int16, device="cuda")
