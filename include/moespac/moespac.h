@@ -297,7 +297,8 @@ moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
  * stamps and wait counters (layer l at offset l*grid*32), or NULL to stop. */
 moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf);
 /* Cross-layer L2 prefetch budget per K3 CTA in bytes (tensor-core K3; 0 = off,
- * default 384 KiB): after its last weight copy, each CTA prefetches into L2
+ * default 0 = off: measured no gain on the BASELINE shapes): after its last
+ * weight copy, each CTA prefetches into L2
  * the start of its next-layer work so HBM stays busy through the launch tail
  * and the layer handoff. */
 moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes);

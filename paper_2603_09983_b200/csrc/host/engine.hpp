@@ -99,7 +99,7 @@ class Engine {
   bool decided_ = false;  // next step's decisions already made
   bool pdl_ = true;                         // programmatic dependent launch between layer kernels
   unsigned long long* k3_trace_ = nullptr;  // profiling: [L][grid][32]
-  int l2_prefetch_ = 384 * 1024;            // per-CTA next-layer L2 prefetch (bytes)
+  int l2_prefetch_ = 0;  // per-CTA next-layer L2 prefetch (bytes); measured no gain, off
   int cold_threads_ = -1;
   int ffn_accum_ = 0;
   int acc_mode_ = 0;
