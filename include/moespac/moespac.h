@@ -221,7 +221,8 @@ typedef struct moespac_ffn_args {
   int32_t kernel;              /* MOESPAC_FFN_* (image layout must match) */
   const uint16_t* hT_dev;      /* tensor-core kernel: moespac_build_hT(h) image */
   uint64_t* debug_ts_dev;      /* optional [grid][32] per-CTA profiling record (%globaltimer stamps, wait counters), or NULL */
-  int32_t accum;               /* tensor-core kernel: 0 auto, 1 shared-memory, 2 L2 (partial-block), 3 TMEM accumulator (d <= 2048) */
+  int32_t accum;               /* tensor-core kernel: 0 auto, 1 shared-memory, 2 L2 (partial-block), 3 TMEM accumulator
+                                  per expert (d <= 2048), 4 grouped: whole-CTA TMEM accumulator (d <= 2048; auto's choice) */
   int32_t l2_policy;           /* weight stream L2 policy: 0 evict_first (default), 1 evict_normal */
 } moespac_ffn_args;
 size_t moespac_ffn_workspace_bytes(int tokens, int d_model, int n_experts, int n_shared_units, int grid);
@@ -239,6 +240,8 @@ typedef struct moespac_combine_args {
   const float* workspace_dev;
   float* y_dev;
   uint16_t* h_out_dev;
+  int32_t accum;               /* the accum selector the K3 launch used (decides the partial-block layout) */
+  int32_t kernel;              /* the MOESPAC_FFN_* kernel the K3 launch used */
 } moespac_combine_args;
 moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream);
 

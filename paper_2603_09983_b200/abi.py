@@ -93,7 +93,7 @@ class CombineArgs(C.Structure):
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("top_k", C.c_int32), ("ids_dev", C.c_void_p),
                 ("hit_ord_dev", C.c_void_p), ("counters_dev", C.c_void_p), ("n_shared_units", C.c_int32),
                 ("grid", C.c_int32), ("workspace_dev", C.c_void_p), ("y_dev", C.c_void_p),
-                ("h_out_dev", C.c_void_p)]
+                ("h_out_dev", C.c_void_p), ("accum", C.c_int32), ("kernel", C.c_int32)]
 
 
 class ModelDesc(C.Structure):

@@ -28,6 +28,7 @@ SOURCES = [
     "kernels/router_hist.cu",
     "kernels/expert_ffn.cu",
     "kernels/expert_ffn_tc.cu",
+    "kernels/expert_ffn_grouped.cu",
     "host/scheduler.cpp",
     "host/step_scheduler.cpp",
     "host/engine.cpp",
@@ -36,7 +37,7 @@ SOURCES = [
     "abi.cpp",
 ]
 HEADERS = [
-    "kernels/common.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
+    "kernels/common.cuh", "kernels/tcgen05.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
     "host/engine.hpp", "host/trace_synth.hpp", "host/cold_executor.hpp",
 ]
 

@@ -447,6 +447,9 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     const FfnPlan plan = kern == kFfnTensorCore ? ffn_tc_plan(a->tokens, a->d_model, static_cast<size_t>(optin), a->accum)
                                                 : ffn_plan(a->tokens, a->d_model, static_cast<size_t>(optin));
     if (!plan.n_stages) throw std::invalid_argument("moespac_expert_ffn: tokens x d_model too large for shared memory");
+    const int grid = a->grid > 0 ? a->grid : device_sms();
+    if (plan.acc_mode == 3 && !ffn_tg_grid_ok(a->n_experts + a->n_shared_units, a->d_ffn, grid))
+      throw std::invalid_argument("moespac_expert_ffn: grid too small for the grouped accumulator (use accum 3)");
     dev::FfnArgs f{};
     f.h = a->h_dev;
     f.T = a->tokens;
@@ -472,7 +475,6 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.hT = a->hT_dev;
     f.dbg = reinterpret_cast<unsigned long long*>(a->debug_ts_dev);
     f.l2_policy = a->l2_policy;
-    const int grid = a->grid > 0 ? a->grid : device_sms();
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_ok(kern == kFfnTensorCore ? launch_expert_ffn_tc(f, grid, plan.smem, st) : launch_expert_ffn(f, grid, plan.smem, st),
             "expert_ffn");
@@ -495,6 +497,12 @@ moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream) 
     c.counters = a->counters_dev;
     c.n_shared = a->n_shared_units;
     c.grid = a->grid > 0 ? a->grid : device_sms();
+    if (ffn_resolve(a->kernel, a->d_model, a->d_ffn) == kFfnTensorCore) {
+      int dev = 0, optin = 0;
+      cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+      cuda_ok(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+      c.per_cta = ffn_tc_plan(a->tokens, a->d_model, static_cast<size_t>(optin), a->accum).acc_mode == 3 ? 1 : 0;
+    }
     c.partial = a->workspace_dev;
     c.y_out = a->y_dev;
     c.h_out = a->h_out_dev;

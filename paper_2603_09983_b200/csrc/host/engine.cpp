@@ -14,7 +14,9 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -121,8 +123,17 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   if (prop.major != 10) throw CudaError("moespac requires an sm_100 (B200) device");
   sms_ = prop.multiProcessorCount;
-  const FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, prop.sharedMemPerBlockOptin, ffn_accum_)
-                                                 : ffn_plan(T_, m.d_model, prop.sharedMemPerBlockOptin);
+  // profiling knobs: MOESPAC_FFN_ACCUM (accumulator selector, see
+  // moespac_ffn_args::accum), MOESPAC_SMEM_SLACK (bytes kept free per SM)
+  if (const char* e = std::getenv("MOESPAC_FFN_ACCUM")) ffn_accum_ = std::atoi(e);
+  size_t smem_optin = prop.sharedMemPerBlockOptin;
+  if (const char* e = std::getenv("MOESPAC_SMEM_SLACK"))
+    smem_optin = std::min<size_t>(smem_optin, 233472 - 1024 - 4096) - static_cast<size_t>(std::atoi(e));
+  FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, smem_optin, ffn_accum_)
+                                           : ffn_plan(T_, m.d_model, smem_optin);
+  if (kernel_ == kFfnTensorCore && plan.acc_mode == 3 &&
+      !ffn_tg_grid_ok(m.n_experts + m.n_shared_units, m.d_ffn, sms_))  // (not at 148 SMs)
+    plan = ffn_tc_plan(T_, m.d_model, smem_optin, 3);
   if (plan.n_stages == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
   stages_ = plan.n_stages;
   global_acc_ = plan.global_acc;
@@ -494,6 +505,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.counters = counters_d + static_cast<size_t>(l) * 8;
     ca.n_shared = n_shared_eff;
     ca.grid = sms_;
+    ca.per_cta = tc && acc_mode_ == 3 ? 1 : 0;
+    if (k3_trace_) ca.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
     ca.partial = work_d_;
     float* yl = y_d_ + static_cast<size_t>(l) * T_ * d;
     ca.y_out = yl;

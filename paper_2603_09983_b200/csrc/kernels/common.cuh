@@ -71,7 +71,10 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
+// bar.sync is warp-aligned (a warp that arrives in divergent pieces is
+// counted once per piece), so reconverge the warp first.
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 

@@ -417,6 +417,20 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
   __shared__ float4 red[COMBINE_WARPS][32];
   __shared__ int rows[COMBINE_WARPS][COMBINE_LIST];
   if (threadIdx.x == 0) pdl_trigger();
+  unsigned long long* dbg = a.dbg ? a.dbg + (blockIdx.y * gridDim.x + blockIdx.x) * 32 : nullptr;
+  auto stamp = [&](int slot) {
+    if (dbg && threadIdx.x == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)::"memory");
+      dbg[slot] = tt;
+    }
+  };
+  stamp(26);
+  if (dbg && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    dbg[29] = smid;
+  }
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.y * 128 + lane * 4;
@@ -431,15 +445,22 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
   if (n > 0 && c < a.d) {
     // 1) this warp's partial rows, in the fixed order (experts ascending,
     //    covering CTAs ascending, dealt round-robin to the warps)
-    int idx = 0, my_n = 0;
+    //    Grouped K3 (per_cta): one block per CTA holding the CTA's sum over
+    //    all its experts; a CTA covering two of the token's experts is listed
+    //    once (entries ascend, so their CTA ranges do too).
+    int idx = 0, my_n = 0, last_b = -1;
     auto list_entry = [&](int o) {
       const int lo = ((o * qpe + 1) * G - 1) / n;
       const int hi = (((o + 1) * qpe) * G - 1) / n;
       for (int b = lo; b <= hi; ++b) {
         // with fewer work units than CTAs some CTAs own nothing
         if ((b * n) / G == ((b + 1) * n) / G) continue;
+        if (a.per_cta) {
+          if (b <= last_b) continue;
+          last_b = b;
+        }
         if ((idx++ % COMBINE_WARPS) != warp) continue;
-        if (lane == 0 && my_n < COMBINE_LIST) rows[warp][my_n] = b + o;
+        if (lane == 0 && my_n < COMBINE_LIST) rows[warp][my_n] = a.per_cta ? b : b + o;
         ++my_n;
       }
     };
@@ -450,6 +471,7 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
     for (int sidx = 0; sidx < a.n_shared; ++sidx) list_entry(n_hits + sidx);
     __syncwarp();
     pdl_wait();  // partials of the K3 launch just before
+    stamp(27);
     auto row_ptr = [&](int r) {
       return reinterpret_cast<const float4*>(a.partial + (static_cast<long long>(r) * a.T + t) * a.d + c);
     };
@@ -471,13 +493,18 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
       }
     } else {  // long lists: same order, one row at a time
       idx = 0;
+      last_b = -1;
       auto add_entry = [&](int o) {
         const int lo = ((o * qpe + 1) * G - 1) / n;
         const int hi = (((o + 1) * qpe) * G - 1) / n;
         for (int b = lo; b <= hi; ++b) {
           if ((b * n) / G == ((b + 1) * n) / G) continue;
+          if (a.per_cta) {
+            if (b <= last_b) continue;
+            last_b = b;
+          }
           if ((idx++ % COMBINE_WARPS) != warp) continue;
-          const float4 v = __ldcg(row_ptr(b + o));
+          const float4 v = __ldcg(row_ptr(a.per_cta ? b : b + o));
           acc.x += v.x;
           acc.y += v.y;
           acc.z += v.z;
@@ -494,6 +521,7 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
   if (!(n > 0 && c < a.d)) pdl_wait();  // (no partials to read; still order after K3)
   red[warp][lane] = acc;
   __syncthreads();
+  stamp(28);
   if (warp != 0 || c >= a.d) return;
   for (int w = 1; w < COMBINE_WARPS; ++w) {
     const float4 v = red[w][lane];

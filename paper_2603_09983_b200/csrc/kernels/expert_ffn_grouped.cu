@@ -1,0 +1,631 @@
+// K3 (grouped tensor-core variant, d <= 2048) — grouped SwiGLU expert FFN
+// whose down-projection accumulator is the whole CTA's work, held in TMEM.
+//
+// Same image layout (v2, see expert_ffn_tc.cu) and the same byte-balanced
+// split of the layer's (expert, 16-row ffn quarter) units over a persistent
+// grid as the per-segment kernel; what changes is how a CTA walks its range:
+//
+//  * Groups, not chunk segments. The CTA's quarters are taken four at a time
+//    in global order, whatever chunk or expert they belong to, and packed into
+//    the four 32-row slots of one M = 128 gate|up tile (slot s = rows
+//    32s..32s+31: 16 gate rows then the 16 up rows of the same ffn rows). A
+//    CTA with 5-6 quarters runs two full-width GU passes instead of 2-3
+//    partial chunk segments.
+//  * One accumulator. The gate of token t for expert e is applied in the
+//    SwiGLU epilogue (a = silu(g)·u·g_{t,e}, 0 for tokens not routed to e),
+//    so the down projections of different experts can share one D2
+//    accumulator: D2[d][16 tokens] in TMEM columns 256-511 sums every group
+//    of the CTA and is drained once, at the end, through shared memory with
+//    bulk stores — one partial block per CTA instead of one per
+//    (CTA, expert) pair.
+//  * h^T resident. The layer's h^T image (d/64 slices of 2 KiB) is loaded
+//    into shared memory once, one mbarrier per slice, instead of riding along
+//    with every GU entry (that re-streamed 64 KiB from L2 per segment: up to a
+//    third of a narrow segment's bytes).
+//
+// The combine reads, for token t, the partial blocks of the CTAs whose
+// range covers a quarter of one of t's experts, in ascending CTA order.
+//
+// Warp roles (192 threads): 0 TMA producer, 1 MMA issuer (TMEM owner),
+// 2-5 epilogue (TMEM lane quarters 2, 3, 0, 1 = group slots).
+#include <cstdint>
+
+#include "common.cuh"
+#include "launch.hpp"
+#include "tcgen05.cuh"
+
+namespace moespac {
+namespace dev {
+namespace tg {
+
+using tc::elect_one;
+using tc::fence_after;
+using tc::fence_before;
+using tc::fence_proxy_async;
+using tc::mma_bf16;
+using tc::mma_commit;
+using tc::Phase;
+using tc::smem_desc;
+
+constexpr int THREADS = 192;
+constexpr int EPI_THREADS = 128;
+constexpr int NSLOT = 32;      // ring entries in flight (mbarrier pairs)
+constexpr int TILE = 16384;    // one gate|up K-tile or down M-tile of a 64-row chunk
+constexpr int QB = 4096;       // one 16-row quarter of a tile
+constexpr int HTS = 2048;      // h^T slice of one K-tile (16 tokens x 64 k)
+constexpr int ENT_MAX = 32;    // entries one CTA may touch (one producer lane each)
+constexpr int MAX_KT = 32;     // d <= 2048
+constexpr int D2_COL0 = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int DBG = 32;
+
+// ---------------------------------------------------------------- groups
+// A group is <= 4 consecutive quarters of the CTA's range; it spans at most
+// two chunk pieces (chunks are 4 quarters and entry boundaries are chunk
+// boundaries because ffn % 64 == 0).
+struct Grp {
+  long long qs;                 // first quarter (global order)
+  int nq, np;
+  int o[2], c[2], qa[2], n[2];  // piece p: quarters [qa, qa + n) of chunk c of entry o
+};
+
+struct GroupIt {
+  long long q, q1;
+  int qpe;
+  __device__ __forceinline__ bool next(Grp& g) {
+    if (q >= q1) return false;
+    const long long qe = q + 4 < q1 ? q + 4 : q1;
+    g.qs = q;
+    g.nq = static_cast<int>(qe - q);
+    // piece 0: up to the end of q's chunk; piece 1: the rest (next chunk)
+    const int o = static_cast<int>(q / qpe), qi = static_cast<int>(q % qpe);
+    const long long cend = static_cast<long long>(o) * qpe + (qi / 4 + 1) * 4;
+    const long long e = cend < qe ? cend : qe;
+    g.o[0] = o;
+    g.c[0] = qi / 4;
+    g.qa[0] = qi % 4;
+    g.n[0] = static_cast<int>(e - q);
+    g.np = e < qe ? 2 : 1;
+    const int o1 = static_cast<int>(e / qpe), qi1 = static_cast<int>(e % qpe);
+    g.o[1] = o1;
+    g.c[1] = qi1 / 4;
+    g.qa[1] = 0;
+    g.n[1] = static_cast<int>(qe - e);
+    q = qe;
+    return true;
+  }
+};
+
+__device__ __forceinline__ int pow2_divisor(int x, int cap) {
+  int m = 1;
+  while (m < cap && x % (2 * m) == 0) m *= 2;
+  return m;
+}
+// tiles per ring entry: >= 32 KiB of weights per entry whatever the width,
+// so the single-warp producer/MMA bookkeeping per entry is amortised
+__device__ __forceinline__ int tiles_per_entry(int nq, int cap) {
+  const int t = nq >= 3 ? 2 : (nq == 2 ? 4 : 8);
+  return t < cap ? t : cap;
+}
+struct Geom {
+  uint32_t size, win;  // bytes; read window from the entry start
+  int m;
+};
+__device__ __forceinline__ Geom gu_geom(int nq, int cap) {
+  const int m = tiles_per_entry(nq, cap);
+  const uint32_t a = static_cast<uint32_t>(nq) * QB;
+  const uint32_t size = static_cast<uint32_t>(m) * a;
+  const uint32_t w = static_cast<uint32_t>(m - 1) * a + TILE;  // an M = 128 A operand reads 16 KiB
+  return {size, size > w ? size : w, m};
+}
+__device__ __forceinline__ Geom dn_geom(int nq, int cap) {
+  const int m = tiles_per_entry(nq, cap);
+  const uint32_t size = static_cast<uint32_t>(m) * static_cast<uint32_t>(nq) * QB;
+  return {size, size, m};
+}
+__device__ __forceinline__ uint32_t ring_place(uint32_t& head, const Geom& g, uint32_t rb) {
+  uint32_t e = head;
+  if (e + g.win > rb) e = 0;
+  head = e + ((g.size + 1023u) & ~1023u);
+  return e;
+}
+
+__device__ __forceinline__ void stamp(const FfnArgs& a, int slot) {
+  if (a.dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+    a.dbg[blockIdx.x * DBG + slot] = t;
+  }
+}
+__device__ __forceinline__ void wait_acc(const FfnArgs& a, uint64_t* bar, uint32_t parity, long long& acc) {
+  if (a.dbg) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+
+__device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_all() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// <= 200 registers so a 4-warp combine CTA still fits next to this CTA
+// (programmatic dependent launch overlaps the two only when they co-reside).
+__global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int d = a.d, T = a.T;
+  const int ktiles = d / 64, mtiles = d / 128;
+  const long long chunk_bytes = 3LL * 64 * d * 2;
+  const int qpe = a.ffn / 16;
+  const uint32_t RB = static_cast<uint32_t>(a.ring_bytes);
+
+  // [a^T 2 x (hi, lo) x 4 KiB][h^T ktiles x 2 KiB][ring][entry gates][entry masks][misc][mbarriers]
+  uint8_t* p = smem_raw;
+  uint8_t* aT = p;
+  p += 2 * 2 * 4096;
+  uint8_t* hts = p;
+  p += static_cast<size_t>(ktiles) * HTS;
+  uint8_t* ring = p;
+  p += RB;
+  float* ent_gate = reinterpret_cast<float*>(p);  // [ENT_MAX][16]
+  p += ENT_MAX * 16 * 4;
+  uint32_t* ent_mask = reinterpret_cast<uint32_t*>(p);  // [ENT_MAX] tokens routed to the entry
+  p += ENT_MAX * 4;
+  int* misc = reinterpret_cast<int*>(p);  // [1] TMEM base
+  p += 16;
+  uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
+  uint64_t* full = bars;
+  uint64_t* empty = full + NSLOT;
+  uint64_t* d1_full = empty + NSLOT;  // [2]
+  uint64_t* d1_empty = d1_full + 2;   // [2]
+  uint64_t* at_full = d1_empty + 2;   // [2]
+  uint64_t* at_empty = at_full + 2;   // [2]
+  uint64_t* d2_full = at_empty + 2;   // [1]
+  uint64_t* ht_full = d2_full + 1;    // [ktiles]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    stamp(a, 0);
+    if (a.dbg) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      a.dbg[blockIdx.x * DBG + 24] = smid;
+    }
+  }
+  const int n_hits = a.counters[7];
+  const long long n = static_cast<long long>(n_hits + a.n_shared) * qpe;
+  const int G = gridDim.x, b = blockIdx.x;
+  const long long q0 = n > 0 ? (b * n) / G : 0;
+  const long long q1 = n > 0 ? ((b + 1) * n) / G : 0;
+  if (q0 >= q1) return;
+  const int o_first = static_cast<int>(q0 / qpe);
+  const int n_ent = static_cast<int>((q1 - 1) / qpe) - o_first + 1;
+  if (n_ent > ENT_MAX) __trap();  // the host plan rules this out (ffn_tg_grid_ok)
+
+  if (tid == 0) {
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&d1_full[i], 1);
+      mbar_init(&d1_empty[i], 4);
+      mbar_init(&at_full[i], 1);
+      mbar_init(&at_empty[i], 1);
+    }
+    mbar_init(d2_full, 1);
+    for (int i = 0; i < ktiles; ++i) mbar_init(&ht_full[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  __syncthreads();
+  if (tid == 0) pdl_trigger();  // the combine may launch and park on its own wait
+
+  const int kcap = pow2_divisor(ktiles, 8), mcap = pow2_divisor(mtiles, 8);
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    // Starts streaming weights right away (they do not depend on the
+    // previous kernel); the h^T slices follow the programmatic-dependency
+    // wait, which it takes the first time the ring is full (or at the end).
+    const bool leader = elect_one();
+    long long w_empty = 0;
+    const uint64_t pol = a.l2_policy == 1 ? l2_evict_normal_policy() : l2_evict_first_policy();
+    const uint64_t pol_h = l2_evict_normal_policy();
+    // entry image bases, one lane per entry of this CTA's range
+    unsigned long long my_base = 0;
+    if (lane < n_ent) {
+      const int o = o_first + lane;
+      const uint16_t* w = o < n_hits ? a.pool + static_cast<long long>(a.slot_of[a.hit_list[o]]) * a.expert_elems
+                                     : a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
+      my_base = reinterpret_cast<unsigned long long>(w);
+    }
+    bool waited = false;
+    auto wait_pred = [&]() {
+      pdl_wait();
+      if (leader) {
+        const uint8_t* hTb = reinterpret_cast<const uint8_t*>(a.hT);
+        for (int kt = 0; kt < ktiles; ++kt) {
+          mbar_arrive_expect_tx(&ht_full[kt], HTS);
+          bulk_g2s(hts + kt * HTS, hTb + static_cast<size_t>(kt) * HTS, HTS, &ht_full[kt], pol_h);
+        }
+      }
+      waited = true;
+      stamp(a, 22);
+    };
+    uint32_t head = 0, idx = 0, tail = 0;
+    // in-flight entry table, one ring slot per lane (NSLOT == 32): the
+    // "does the new entry overlap an unreleased one" test is one warp vote
+    uint32_t my_off = 0, my_size = 0, my_idx = 0xFFFFFFFFu;
+    auto reserve = [&](const Geom& g) -> uint32_t {
+      uint32_t e = head;
+      if (e + g.win > RB) e = 0;
+      for (;;) {
+        const bool mine = my_idx != 0xFFFFFFFFu && my_idx >= tail && my_off < e + g.size && e < my_off + my_size;
+        const bool over = idx - tail >= static_cast<uint32_t>(NSLOT) || __any_sync(0xffffffffu, mine);
+        if (!over) break;
+        if (!waited) wait_pred();
+        wait_acc(a, &empty[tail % NSLOT], (tail / NSLOT) & 1u, w_empty);
+        ++tail;
+      }
+      if (lane == static_cast<int>(idx % NSLOT)) {
+        my_off = e;
+        my_size = g.size;
+        my_idx = idx;
+      }
+      head = e + ((g.size + 1023u) & ~1023u);
+      return e;
+    };
+    // chunk bases of a group's pieces (warp-uniform: every lane shuffles)
+    auto piece_bases = [&](const Grp& g, const uint8_t* (&pb)[2]) {
+      const unsigned long long b0 = __shfl_sync(0xffffffffu, my_base, g.o[0] - o_first);
+      const unsigned long long b1 = __shfl_sync(0xffffffffu, my_base, g.np > 1 ? g.o[1] - o_first : 0);
+      pb[0] = reinterpret_cast<const uint8_t*>(b0) + static_cast<long long>(g.c[0]) * chunk_bytes;
+      pb[1] = reinterpret_cast<const uint8_t*>(b1) + static_cast<long long>(g.np > 1 ? g.c[1] : 0) * chunk_bytes;
+    };
+    // tiles [t0, t0 + m) (tile index within the chunk: K-tiles then M-tiles)
+    // of every piece, slot-packed: tile j of the entry at j * nq * 4 KiB
+    auto copy_entry = [&](const Grp& g, const uint8_t* const (&pb)[2], int t0, int m, uint32_t e, uint64_t* bar) {
+      if (!leader) return;
+      const uint32_t ab = static_cast<uint32_t>(g.nq) * QB;
+      const uint32_t n0 = static_cast<uint32_t>(g.n[0]) * QB;
+      for (int j = 0; j < m; ++j) {
+        bulk_g2s(ring + e + j * ab, pb[0] + static_cast<size_t>(t0 + j) * TILE + g.qa[0] * QB, n0, bar, pol);
+        if (g.np > 1)
+          bulk_g2s(ring + e + j * ab + n0, pb[1] + static_cast<size_t>(t0 + j) * TILE,
+                   static_cast<uint32_t>(g.n[1]) * QB, bar, pol);
+      }
+    };
+    GroupIt it{q0, q1, qpe};
+    Grp cur, prev;
+    bool more = it.next(cur), has_prev = false;
+    const uint8_t* cb[2];
+    const uint8_t* pbs[2];
+    piece_bases(cur, cb);
+    while (more || has_prev) {
+      if (more) {  // GU(i)
+        const Geom g = gu_geom(cur.nq, kcap);
+        for (int kt = 0; kt < ktiles; kt += g.m) {
+          const uint32_t e = reserve(g);
+          uint64_t* bar = &full[idx % NSLOT];
+          if (leader) mbar_arrive_expect_tx(bar, g.size);
+          copy_entry(cur, cb, kt, g.m, e, bar);
+          ++idx;
+        }
+      }
+      if (has_prev) {  // DN(i-1)
+        const Geom g = dn_geom(prev.nq, mcap);
+        for (int mt = 0; mt < mtiles; mt += g.m) {
+          const uint32_t e = reserve(g);
+          uint64_t* bar = &full[idx % NSLOT];
+          if (leader) mbar_arrive_expect_tx(bar, g.size);
+          copy_entry(prev, pbs, ktiles + mt, g.m, e, bar);
+          ++idx;
+        }
+      }
+      has_prev = more;
+      if (more) {
+        prev = cur;
+        pbs[0] = cb[0];
+        pbs[1] = cb[1];
+        more = it.next(cur);
+        if (more) piece_bases(cur, cb);
+      }
+    }
+    if (!waited) wait_pred();
+    if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
+  } else {
+    // TMEM allocation (MMA warp) and routing staging (epilogue warps) run
+    // while the producer's first copies are in flight.
+    if (warp == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&misc[1])),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      // entry r (= o_first + r): per-token gate (0 for tokens not routed to
+      // it) and the token mask; one warp per entry, one lane per routed slot
+      const int ew = warp - 2;
+      {  // a^T columns of tokens >= T stay zero for the whole launch
+        uint4* z = reinterpret_cast<uint4*>(aT);
+        for (int i = tid - 64; i < 2 * 2 * 4096 / 16; i += EPI_THREADS) z[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      for (int r = ew; r < n_ent; r += 4) {
+        const int o = o_first + r;
+        if (lane < 16) ent_gate[r * 16 + lane] = 0.f;
+        __syncwarp();
+        uint32_t bit = 0;
+        if (o < n_hits) {
+          const int e = a.hit_list[o];
+          const int p0 = a.offsets[e];
+          const int nt = a.offsets[e + 1] - p0;
+          if (lane < nt) {
+            const int ix = a.perm[p0 + lane];
+            const int t = ix / a.k;
+            ent_gate[r * 16 + t] = a.gates[ix];
+            bit = 1u << t;
+          }
+        } else if (lane < T) {
+          ent_gate[r * 16 + lane] = 1.f;
+          bit = 1u << lane;
+        }
+        bit = __reduce_or_sync(0xffffffffu, bit);
+        if (lane == 0) ent_mask[r] = bit;
+        __syncwarp();
+      }
+    }
+    fence_before();
+    named_bar_sync(1, 32 + EPI_THREADS);
+    fence_after();
+    const uint32_t tmem = static_cast<uint32_t>(misc[1]);
+
+    if (warp == 1) {
+      // ------------------------------------------------ MMA issuer
+      // whole warp in convergent flow (warp-uniform descriptors); one elected
+      // lane issues the MMAs and commits
+      const bool leader = elect_one();
+      long long w_full = 0, w_at = 0, w_d1e = 0;
+      Phase d1e[2], ate[2];
+      uint32_t head = 0, idx = 0;
+      int ht_ok = 0;  // h^T slices [0, ht_ok) known to have landed
+      const uint32_t ring_addr = smem_u32(ring), at_addr = smem_u32(aT), ht_addr = smem_u32(hts);
+      GroupIt it{q0, q1, qpe};
+      Grp cur, prev;
+      bool more = it.next(cur), has_prev = false;
+      int i = 0;
+      while (more || has_prev) {
+        if (more) {  // GU(i): D1[i & 1] = W_gu(group) x h^T
+          const int b1 = i & 1;
+          wait_acc(a, &d1_empty[b1], d1e[b1].bit ^ 1u, w_d1e);
+          d1e[b1].flip();
+          fence_after();
+          const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
+          const Geom g = gu_geom(cur.nq, kcap);
+          const uint32_t ab = static_cast<uint32_t>(cur.nq) * QB;
+          for (int kt = 0; kt < ktiles; kt += g.m) {
+            const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
+            wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
+            ++idx;
+            for (; ht_ok < kt + g.m; ++ht_ok) mbar_wait(&ht_full[ht_ok], 0);
+            if (i == 0 && kt == 0 && leader) stamp(a, 2);
+            fence_after();
+            if (leader) {
+              for (int j = 0; j < g.m; ++j) {
+                const uint64_t adesc = smem_desc(ring_addr + off + j * ab, 128, 1024);
+                const uint64_t bdesc = smem_desc(ht_addr + (kt + j) * HTS, 128, 1024);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
+                  mma_bf16(d1, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0);
+              }
+              mma_commit(&empty[slot]);
+            }
+            __syncwarp();
+          }
+          if (leader) mma_commit(&d1_full[b1]);
+          __syncwarp();
+          if (i == 0 && leader) stamp(a, 3);
+        }
+        if (has_prev) {  // DN(i-1): D2 += W_down(group) x a^T(i-1), hi + lo
+          const int ab_ = (i - 1) & 1;
+          wait_acc(a, &at_full[ab_], ate[ab_].bit, w_at);
+          ate[ab_].flip();
+          fence_after();
+          const uint32_t ahi = at_addr + static_cast<uint32_t>(ab_) * 8192u;
+          const uint64_t bhi = smem_desc(ahi, 256, 128), blo = smem_desc(ahi + 4096u, 256, 128);
+          const Geom g = dn_geom(prev.nq, mcap);
+          const uint32_t ab = static_cast<uint32_t>(prev.nq) * QB;
+          for (int mt = 0; mt < mtiles; mt += g.m) {
+            const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
+            wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
+            ++idx;
+            fence_after();
+            if (leader) {
+              for (int j = 0; j < g.m; ++j) {
+                const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>((mt + j) * 16);
+                for (int s = 0; s < prev.nq; ++s) {  // slot s = K-step s of a^T (+512 B = +32)
+                  const uint64_t adn = smem_desc(ring_addr + off + j * ab + s * QB, 2048, 128);
+                  mma_bf16(d2, adn, bhi + 32 * s, (i == 1 && s == 0) ? 0u : 1u);
+                  mma_bf16(d2, adn, blo + 32 * s, 1u);
+                }
+              }
+              mma_commit(&empty[slot]);
+            }
+            __syncwarp();
+          }
+          if (leader) mma_commit(&at_empty[ab_]);
+          __syncwarp();
+        }
+        has_prev = more;
+        if (more) {
+          prev = cur;
+          more = it.next(cur);
+        }
+        ++i;
+      }
+      if (leader) mma_commit(d2_full);
+      __syncwarp();
+      if (a.dbg && leader) {
+        a.dbg[blockIdx.x * DBG + 9] = static_cast<unsigned long long>(w_full);
+        a.dbg[blockIdx.x * DBG + 10] = static_cast<unsigned long long>(w_at);
+        a.dbg[blockIdx.x * DBG + 12] = static_cast<unsigned long long>(w_d1e);
+      }
+    } else {
+      // ------------------------------------------------ epilogue (4 warps)
+      pdl_wait();  // partial blocks are still being read by the previous combine
+      const int q = warp & 3;   // TMEM lane quarter = group slot
+      const int et = tid - 64;  // 0..127
+      Phase d1f[2], atf[2];
+      long long w_d1f = 0, w_d2f = 0;
+      GroupIt it{q0, q1, qpe};
+      Grp g;
+      int i = 0;
+      while (it.next(g)) {
+        // ---- A(i): D1 -> a^T (bf16 hi/lo) for DN(i)
+        const int b1 = i & 1;
+        wait_acc(a, &d1_full[b1], d1f[b1].bit, w_d1f);
+        d1f[b1].flip();
+        fence_after();
+        float v[16];
+        tc::tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b1 * 16), v);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d1_empty[b1]);
+        const int ab = i & 1;
+        mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);  // DN(i-2) done with this buffer
+        atf[ab].flip();
+        if (q < g.nq) {
+          // lanes 0-15: gate rows f = 16q + s; lanes 16-31: the up rows of the same f
+          const float* gs = ent_gate + (static_cast<int>((g.qs + q) / qpe) - o_first) * 16;
+          const int f = 16 * q + (lane & 15);
+          uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
+          uint16_t* lo = hi + 2048;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            if (t < T) {
+              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 16);
+              if ((t & 1) == (lane >> 4)) {  // lanes 0-15 even tokens, 16-31 odd tokens
+                const float gv = lane < 16 ? v[t] : pv;
+                const float uv = lane < 16 ? pv : v[t];
+                const float gt = gs[t];
+                const float av = gt != 0.f ? __fdividef(gv, 1.f + __expf(-gv)) * uv * gt : 0.f;
+                const uint16_t h16 = f32_to_bf16_rn(av);
+                const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
+                // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
+                const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
+                hi[off] = h16;
+                lo[off] = f32_to_bf16_rn(rem);
+              }
+            }
+          }
+        }
+        fence_proxy_async();
+        named_bar_sync(2, EPI_THREADS);
+        if (et == 0) {
+          mbar_arrive(&at_full[ab]);
+          if (i == 0) stamp(a, 4);
+        }
+        ++i;
+      }
+      // ---- drain: D2 (all M-tiles, the CTA's whole sum) -> shared memory
+      // [T][d] fp32 (the ring is idle: every entry has been consumed) -> one
+      // bulk store per token row this CTA touched
+      wait_acc(a, d2_full, 0, w_d2f);
+      if (et == 0) stamp(a, 18);
+      fence_after();
+      uint32_t tmask = 0;  // tokens this CTA touched
+      for (int r = 0; r < n_ent; ++r) tmask |= ent_mask[r];
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0);
+      float* stg = reinterpret_cast<float*>(ring);
+      for (int mt = 0; mt < mtiles; mt += 2) {
+        uint32_t y0[16], y1[16];
+        const bool two = mt + 1 < mtiles;
+        if (T <= 8) {
+          tc::tmem_ld8_nw(tbase + static_cast<uint32_t>(mt * 16), y0);
+          if (two) tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + 1) * 16), y1);
+        } else {
+          tc::tmem_ld16_nw(tbase + static_cast<uint32_t>(mt * 16), y0);
+          if (two) tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + 1) * 16), y1);
+        }
+        tc::tmem_wait_ld();
+        float* r0 = stg + mt * 128 + 32 * q + lane;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < T) {
+            r0[static_cast<size_t>(t) * d] = __uint_as_float(y0[t]);
+            if (two) r0[static_cast<size_t>(t) * d + 128] = __uint_as_float(y1[t]);
+          }
+      }
+      fence_before();
+      fence_proxy_async();
+      named_bar_sync(2, EPI_THREADS);
+      if (et == 0) stamp(a, 19);
+      if (q == 0 && lane < T) {  // one lane per token row
+        if ((tmask >> lane) & 1u)
+          bulk_s2g(a.partial + (static_cast<long long>(b) * T + lane) * d, stg + static_cast<size_t>(lane) * d,
+                   static_cast<uint32_t>(d) * 4u);
+        bulk_commit_wait_all();
+      }
+      if (et == 0) stamp(a, 20);
+      if (a.dbg && tid == 64) {
+        a.dbg[blockIdx.x * DBG + 13] = static_cast<unsigned long long>(w_d1f);
+        a.dbg[blockIdx.x * DBG + 14] = static_cast<unsigned long long>(w_d2f);
+      }
+    }
+  }
+  __syncwarp();  // bar.sync is warp-aligned: a warp arriving in pieces is counted once per piece
+  fence_before();
+  __syncthreads();
+  if (tid == 0) stamp(a, 6);
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(static_cast<uint32_t>(misc[1])),
+                 "r"(TMEM_COLS));
+    if (lane == 0) stamp(a, 23);
+  }
+}
+
+}  // namespace tg
+}  // namespace dev
+
+size_t ffn_tg_smem_bytes(int d, int ring_bytes) {
+  return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * dev::tg::HTS + static_cast<size_t>(ring_bytes) +
+         dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
+}
+
+// Every CTA's range must touch <= ENT_MAX entries (one producer lane each).
+bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid) {
+  const long long qpe = d_ffn / 16, n = static_cast<long long>(n_entries) * qpe;
+  const long long maxq = (n + grid - 1) / grid;
+  return grid > 0 && (maxq > 0 ? (maxq - 1) / qpe + 2 : 1) <= dev::tg::ENT_MAX;
+}
+
+// Grouped mode: d <= 2048 (D2 for all d/128 M-tiles fits in TMEM columns
+// 256-511), the drain's [T][d] fp32 staging fits in the ring, and the ring
+// holds the widest entry window (44 KiB).
+int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
+  if (d > dev::tg::MAX_KT * 64 || d % 128 || T > 16) return 0;
+  const size_t fixed = ffn_tg_smem_bytes(d, 0);
+  if (fixed >= smem_limit) return 0;
+  const int rb = static_cast<int>(((smem_limit - fixed) / 1024) * 1024);
+  const int need = static_cast<int>(T) * d * 4 > 45056 ? T * d * 4 : 45056;
+  return rb >= need ? rb : 0;
+}
+
+cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(dev::tg::expert_ffn_tg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, a);
+}
+
+}  // namespace moespac

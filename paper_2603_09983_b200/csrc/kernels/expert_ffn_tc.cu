@@ -36,6 +36,7 @@
 
 #include "common.cuh"
 #include "launch.hpp"
+#include "tcgen05.cuh"
 
 namespace moespac {
 namespace dev {
@@ -51,70 +52,10 @@ constexpr int FCH = 64;  // ffn rows per chunk
 constexpr int QROWS = 16;
 constexpr int TMEM_COLS = 512;
 constexpr int D2_COL0 = 256;
-constexpr int ACC_SMEM = 0, ACC_GLOBAL = 1, ACC_TMEM = 2;  // FfnArgs::acc_mode
+constexpr int ACC_SMEM = 0, ACC_GLOBAL = 1, ACC_TMEM = 2, ACC_GROUP = 3;  // FfnArgs::acc_mode
 constexpr int TMEM_ACC_MAX_D = (512 - D2_COL0) / 16 * 128;  // TMEM mode: D2 for all M-tiles fits
 constexpr int PASS_TILES = 8;
 constexpr int ENT_PRE = 8;  // entries whose routing is staged in the prologue
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
-
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
-  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
-         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
-}
-
-__device__ __forceinline__ bool elect_one() {
-  uint32_t p = 0;
-  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}" : "=r"(p));
-  return p != 0;
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-struct Phase {
-  uint32_t bit = 0;
-  __device__ __forceinline__ void flip() { bit ^= 1u; }
-};
-
 struct Ring {
   int stage = 0;
   uint32_t ph = 0;
@@ -192,7 +133,7 @@ constexpr int DBG = 32;  // debug slots per CTA
 __device__ __forceinline__ void stamp(const FfnArgs& a, int slot) {
   if (a.dbg) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
     a.dbg[blockIdx.x * DBG + slot] = t;
   }
 }
@@ -335,6 +276,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
       ent_n[e] = nt;
     }
   }
+  __syncwarp();  // bar.sync is warp-aligned: a warp arriving in pieces is counted once per piece
   fence_before();
   __syncthreads();
   fence_after();
@@ -900,6 +842,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
   if (tid == 64) {
     stamp(a, 5);  // epilogue finished (all flushes written)
   }
+  __syncwarp();  // bar.sync is warp-aligned: a warp arriving in pieces is counted once per piece
   fence_before();
   __syncthreads();
   if (tid == 0) {
@@ -968,7 +911,8 @@ size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, int acc_mode) {
 }
 
 // accum: 0 auto, 1 shared-memory accumulator, 2 global (L2) accumulator,
-// 3 TMEM accumulator. Auto: TMEM when D2 for every M-tile fits next to the
+// 3 TMEM accumulator, 4 grouped (whole-CTA TMEM accumulator, separate
+// kernel). Auto: grouped when d <= 2048, else TMEM when D2 for every M-tile fits next to the
 // D1 buffers (d <= 2048) — no per-segment accumulate pass at all and the
 // whole remaining shared memory for the ring; else shared memory when it
 // leaves a >= 64 KiB ring; else global. Measured: the L2 accumulator puts
@@ -991,6 +935,16 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
     return p;
   };
   const bool tmem_ok = d <= dev::tc::TMEM_ACC_MAX_D;
+  if (accum == 4 || (accum == 0 && tmem_ok)) {
+    // grouped kernel (expert_ffn_grouped.cu): whole-CTA TMEM accumulator
+    const int rb = ffn_tg_ring_bytes(T, d, smem_limit);
+    if (rb > 0) {
+      FfnPlan p{rb / 1024, false, ffn_tg_smem_bytes(d, rb)};
+      p.acc_mode = dev::tc::ACC_GROUP;
+      return p;
+    }
+    if (accum == 4) return {0, false, 0};
+  }
   if (accum == 3 || (accum == 0 && tmem_ok)) {
     if (!tmem_ok) return {0, false, 0};
     const int rb = ring_for(dev::tc::ACC_TMEM);
@@ -1007,6 +961,7 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
 }
 
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
+  if (a.acc_mode == dev::tc::ACC_GROUP) return launch_expert_ffn_tg(a, grid, smem, stream, pdl);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =

@@ -43,7 +43,8 @@ struct FfnArgs {
   int n_stages;             // CUDA-core kernel: ring stages
   int ring_bytes;           // tensor-core kernel: byte-ring size
   int global_acc;           // 1: accumulate down-proj partials in `partial` (large T*d)
-  int acc_mode;             // tensor-core kernel: 0 shared-memory, 1 global (L2), 2 TMEM accumulator
+  int acc_mode;             // tensor-core kernel: 0 shared-memory, 1 global (L2), 2 TMEM accumulator,
+                            // 3 grouped (whole-CTA TMEM accumulator, expert_ffn_grouped.cu)
   const uint16_t* hT;       // tcgen05 variant: h^T UMMA image [d/64][16 tok][64] (build_hT)
   unsigned long long* dbg;  // optional per-CTA profiling record [grid][32]
   int l2_policy;            // weight stream L2 policy: 0 evict_first, 1 evict_normal
@@ -68,10 +69,12 @@ struct CombineArgs {
   const int32_t* counters;  // counters[7] = local hits
   int n_shared;
   int grid;                 // K3 grid size
+  int per_cta;              // 1: one partial block per K3 CTA (grouped K3), else per (CTA, entry) pair
   const float* partial;
   float* y_out;             // [T][d] fp32 (may be null)
   uint16_t* h_out;          // [T][d] bf16 (may be null)
   uint16_t* hT_out;         // optional h^T UMMA image of h_out (next layer's tensor-core K3 operand)
+  unsigned long long* dbg;  // optional per-CTA profiling record (K3 trace rows, slots 26-29), or null
 };
 
 }  // namespace dev
@@ -84,7 +87,7 @@ struct FfnPlan {
   int n_stages;     // CUDA-core: ring stages; tensor-core: ring KiB
   bool global_acc;
   size_t smem;
-  int acc_mode = 0; // tensor-core: 0 shared-memory, 1 global (L2), 2 TMEM accumulator
+  int acc_mode = 0; // tensor-core: 0 shared-memory, 1 global (L2), 2 TMEM accumulator, 3 grouped
 };
 size_t ffn_smem_bytes(int T, int d, int n_stages, bool global_acc);
 FfnPlan ffn_plan(int T, int d, size_t smem_limit);
@@ -92,6 +95,10 @@ cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cuda
 size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, int acc_mode);
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum = 0);
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
+size_t ffn_tg_smem_bytes(int d, int ring_bytes);
+int ffn_tg_ring_bytes(int T, int d, size_t smem_limit);
+bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid);
+cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
 cudaError_t launch_build_hT(const uint16_t* h, int T, int d, uint16_t* out, cudaStream_t stream, bool pdl = false);
 cudaError_t launch_pack_expert_tc(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                   uint16_t* out, cudaStream_t stream);

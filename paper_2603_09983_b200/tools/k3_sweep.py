@@ -28,11 +28,12 @@ def main():
     ap.add_argument("--kernels", default="2,1")
     ap.add_argument("--accum", type=int, default=0)
     ap.add_argument("--l2", type=int, default=0)
+    ap.add_argument("--grid", type=int, default=0, help="CTAs (0: one per SM)")
     ap.add_argument("--stamps", action="store_true", help="dump per-CTA timeline (tensor-core kernel)")
     args = ap.parse_args()
     d, ffn, T, k, N = args.d, args.ffn, args.T, args.k, args.N
     dev = torch.device("cuda")
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sms = args.grid or torch.cuda.get_device_properties(0).multi_processor_count
     img = 3 * d * ffn
     pool = torch.empty(N * img, dtype=torch.int16, device=dev)
     abi.check(abi.lib().moespac_fill_synthetic(abi.ptr(pool), pool.numel(), 7, 0.02, abi._stream(None)))

@@ -92,6 +92,25 @@ def main():
     ends = (x[:, 6] - base) / 1e3
     first = (x[:, 2] - base) / 1e3
     sm = x[:, 24].astype(int)
+    # work shape of every CTA of that layer (the kernel's static split)
+    cnt = abi.fetch(ctx.views().counters_dev, (L, 8), np.int32)
+    G = x.shape[0]
+    n_units = (int(cnt[lm, 7]) + w.n_shared_units) * qpe
+    quarters = np.array([((b + 1) * n_units) // G - (b * n_units) // G for b in range(G)])
+    segs = []
+    for b in range(G):
+        q, q1, ns = (b * n_units) // G, ((b + 1) * n_units) // G, 0
+        while q < q1:
+            q = min((q // 4 + 1) * 4, q1)
+            ns += 1
+        segs.append(ns)
+    segs = np.array(segs)
+    for nq in sorted(set(quarters.tolist())):
+        m = quarters == nq
+        print(json.dumps({"layer": lm, "quarters": nq, "ctas": int(m.sum()),
+                          "end_us_med": round(float(np.median(ends[m])), 2),
+                          "end_us_max": round(float(ends[m].max()), 2),
+                          "segs_mean": round(float(segs[m].mean()), 2)}))
     print(json.dumps({"layer": lm, "end_pct_us": [round(float(np.percentile(ends, p)), 2) for p in (0, 10, 50, 90, 100)],
                       "first_data_pct_us": [round(float(np.percentile(first, p)), 2) for p in (0, 50, 100)],
                       "slowest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(-ends)[:8]],
@@ -113,6 +132,36 @@ def main():
                                           "std_of_sm_means": round(float(np.std(list(sm_mean.values()))), 4),
                                           "latest_sms": [[s_, round(sm_mean[s_], 4)] for s_ in order[:10]],
                                           "earliest_sms": [[s_, round(sm_mean[s_], 4)] for s_ in order[-10:]]}}))
+    # layer handoff per SM: next layer's K3 CTA entry / predecessor-done on the
+    # same SM minus this layer's K3 CTA end there
+    x0, x1 = t[lm], t[lm + 1] if lm + 1 < L else None
+    if x1 is not None and (x0[:, 24] != x1[:, 24]).any() or True:
+        end_by_sm = {int(x0[b_, 24]): x0[b_, 6] for b_ in range(x0.shape[0]) if x0[b_, 6] > 0}
+        ent, prd = [], []
+        for b_ in range(x1.shape[0]):
+            s_ = int(x1[b_, 24])
+            if s_ in end_by_sm and x1[b_, 0] > 0:
+                ent.append((x1[b_, 0] - end_by_sm[s_]) / 1e3)
+                prd.append((x1[b_, 22] - end_by_sm[s_]) / 1e3)
+        lend = (x0[:, 6].max() - x0[:, 6]) / 1e3
+        print(json.dumps({"layer": lm, "next_entry_minus_sm_end_us_pct": [round(float(np.percentile(ent, p_)), 2) for p_ in (0, 10, 50, 90, 100)],
+                          "next_pred_minus_sm_end_us_pct": [round(float(np.percentile(prd, p_)), 2) for p_ in (0, 10, 50, 90, 100)],
+                          "layer_end_max_minus_cta_end_pct": [round(float(np.percentile(lend, p_)), 2) for p_ in (0, 50, 100)]}))
+    # combine CTAs of that layer (slots 26-29 of the same rows): start, after
+    # their predecessor wait, end — relative to this layer's last K3 CTA end
+    cb = t[lm][:, 26] > 0
+    if cb.any():
+        kend = t[lm][:, 6].max()
+        rel = lambda j: [round(float(np.percentile((t[lm][cb, j] - kend) / 1e3, p_)), 2) for p_ in (0, 50, 100)]
+        xs = t[lm]
+        print(json.dumps({"layer": lm, "slot_minus_end_us_med": {str(j): round(float(np.median((xs[xs[:, j] > 0, j] - xs[xs[:, j] > 0, 6]) / 1e3)), 2)
+                                                                for j in (0, 2, 3, 4, 17, 18, 19, 20, 21, 22, 23, 25) if (xs[:, j] > 0).any()}}))
+        dz = t[lm][:, 23] > 0
+        if dz.any():
+            print(json.dumps({"layer": lm, "dealloc_minus_end_us_pct": [round(float(np.percentile((t[lm][dz, 23] - t[lm][dz, 6]) / 1e3, p_)), 2) for p_ in (0, 50, 100)],
+                              "predealloc_minus_end_us_pct": [round(float(np.percentile((t[lm][dz, 25] - t[lm][dz, 6]) / 1e3, p_)), 2) for p_ in (0, 50, 100)]}))
+        print(json.dumps({"layer": lm, "combine_ctas": int(cb.sum()), "combine_start_rel_k3_end": rel(26),
+                          "combine_pred_rel_k3_end": rel(27), "combine_end_rel_k3_end": rel(28)}))
     gaps = [r["gap_to_next_us"] for r in rows if "gap_to_next_us" in r]
     spans = [r["k3_span_us"] for r in rows if "k3_span_us" in r]
     print(json.dumps({"config": args.config, "pf": args.pf, "timed_step_ms": round(step_ms, 4),

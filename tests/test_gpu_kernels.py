@@ -175,7 +175,7 @@ def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_f
     _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, 0)
 
 
-@pytest.mark.parametrize("accum", [1, 2, 3], ids=["smem", "global", "tmem"])
+@pytest.mark.parametrize("accum", [1, 2, 3, 4], ids=["smem", "global", "tmem", "grouped"])
 @pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
     (128, 8, 9, 2048, 768, 0, 0, 0.6),     # Qwen3 shape
     (16, 4, 16, 1024, 128, 1, 0, 0.7),     # T = 16 + shared unit
@@ -184,13 +184,37 @@ def test_expert_ffn_and_combine(N, k, T, d, ffn, n_shared, gate_mode, resident_f
 ])
 def test_expert_ffn_tc_accumulator_modes(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, accum):
     """Every down-projection accumulator of the tensor-core K3 (shared memory,
-    global partial block, TMEM) against the fp64 oracle."""
+    global partial block, TMEM per expert, grouped whole-CTA TMEM) against the
+    fp64 oracle."""
     if abi.FFN_TENSOR not in _kernels(d, ffn):
         pytest.skip("shape not supported by the tensor-core kernel")
     _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, accum)
 
 
-def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum):
+@pytest.mark.parametrize("grid", [1, 7, 16, 37, 148, 300])
+@pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
+    (128, 8, 9, 2048, 768, 0, 0, 0.6),     # Qwen3 shape
+    (64, 6, 9, 2048, 1408, 2, 1, 0.3),     # DeepSeek-V2-Lite shape (shared units)
+    (16, 4, 16, 1024, 128, 1, 0, 0.7),     # T = 16, 2 quarters/entry chunk crossings
+    (4, 4, 3, 512, 64, 0, 0, 1.0),         # every token on every expert, 1 chunk per expert
+])
+def test_expert_ffn_grouped_grids(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, grid):
+    """Grouped K3: groups of four quarters cross chunk and expert boundaries
+    and CTAs own 0..many quarters depending on the grid; the combine's
+    per-CTA row lists must cover exactly the CTAs that touched each token."""
+    import ctypes
+    if abi.FFN_TENSOR not in _kernels(d, ffn):
+        pytest.skip("shape not supported by the tensor-core kernel")
+    qpe = ffn // 16
+    maxq = -(-((N + n_shared) * qpe) // grid)
+    if (maxq - 1) // qpe + 2 > 32:
+        pytest.skip("grid below the grouped kernel's per-CTA entry limit")
+    # few CTAs -> long TMEM accumulation chains over many experts; a = silu(g)u·g
+    # enters the down MMA as bf16 hi + lo (~2^-17 relative), so allow 3e-5
+    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 4, grid=grid, tol=3e-5)
+
+
+def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum, grid=None, tol=1e-5):
     rng = np.random.default_rng(N * 7 + T)
     experts = _rand_experts(rng, N, d, ffn)
     shared = _rand_experts(rng, n_shared, d, ffn)
@@ -216,9 +240,9 @@ def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum
                     abi.ptr(bufs["ho"]), abi.ptr(bufs["cnt"]), abi.ptr(bufs["sc"]))
     s0 = abi._stream(None)
     abi.check(abi.lib().moespac_hist_scan_observe(ctypes.byref(a2), s0))
-    grid = torch.cuda.get_device_properties(0).multi_processor_count
-    ws = torch.empty(abi.lib().moespac_ffn_workspace_bytes(T, d, N, n_shared, grid) // 4, dtype=torch.float32,
-                     device="cuda")
+    grid = grid or torch.cuda.get_device_properties(0).multi_processor_count
+    ws = torch.full((abi.lib().moespac_ffn_workspace_bytes(T, d, N, n_shared, grid) // 4,), float("nan"),
+                    dtype=torch.float32, device="cuda")
     h_t = torch.from_numpy(h.view(np.int16)).cuda()
     hT = abi.build_hT(h_t)
     fa = abi.FfnArgs(abi.ptr(h_t), T, d, ffn, k, N, abi.ptr(bufs["perm"]), abi.ptr(bufs["offsets"]), abi.ptr(gates),
@@ -228,13 +252,13 @@ def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum
     y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
     h_out = torch.zeros((T, d), dtype=torch.int16, device="cuda")
     ca = abi.CombineArgs(abi.ptr(h_t), None, T, d, ffn, k, abi.ptr(ids), abi.ptr(bufs["ho"]), abi.ptr(bufs["cnt"]),
-                         n_shared, grid, abi.ptr(ws), abi.ptr(y), abi.ptr(h_out))
+                         n_shared, grid, abi.ptr(ws), abi.ptr(y), abi.ptr(h_out), accum, kernel)
     abi.check(abi.lib().moespac_ffn_combine(ctypes.byref(ca), s0))
     torch.cuda.synchronize()
     y_ref = O.moe_layer(h, ids_ref, gates_ref, {e: experts[e] for e in range(N) if resident[e]}, shared)
     yg = y.cpu().numpy().astype(np.float64)
     rel = np.linalg.norm(yg - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
-    assert rel <= 1e-5, rel
+    assert rel <= tol, rel
     # bf16 layer output: within one bf16 ulp of bf16(h + y_ref)
     _check_bf16_residual(h, y_ref, h_out.cpu().numpy().view(np.uint16))
 
@@ -267,7 +291,7 @@ def test_expert_ffn_deterministic(kernel):
         abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
         y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
         ca = abi.CombineArgs(None, None, T, d, ffn, k, abi.ptr(ids), abi.ptr(bufs["ho"]), abi.ptr(bufs["cnt"]), 0,
-                             148, abi.ptr(ws), abi.ptr(y), None)
+                             148, abi.ptr(ws), abi.ptr(y), None, 0, kernel)
         abi.check(abi.lib().moespac_ffn_combine(ctypes.byref(ca), abi._stream(None)))
         torch.cuda.synchronize()
         outs.append(y.cpu().numpy())
