@@ -293,6 +293,7 @@ def run_ours(args, w, rank, world, local_rank):
     out = {
         "ms": ms, "ms_e2e": ms_e2e, "ms_timed": ms_t, "tokens": tokens, "ffn_ms": ffn_ms, "ffn_bytes": ffn_bytes,
         "ffn_launches": args.steps * L, "launches": launches, "hits": hits, "misses": misses, "loads": loads,
+        "k3_kernel": ctx.k3_kernel(),
         "h2d": float(np.mean([r.h2d_bytes for r in reps_e2e])), "d2h": float(np.mean([r.d2h_bytes for r in reps_e2e])),
         "router_ms": float(np.mean([r.gpu_ms_router for r in reps])),
         "hist_ms": float(np.mean([r.gpu_ms_hist for r in reps])),
@@ -371,7 +372,7 @@ def main():
     line = dict(base, value=tps, ms_per_step=r["ms"] / args.steps, scaling="strong" if world > 1 else "weak")
     line["e2e"] = {"value": r["tokens"] / (r["ms_e2e"] * 1e-3), "unit": "tokens/s",
                    "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])}
-    line["roofline"] = {"bound": "hbm", "kernel": "expert_ffn_kernel (K3)", "achieved": achieved, "peak": hbm_peak,
+    line["roofline"] = {"bound": "hbm", "kernel": r["k3_kernel"], "achieved": achieved, "peak": hbm_peak,
                         "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)" if peak_kind == "measured"
                         else "fallback 6650 GB/s (B200_PROFILING.md)",
                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,

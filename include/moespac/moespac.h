@@ -308,6 +308,15 @@ moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a
  * step runs on it, so events recorded there bracket whole steps. */
 void* moespac_ctx_stream(const moespac_ctx* c);
+/* Which K3 the context's plan picked (for reports and profiles):
+ * CUDA-core GEMV, tcgen05 kernel with its per-segment accumulator (shared
+ * memory / L2 partial block / TMEM), or the grouped tcgen05 kernel. */
+#define MOESPAC_K3_CUDACORE 0
+#define MOESPAC_K3_TC_SMEM 1
+#define MOESPAC_K3_TC_L2 2
+#define MOESPAC_K3_TC_TMEM 3
+#define MOESPAC_K3_GROUPED 4
+int moespac_ctx_k3_variant(const moespac_ctx* c);
 
 /* One verification step end to end with HOST buffers: H2D logits [L][T][N]
  * fp64 and h_in [T][d] bf16, run, D2H h_out [T][d] bf16 + the step's

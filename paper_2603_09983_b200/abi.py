@@ -174,6 +174,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_get_views": (C.c_int, [vp, C.POINTER(CtxViews)]),
         "moespac_ctx_sched": (vp, [vp]),
         "moespac_ctx_stream": (vp, [vp]),
+        "moespac_ctx_k3_variant": (C.c_int, [vp]),
         "moespac_ctx_step_tables": (C.c_int, [vp, vp, vp, vp, vp]),
         "moespac_trace_synth_create": (C.c_int, [C.POINTER(SchedConfig), C.POINTER(vp)]),
         "moespac_trace_synth_next": (C.c_int, [vp, vp, vp]),
@@ -452,6 +453,13 @@ class Context:
 
     def stream(self) -> int:
         return lib().moespac_ctx_stream(self._h) or 0
+
+    K3_NAMES = {0: "expert_ffn_kernel (K3, CUDA-core GEMV)", 1: "expert_ffn_tc_kernel (K3, smem accumulator)",
+                2: "expert_ffn_tc_kernel (K3, L2 accumulator)", 3: "expert_ffn_tc_kernel (K3, TMEM accumulator)",
+                4: "expert_ffn_tg_kernel (K3, grouped)"}
+
+    def k3_kernel(self) -> str:
+        return self.K3_NAMES[lib().moespac_ctx_k3_variant(self._h)]
 
     def views(self) -> CtxViews:
         v = CtxViews()

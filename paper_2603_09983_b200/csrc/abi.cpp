@@ -593,6 +593,16 @@ moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
 
 void* moespac_ctx_stream(const moespac_ctx* c) { return c->e.stream(); }
 
+int moespac_ctx_k3_variant(const moespac_ctx* c) {
+  if (c->e.ffn_kernel() != kFfnTensorCore) return MOESPAC_K3_CUDACORE;
+  switch (c->e.ffn_acc_mode()) {
+    case 0: return MOESPAC_K3_TC_SMEM;
+    case 1: return MOESPAC_K3_TC_L2;
+    case 2: return MOESPAC_K3_TC_TMEM;
+    default: return MOESPAC_K3_GROUPED;
+  }
+}
+
 moespac_status moespac_step(moespac_ctx* c, const double* logits, const uint16_t* h_in, int accepted, uint16_t* h_out,
                             moespac_step_report* rep, moespac_layer_timing* layers) {
   return guard([&] { c->e.step(logits, true, h_in, true, accepted, h_out, true, rep, layers); });

@@ -71,9 +71,11 @@ void ColdExecutor::chunk(const ColdItem& it, int c, const float* hf, float* y, s
         const uint16_t* rp = tile + (row >> 3) * 512 + (row & 7) * 8;
         for (int j = 0; j < 8; ++j)
           for (int e = 0; e < 8; ++e) w[j * 8 + e] = bf(rp[j * 64 + e]);
-        // 16-row quarter q = row / 32: 16 gate rows then 16 up rows
+        // 16-row quarter q = row / 32, octet-interleaved: gate rows f 0-7,
+        // up rows f 0-7, gate rows f 8-15, up rows f 8-15 (f within the quarter)
         const int qq = row >> 5, s = row & 31;
-        float* ar = acc + (s < 16 ? qq * 16 + s : R + qq * 16 + (s - 16)) * 16;
+        const int fl = qq * 16 + ((s >> 4) << 3) + (s & 7);
+        float* ar = acc + (((s >> 3) & 1) ? R + fl : fl) * 16;
         for (int i = 0; i < n; ++i) {
           const float* hv = hf + static_cast<size_t>(it.tok[i]) * d + kt * 64;
           float s = 0.f;

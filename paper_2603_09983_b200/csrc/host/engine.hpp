@@ -52,6 +52,7 @@ class Engine {
   // decision tables the last executed step ran with
   void step_tables(int32_t* taus, uint32_t* rb, uint32_t* lb, int32_t* slots) const;
   int ffn_kernel() const { return kernel_; }
+  int ffn_acc_mode() const { return acc_mode_; }
   const StepScheduler& sched() const { return *sched_; }
   void* stream() const { return compute_; }
 
@@ -103,6 +104,7 @@ class Engine {
   int cold_threads_ = -1;
   int ffn_accum_ = 0;
   int acc_mode_ = 0;
+
   std::unique_ptr<ColdExecutor> cold_;
   float* ycold_d_ = nullptr;   // [L][T][d] host-computed cold-expert outputs
   float* ycold_h_ = nullptr;   // pinned staging of the same

@@ -412,6 +412,9 @@ constexpr int COMBINE_WARPS = 4;  // small footprint: must co-reside with a K3 C
 constexpr int COMBINE_BATCH = 16;  // partial rows in flight per warp
 constexpr int COMBINE_LIST = 48;  // per-warp row list capacity (else streamed)
 
+__device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, const float4 (*red)[32], int t,
+                                              int c, int lane);
+
 // (<= 112 registers: see expert_ffn_tc_kernel)
 __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs a) {
   __shared__ float4 red[COMBINE_WARPS][32];
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.y * 128 + lane * 4;
-  const int qpe = a.ffn / FC;
+  const int qpe = a.per_cta ? a.ffn / 8 : a.ffn / FC;  // work units per entry (grouped K3: 8-row units)
   // The routing (K2 outputs: counters, ids, hit order) was final several
   // kernels ago, so the row list is built before waiting for the K3 launch
   // whose partials it sums: only the partial loads sit on the critical path.
@@ -523,6 +526,12 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
   __syncthreads();
   stamp(28);
   if (warp != 0 || c >= a.d) return;
+  combine_store(a, acc, red, t, c, lane);
+}
+
+// warp 0 of a combine CTA: cross-warp sum, y / residual / bf16 / h^T stores
+__device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, const float4 (*red)[32], int t,
+                                              int c, int lane) {
   for (int w = 1; w < COMBINE_WARPS; ++w) {
     const float4 v = red[w][lane];
     acc.x += v.x;

@@ -8,7 +8,7 @@
 //  * Groups, not chunk segments. The CTA's quarters are taken four at a time
 //    in global order, whatever chunk or expert they belong to, and packed into
 //    the four 32-row slots of one M = 128 gate|up tile (slot s = rows
-//    32s..32s+31: 16 gate rows then the 16 up rows of the same ffn rows). A
+//    32s..32s+31: gate and up rows of the same 16 ffn rows, octet-interleaved). A
 //    CTA with 5-6 quarters runs two full-width GU passes instead of 2-3
 //    partial chunk segments.
 //  * One accumulator. The gate of token t for expert e is applied in the
@@ -51,7 +51,9 @@ constexpr int THREADS = 192;
 constexpr int EPI_THREADS = 128;
 constexpr int NSLOT = 32;      // ring entries in flight (mbarrier pairs)
 constexpr int TILE = 16384;    // one gate|up K-tile or down M-tile of a 64-row chunk
-constexpr int QB = 4096;       // one 16-row quarter of a tile
+constexpr int UB = 2048;       // one 8-row unit (gate + up octet) of a gate|up tile, or 8 k of a down tile
+constexpr int UPC = 8;         // units per 64-row chunk
+constexpr int GMAX = 8;        // units per group (one M = 128 gate|up tile)
 constexpr int HTS = 2048;      // h^T slice of one K-tile (16 tokens x 64 k)
 constexpr int ENT_MAX = 32;    // entries one CTA may touch (one producer lane each)
 constexpr int MAX_KT = 32;     // d <= 2048
@@ -60,38 +62,39 @@ constexpr int TMEM_COLS = 512;
 constexpr int DBG = 32;
 
 // ---------------------------------------------------------------- groups
-// A group is <= 4 consecutive quarters of the CTA's range; it spans at most
-// two chunk pieces (chunks are 4 quarters and entry boundaries are chunk
-// boundaries because ffn % 64 == 0).
+// Work unit = 8 ffn rows of one expert (its 8 gate + 8 up rows: one 2 KiB
+// run per gate|up K-tile, one 2 KiB k-chunk per down M-tile). A group is <= 8
+// consecutive units of the CTA's range; it spans at most two chunk pieces
+// (chunks are 8 units and entry boundaries are chunk boundaries because
+// ffn % 64 == 0).
 struct Grp {
-  long long qs;                 // first quarter (global order)
-  int nq, np;
-  int o[2], c[2], qa[2], n[2];  // piece p: quarters [qa, qa + n) of chunk c of entry o
+  long long us;                 // first unit (global order)
+  int nu, np;
+  int o[2], c[2], pa[2], n[2];  // piece p: units [pa, pa + n) of chunk c of entry o
 };
 
 struct GroupIt {
-  long long q, q1;
-  int qpe;
+  long long u, u1;
+  int upe;  // units per entry = ffn / 8
   __device__ __forceinline__ bool next(Grp& g) {
-    if (q >= q1) return false;
-    const long long qe = q + 4 < q1 ? q + 4 : q1;
-    g.qs = q;
-    g.nq = static_cast<int>(qe - q);
-    // piece 0: up to the end of q's chunk; piece 1: the rest (next chunk)
-    const int o = static_cast<int>(q / qpe), qi = static_cast<int>(q % qpe);
-    const long long cend = static_cast<long long>(o) * qpe + (qi / 4 + 1) * 4;
-    const long long e = cend < qe ? cend : qe;
+    if (u >= u1) return false;
+    const long long ue = u + GMAX < u1 ? u + GMAX : u1;
+    g.us = u;
+    g.nu = static_cast<int>(ue - u);
+    // piece 0: up to the end of u's chunk; piece 1: the rest (next chunk)
+    const int o = static_cast<int>(u / upe), ui = static_cast<int>(u % upe);
+    const long long cend = static_cast<long long>(o) * upe + (ui / UPC + 1) * UPC;
+    const long long e = cend < ue ? cend : ue;
     g.o[0] = o;
-    g.c[0] = qi / 4;
-    g.qa[0] = qi % 4;
-    g.n[0] = static_cast<int>(e - q);
-    g.np = e < qe ? 2 : 1;
-    const int o1 = static_cast<int>(e / qpe), qi1 = static_cast<int>(e % qpe);
-    g.o[1] = o1;
-    g.c[1] = qi1 / 4;
-    g.qa[1] = 0;
-    g.n[1] = static_cast<int>(qe - e);
-    q = qe;
+    g.c[0] = ui / UPC;
+    g.pa[0] = ui % UPC;
+    g.n[0] = static_cast<int>(e - u);
+    g.np = e < ue ? 2 : 1;
+    g.o[1] = static_cast<int>(e / upe);
+    g.c[1] = static_cast<int>(e % upe) / UPC;
+    g.pa[1] = 0;
+    g.n[1] = static_cast<int>(ue - e);
+    u = ue;
     return true;
   }
 };
@@ -101,26 +104,27 @@ __device__ __forceinline__ int pow2_divisor(int x, int cap) {
   while (m < cap && x % (2 * m) == 0) m *= 2;
   return m;
 }
-// tiles per ring entry: >= 32 KiB of weights per entry whatever the width,
-// so the single-warp producer/MMA bookkeeping per entry is amortised
-__device__ __forceinline__ int tiles_per_entry(int nq, int cap) {
-  const int t = nq >= 3 ? 2 : (nq == 2 ? 4 : 8);
+// tiles per ring entry: >= 32 KiB of weights per entry whatever the width
+// (capped by the power-of-two divisor of the tile count), so the
+// single-warp producer/MMA bookkeeping per entry is amortised
+__device__ __forceinline__ int tiles_per_entry(int nu, int cap) {
+  const int t = nu >= 8 ? 2 : (nu >= 4 ? 4 : 8);
   return t < cap ? t : cap;
 }
 struct Geom {
   uint32_t size, win;  // bytes; read window from the entry start
   int m;
 };
-__device__ __forceinline__ Geom gu_geom(int nq, int cap) {
-  const int m = tiles_per_entry(nq, cap);
-  const uint32_t a = static_cast<uint32_t>(nq) * QB;
+__device__ __forceinline__ Geom gu_geom(int nu, int cap) {
+  const int m = tiles_per_entry(nu, cap);
+  const uint32_t a = static_cast<uint32_t>(nu) * UB;
   const uint32_t size = static_cast<uint32_t>(m) * a;
   const uint32_t w = static_cast<uint32_t>(m - 1) * a + TILE;  // an M = 128 A operand reads 16 KiB
   return {size, size > w ? size : w, m};
 }
-__device__ __forceinline__ Geom dn_geom(int nq, int cap) {
-  const int m = tiles_per_entry(nq, cap);
-  const uint32_t size = static_cast<uint32_t>(m) * static_cast<uint32_t>(nq) * QB;
+__device__ __forceinline__ Geom dn_geom(int nu, int cap) {
+  const int m = tiles_per_entry(nu, cap);
+  const uint32_t size = static_cast<uint32_t>(m) * static_cast<uint32_t>(nu) * UB;
   return {size, size, m};
 }
 __device__ __forceinline__ uint32_t ring_place(uint32_t& head, const Geom& g, uint32_t rb) {
@@ -164,10 +168,10 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   const int d = a.d, T = a.T;
   const int ktiles = d / 64, mtiles = d / 128;
   const long long chunk_bytes = 3LL * 64 * d * 2;
-  const int qpe = a.ffn / 16;
+  const int upe = a.ffn / 8;
   const uint32_t RB = static_cast<uint32_t>(a.ring_bytes);
 
-  // [a^T 2 x (hi, lo) x 4 KiB][h^T ktiles x 2 KiB][ring][entry gates][entry masks][misc][mbarriers]
+  // [a^T 2 x (hi, lo) x 4 KiB][h^T ktiles x 2 KiB][ring][2 KiB zeros][entry gates][entry masks][misc][mbarriers]
   uint8_t* p = smem_raw;
   uint8_t* aT = p;
   p += 2 * 2 * 4096;
@@ -175,6 +179,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   p += static_cast<size_t>(ktiles) * HTS;
   uint8_t* ring = p;
   p += RB;
+  uint8_t* zeros = p;  // the missing half of an odd group's last down K-step (finite, times a^T = 0)
+  p += UB;
   float* ent_gate = reinterpret_cast<float*>(p);  // [ENT_MAX][16]
   p += ENT_MAX * 16 * 4;
   uint32_t* ent_mask = reinterpret_cast<uint32_t*>(p);  // [ENT_MAX] tokens routed to the entry
@@ -201,13 +207,13 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     }
   }
   const int n_hits = a.counters[7];
-  const long long n = static_cast<long long>(n_hits + a.n_shared) * qpe;
+  const long long n = static_cast<long long>(n_hits + a.n_shared) * upe;
   const int G = gridDim.x, b = blockIdx.x;
-  const long long q0 = n > 0 ? (b * n) / G : 0;
-  const long long q1 = n > 0 ? ((b + 1) * n) / G : 0;
-  if (q0 >= q1) return;
-  const int o_first = static_cast<int>(q0 / qpe);
-  const int n_ent = static_cast<int>((q1 - 1) / qpe) - o_first + 1;
+  const long long u0 = n > 0 ? (b * n) / G : 0;
+  const long long u1 = n > 0 ? ((b + 1) * n) / G : 0;
+  if (u0 >= u1) return;
+  const int o_first = static_cast<int>(u0 / upe);
+  const int n_ent = static_cast<int>((u1 - 1) / upe) - o_first + 1;
   if (n_ent > ENT_MAX) __trap();  // the host plan rules this out (ffn_tg_grid_ok)
 
   if (tid == 0) {
@@ -291,19 +297,19 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       pb[1] = reinterpret_cast<const uint8_t*>(b1) + static_cast<long long>(g.np > 1 ? g.c[1] : 0) * chunk_bytes;
     };
     // tiles [t0, t0 + m) (tile index within the chunk: K-tiles then M-tiles)
-    // of every piece, slot-packed: tile j of the entry at j * nq * 4 KiB
+    // of every piece, slot-packed: tile j of the entry at j * nu * 2 KiB
     auto copy_entry = [&](const Grp& g, const uint8_t* const (&pb)[2], int t0, int m, uint32_t e, uint64_t* bar) {
       if (!leader) return;
-      const uint32_t ab = static_cast<uint32_t>(g.nq) * QB;
-      const uint32_t n0 = static_cast<uint32_t>(g.n[0]) * QB;
+      const uint32_t ab = static_cast<uint32_t>(g.nu) * UB;
+      const uint32_t n0 = static_cast<uint32_t>(g.n[0]) * UB;
       for (int j = 0; j < m; ++j) {
-        bulk_g2s(ring + e + j * ab, pb[0] + static_cast<size_t>(t0 + j) * TILE + g.qa[0] * QB, n0, bar, pol);
+        bulk_g2s(ring + e + j * ab, pb[0] + static_cast<size_t>(t0 + j) * TILE + g.pa[0] * UB, n0, bar, pol);
         if (g.np > 1)
           bulk_g2s(ring + e + j * ab + n0, pb[1] + static_cast<size_t>(t0 + j) * TILE,
-                   static_cast<uint32_t>(g.n[1]) * QB, bar, pol);
+                   static_cast<uint32_t>(g.n[1]) * UB, bar, pol);
       }
     };
-    GroupIt it{q0, q1, qpe};
+    GroupIt it{u0, u1, upe};
     Grp cur, prev;
     bool more = it.next(cur), has_prev = false;
     const uint8_t* cb[2];
@@ -311,7 +317,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     piece_bases(cur, cb);
     while (more || has_prev) {
       if (more) {  // GU(i)
-        const Geom g = gu_geom(cur.nq, kcap);
+        const Geom g = gu_geom(cur.nu, kcap);
         for (int kt = 0; kt < ktiles; kt += g.m) {
           const uint32_t e = reserve(g);
           uint64_t* bar = &full[idx % NSLOT];
@@ -321,7 +327,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         }
       }
       if (has_prev) {  // DN(i-1)
-        const Geom g = dn_geom(prev.nq, mcap);
+        const Geom g = dn_geom(prev.nu, mcap);
         for (int mt = 0; mt < mtiles; mt += g.m) {
           const uint32_t e = reserve(g);
           uint64_t* bar = &full[idx % NSLOT];
@@ -339,6 +345,32 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         if (more) piece_bases(cur, cb);
       }
     }
+    if (a.nx_counters && a.pf_bytes > 0 && leader) {
+      // ---- cross-layer L2 prefetch: the next layer's routing is final (K2
+      // ran for all layers), so walk what this CTA index streams next layer,
+      // in stream order, and prefetch its runs into L2 (HBM otherwise idles
+      // through this launch's tail and the layer handoff)
+      const int nh = a.nx_counters[7];
+      const long long nn = static_cast<long long>(nh + a.n_shared) * upe;
+      const long long p0 = nn > 0 ? (b * nn) / G : 0, p1 = nn > 0 ? ((b + 1) * nn) / G : 0;
+      GroupIt pit{p0, p1, upe};
+      Grp pg;
+      long long budget = a.pf_bytes;
+      while (budget > 0 && pit.next(pg)) {
+        for (int i = 0; i < pg.np && budget > 0; ++i) {
+          const int o = pg.o[i];
+          const uint16_t* w = o < nh ? a.nx_pool + static_cast<long long>(a.nx_slot_of[a.nx_hit_list[o]]) * a.expert_elems
+                                     : a.nx_shared_w + static_cast<long long>(o - nh) * a.expert_elems;
+          const uint8_t* base = reinterpret_cast<const uint8_t*>(w) + pg.c[i] * chunk_bytes + pg.pa[i] * UB;
+          const uint32_t run = static_cast<uint32_t>(pg.n[i]) * UB;
+          for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE), "r"(run)
+                         : "memory");
+            budget -= run;
+          }
+        }
+      }
+    }
     if (!waited) wait_pred();
     if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
   } else {
@@ -352,9 +384,11 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       // entry r (= o_first + r): per-token gate (0 for tokens not routed to
       // it) and the token mask; one warp per entry, one lane per routed slot
       const int ew = warp - 2;
-      {  // a^T columns of tokens >= T stay zero for the whole launch
+      {  // a^T columns of tokens >= T stay zero for the whole launch; so does the zero buffer
         uint4* z = reinterpret_cast<uint4*>(aT);
         for (int i = tid - 64; i < 2 * 2 * 4096 / 16; i += EPI_THREADS) z[i] = make_uint4(0u, 0u, 0u, 0u);
+        uint4* zz = reinterpret_cast<uint4*>(zeros);
+        for (int i = tid - 64; i < UB / 16; i += EPI_THREADS) zz[i] = make_uint4(0u, 0u, 0u, 0u);
       }
       for (int r = ew; r < n_ent; r += 4) {
         const int o = o_first + r;
@@ -395,7 +429,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       uint32_t head = 0, idx = 0;
       int ht_ok = 0;  // h^T slices [0, ht_ok) known to have landed
       const uint32_t ring_addr = smem_u32(ring), at_addr = smem_u32(aT), ht_addr = smem_u32(hts);
-      GroupIt it{q0, q1, qpe};
+      const uint32_t zero_addr = smem_u32(zeros);
+      GroupIt it{u0, u1, upe};
       Grp cur, prev;
       bool more = it.next(cur), has_prev = false;
       int i = 0;
@@ -406,8 +441,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           d1e[b1].flip();
           fence_after();
           const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
-          const Geom g = gu_geom(cur.nq, kcap);
-          const uint32_t ab = static_cast<uint32_t>(cur.nq) * QB;
+          const Geom g = gu_geom(cur.nu, kcap);
+          const uint32_t ab = static_cast<uint32_t>(cur.nu) * UB;
           for (int kt = 0; kt < ktiles; kt += g.m) {
             const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
             wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
@@ -438,8 +473,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           fence_after();
           const uint32_t ahi = at_addr + static_cast<uint32_t>(ab_) * 8192u;
           const uint64_t bhi = smem_desc(ahi, 256, 128), blo = smem_desc(ahi + 4096u, 256, 128);
-          const Geom g = dn_geom(prev.nq, mcap);
-          const uint32_t ab = static_cast<uint32_t>(prev.nq) * QB;
+          const Geom g = dn_geom(prev.nu, mcap);
+          const uint32_t ab = static_cast<uint32_t>(prev.nu) * UB;
           for (int mt = 0; mt < mtiles; mt += g.m) {
             const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
             wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
@@ -448,10 +483,15 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
                 const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>((mt + j) * 16);
-                for (int s = 0; s < prev.nq; ++s) {  // slot s = K-step s of a^T (+512 B = +32)
-                  const uint64_t adn = smem_desc(ring_addr + off + j * ab + s * QB, 2048, 128);
-                  mma_bf16(d2, adn, bhi + 32 * s, (i == 1 && s == 0) ? 0u : 1u);
-                  mma_bf16(d2, adn, blo + 32 * s, 1u);
+                // K-step s2 = units 2 s2, 2 s2 + 1 (two 8-k core-matrix columns,
+                // LBO apart); an odd group's last step takes its second
+                // column from the zero buffer (a^T rows there are 0 too)
+                for (int s2 = 0; 2 * s2 < prev.nu; ++s2) {
+                  const uint32_t run = ring_addr + off + j * ab + 2 * s2 * UB;
+                  const uint32_t lbo = 2 * s2 + 1 < prev.nu ? UB : zero_addr - run;
+                  const uint64_t adn = smem_desc(run, lbo, 128);
+                  mma_bf16(d2, adn, bhi + 32 * s2, (i == 1 && s2 == 0) ? 0u : 1u);  // +512 B of a^T per step
+                  mma_bf16(d2, adn, blo + 32 * s2, 1u);
                 }
               }
               mma_commit(&empty[slot]);
@@ -482,7 +522,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       const int et = tid - 64;  // 0..127
       Phase d1f[2], atf[2];
       long long w_d1f = 0, w_d2f = 0;
-      GroupIt it{q0, q1, qpe};
+      GroupIt it{u0, u1, upe};
       Grp g;
       int i = 0;
       while (it.next(g)) {
@@ -499,20 +539,27 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         const int ab = i & 1;
         mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);  // DN(i-2) done with this buffer
         atf[ab].flip();
-        if (q < g.nq) {
-          // lanes 0-15: gate rows f = 16q + s; lanes 16-31: the up rows of the same f
-          const float* gs = ent_gate + (static_cast<int>((g.qs + q) / qpe) - o_first) * 16;
-          const int f = 16 * q + (lane & 15);
+        {
+          // this warp's TMEM lanes are group slots 2q (lanes 0-15) and 2q+1
+          // (lanes 16-31); in a slot, lanes 0-7 hold the gate rows of
+          // f = 8 slot + (lane & 7), lanes 8-15 the up rows of the same f.
+          // Slots past the group's last unit get a = 0 (an odd group's last
+          // down K-step reads them).
+          const int slot = 2 * q + (lane >> 4);
+          const bool valid = slot < g.nu;
+          const float* gs = ent_gate + (valid ? static_cast<int>((g.us + slot) / upe) - o_first : 0) * 16;
+          const int f = 8 * slot + (lane & 7);
+          const int up = (lane >> 3) & 1;
           uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
           uint16_t* lo = hi + 2048;
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             if (t < T) {
-              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 16);
-              if ((t & 1) == (lane >> 4)) {  // lanes 0-15 even tokens, 16-31 odd tokens
-                const float gv = lane < 16 ? v[t] : pv;
-                const float uv = lane < 16 ? pv : v[t];
-                const float gt = gs[t];
+              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 8);
+              if ((t & 1) == up) {  // gate lanes even tokens, up lanes odd tokens
+                const float gv = up ? pv : v[t];
+                const float uv = up ? v[t] : pv;
+                const float gt = valid ? gs[t] : 0.f;
                 const float av = gt != 0.f ? __fdividef(gv, 1.f + __expf(-gv)) * uv * gt : 0.f;
                 const uint16_t h16 = f32_to_bf16_rn(av);
                 const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
@@ -594,15 +641,15 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 }  // namespace dev
 
 size_t ffn_tg_smem_bytes(int d, int ring_bytes) {
-  return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * dev::tg::HTS + static_cast<size_t>(ring_bytes) +
+  return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * dev::tg::HTS + static_cast<size_t>(ring_bytes) + dev::tg::UB +
          dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
 }
 
 // Every CTA's range must touch <= ENT_MAX entries (one producer lane each).
 bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid) {
-  const long long qpe = d_ffn / 16, n = static_cast<long long>(n_entries) * qpe;
-  const long long maxq = (n + grid - 1) / grid;
-  return grid > 0 && (maxq > 0 ? (maxq - 1) / qpe + 2 : 1) <= dev::tg::ENT_MAX;
+  const long long upe = d_ffn / 8, n = static_cast<long long>(n_entries) * upe;
+  const long long maxu = (n + grid - 1) / grid;
+  return grid > 0 && (maxu > 0 ? (maxu - 1) / upe + 2 : 1) <= dev::tg::ENT_MAX;
 }
 
 // Grouped mode: d <= 2048 (D2 for all d/128 M-tiles fits in TMEM columns

@@ -14,7 +14,10 @@
 // Tiled expert image (v2), per chunk of 64 ffn rows (ffn % 64 == 0):
 //   d/64 gate|up K-tiles, each [128 rows][64 k] bf16 in UMMA K-major
 //     core-matrix order (8 rows x 16 B core matrices; row-group outer:
-//     byte = g*1024 + j*128 + r*16 + e*2, rows 0-63 gate, 64-127 up);
+//     byte = g*1024 + j*128 + r*16 + e*2); rows are quarter-major and
+//     octet-interleaved: rows 32q..32q+31 = gate f 16q+0..7, up f 16q+0..7,
+//     gate f 16q+8..15, up f 16q+8..15, so a quarter is one 4 KiB run and an
+//     8-row half of it (gate + up octet) one 2 KiB run;
 //   d/128 down M-tiles, each [128 out rows][64 f] of W_down, core matrices
 //     k-chunk outer (byte = j*2048 + g*128 + r*16 + e*2) so that a 16-row
 //     quarter of the chunk (k-chunks 2q, 2q+1) is one contiguous 4 KiB run.
@@ -714,19 +717,21 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         // a^T buffer ab is free once DN(i-2) completed
         mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);
         atf[ab].flip();
-        // This warp's TMEM lanes are chunk quarter q: lanes 0-15 hold the
-        // gate rows f = 16q + s, lanes 16-31 the up rows of the same f.
+        // This warp's TMEM lanes are chunk quarter q, octet-interleaved:
+        // lanes 8h..8h+7 hold the gate rows f = 16q + 8h + (lane & 7), lanes
+        // 8h+8..8h+15 the up rows of the same f (h = lane >> 4).
         if (q >= cur.qa && q < cur.qb) {
-          const int s = lane & 15, f = 16 * q + s;
+          const int f = 16 * q + ((lane >> 4) << 3) + (lane & 7);
+          const int up = (lane >> 3) & 1;
           uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
           uint16_t* lo = hi + 2048;
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             if (t < T) {
-              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 16);
-              if ((t & 1) == (lane >> 4)) {  // lanes 0-15 even tokens, 16-31 odd tokens
-                const float g = lane < 16 ? v[t] : pv;
-                const float u = lane < 16 ? pv : v[t];
+              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 8);
+              if ((t & 1) == up) {  // gate lanes even tokens, up lanes odd tokens
+                const float g = up ? pv : v[t];
+                const float u = up ? v[t] : pv;
                 const float av = __fdividef(g, 1.f + __expf(-g)) * u * gs[t];
                 const uint16_t h16 = f32_to_bf16_rn(av);
                 const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
@@ -883,11 +888,12 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
       const long long kt = r0 / 8192;
       const int w = static_cast<int>(r0 % 8192);
       const int g = w >> 9, j = (w >> 6) & 7, r = (w >> 3) & 7, e = w & 7;
-      const int row = g * 8 + r;            // quarter q = row / 32: 16 gate rows then 16 up rows
+      // quarter q = row / 32, octet-interleaved: gate f 0-7, up f 0-7, gate f 8-15, up f 8-15
+      const int row = g * 8 + r;
       const int qq = row >> 5, s = row & 31;
-      const long long f = c * FCH + qq * 16 + (s & 15);
+      const long long f = c * FCH + qq * 16 + ((s >> 4) << 3) + (s & 7);
       const long long k = kt * 64 + j * 8 + e;
-      v = s < 16 ? wg[f * d + k] : wu[f * d + k];
+      v = ((s >> 3) & 1) ? wu[f * d + k] : wg[f * d + k];
     } else {
       const long long r2 = r0 - gu;
       const long long mt = r2 / 8192;

@@ -25,14 +25,25 @@ def main():
                  "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(u, 1)
         return v * scale
 
-    r = [x for x in rows[2:] if "expert_ffn_tc" in x[hdr.index("Kernel Name")]][0]
+    r = [x for x in rows[2:] if "expert_ffn_t" in x[hdr.index("Kernel Name")]][0]
+    kname = r[hdr.index("Kernel Name")]
     rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
     t = val(r, "gpu__time_duration.sum")
-    out = {"config": name, "kernel": "expert_ffn_tc_kernel (K3)", "report": os.path.basename(rep),
+    out = {"config": name, "kernel": kname, "report": os.path.basename(rep),
            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
            "duration_s_under_ncu": t, "dram_GBps_under_ncu": (rd + wr) / t / 1e9,
            "note": "one launch, ncu --set full --clock-control none (serialised, cache-control all): "
                    "its time is not a bench number; traffic is compared with the launch's algorithmic bytes"}
+    # algorithmic bytes of that launch: the number of expert images it streamed
+    # is the nearest integer to DRAM reads / image bytes (activations and
+    # partials are < 2% of an image at these shapes)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2603_09983_b200.configs import CONFIGS
+    w = CONFIGS[name]
+    img = 3 * w.d_model * w.d_ffn * 2
+    n_img = max(1, round(rd / img))
+    out.update({"expert_image_bytes": img, "images_streamed_in_launch (inferred)": n_img,
+                "algorithmic_bytes_of_launch": n_img * img, "traffic_over_algorithmic": round((rd + wr) / (n_img * img), 4)})
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"ncu_k3_{name}.json")
     json.dump(out, open(path, "w"), indent=1)
     print(json.dumps(out))

@@ -191,7 +191,7 @@ def test_expert_ffn_tc_accumulator_modes(N, k, T, d, ffn, n_shared, gate_mode, r
     _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, accum)
 
 
-@pytest.mark.parametrize("grid", [1, 7, 16, 37, 148, 300])
+@pytest.mark.parametrize("grid", [1, 7, 16, 37, 148, 300, 1000])
 @pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
     (128, 8, 9, 2048, 768, 0, 0, 0.6),     # Qwen3 shape
     (64, 6, 9, 2048, 1408, 2, 1, 0.3),     # DeepSeek-V2-Lite shape (shared units)
@@ -199,15 +199,16 @@ def test_expert_ffn_tc_accumulator_modes(N, k, T, d, ffn, n_shared, gate_mode, r
     (4, 4, 3, 512, 64, 0, 0, 1.0),         # every token on every expert, 1 chunk per expert
 ])
 def test_expert_ffn_grouped_grids(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, grid):
-    """Grouped K3: groups of four quarters cross chunk and expert boundaries
-    and CTAs own 0..many quarters depending on the grid; the combine's
+    """Grouped K3: groups of eight 8-row units cross chunk and expert
+    boundaries, odd groups take their last down K-step half from the zero
+    buffer, and CTAs own 0..many units depending on the grid; the combine's
     per-CTA row lists must cover exactly the CTAs that touched each token."""
     import ctypes
     if abi.FFN_TENSOR not in _kernels(d, ffn):
         pytest.skip("shape not supported by the tensor-core kernel")
-    qpe = ffn // 16
-    maxq = -(-((N + n_shared) * qpe) // grid)
-    if (maxq - 1) // qpe + 2 > 32:
+    upe = ffn // 8
+    maxu = -(-((N + n_shared) * upe) // grid)
+    if (maxu - 1) // upe + 2 > 32:
         pytest.skip("grid below the grouped kernel's per-CTA entry limit")
     # few CTAs -> long TMEM accumulation chains over many experts; a = silu(g)u·g
     # enters the down MMA as bf16 hi + lo (~2^-17 relative), so allow 3e-5
