@@ -156,6 +156,40 @@ moespac_status moespac_trace_synth_create(const moespac_sched_config* cfg, moesp
 moespac_status moespac_trace_synth_next(moespac_trace_synth* s, double* logits_host, int32_t* accepted);
 void moespac_trace_synth_destroy(moespac_trace_synth* s);
 
+/* ------------------------------------------------------------------ routing traces
+ * The reference's line format `#moetrace v1` (core/src/trace_model.cpp:132-254):
+ * ids [n_steps][n_layers][gamma+1][top_k] in file order, accepted [n_steps].
+ * read: call once with ids == NULL to get shape[4] = layers, experts, k,
+ * gamma and *n_steps, then with buffers of cap_steps steps. Parse errors are
+ * MOESPAC_E_IO with the reference's message ("read_trace: <path>:<line>: ..."). */
+moespac_status moespac_trace_write(const char* path, int n_layers, int n_experts, int top_k, int gamma,
+                                   int64_t n_steps, const int32_t* ids, const int32_t* accepted);
+moespac_status moespac_trace_read(const char* path, int32_t* shape4, int64_t* n_steps, int32_t* ids,
+                                  int32_t* accepted, int64_t cap_steps);
+
+/* ------------------------------------------------------------------ run metrics
+ * RunSummary / summarize / emit / parse_metrics in the reference's
+ * `#moesim-metrics v1` schema (core/src/metrics_report.cpp:12-183).
+ * summarize: n step reports with their layer timings [n][n_layers];
+ * measured != 0 replaces each step's modeled wall time by its device time
+ * (gpu_ms_total, needs moespac_ctx_set_timing) for tps / latency. series
+ * [n] receives the per-step accuracy series (may be NULL).
+ * emit: format 0 = CSV, 1 = JSONL; series = the n summaries' accuracy
+ * series concatenated (lengths in n_series). parse: up to cap summaries,
+ * their series concatenated into series (series_cap values); *n_out = count. */
+typedef struct moespac_run_summary {
+  char axis_name[64];
+  double axis_value, tps, latency_s, hit_rate, bubble_ratio, fault_rate, fn_rate, fp_rate, mean_accuracy;
+  int64_t total_tokens, total_time_ns;
+  int64_t n_series;
+} moespac_run_summary;
+moespac_status moespac_summarize(const moespac_step_report* reps, const moespac_layer_timing* layers, int64_t n,
+                                 int measured, moespac_run_summary* out, double* series);
+moespac_status moespac_metrics_emit(const moespac_run_summary* summaries, const double* series, int64_t n, int format,
+                                    const char* path);
+moespac_status moespac_metrics_parse(const char* path, moespac_run_summary* out, int64_t cap, double* series,
+                                     int64_t series_cap, int64_t* n_out);
+
 /* ------------------------------------------------------------------ device kernels (stateless)
  * K1 — router top-k + gates. Replaces the selection block of
  * TraceGenerator::next_step (core/src/trace_model.cpp:87-104).
@@ -327,6 +361,13 @@ moespac_status moespac_step(moespac_ctx* c, const double* logits_host, const uin
 moespac_status moespac_step_device(moespac_ctx* c, const double* logits_dev, const uint16_t* h_in_dev,
                                    int accepted, uint16_t* h_out_dev, moespac_step_report* rep,
                                    moespac_layer_timing* layers);
+
+/* Trace replay: one verification step with recorded routing instead of K1
+ * over logits — ids [L][T][k] (any order within a token; sorted here),
+ * gates [L][T][k] or NULL for uniform 1/k — host buffers as moespac_step. */
+moespac_status moespac_step_ids(moespac_ctx* c, const int32_t* ids_host, const float* gates_host,
+                                const uint16_t* h_in_host, int accepted, uint16_t* h_out_host,
+                                moespac_step_report* rep, moespac_layer_timing* layers);
 
 /* Device views of the last step (for parity checks; pointers owned by ctx). */
 typedef struct moespac_ctx_views {

@@ -253,6 +253,12 @@ def ref() -> C.CDLL:
         lib.ref_update_ratio_estimates.argtypes = [_f64p, _f64p, C.c_int, C.c_int, C.c_double, C.c_double,
                                                    C.c_double]
         lib.ref_layer_capacity_experts.argtypes = [C.c_double, C.c_int]
+        vp = C.c_void_p
+        lib.ref_write_trace.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]
+        lib.ref_read_trace.argtypes = [C.c_char_p, vp, vp, vp, vp, C.c_int64]
+        lib.ref_summarize.argtypes = [vp, vp, C.c_int, vp, vp, vp]
+        lib.ref_emit.argtypes = [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_char_p]
+        lib.ref_parse.argtypes = [C.c_char_p, vp, vp, vp, vp, vp, C.c_int, C.c_int64, vp]
         _ref = lib
     return _ref
 
@@ -319,3 +325,101 @@ def ref_solve_threshold(scores, resident, gamma, top_k, b_est, rc, rg, t_cpu, t_
                                      np.ascontiguousarray(rc, np.float64), np.ascontiguousarray(rg, np.float64),
                                      cap, t_cpu, t_gpu, t_io, expert_bytes, vram_left, draft_credit, out))
     return out
+
+
+# ---------------------------------------------------------------- reference trace I/O and metrics
+# status: 0 ok, -1 runtime_error, -2 invalid_argument, -3 out_of_range, -4 other
+REF_ERR = {-1: "runtime_error", -2: "invalid_argument", -3: "out_of_range", -4: "other"}
+
+
+def ref_write_trace(path, ids, accepted, n_experts):
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    acc = np.ascontiguousarray(accepted, dtype=np.int32)
+    S, L, T, k = ids.shape
+    rc = ref().ref_write_trace(path.encode(), L, n_experts, k, T - 1, S, ids.ctypes.data, acc.ctypes.data)
+    return rc, ref().ref_last_error().decode() if rc else ""
+
+
+def ref_read_trace(path):
+    """-> (rc, message, shape dict, ids, accepted)"""
+    shape = np.zeros(4, dtype=np.int32)
+    n = np.zeros(1, dtype=np.int64)
+    rc = ref().ref_read_trace(path.encode(), shape.ctypes.data, n.ctypes.data, None, None, 0)
+    if rc:
+        return rc, ref().ref_last_error().decode(), None, None, None
+    L, N, k, g = (int(x) for x in shape)
+    S = int(n[0])
+    ids = np.zeros((S, L, g + 1, k), dtype=np.int32) if S else np.zeros((0, max(L, 0), max(g + 1, 0), max(k, 0)),
+                                                                          dtype=np.int32)
+    acc = np.zeros(S, dtype=np.int32)
+    if S:
+        rc = ref().ref_read_trace(path.encode(), shape.ctypes.data, n.ctypes.data, ids.ctypes.data, acc.ctypes.data, S)
+    return rc, "", {"n_layers": L, "n_experts": N, "top_k": k, "gamma": g}, ids, acc
+
+
+# flattened StepReport / LayerTiming of the shim (sim_core.hpp:38-61)
+REF_STEP = np.dtype([("draft_ns", "<i8"), ("cache_hits", "<i8"), ("cache_misses", "<i8"), ("faults_fn", "<i8"),
+                     ("faults_fp", "<i8"), ("step_wall_ns", "<i8"), ("accuracy", "<f8"), ("accepted_tokens", "<i4"),
+                     ("n_experts", "<i4"), ("n_layers", "<i4"), ("_pad", "<i4")])
+REF_LAYER = np.dtype([("t_cpu_ns", "<i8"), ("t_gpu_ns", "<i8"), ("t_io_used_ns", "<i8"), ("stall_ns", "<i8"),
+                      ("bubble_ns", "<i8"), ("wall_ns", "<i8"), ("tau", "<i4"), ("fallback", "<i4"),
+                      ("n_prefetch", "<i4"), ("_pad", "<i4")])
+SUMMARY_KEYS = ["axis_value", "tps", "latency_s", "hit_rate", "bubble_ratio", "fault_rate", "fn_rate", "fp_rate",
+                "mean_accuracy"]
+
+
+def ref_summarize(steps, layers):
+    """steps: REF_STEP array [n]; layers: REF_LAYER array [sum n_layers] -> (rc, msg, dict)"""
+    steps = np.ascontiguousarray(steps)
+    layers = np.ascontiguousarray(layers)
+    vals = np.zeros(10)
+    ints = np.zeros(2, dtype=np.int64)
+    series = np.zeros(max(1, len(steps)))
+    rc = ref().ref_summarize(steps.ctypes.data, layers.ctypes.data, len(steps), vals.ctypes.data, ints.ctypes.data,
+                             series.ctypes.data)
+    if rc:
+        return rc, ref().ref_last_error().decode(), None
+    d = dict(zip(SUMMARY_KEYS, vals[:9].tolist()))
+    d.update(total_tokens=int(ints[0]), total_time_ns=int(ints[1]), accuracy_series=series[:len(steps)].tolist())
+    return 0, "", d
+
+
+def ref_emit(path, summaries, fmt):
+    """summaries: list of dicts (SUMMARY_KEYS + axis, total_tokens, total_time_ns, accuracy_series)."""
+    n = len(summaries)
+    vals = np.zeros((max(1, n), 10))
+    ints = np.zeros((max(1, n), 2), dtype=np.int64)
+    axis = np.zeros((max(1, n), 64), dtype=np.uint8)
+    nser = np.zeros(max(1, n), dtype=np.int64)
+    for i, s in enumerate(summaries):
+        vals[i, :9] = [s[k] for k in SUMMARY_KEYS]
+        ints[i] = [s["total_tokens"], s["total_time_ns"]]
+        b = s["axis"].encode()[:63]
+        axis[i, :len(b)] = np.frombuffer(b, dtype=np.uint8)
+        nser[i] = len(s["accuracy_series"])
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(s["accuracy_series"], dtype=np.float64)
+                                                for s in summaries]) if n else np.zeros(1))
+    rc = ref().ref_emit(vals.ctypes.data, ints.ctypes.data, axis.ctypes.data, flat.ctypes.data, nser.ctypes.data, n,
+                        0 if fmt == "csv" else 1, path.encode())
+    return rc, ref().ref_last_error().decode() if rc else ""
+
+
+def ref_parse(path, cap=64, series_cap=1 << 16):
+    vals = np.zeros((cap, 10))
+    ints = np.zeros((cap, 2), dtype=np.int64)
+    axis = np.zeros((cap, 64), dtype=np.uint8)
+    series = np.zeros(series_cap)
+    nser = np.zeros(cap, dtype=np.int64)
+    n = np.zeros(1, dtype=np.int32)
+    rc = ref().ref_parse(path.encode(), vals.ctypes.data, ints.ctypes.data, axis.ctypes.data, series.ctypes.data,
+                         nser.ctypes.data, cap, series_cap, n.ctypes.data)
+    if rc:
+        return rc, ref().ref_last_error().decode(), None
+    out, pos = [], 0
+    for i in range(int(n[0])):
+        d = dict(zip(SUMMARY_KEYS, vals[i, :9].tolist()))
+        d.update(axis=bytes(axis[i]).split(b"\0")[0].decode(), total_tokens=int(ints[i, 0]),
+                 total_time_ns=int(ints[i, 1]), accuracy_series=series[pos:pos + nser[i]].tolist())
+        pos += int(nser[i])
+        out.append(d)
+    return 0, "", out

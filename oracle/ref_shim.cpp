@@ -10,6 +10,8 @@
 //                                          proj/core/src/policies.cpp:71-84
 //   - update_ratio_estimates               proj/core/src/workload_balancer.cpp:169-199
 //   - Simulation::run_utility_step         proj/core/src/sim_core.cpp:157-316
+//   - write_trace / read_trace              proj/core/src/trace_model.cpp:132-254
+//   - summarize / emit / parse_metrics     proj/core/src/metrics_report.cpp:12-183
 // Only the shim is ours; every algorithm runs inside the reference objects.
 
 #include <chrono>
@@ -22,6 +24,7 @@
 
 #include "moesim/config.hpp"
 #include "moesim/execution_engine.hpp"
+#include "moesim/metrics_report.hpp"
 #include "moesim/policies.hpp"
 #include "moesim/sim_core.hpp"
 #include "moesim/trace_model.hpp"
@@ -369,6 +372,183 @@ int ref_layer_capacity_experts(double cache_ratio, int n_experts) {
   s.cache_ratio = cache_ratio;
   s.trace.n_experts = n_experts;
   return layer_capacity_experts(s);
+}
+
+
+// ---- trace wire format and run metrics (status: 0 ok, -1 runtime_error,
+// -2 invalid_argument, -3 out_of_range, -4 other; message in ref_last_error)
+static int classify(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return -2;
+  if (dynamic_cast<const std::out_of_range*>(&e)) return -3;
+  if (dynamic_cast<const std::runtime_error*>(&e)) return -1;
+  return -4;
+}
+
+int ref_write_trace(const char* path, int L, int N, int k, int gamma, int n_steps, const int32_t* ids,
+                    const int32_t* accepted) {
+  try {
+    Trace t;
+    t.n_layers = L;
+    t.n_experts = N;
+    t.top_k = k;
+    t.gamma = gamma;
+    size_t pos = 0;
+    for (int s = 0; s < n_steps; ++s) {
+      StepActivations a;
+      a.accepted_count = accepted[s];
+      a.experts.resize(static_cast<size_t>(L));
+      for (int l = 0; l < L; ++l) {
+        a.experts[static_cast<size_t>(l)].resize(static_cast<size_t>(gamma + 1));
+        for (auto& tok : a.experts[static_cast<size_t>(l)]) {
+          tok.resize(static_cast<size_t>(k));
+          for (int& e : tok) e = ids[pos++];
+        }
+      }
+      t.steps.push_back(std::move(a));
+    }
+    write_trace(t, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+int ref_read_trace(const char* path, int32_t* shape4, int64_t* n_steps, int32_t* ids, int32_t* accepted,
+                   int64_t cap_steps) {
+  try {
+    const Trace t = read_trace(path);
+    shape4[0] = t.n_layers;
+    shape4[1] = t.n_experts;
+    shape4[2] = t.top_k;
+    shape4[3] = t.gamma;
+    *n_steps = static_cast<int64_t>(t.steps.size());
+    if (ids && static_cast<int64_t>(t.steps.size()) <= cap_steps) {
+      size_t pos = 0;
+      for (size_t s = 0; s < t.steps.size(); ++s) {
+        accepted[s] = t.steps[s].accepted_count;
+        for (const auto& layer : t.steps[s].experts)
+          for (const auto& tok : layer)
+            for (int e : tok) ids[pos++] = e;
+      }
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+// StepReport / LayerTiming flattened (sim_core.hpp:38-61)
+struct ref_step_report {
+  int64_t draft_ns, cache_hits, cache_misses, faults_fn, faults_fp, step_wall_ns;
+  double accuracy;
+  int32_t accepted_tokens, n_experts, n_layers, _pad;
+};
+struct ref_layer_timing {
+  int64_t t_cpu_ns, t_gpu_ns, t_io_used_ns, stall_ns, bubble_ns, wall_ns;
+  int32_t tau, fallback, n_prefetch, _pad;
+};
+// RunSummary numbers: vals[10] = axis_value, tps, latency_s, hit_rate,
+// bubble_ratio, fault_rate, fn_rate, fp_rate, mean_accuracy, (unused);
+// ints[2] = total_tokens, total_time_ns
+static void put_summary(const RunSummary& r, double* v, int64_t* i) {
+  const double x[10] = {r.axis_value, r.tps, r.latency_s, r.hit_rate, r.bubble_ratio,
+                        r.fault_rate, r.fn_rate, r.fp_rate, r.mean_accuracy, 0.0};
+  std::memcpy(v, x, sizeof(x));
+  i[0] = r.total_tokens;
+  i[1] = r.total_time_ns;
+}
+
+int ref_summarize(const ref_step_report* reps, const ref_layer_timing* layers, int n, double* vals, int64_t* ints,
+                  double* series) {
+  try {
+    std::vector<StepReport> v(static_cast<size_t>(n));
+    const ref_layer_timing* lt = layers;
+    for (int i = 0; i < n; ++i) {
+      StepReport& s = v[static_cast<size_t>(i)];
+      s.draft_ns = reps[i].draft_ns;
+      s.accepted_tokens = reps[i].accepted_tokens;
+      s.cache_hits = reps[i].cache_hits;
+      s.cache_misses = reps[i].cache_misses;
+      s.accuracy = reps[i].accuracy;
+      s.faults_fn = reps[i].faults_fn;
+      s.faults_fp = reps[i].faults_fp;
+      s.n_experts = reps[i].n_experts;
+      s.step_wall_ns = reps[i].step_wall_ns;
+      s.layers.resize(static_cast<size_t>(reps[i].n_layers));
+      for (auto& x : s.layers) {
+        x.t_cpu_ns = lt->t_cpu_ns;
+        x.t_gpu_ns = lt->t_gpu_ns;
+        x.t_io_used_ns = lt->t_io_used_ns;
+        x.stall_ns = lt->stall_ns;
+        x.bubble_ns = lt->bubble_ns;
+        x.wall_ns = lt->wall_ns;
+        x.tau = lt->tau;
+        x.fallback = lt->fallback != 0;
+        x.n_prefetch = lt->n_prefetch;
+        ++lt;
+      }
+    }
+    const RunSummary r = summarize(v);
+    put_summary(r, vals, ints);
+    if (series) std::memcpy(series, r.accuracy_series.data(), sizeof(double) * r.accuracy_series.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+// axis: n NUL-terminated names at a 64-byte stride; series concatenated.
+int ref_emit(const double* vals, const int64_t* ints, const char* axis, const double* series, const int64_t* n_series,
+             int n, int format, const char* path) {
+  try {
+    std::vector<RunSummary> v(static_cast<size_t>(n));
+    const double* sp = series;
+    for (int i = 0; i < n; ++i) {
+      RunSummary& r = v[static_cast<size_t>(i)];
+      r.axis_name = std::string(axis + 64 * i);
+      const double* x = vals + 10 * i;
+      r.axis_value = x[0];
+      r.tps = x[1];
+      r.latency_s = x[2];
+      r.hit_rate = x[3];
+      r.bubble_ratio = x[4];
+      r.fault_rate = x[5];
+      r.fn_rate = x[6];
+      r.fp_rate = x[7];
+      r.mean_accuracy = x[8];
+      r.total_tokens = ints[2 * i];
+      r.total_time_ns = ints[2 * i + 1];
+      r.accuracy_series.assign(sp, sp + n_series[i]);
+      sp += n_series[i];
+    }
+    emit(v, format == 0 ? MetricsFormat::csv : MetricsFormat::jsonl, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+int ref_parse(const char* path, double* vals, int64_t* ints, char* axis, double* series, int64_t* n_series, int cap,
+              int64_t series_cap, int* n_out) {
+  try {
+    const std::vector<RunSummary> v = parse_metrics(path);
+    *n_out = static_cast<int>(v.size());
+    if (static_cast<int>(v.size()) > cap) return 0;
+    int64_t used = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      put_summary(v[i], vals + 10 * i, ints + 2 * i);
+      std::memset(axis + 64 * i, 0, 64);
+      std::strncpy(axis + 64 * i, v[i].axis_name.c_str(), 63);
+      n_series[i] = static_cast<int64_t>(v[i].accuracy_series.size());
+      if (used + n_series[i] <= series_cap)
+        std::memcpy(series + used, v[i].accuracy_series.data(), sizeof(double) * v[i].accuracy_series.size());
+      used += n_series[i];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
 }
 
 }  // extern "C"

@@ -96,6 +96,20 @@ class CombineArgs(C.Structure):
                 ("h_out_dev", C.c_void_p), ("accum", C.c_int32), ("kernel", C.c_int32)]
 
 
+class RunSummary(C.Structure):
+    """moespac_run_summary — the reference's RunSummary (metrics_report.hpp:15-30)."""
+    _fields_ = [("axis_name", C.c_char * 64)] + [(n, C.c_double) for n in (
+        "axis_value", "tps", "latency_s", "hit_rate", "bubble_ratio", "fault_rate", "fn_rate", "fp_rate",
+        "mean_accuracy")] + [("total_tokens", C.c_int64), ("total_time_ns", C.c_int64), ("n_series", C.c_int64)]
+
+    def as_dict(self, series=None) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("axis_name", "n_series")}
+        d["axis"] = self.axis_name.decode()
+        if series is not None:
+            d["accuracy_series"] = list(series)
+        return d
+
+
 class ModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("n_shared_units", C.c_int32),
@@ -179,6 +193,12 @@ def lib() -> C.CDLL:
         "moespac_trace_synth_create": (C.c_int, [C.POINTER(SchedConfig), C.POINTER(vp)]),
         "moespac_trace_synth_next": (C.c_int, [vp, vp, vp]),
         "moespac_trace_synth_destroy": (None, [vp]),
+        "moespac_trace_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, i64, vp, vp]),
+        "moespac_trace_read": (C.c_int, [C.c_char_p, vp, C.POINTER(i64), vp, vp, i64]),
+        "moespac_summarize": (C.c_int, [vp, vp, i64, C.c_int, C.POINTER(RunSummary), vp]),
+        "moespac_metrics_emit": (C.c_int, [vp, vp, i64, C.c_int, C.c_char_p]),
+        "moespac_metrics_parse": (C.c_int, [C.c_char_p, vp, i64, vp, i64, C.POINTER(i64)]),
+        "moespac_step_ids": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -334,6 +354,71 @@ class TraceSynth:
 
 
 # ---------------------------------------------------------------- device kernels
+# ---------------------------------------------------------------- routing traces (#moetrace v1)
+def trace_write(path: str, ids: np.ndarray, accepted: np.ndarray, n_experts: int) -> None:
+    """ids [S][L][gamma+1][k] int32, accepted [S] — the reference's write_trace."""
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    acc = np.ascontiguousarray(accepted, dtype=np.int32)
+    S, L, T, k = ids.shape
+    check(lib().moespac_trace_write(path.encode(), L, n_experts, k, T - 1, S, ids.ctypes.data, acc.ctypes.data))
+
+
+def trace_read(path: str):
+    """-> (shape dict, ids [S][L][gamma+1][k], accepted [S]) — the reference's read_trace."""
+    shape = np.zeros(4, dtype=np.int32)
+    n = C.c_int64(0)
+    check(lib().moespac_trace_read(path.encode(), shape.ctypes.data, C.byref(n), None, None, 0))
+    L, N, k, g = (int(x) for x in shape)
+    ids = np.zeros((n.value, L, g + 1, k) if n.value else (0, max(L, 0), max(g + 1, 0), max(k, 0)), dtype=np.int32)
+    acc = np.zeros(n.value, dtype=np.int32)
+    if n.value:
+        check(lib().moespac_trace_read(path.encode(), shape.ctypes.data, C.byref(n), ids.ctypes.data,
+                                       acc.ctypes.data, n.value))
+    return {"n_layers": L, "n_experts": N, "top_k": k, "gamma": g}, ids, acc
+
+
+# ---------------------------------------------------------------- run metrics (#moesim-metrics v1)
+def summarize(reports, layers=None, measured: bool = False):
+    """reports: sequence of StepReport, layers: [n][L] LayerTiming (or None).
+    -> (RunSummary, accuracy series)"""
+    n = len(reports)
+    reps = (StepReport * max(1, n))(*reports)
+    lay = None
+    if layers is not None:
+        flat = [x for row in layers for x in row]
+        lay = (LayerTiming * max(1, len(flat)))(*flat)
+    out = RunSummary()
+    series = np.zeros(max(1, n), dtype=np.float64)
+    check(lib().moespac_summarize(C.addressof(reps), C.addressof(lay) if lay is not None else None, n,
+                                  int(measured), C.byref(out), series.ctypes.data))
+    return out, series[:n]
+
+
+def metrics_emit(path: str, summaries, series_list, fmt: str = "csv") -> None:
+    arr = (RunSummary * max(1, len(summaries)))(*summaries)
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.float64) for s in series_list])
+                                if series_list else np.zeros(0), dtype=np.float64)
+    check(lib().moespac_metrics_emit(C.addressof(arr), flat.ctypes.data if flat.size else None, len(summaries),
+                                     0 if fmt == "csv" else 1, path.encode()))
+
+
+def metrics_parse(path: str):
+    """-> list of (RunSummary, series)"""
+    n = C.c_int64(0)
+    check(lib().moespac_metrics_parse(path.encode(), None, 0, None, 0, C.byref(n)))
+    arr = (RunSummary * max(1, n.value))()
+    check(lib().moespac_metrics_parse(path.encode(), C.addressof(arr), n.value, None, 0, C.byref(n)))
+    total = sum(arr[i].n_series for i in range(n.value))
+    flat = np.zeros(max(1, total), dtype=np.float64)
+    check(lib().moespac_metrics_parse(path.encode(), C.addressof(arr), n.value, flat.ctypes.data, total, C.byref(n)))
+    out, pos = [], 0
+    for i in range(n.value):
+        ns = arr[i].n_series
+        out.append((arr[i], flat[pos:pos + ns].copy()))
+        pos += ns
+    return out
+
+
 def _stream(stream):
     if stream is None:
         import torch
@@ -442,6 +527,17 @@ class Context:
         lay = (LayerTiming * self.model.n_layers)()
         check(lib().moespac_step(self._h, ptr(logits_host), ptr(h_in_host), accepted, ptr(h_out_host),
                                  C.byref(rep), lay))
+        return rep, list(lay)
+
+    def step_ids(self, ids_host: np.ndarray, gates_host, h_in_host: np.ndarray, accepted: int,
+                 h_out_host: np.ndarray):
+        """Trace replay: recorded routing ids [L][T][k] (gates or None = 1/k)."""
+        rep = StepReport()
+        lay = (LayerTiming * self.model.n_layers)()
+        ids = np.ascontiguousarray(ids_host, dtype=np.int32)
+        g = None if gates_host is None else np.ascontiguousarray(gates_host, dtype=np.float32)
+        check(lib().moespac_step_ids(self._h, ptr(ids), ptr(g), ptr(h_in_host), accepted, ptr(h_out_host),
+                                     C.byref(rep), lay))
         return rep, list(lay)
 
     def step_device(self, logits_dev, h_in_dev, accepted: int, h_out_dev):

@@ -7,7 +7,11 @@
 #include <string>
 
 #include "../../include/moespac/moespac.h"
+#include <cmath>
+
 #include "host/engine.hpp"
+#include "host/metrics.hpp"
+#include "host/trace_io.hpp"
 #include "host/step_scheduler.hpp"
 #include "host/trace_synth.hpp"
 #include "kernels/launch.hpp"
@@ -608,6 +612,11 @@ moespac_status moespac_step(moespac_ctx* c, const double* logits, const uint16_t
   return guard([&] { c->e.step(logits, true, h_in, true, accepted, h_out, true, rep, layers); });
 }
 
+moespac_status moespac_step_ids(moespac_ctx* c, const int32_t* ids, const float* gates, const uint16_t* h_in,
+                                int accepted, uint16_t* h_out, moespac_step_report* rep, moespac_layer_timing* layers) {
+  return guard([&] { c->e.step_ids(ids, gates, h_in, true, accepted, h_out, true, rep, layers); });
+}
+
 moespac_status moespac_step_device(moespac_ctx* c, const double* logits, const uint16_t* h_in, int accepted,
                                    uint16_t* h_out, moespac_step_report* rep, moespac_layer_timing* layers) {
   return guard([&] { c->e.step(logits, false, h_in, false, accepted, h_out, false, rep, layers); });
@@ -628,3 +637,158 @@ const moespac_sched* moespac_ctx_sched(const moespac_ctx* c) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ routing traces
+moespac_status moespac_trace_write(const char* path, int L, int N, int k, int gamma, int64_t n_steps,
+                                   const int32_t* ids, const int32_t* accepted) {
+  return guard([&] {
+    if (!path || n_steps < 0 || (n_steps > 0 && (!ids || !accepted)))
+      throw std::invalid_argument("moespac_trace_write: arguments");
+    TraceData tr;
+    tr.n_layers = L;
+    tr.n_experts = N;
+    tr.top_k = k;
+    tr.gamma = gamma;
+    tr.accepted.assign(accepted, accepted + n_steps);
+    tr.ids.assign(ids, ids + n_steps * L * (gamma + 1) * k);
+    write_trace(tr, path);
+  });
+}
+
+moespac_status moespac_trace_read(const char* path, int32_t* shape4, int64_t* n_steps, int32_t* ids,
+                                  int32_t* accepted, int64_t cap_steps) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("moespac_trace_read: path");
+    const TraceData tr = read_trace(path);
+    if (shape4) {
+      shape4[0] = tr.n_layers;
+      shape4[1] = tr.n_experts;
+      shape4[2] = tr.top_k;
+      shape4[3] = tr.gamma;
+    }
+    if (n_steps) *n_steps = tr.steps();
+    if (ids || accepted) {
+      if (cap_steps < tr.steps()) throw std::out_of_range("moespac_trace_read: buffer too small");
+      if (ids) std::memcpy(ids, tr.ids.data(), sizeof(int32_t) * tr.ids.size());
+      if (accepted) std::memcpy(accepted, tr.accepted.data(), sizeof(int32_t) * tr.accepted.size());
+    }
+  });
+}
+
+// ------------------------------------------------------------------ run metrics
+namespace {
+
+void to_c(const RunSummary& s, moespac_run_summary* o) {
+  std::memset(o, 0, sizeof(*o));
+  std::strncpy(o->axis_name, s.axis_name.c_str(), sizeof(o->axis_name) - 1);
+  o->axis_value = s.axis_value;
+  o->tps = s.tps;
+  o->latency_s = s.latency_s;
+  o->hit_rate = s.hit_rate;
+  o->bubble_ratio = s.bubble_ratio;
+  o->fault_rate = s.fault_rate;
+  o->fn_rate = s.fn_rate;
+  o->fp_rate = s.fp_rate;
+  o->mean_accuracy = s.mean_accuracy;
+  o->total_tokens = s.total_tokens;
+  o->total_time_ns = s.total_time_ns;
+  o->n_series = static_cast<int64_t>(s.accuracy_series.size());
+}
+
+}  // namespace
+
+moespac_status moespac_summarize(const moespac_step_report* reps, const moespac_layer_timing* layers, int64_t n,
+                                 int measured, moespac_run_summary* out, double* series) {
+  return guard([&] {
+    if (n < 0 || (n > 0 && !reps) || !out) throw std::invalid_argument("moespac_summarize: arguments");
+    std::vector<StepReport> v(static_cast<size_t>(n));
+    const moespac_layer_timing* lt = layers;
+    for (int64_t i = 0; i < n; ++i) {
+      const moespac_step_report& r = reps[i];
+      StepReport& s = v[static_cast<size_t>(i)];
+      s.draft_ns = r.draft_ns;
+      s.accepted_tokens = r.accepted_tokens;
+      s.cache_hits = r.cache_hits;
+      s.cache_misses = r.cache_misses;
+      s.accuracy = r.accuracy;
+      s.faults_fn = r.faults_fn;
+      s.faults_fp = r.faults_fp;
+      s.n_experts = r.n_experts;
+      s.step_wall_ns = measured && r.gpu_ms_total > 0.f ? std::llround(static_cast<double>(r.gpu_ms_total) * 1e6)
+                                                        : r.step_wall_ns;
+      if (lt) {
+        s.layers.resize(static_cast<size_t>(r.n_layers));
+        for (int l = 0; l < r.n_layers; ++l, ++lt) {
+          LayerTiming& x = s.layers[static_cast<size_t>(l)];
+          x.t_cpu_ns = lt->t_cpu_ns;
+          x.t_gpu_ns = lt->t_gpu_ns;
+          x.t_io_used_ns = lt->t_io_used_ns;
+          x.stall_ns = lt->stall_ns;
+          x.bubble_ns = lt->bubble_ns;
+          x.wall_ns = lt->wall_ns;
+          x.tau = lt->tau;
+          x.fallback = lt->fallback != 0;
+          x.n_prefetch = lt->n_prefetch;
+        }
+      } else {
+        s.layers.resize(static_cast<size_t>(r.n_layers));
+      }
+    }
+    const RunSummary rs = summarize(v);
+    to_c(rs, out);
+    if (series) std::memcpy(series, rs.accuracy_series.data(), sizeof(double) * rs.accuracy_series.size());
+  });
+}
+
+moespac_status moespac_metrics_emit(const moespac_run_summary* summaries, const double* series, int64_t n, int format,
+                                    const char* path) {
+  return guard([&] {
+    if (!path || n < 0 || (n > 0 && !summaries) || (format != 0 && format != 1))
+      throw std::invalid_argument("moespac_metrics_emit: arguments");
+    std::vector<RunSummary> v(static_cast<size_t>(n));
+    const double* sp = series;
+    for (int64_t i = 0; i < n; ++i) {
+      const moespac_run_summary& c = summaries[i];
+      RunSummary& s = v[static_cast<size_t>(i)];
+      s.axis_name.assign(c.axis_name, strnlen(c.axis_name, sizeof(c.axis_name)));
+      s.axis_value = c.axis_value;
+      s.tps = c.tps;
+      s.latency_s = c.latency_s;
+      s.hit_rate = c.hit_rate;
+      s.bubble_ratio = c.bubble_ratio;
+      s.fault_rate = c.fault_rate;
+      s.fn_rate = c.fn_rate;
+      s.fp_rate = c.fp_rate;
+      s.mean_accuracy = c.mean_accuracy;
+      s.total_tokens = c.total_tokens;
+      s.total_time_ns = c.total_time_ns;
+      if (c.n_series > 0) {
+        if (!sp) throw std::invalid_argument("moespac_metrics_emit: series required");
+        s.accuracy_series.assign(sp, sp + c.n_series);
+        sp += c.n_series;
+      }
+    }
+    emit(v, format == 0 ? MetricsFormat::csv : MetricsFormat::jsonl, path);
+  });
+}
+
+moespac_status moespac_metrics_parse(const char* path, moespac_run_summary* out, int64_t cap, double* series,
+                                     int64_t series_cap, int64_t* n_out) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("moespac_metrics_parse: path");
+    const std::vector<RunSummary> v = parse_metrics(path);
+    if (n_out) *n_out = static_cast<int64_t>(v.size());
+    if (!out) return;
+    if (cap < static_cast<int64_t>(v.size())) throw std::out_of_range("moespac_metrics_parse: buffer too small");
+    int64_t used = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+      to_c(v[i], &out[i]);
+      const int64_t ns = static_cast<int64_t>(v[i].accuracy_series.size());
+      if (series) {
+        if (used + ns > series_cap) throw std::out_of_range("moespac_metrics_parse: series buffer too small");
+        std::memcpy(series + used, v[i].accuracy_series.data(), sizeof(double) * static_cast<size_t>(ns));
+      }
+      used += ns;
+    }
+  });
+}

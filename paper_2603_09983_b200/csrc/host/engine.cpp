@@ -330,6 +330,32 @@ void Engine::set_nccl(const void* uid, int nranks, int rank) {
   if (r != 0) throw NcclError(std::string("ncclCommInitRank: ") + (nccl_->error_string ? nccl_->error_string(r) : "?"));
 }
 
+void Engine::step_ids(const int32_t* ids, const float* gates, const uint16_t* h_in, bool h_in_host, int accepted,
+                      uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers) {
+  if (!ids) throw std::invalid_argument("moespac_step_ids: ids required");
+  // validate before any state changes: ids in range, distinct within a token
+  const int N = m_.n_experts, k = m_.top_k;
+  for (int r = 0; r < m_.n_layers * T_; ++r) {
+    const int32_t* row = ids + static_cast<size_t>(r) * k;
+    for (int j = 0; j < k; ++j) {
+      if (row[j] < 0 || row[j] >= N) throw std::out_of_range("moespac_step_ids: expert id out of range");
+      for (int i = 0; i < j; ++i)
+        if (row[i] == row[j]) throw std::invalid_argument("moespac_step_ids: duplicate expert in a token's top-k");
+    }
+  }
+  replay_ids_ = ids;
+  replay_gates_ = gates;
+  try {
+    step(nullptr, true, h_in, h_in_host, accepted, h_out, h_out_host, rep, layers);
+  } catch (...) {
+    replay_ids_ = nullptr;
+    replay_gates_ = nullptr;
+    throw;
+  }
+  replay_ids_ = nullptr;
+  replay_gates_ = nullptr;
+}
+
 void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
                   uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers) {
   if (!finalized_) throw std::logic_error("moespac_step: context not finalized");
@@ -385,7 +411,9 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   // ---- compute stream
   check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
-  if (logits_host) {
+  if (replay_ids_) {
+    lg = nullptr;
+  } else if (logits_host) {
     check(cudaMemcpyAsync(logits_d_, logits, sizeof(double) * L * T_ * N, cudaMemcpyHostToDevice, compute_),
           "H2D logits");
     lg = logits_d_;
@@ -394,7 +422,28 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
                         h_in_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, compute_),
         "h_in");
   if (timing_) check(cudaEventRecord(ev_[1], compute_), "event");
-  check(launch_router_topk(lg, L * T_, N, k, m_.gate_mode, ids_d_, gates_d_, compute_), "K1 router");
+  if (replay_ids_) {
+    // recorded routing: ids ascending per token (the order K1 emits and the
+    // combine's row lists rely on), gates carried along
+    int32_t* ih = reinterpret_cast<int32_t*>(route_h_);
+    float* gh = reinterpret_cast<float*>(route_h_ + sizeof(int32_t) * L * T_ * k);
+    std::vector<std::pair<int32_t, float>> row(static_cast<size_t>(k));
+    for (int r = 0; r < L * T_; ++r) {
+      for (int j = 0; j < k; ++j) {
+        const int32_t e = replay_ids_[static_cast<size_t>(r) * k + j];
+        row[static_cast<size_t>(j)] = {e, replay_gates_ ? replay_gates_[static_cast<size_t>(r) * k + j] : 1.f / k};
+      }
+      std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (int j = 0; j < k; ++j) {
+        ih[static_cast<size_t>(r) * k + j] = row[static_cast<size_t>(j)].first;
+        gh[static_cast<size_t>(r) * k + j] = row[static_cast<size_t>(j)].second;
+      }
+    }
+    check(cudaMemcpyAsync(ids_d_, ih, sizeof(int32_t) * L * T_ * k, cudaMemcpyHostToDevice, compute_), "H2D ids");
+    check(cudaMemcpyAsync(gates_d_, gh, sizeof(float) * L * T_ * k, cudaMemcpyHostToDevice, compute_), "H2D gates");
+  } else {
+    check(launch_router_topk(lg, L * T_, N, k, m_.gate_mode, ids_d_, gates_d_, compute_), "K1 router");
+  }
   if (timing_) check(cudaEventRecord(ev_[2], compute_), "event");
   dev::K2Args a2{};
   a2.ids = ids_d_;
@@ -622,11 +671,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     for (int l = 0; l < L; ++l) units += oc[static_cast<size_t>(l)].n_local_hits + n_shared_eff;
     rep->ffn_bytes = units * image_elems_ * 2;
     rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads) * image_elems_ * 2 +
-                     (logits_host ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
+                     (logits_host && !replay_ids_ ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
+                     (replay_ids_ ? static_cast<int64_t>(sizeof(int32_t) + sizeof(float)) * L * T_ * k : 0) +
                      (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
     rep->d2h_bytes =
         static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
-    rep->kernel_launches = 2 + 2 * L + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
+    rep->kernel_launches = (replay_ids_ ? 1 : 2) + 2 * L + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
     rep->cold_experts = cold_experts;
     rep->cpu_ms_cold = cpu_ms_cold;
     if (timing_) {

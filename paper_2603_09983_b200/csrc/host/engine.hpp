@@ -48,6 +48,10 @@ class Engine {
   void set_cold_threads(int n) { cold_threads_ = n; }
   void step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
             uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
+  // Trace replay (#moetrace v1, trace_io.hpp): routing ids [L][T][k] (and
+  // gates, or uniform 1/k when null) from the host instead of K1 over logits.
+  void step_ids(const int32_t* ids, const float* gates, const uint16_t* h_in, bool h_in_host, int accepted,
+                uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
   void views(moespac_ctx_views* v) const;
   // decision tables the last executed step ran with
   void step_tables(int32_t* taus, uint32_t* rb, uint32_t* lb, int32_t* slots) const;
@@ -103,6 +107,8 @@ class Engine {
   int l2_prefetch_ = 0;  // per-CTA next-layer L2 prefetch (bytes); measured no gain, off
   int cold_threads_ = -1;
   int ffn_accum_ = 0;
+  const int32_t* replay_ids_ = nullptr;  // set for the duration of step_ids()
+  const float* replay_gates_ = nullptr;
   int acc_mode_ = 0;
 
   std::unique_ptr<ColdExecutor> cold_;

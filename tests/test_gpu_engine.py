@@ -170,3 +170,61 @@ def test_step_argument_errors():
         ctx.step(logits, h, g + 2, h.copy())
     assert ei.value.code == "E_RANGE"
     ctx.close()
+
+
+@pytest.mark.parametrize("kernel", [abi.FFN_TENSOR, abi.FFN_CUDACORE])
+def test_trace_replay_matches_logits_path(tmp_path, kernel):
+    """#moetrace v1 replay (moespac_step_ids): routing recorded from the
+    logits path, written to a trace file and read back, replays to the same
+    bits — h_out, scheduling reports and SimEvent log — when the gates are
+    carried along; with gates omitted every expert gets 1/k (checked against
+    the fp64 oracle)."""
+    L, N, k, g, d, ffn, cache = 2, 16, 4, 6, 1024, 128, 0.5
+    rng = np.random.default_rng(42)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    a, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, cache, std, shared, kernel, cold=0)
+    b, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, cache, std, shared, kernel, cold=0)
+    T = g + 1
+    gen = O.Generator(L, N, k, g, seed=7)
+    steps, hs, outs, gates, ids_all, accs = 6, [], [], [], [], []
+    for s in range(steps):
+        logits, ids, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        h_out = np.zeros_like(h0)
+        rep, lay = a.step(logits, h0, acc, h_out)
+        v = a.views()
+        gates.append(abi.fetch(v.gates_dev, (L, T, k), np.float32))
+        ids_all.append(ids)
+        accs.append(acc)
+        hs.append(h0)
+        outs.append((h_out, rep, [(x.tau, x.n_prefetch, x.t_cpu_ns, x.t_gpu_ns) for x in lay]))
+    path = str(tmp_path / "replay.trace")
+    abi.trace_write(path, np.stack(ids_all), np.array(accs), N)
+    shape, ids_rd, acc_rd = abi.trace_read(path)
+    assert shape == {"n_layers": L, "n_experts": N, "top_k": k, "gamma": g}
+    for s in range(steps):
+        # shuffle each token's (id, gate) pairs: the replay path sorts them
+        perm = np.argsort(rng.random((L, T, k)), axis=-1)
+        ids_s = np.take_along_axis(ids_rd[s], perm, -1)
+        gates_s = np.take_along_axis(gates[s], perm, -1)
+        h_out = np.zeros_like(hs[s])
+        rep, lay = b.step_ids(ids_s, gates_s, hs[s], int(acc_rd[s]), h_out)
+        want_h, want_rep, want_lay = outs[s]
+        assert np.array_equal(h_out, want_h), s
+        assert [rep.cache_hits, rep.cache_misses, rep.faults_fn, rep.faults_fp, rep.n_loads] == \
+            [want_rep.cache_hits, want_rep.cache_misses, want_rep.faults_fn, want_rep.faults_fp, want_rep.n_loads]
+        assert [(x.tau, x.n_prefetch, x.t_cpu_ns, x.t_gpu_ns) for x in lay] == want_lay
+    assert np.array_equal(a.sched_events(), b.sched_events())
+    # gates omitted -> uniform 1/k
+    h_out = np.zeros_like(hs[0])
+    b.step_ids(ids_rd[0], None, hs[0], int(acc_rd[0]), h_out)
+    v = b.views()
+    ys = abi.fetch(v.y_dev, (L, T, d), np.float32)
+    _, rb, _, _ = b.step_tables()
+    y_ref = O.moe_layer(hs[0], ids_rd[0][0], np.full((T, k), 1.0 / k),
+                        {e: std[(0, e)] for e in _resident(rb, 0, N)}, [])
+    assert np.linalg.norm(ys[0] - y_ref) / np.linalg.norm(y_ref) <= 1e-5
+    with pytest.raises(abi.MoespacError):
+        bad = ids_rd[0].copy()
+        bad[0, 0, 1] = bad[0, 0, 0]
+        b.step_ids(bad, None, hs[0], 1, h_out)
