@@ -56,6 +56,9 @@ def parse_args():
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--trace-steps", type=int, default=64)
     ap.add_argument("--ffn-kernel", type=int, default=0, help="0 auto (tcgen05), 1 CUDA-core GEMV, 2 tcgen05")
+    ap.add_argument("--router-gemv", action="store_true",
+                    help="model mode: routing from the on-device router GEMV W_g h_l of random-init router weights "
+                         "(K0 -> K1 -> K2 per layer) instead of the trace generator's logits; cold path off")
     return ap.parse_args()
 
 
@@ -216,7 +219,13 @@ def run_ours(args, w, rank, world, local_rank):
     n_images = min(L * N, max(N, 8))
     ctx.host_arena(n_images)
     ctx.fill_synthetic(seed=3, stdv=0.02)
+    if args.router_gemv:
+        ctx.set_cold_threads(0)
     ctx.finalize()
+    if args.router_gemv:
+        gw = torch.Generator().manual_seed(4)
+        for l in range(L):
+            ctx.set_router(l, (torch.randn((N, d), generator=gw) * 0.05).to(torch.bfloat16).cuda())
     if world > 1:
         import torch.distributed as dist
         obj = [abi.nccl_unique_id() if rank == 0 else None]
@@ -267,6 +276,10 @@ def run_ours(args, w, rank, world, local_rank):
     dev_step = lambda s: ctx.step_device(logits_d[s], h_d[s], accepted[s], h_out_d)[0]  # noqa: E731
     host_step = lambda s: ctx.step(logits_h[s].numpy(), h_h[s].view(torch.int16).numpy(), accepted[s],  # noqa: E731
                                    h_out_h.view(torch.int16).numpy())[0]
+    if args.router_gemv:
+        dev_step = lambda s: ctx.step_model_device(h_d[s], accepted[s], h_out_d)[0]  # noqa: E731
+        host_step = lambda s: ctx.step_model(h_h[s].view(torch.int16).numpy(), accepted[s],  # noqa: E731
+                                             h_out_h.view(torch.int16).numpy())[0]
     for i in range(args.warmup):
         dev_step(i % S)
     with ClockSampler(local_rank) as clk:
@@ -328,6 +341,8 @@ def main():
                 "top_k": w.top_k, "draft_len": w.gamma, "d_model": w.d_model, "d_ffn": w.d_ffn,
                 "shared_units": w.n_shared_units, "cache_ratio": w.cache_ratio,
                 "parallelism": f"ep{world}" if world > 1 else "single",
+                "routing": "model: on-device router GEMV W_g h_l (random-init router), cold path off"
+                if args.router_gemv else "trace: reference TraceGenerator logits (K1 top-k on device)",
                 "l2": "inputs > L2: every step streams each resident activated expert (>= 9 MB each, "
                       "GBs per step) through HBM; no L2 flush needed"}
     base = {"metric": "decode TPS and expert-FFN HBM GB/s (roofline %) at 1/2/4/8 B200 vs host CPU",

@@ -369,6 +369,18 @@ moespac_status moespac_step_ids(moespac_ctx* c, const int32_t* ids_host, const f
                                 const uint16_t* h_in_host, int accepted, uint16_t* h_out_host,
                                 moespac_step_report* rep, moespac_layer_timing* layers);
 
+/* Model mode (the router GEMV s = W_g h of Eq. 3, feeding K1):
+ * router weights of layer l, [n_experts][d_model] bf16 (host or device
+ * pointer; d_model % 256 == 0), then steps whose routing is computed on the
+ * device from each layer's input h_l — K0 GEMV (fp32, fixed summation order)
+ * -> K1 -> K2 for that layer -> K3 — instead of from trace logits. Needs the
+ * cold-expert host path off (moespac_ctx_set_cold_threads(ctx, 0)). */
+moespac_status moespac_ctx_set_router(moespac_ctx* c, int layer, const uint16_t* w_router);
+moespac_status moespac_step_model(moespac_ctx* c, const uint16_t* h_in_host, int accepted, uint16_t* h_out_host,
+                                  moespac_step_report* rep, moespac_layer_timing* layers);
+moespac_status moespac_step_model_device(moespac_ctx* c, const uint16_t* h_in_dev, int accepted, uint16_t* h_out_dev,
+                                         moespac_step_report* rep, moespac_layer_timing* layers);
+
 /* Device views of the last step (for parity checks; pointers owned by ctx). */
 typedef struct moespac_ctx_views {
   const int32_t* ids_dev;       /* [L][T][k] */
@@ -381,6 +393,7 @@ typedef struct moespac_ctx_views {
   const uint16_t* h_dev;        /* [L+1][T][d] bf16 layer inputs / final output */
   const float* y_dev;           /* [L][T][d] fp32 MoE outputs (this rank's partial before all-reduce) */
   const uint16_t* pool_dev;     /* [L][slots][image] */
+  const double* logits_dev;     /* [L][T][N] router logits (trace input, or K0's output in model mode) */
   int64_t slots_per_layer, image_elems;
 } moespac_ctx_views;
 moespac_status moespac_ctx_get_views(const moespac_ctx* c, moespac_ctx_views* out);

@@ -314,6 +314,34 @@ void orc_expert_apply(const uint16_t* h, int d, int ffn, const int32_t* tok, con
   free(a);
 }
 
+/* Router GEMV s = W_g h (Eq. 3). The
+ * reference has no router weights (its logits are a synthetic random walk),
+ * so this is parity-unpinned against the reference and pinned instead to the
+ * device K0's summation order (router_hist.cu, router_gemv_kernel): for each
+ * (t, e), lane j in 0..31 accumulates k = 256 i + 8 j + q (i ascending,
+ * q = 0..7) with fmaf in fp32, then a xor butterfly over m = 16, 8, 4, 2, 1
+ * adds lane L ^ m into lane L. W [N][d], h [T][d] bf16; d % 256 == 0. */
+void orc_router_gemv(const uint16_t* W, const uint16_t* h, int T, int N, int d, double* logits) {
+  for (int t = 0; t < T; ++t)
+    for (int e = 0; e < N; ++e) {
+      float v[32], nv[32];
+      for (int j = 0; j < 32; ++j) {
+        float acc = 0.f;
+        for (int i = 0; i < d / 256; ++i)
+          for (int q = 0; q < 8; ++q) {
+            const int k = 256 * i + 8 * j + q;
+            acc = fmaf(bf16_to_f32(W[(size_t)e * d + k]), bf16_to_f32(h[(size_t)t * d + k]), acc);
+          }
+        v[j] = acc;
+      }
+      for (int m = 16; m > 0; m >>= 1) {
+        for (int L = 0; L < 32; ++L) nv[L] = v[L] + v[L ^ m];
+        memcpy(v, nv, sizeof(v));
+      }
+      logits[(size_t)t * N + e] = (double)v[0];
+    }
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

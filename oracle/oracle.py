@@ -60,6 +60,7 @@ def orc() -> C.CDLL:
                                          C.c_void_p, C.c_void_p, C.c_void_p, _f64p, C.c_int]
         lib.orc_expert_apply_f32.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, _f32p, C.c_int,
                                              C.c_void_p, C.c_void_p, C.c_void_p, _f32p, C.c_int]
+        lib.orc_router_gemv.argtypes = [_u16p, _u16p, C.c_int, C.c_int, C.c_int, _f64p]
         lib.orc_max_threads.restype = C.c_int
         lib.orc_f32_to_bf16.restype = C.c_uint16
         lib.orc_f32_to_bf16.argtypes = [C.c_float]
@@ -95,6 +96,17 @@ class Generator:
         if getattr(self, "_h", None):
             self._lib.orc_gen_destroy(self._h)
             self._h = None
+
+
+def router_gemv(W: np.ndarray, h: np.ndarray) -> np.ndarray:
+    """Router logits W_g h [T][N] (fp64 widened from the device K0's fp32 order)."""
+    W = np.ascontiguousarray(W, np.uint16)
+    h = np.ascontiguousarray(h, np.uint16)
+    N, d = W.shape
+    T = h.shape[0]
+    out = np.empty((T, N), np.float64)
+    orc().orc_router_gemv(W.reshape(-1), h.reshape(-1), T, N, d, out.reshape(-1))
+    return out
 
 
 def router_topk(logits: np.ndarray, k: int, gate_mode: int = 0):

@@ -120,7 +120,8 @@ class CtxViews(C.Structure):
     _fields_ = [("ids_dev", C.c_void_p), ("gates_dev", C.c_void_p), ("freqs_dev", C.c_void_p),
                 ("offsets_dev", C.c_void_p), ("perm_dev", C.c_void_p), ("counters_dev", C.c_void_p),
                 ("est_state_dev", C.c_void_p), ("h_dev", C.c_void_p), ("y_dev", C.c_void_p),
-                ("pool_dev", C.c_void_p), ("slots_per_layer", C.c_int64), ("image_elems", C.c_int64)]
+                ("pool_dev", C.c_void_p), ("logits_dev", C.c_void_p), ("slots_per_layer", C.c_int64),
+                ("image_elems", C.c_int64)]
 
 
 POLICIES = ["moe_spac", "on_demand_gpu", "lru_cache", "static_split", "ar_mode",
@@ -199,6 +200,9 @@ def lib() -> C.CDLL:
         "moespac_metrics_emit": (C.c_int, [vp, vp, i64, C.c_int, C.c_char_p]),
         "moespac_metrics_parse": (C.c_int, [C.c_char_p, vp, i64, vp, i64, C.POINTER(i64)]),
         "moespac_step_ids": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, vp, vp]),
+        "moespac_ctx_set_router": (C.c_int, [vp, C.c_int, vp]),
+        "moespac_step_model": (C.c_int, [vp, vp, C.c_int, vp, vp, vp]),
+        "moespac_step_model_device": (C.c_int, [vp, vp, C.c_int, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -538,6 +542,25 @@ class Context:
         g = None if gates_host is None else np.ascontiguousarray(gates_host, dtype=np.float32)
         check(lib().moespac_step_ids(self._h, ptr(ids), ptr(g), ptr(h_in_host), accepted, ptr(h_out_host),
                                      C.byref(rep), lay))
+        return rep, list(lay)
+
+    def set_router(self, layer: int, w) -> None:
+        """Router weights W_g of a layer, [n_experts][d_model] bf16 (host array or device tensor)."""
+        if isinstance(w, np.ndarray):
+            w = np.ascontiguousarray(w.view(np.uint16))
+        check(lib().moespac_ctx_set_router(self._h, layer, ptr(w)))
+
+    def step_model(self, h_in_host: np.ndarray, accepted: int, h_out_host: np.ndarray):
+        """Model mode: routing from the on-device router GEMV of each layer's input."""
+        rep = StepReport()
+        lay = (LayerTiming * self.model.n_layers)()
+        check(lib().moespac_step_model(self._h, ptr(h_in_host), accepted, ptr(h_out_host), C.byref(rep), lay))
+        return rep, list(lay)
+
+    def step_model_device(self, h_in_dev, accepted: int, h_out_dev):
+        rep = StepReport()
+        lay = (LayerTiming * self.model.n_layers)()
+        check(lib().moespac_step_model_device(self._h, ptr(h_in_dev), accepted, ptr(h_out_dev), C.byref(rep), lay))
         return rep, list(lay)
 
     def step_device(self, logits_dev, h_in_dev, accepted: int, h_out_dev):

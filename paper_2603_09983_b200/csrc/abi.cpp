@@ -612,6 +612,23 @@ moespac_status moespac_step(moespac_ctx* c, const double* logits, const uint16_t
   return guard([&] { c->e.step(logits, true, h_in, true, accepted, h_out, true, rep, layers); });
 }
 
+moespac_status moespac_ctx_set_router(moespac_ctx* c, int layer, const uint16_t* w) {
+  return guard([&] {
+    if (!w) throw std::invalid_argument("moespac_ctx_set_router: weights");
+    c->e.set_router(layer, w);
+  });
+}
+
+moespac_status moespac_step_model(moespac_ctx* c, const uint16_t* h_in, int accepted, uint16_t* h_out,
+                                  moespac_step_report* rep, moespac_layer_timing* layers) {
+  return guard([&] { c->e.step_model(h_in, true, accepted, h_out, true, rep, layers); });
+}
+
+moespac_status moespac_step_model_device(moespac_ctx* c, const uint16_t* h_in, int accepted, uint16_t* h_out,
+                                         moespac_step_report* rep, moespac_layer_timing* layers) {
+  return guard([&] { c->e.step_model(h_in, false, accepted, h_out, false, rep, layers); });
+}
+
 moespac_status moespac_step_ids(moespac_ctx* c, const int32_t* ids, const float* gates, const uint16_t* h_in,
                                 int accepted, uint16_t* h_out, moespac_step_report* rep, moespac_layer_timing* layers) {
   return guard([&] { c->e.step_ids(ids, gates, h_in, true, accepted, h_out, true, rep, layers); });

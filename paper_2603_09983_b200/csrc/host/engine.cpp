@@ -212,7 +212,7 @@ Engine::~Engine() {
                   static_cast<void*>(offsets_d_), static_cast<void*>(perm_d_), static_cast<void*>(hit_list_d_),
                   static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
-                  static_cast<void*>(out_d_)})
+                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_)})
     if (p) cudaFree(p);
   cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
@@ -356,6 +356,37 @@ void Engine::step_ids(const int32_t* ids, const float* gates, const uint16_t* h_
   replay_gates_ = nullptr;
 }
 
+void Engine::set_router(int layer, const uint16_t* w_dev) {
+  const int L = m_.n_layers, N = m_.n_experts, d = m_.d_model;
+  if (layer < 0 || layer >= L) throw std::out_of_range("moespac_ctx_set_router: layer");
+  if (d % 256) throw std::invalid_argument("moespac_ctx_set_router: router GEMV needs d_model % 256 == 0");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  if (!wg_d_) {
+    check(cudaMalloc(reinterpret_cast<void**>(&wg_d_), sizeof(uint16_t) * L * N * d), "cudaMalloc router");
+    router_set_.assign(static_cast<size_t>(L), false);
+  }
+  check(cudaMemcpy(wg_d_ + static_cast<size_t>(layer) * N * d, w_dev, sizeof(uint16_t) * N * d, cudaMemcpyDefault),
+        "router weights");
+  router_set_[static_cast<size_t>(layer)] = true;
+}
+
+void Engine::step_model(const uint16_t* h_in, bool h_in_host, int accepted, uint16_t* h_out, bool h_out_host,
+                        moespac_step_report* rep, moespac_layer_timing* layers) {
+  if (!wg_d_) throw std::logic_error("moespac_step_model: no router weights (moespac_ctx_set_router)");
+  for (bool b : router_set_)
+    if (!b) throw std::logic_error("moespac_step_model: router weights missing for a layer");
+  if (cold_) throw std::logic_error("moespac_step_model: the cold-expert host path needs the routing up front "
+                                    "(moespac_ctx_set_cold_threads(ctx, 0) before finalize)");
+  model_mode_ = true;
+  try {
+    step(nullptr, true, h_in, h_in_host, accepted, h_out, h_out_host, rep, layers);
+  } catch (...) {
+    model_mode_ = false;
+    throw;
+  }
+  model_mode_ = false;
+}
+
 void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
                   uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers) {
   if (!finalized_) throw std::logic_error("moespac_step: context not finalized");
@@ -411,7 +442,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   // ---- compute stream
   check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
-  if (replay_ids_) {
+  if (replay_ids_ || model_mode_) {
     lg = nullptr;
   } else if (logits_host) {
     check(cudaMemcpyAsync(logits_d_, logits, sizeof(double) * L * T_ * N, cudaMemcpyHostToDevice, compute_),
@@ -441,7 +472,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     }
     check(cudaMemcpyAsync(ids_d_, ih, sizeof(int32_t) * L * T_ * k, cudaMemcpyHostToDevice, compute_), "H2D ids");
     check(cudaMemcpyAsync(gates_d_, gh, sizeof(float) * L * T_ * k, cudaMemcpyHostToDevice, compute_), "H2D gates");
-  } else {
+  } else if (!model_mode_) {
     check(launch_router_topk(lg, L * T_, N, k, m_.gate_mode, ids_d_, gates_d_, compute_), "K1 router");
   }
   if (timing_) check(cudaEventRecord(ev_[2], compute_), "event");
@@ -472,11 +503,15 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   int32_t* counters_d = out_d_ + static_cast<size_t>(L) * N;
   a2.counters = counters_d;
   a2.scores_out = scores_out_d;
-  check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
+  a2.gates = gates_d_;
+  if (!model_mode_) check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
   if (timing_) check(cudaEventRecord(ev_[3], compute_), "event");
   // scores + counters (+ routing for the cold path) back to the host right
   // away: the host scheduler works on them while the device runs the layers
-  check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
+  // (model mode: each layer's routing is known only after the layer before
+  // it, so the copy follows the last layer)
+  if (!model_mode_)
+    check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
   const bool cold = static_cast<bool>(cold_);
   int32_t* ids_h = reinterpret_cast<int32_t*>(route_h_);
   float* gates_h = reinterpret_cast<float*>(route_h_ + sizeof(int32_t) * L * T_ * k);
@@ -487,7 +522,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     if (!h_in_host)
       check(cudaMemcpyAsync(hcold_h_, h_d_, sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_), "D2H h0");
   }
-  check(cudaEventRecord(k2_done_, compute_), "event");
+  if (!model_mode_) check(cudaEventRecord(k2_done_, compute_), "event");
 
   const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
   const bool tc = kernel_ == kFfnTensorCore;
@@ -588,8 +623,21 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   if (!cold) {
     // ---- all layers on the device back to back; host accounting overlaps
     for (int l = 0; l < L; ++l) {
+      if (model_mode_) {
+        // K0 router GEMV on h_l, then K1 + K2 for layer l
+        const bool pdl = pdl_ && !timing_;
+        check(launch_router_gemv(wg_d_ + static_cast<size_t>(l) * N * d, h_d_ + static_cast<size_t>(l) * T_ * d, T_, N,
+                                 d, logits_d_ + static_cast<size_t>(l) * T_ * N, compute_, pdl),
+              "K0 router GEMV");
+        check(launch_route_layer(logits_d_ + static_cast<size_t>(l) * T_ * N, k, m_.gate_mode, a2, l, compute_, pdl),
+              "K1+K2 layer routing");
+      }
       launch_ffn(l);
       launch_combine_layer(l, nullptr);
+    }
+    if (model_mode_) {
+      check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
+      check(cudaEventRecord(k2_done_, compute_), "event");
     }
     check(cudaEventSynchronize(k2_done_), "sync K2");
     host_account();
@@ -671,12 +719,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     for (int l = 0; l < L; ++l) units += oc[static_cast<size_t>(l)].n_local_hits + n_shared_eff;
     rep->ffn_bytes = units * image_elems_ * 2;
     rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads) * image_elems_ * 2 +
-                     (logits_host && !replay_ids_ ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
+                     (logits_host && !replay_ids_ && !model_mode_ ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
                      (replay_ids_ ? static_cast<int64_t>(sizeof(int32_t) + sizeof(float)) * L * T_ * k : 0) +
                      (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
     rep->d2h_bytes =
         static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
-    rep->kernel_launches = (replay_ids_ ? 1 : 2) + 2 * L + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
+    rep->kernel_launches = (model_mode_ ? 4 * L : (replay_ids_ ? 1 : 2) + 2 * L) + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
     rep->cold_experts = cold_experts;
     rep->cpu_ms_cold = cpu_ms_cold;
     if (timing_) {
@@ -736,6 +784,7 @@ void Engine::views(moespac_ctx_views* v) const {
   v->h_dev = h_d_;
   v->y_dev = y_d_;
   v->pool_dev = pool_;
+  v->logits_dev = logits_d_;
   v->slots_per_layer = slots_;
   v->image_elems = image_elems_;
 }

@@ -52,6 +52,11 @@ class Engine {
   // gates, or uniform 1/k when null) from the host instead of K1 over logits.
   void step_ids(const int32_t* ids, const float* gates, const uint16_t* h_in, bool h_in_host, int accepted,
                 uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
+  // Model mode (router GEMV): routing from W_g h_l on
+  // the device, layer by layer, instead of trace logits.
+  void set_router(int layer, const uint16_t* w_dev);
+  void step_model(const uint16_t* h_in, bool h_in_host, int accepted, uint16_t* h_out, bool h_out_host,
+                  moespac_step_report* rep, moespac_layer_timing* layers);
   void views(moespac_ctx_views* v) const;
   // decision tables the last executed step ran with
   void step_tables(int32_t* taus, uint32_t* rb, uint32_t* lb, int32_t* slots) const;
@@ -109,6 +114,9 @@ class Engine {
   int ffn_accum_ = 0;
   const int32_t* replay_ids_ = nullptr;  // set for the duration of step_ids()
   const float* replay_gates_ = nullptr;
+  uint16_t* wg_d_ = nullptr;      // [L][N][d] bf16 router weights (model mode)
+  std::vector<bool> router_set_;
+  bool model_mode_ = false;       // set for the duration of step_model()
   int acc_mode_ = 0;
 
   std::unique_ptr<ColdExecutor> cold_;

@@ -24,6 +24,7 @@ struct K2Args {
   int32_t* hit_ord;    // [L][N] ordinal in hit_list or -1
   int32_t* counters;   // [L][8] distinct, hits, hit_tok, miss_tok, agree, fn, fp, n_local_hits
   int32_t* scores_out; // [L][N] post-update scores (next step's snapshot)
+  float* gates;        // [L][T][k] (route_layer_kernel only: K1 gates of the layer)
 };
 
 struct FfnArgs {
@@ -83,6 +84,11 @@ cudaError_t launch_router_topk(const double* logits, int rows, int N, int k, int
                                float* gates, cudaStream_t stream);
 cudaError_t launch_hist_scan_observe(const dev::K2Args& a, cudaStream_t stream);
 cudaError_t launch_estimator_init(int32_t* st, int n, int up, int down, cudaStream_t stream);
+// model mode: K0 router GEMV (d % 256 == 0, T <= 16) and one layer's K1 + K2
+cudaError_t launch_router_gemv(const uint16_t* wg, const uint16_t* h, int T, int N, int d, double* logits,
+                               cudaStream_t stream, bool pdl = false);
+cudaError_t launch_route_layer(const double* logits_l, int k, int gate_mode, const dev::K2Args& a, int l,
+                               cudaStream_t stream, bool pdl = false);
 struct FfnPlan {
   int n_stages;     // CUDA-core: ring stages; tensor-core: ring KiB
   bool global_acc;

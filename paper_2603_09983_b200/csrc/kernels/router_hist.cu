@@ -27,14 +27,10 @@ namespace moespac {
 namespace dev {
 
 // ------------------------------------------------------------------ K1
+// one warp, one token row: v [N] -> ids [k] ascending, gates [k]
 template <int VPL>
-__global__ void __launch_bounds__(256) router_topk_kernel(const double* __restrict__ logits, int rows, int N,
-                                                          int k, int gate_mode, int32_t* __restrict__ ids,
-                                                          float* __restrict__ gates) {
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const double* v = logits + static_cast<size_t>(row) * N;
+__device__ __forceinline__ void topk_row(const double* __restrict__ v, int N, int k, int gate_mode,
+                                         int32_t* __restrict__ ids_row, float* __restrict__ gates_row, int lane) {
   double x[VPL];
   uint32_t taken = 0;  // bit i <-> expert lane + 32*i
 #pragma unroll
@@ -94,11 +90,22 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const double* __restri
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = base + __popc(m & ((1u << lane) - 1u));
-      ids[static_cast<size_t>(row) * k + pos] = lane + 32 * i;
-      if (gates) gates[static_cast<size_t>(row) * k + pos] = expf(static_cast<float>(x[i] - vmax_sel)) / denom;
+      ids_row[pos] = lane + 32 * i;
+      if (gates_row) gates_row[pos] = expf(static_cast<float>(x[i] - vmax_sel)) / denom;
     }
     base += __popc(m);
   }
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) router_topk_kernel(const double* __restrict__ logits, int rows, int N,
+                                                          int k, int gate_mode, int32_t* __restrict__ ids,
+                                                          float* __restrict__ gates) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  topk_row<VPL>(logits + static_cast<size_t>(row) * N, N, k, gate_mode, ids + static_cast<size_t>(row) * k,
+                gates ? gates + static_cast<size_t>(row) * k : nullptr, lane);
 }
 
 // ------------------------------------------------------------------ K2
@@ -117,12 +124,12 @@ constexpr int K2_THREADS = 256;
 constexpr int K2_MAX_N = 4096;
 constexpr int K2_MAX_TK = 2048;
 
-__global__ void __launch_bounds__(K2_THREADS) hist_scan_observe_kernel(K2Args a) {
+// one CTA (K2_THREADS), one layer l of the K2 argument block
+__device__ __forceinline__ void hist_scan_observe_layer(const K2Args& a, int l) {
   __shared__ int32_t s_freq[K2_MAX_N];
   __shared__ int32_t s_ids[K2_MAX_TK];
   __shared__ int32_t s_scan[K2_THREADS];
   __shared__ int32_t s_cnt[8];
-  const int l = blockIdx.x;
   const int N = a.N, TK = a.T * a.k, tid = threadIdx.x;
   const int W = (N + 31) / 32;
   const int32_t* ids = a.ids + static_cast<size_t>(l) * TK;
@@ -245,6 +252,82 @@ __global__ void __launch_bounds__(K2_THREADS) hist_scan_observe_kernel(K2Args a)
   }
 }
 
+__global__ void __launch_bounds__(K2_THREADS) hist_scan_observe_kernel(K2Args a) {
+  hist_scan_observe_layer(a, blockIdx.x);
+}
+
+// ------------------------------------------------------------------ K0 + per-layer routing (model mode)
+// K0 — router GEMV s = W_g h of Eq. 3, the "model mode" that
+// replaces the synthetic trace's logits:
+// logits[t][e] = sum_k W_g[e][k] h[t][k], bf16 inputs, fp32 accumulation in a
+// fixed order that the C oracle restates (oracle_router_gemv): lane j of the
+// warp owning expert e accumulates k = 256 i + 8 j + q (i ascending, q = 0..7)
+// with fmaf, then a xor butterfly over 16, 8, 4, 2, 1 sums the lanes. The
+// fp32 result is widened to fp64 for K1, so ids/gates are bit-exact with the
+// oracle's top-k on the oracle's logits. h_l [T][d] is staged in shared memory
+// once per CTA; a CTA covers K0_WARPS experts.
+constexpr int K0_WARPS = 8;
+
+__global__ void __launch_bounds__(K0_WARPS * 32) router_gemv_kernel(const uint16_t* __restrict__ wg,
+                                                                   const uint16_t* __restrict__ h, int T, int N,
+                                                                   int d, double* __restrict__ logits) {
+  extern __shared__ uint4 hs[];  // [T][d] bf16
+  pdl_wait();                    // h_l comes from the previous layer's combine
+  pdl_trigger();
+  const int nvec = T * d / 8;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) hs[i] = reinterpret_cast<const uint4*>(h)[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * K0_WARPS + warp;
+  if (e >= N) return;
+  float acc[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) acc[t] = 0.f;
+  const uint4* w = reinterpret_cast<const uint4*>(wg + static_cast<size_t>(e) * d);
+  const int dv = d / 8;
+  for (int i = 0; i < d / 256; ++i) {
+    const uint4 wv = __ldg(w + i * 32 + lane);
+    const float wf[8] = {bf_lo(wv.x), bf_hi(wv.x), bf_lo(wv.y), bf_hi(wv.y),
+                         bf_lo(wv.z), bf_hi(wv.z), bf_lo(wv.w), bf_hi(wv.w)};
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      if (t < T) {
+        const uint4 hv = hs[t * dv + i * 32 + lane];
+        const float hf[8] = {bf_lo(hv.x), bf_hi(hv.x), bf_lo(hv.y), bf_hi(hv.y),
+                             bf_lo(hv.z), bf_hi(hv.z), bf_lo(hv.w), bf_hi(hv.w)};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[t] = __fmaf_rn(wf[q], hf[q], acc[t]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    if (t < T) {
+      float v = acc[t];
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, m));
+      if (lane == 0) logits[static_cast<size_t>(t) * N + e] = static_cast<double>(v);
+    }
+  }
+}
+
+// One layer's routing after K0: K1 (one warp per token) then K2 for that
+// layer, in one CTA. No launch_dependents: the K3 that follows stages this
+// layer's routing in its prologue, before its own dependency wait, so it must
+// launch only once this grid has completed.
+template <int VPL>
+__global__ void __launch_bounds__(K2_THREADS) route_layer_kernel(const double* __restrict__ logits_l, int k,
+                                                                 int gate_mode, K2Args a, int l) {
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* ids_l = const_cast<int32_t*>(a.ids) + static_cast<size_t>(l) * a.T * k;
+  for (int t = warp; t < a.T; t += K2_THREADS / 32)
+    topk_row<VPL>(logits_l + static_cast<size_t>(t) * a.N, a.N, k, gate_mode, ids_l + static_cast<size_t>(t) * k,
+                  a.gates ? a.gates + (static_cast<size_t>(l) * a.T + t) * k : nullptr, lane);
+  __syncthreads();  // this CTA's global id writes are visible to the whole CTA
+  hist_scan_observe_layer(a, l);
+}
+
 __global__ void estimator_init_kernel(int32_t* st, int n, int up, int down) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) *reinterpret_cast<int4*>(st + 4 * i) = make_int4(0, up, down, 0);
@@ -272,6 +355,35 @@ cudaError_t launch_hist_scan_observe(const dev::K2Args& a, cudaStream_t stream) 
   if (a.N > dev::K2_MAX_N || a.T * a.k > dev::K2_MAX_TK) return cudaErrorInvalidValue;
   dev::hist_scan_observe_kernel<<<a.L, dev::K2_THREADS, 0, stream>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_router_gemv(const uint16_t* wg, const uint16_t* h, int T, int N, int d, double* logits,
+                               cudaStream_t stream, bool pdl) {
+  if (d % 256 || T < 1 || T > 16) return cudaErrorInvalidValue;
+  const size_t smem = static_cast<size_t>(T) * d * 2;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(dev::router_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               16 * 4096 * 2);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(dev::router_gemv_kernel, dim3((N + dev::K0_WARPS - 1) / dev::K0_WARPS),
+                    dim3(dev::K0_WARPS * 32), smem, stream, pdl, wg, h, T, N, d, logits);
+}
+
+cudaError_t launch_route_layer(const double* logits_l, int k, int gate_mode, const dev::K2Args& a, int l,
+                               cudaStream_t stream, bool pdl) {
+  if (a.N > dev::K2_MAX_N || a.T * a.k > dev::K2_MAX_TK) return cudaErrorInvalidValue;
+  const int vpl = (a.N + 31) / 32;
+  const dim3 g(1), b(dev::K2_THREADS);
+  if (vpl <= 1) return launch_pdl(dev::route_layer_kernel<1>, g, b, 0, stream, pdl, logits_l, k, gate_mode, a, l);
+  if (vpl <= 2) return launch_pdl(dev::route_layer_kernel<2>, g, b, 0, stream, pdl, logits_l, k, gate_mode, a, l);
+  if (vpl <= 4) return launch_pdl(dev::route_layer_kernel<4>, g, b, 0, stream, pdl, logits_l, k, gate_mode, a, l);
+  if (vpl <= 8) return launch_pdl(dev::route_layer_kernel<8>, g, b, 0, stream, pdl, logits_l, k, gate_mode, a, l);
+  if (vpl <= 16) return launch_pdl(dev::route_layer_kernel<16>, g, b, 0, stream, pdl, logits_l, k, gate_mode, a, l);
+  if (vpl <= 32) return launch_pdl(dev::route_layer_kernel<32>, g, b, 0, stream, pdl, logits_l, k, gate_mode, a, l);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_estimator_init(int32_t* st, int n, int up, int down, cudaStream_t stream) {

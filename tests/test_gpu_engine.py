@@ -228,3 +228,67 @@ def test_trace_replay_matches_logits_path(tmp_path, kernel):
         bad = ids_rd[0].copy()
         bad[0, 0, 1] = bad[0, 0, 0]
         b.step_ids(bad, None, hs[0], 1, h_out)
+
+
+@pytest.mark.parametrize("L,N,k,g,d,ffn,gate_mode,cache,kernel", [
+    (3, 16, 4, 6, 1024, 128, 0, 0.5, abi.FFN_TENSOR),
+    (2, 60, 4, 6, 2048, 64, 1, 1.0, abi.FFN_TENSOR),
+    (2, 8, 2, 4, 512, 64, 0, 0.25, abi.FFN_CUDACORE),
+])
+def test_model_mode_router_gemv(L, N, k, g, d, ffn, gate_mode, cache, kernel):
+    """Model mode: K0 router logits bit-exact with the
+    C oracle's restatement of its fp32 order, K1 ids bit-exact on them, FFN
+    outputs within tolerance, and the scheduler's record equal to the
+    reference Simulation replaying the routing the model produced."""
+    ref_or_skip()
+    rng = np.random.default_rng(L * 31 + N)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    ctx, _ = _make_ctx(L, N, k, g, d, ffn, 0, gate_mode, cache, std, shared, kernel, cold=0)
+    T = g + 1
+    h_tmp = np.zeros((T, d), np.uint16)
+    with pytest.raises(abi.MoespacError):  # no router weights yet
+        ctx.step_model(h_tmp, 1, h_tmp.copy())
+    Wg = [O.f32_to_bf16_bits(rng.normal(0, 0.05, (N, d)).astype(np.float32)) for _ in range(L)]
+    for l in range(L):
+        ctx.set_router(l, Wg[l])
+    gen = O.Generator(L, N, k, g, seed=3)
+    steps, all_ids, accs = 6, [], []
+    for s in range(steps):
+        _, _, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        h_out = np.zeros_like(h0)
+        rep, lay = ctx.step_model(h0, acc, h_out)
+        v = ctx.views()
+        logits = abi.fetch(v.logits_dev, (L, T, N), np.float64)
+        ids = abi.fetch(v.ids_dev, (L, T, k), np.int32)
+        gates = abi.fetch(v.gates_dev, (L, T, k), np.float32)
+        hs = abi.fetch(v.h_dev, (L + 1, T, d), np.uint16)
+        ys = abi.fetch(v.y_dev, (L, T, d), np.float32)
+        assert np.array_equal(hs[0], h0) and np.array_equal(hs[L], h_out)
+        _, rb, _, _ = ctx.step_tables()
+        for l in range(L):
+            lg_ref = O.router_gemv(Wg[l], hs[l])
+            assert np.array_equal(logits[l], lg_ref), (s, l)
+            ids_ref, gates_ref = O.router_topk(lg_ref, k, gate_mode)
+            assert np.array_equal(ids[l], ids_ref), (s, l)
+            np.testing.assert_allclose(gates[l], gates_ref, rtol=3e-6, atol=1e-7)
+            y_ref = O.moe_layer(hs[l], ids_ref, gates_ref, {e: std[(l, e)] for e in _resident(rb, l, N)}, [])
+            rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
+            assert rel <= 1e-5, (s, l, rel)
+        all_ids.append(ids)
+        accs.append(acc)
+    rcfg = O.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache, token_budget=0)
+    run = O.ref_sim_run(rcfg, np.stack(all_ids), np.array(accs, np.int32))
+    assert np.array_equal(ctx.sched_events(), run.events)
+
+
+def test_model_mode_needs_cold_path_off():
+    L, N, k, g, d, ffn = 1, 8, 2, 4, 512, 64
+    rng = np.random.default_rng(1)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    ctx, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, 0.25, std, shared, abi.FFN_TENSOR, cold=2)
+    ctx.set_router(0, O.f32_to_bf16_bits(rng.normal(0, 0.05, (N, d)).astype(np.float32)))
+    h = np.zeros((g + 1, d), np.uint16)
+    with pytest.raises(abi.MoespacError) as ei:
+        ctx.step_model(h, 1, h.copy())
+    assert ei.value.code == "E_LOGIC"

@@ -164,3 +164,16 @@ def test_oracle_estimator_vs_live_reference_fuzz():
         for f in fs:
             got = O.estimator_observe(got, f, cap, lam)
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("T,N,d", [(5, 8, 512), (9, 128, 2048), (16, 60, 1024)])
+def test_router_gemv_restatement(T, N, d):
+    """The fp32 fixed-order router GEMV (model mode, K0's order) is the dot
+    product W_g h to fp32 accuracy."""
+    rng = np.random.default_rng(T * N)
+    W = O.f32_to_bf16_bits(rng.normal(0, 0.05, (N, d)).astype(np.float32))
+    h = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+    got = O.router_gemv(W, h)
+    want = O.bf16_bits_to_f32(h).astype(np.float64) @ O.bf16_bits_to_f32(W).astype(np.float64).T
+    assert np.all(np.abs(got - want) <= 1e-5 * np.abs(want).max() + 1e-6)
+    assert np.array_equal(got, O.router_gemv(W, h))
