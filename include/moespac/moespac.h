@@ -318,6 +318,15 @@ moespac_status moespac_ctx_finalize(moespac_ctx* c);
 /* Expert-parallel combine over NCCL: 128-byte ncclUniqueId from rank 0. */
 moespac_status moespac_nccl_unique_id(void* out128);
 moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* unique_id128, int nranks, int rank);
+/* In-process stand-in for the expert-parallel all-reduce: `world` contexts on
+ * ONE device (one host thread each) exchange their per-layer partial outputs
+ * through device slots instead of NCCL (which refuses two ranks on one GPU).
+ * Test harness for the expert-parallel device path on a single GPU;
+ * max_elems >= tokens * d_model. Use instead of moespac_ctx_set_nccl. */
+typedef struct moespac_loopback moespac_loopback;
+moespac_status moespac_loopback_create(int device, int world, int64_t max_elems, moespac_loopback** out);
+void moespac_loopback_destroy(moespac_loopback* g);
+moespac_status moespac_ctx_set_loopback(moespac_ctx* c, moespac_loopback* g);
 /* Per-kernel CUDA-event timing in moespac_step_report (off by default). While
  * timing is on, layer kernels are launched without programmatic dependent
  * launch so each K3 event pair brackets exactly that kernel. */
@@ -391,7 +400,7 @@ typedef struct moespac_ctx_views {
   const int32_t* counters_dev;  /* [L][8] */
   const int32_t* est_state_dev; /* [L][N][4] */
   const uint16_t* h_dev;        /* [L+1][T][d] bf16 layer inputs / final output */
-  const float* y_dev;           /* [L][T][d] fp32 MoE outputs (this rank's partial before all-reduce) */
+  const float* y_dev;           /* [L][T][d] fp32 MoE outputs (expert-parallel: after the all-reduce) */
   const uint16_t* pool_dev;     /* [L][slots][image] */
   const double* logits_dev;     /* [L][T][N] router logits (trace input, or K0's output in model mode) */
   int64_t slots_per_layer, image_elems;

@@ -203,6 +203,9 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_router": (C.c_int, [vp, C.c_int, vp]),
         "moespac_step_model": (C.c_int, [vp, vp, C.c_int, vp, vp, vp]),
         "moespac_step_model_device": (C.c_int, [vp, vp, C.c_int, vp, vp, vp]),
+        "moespac_loopback_create": (C.c_int, [C.c_int, C.c_int, i64, C.POINTER(vp)]),
+        "moespac_loopback_destroy": (None, [vp]),
+        "moespac_ctx_set_loopback": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -563,6 +566,9 @@ class Context:
         check(lib().moespac_step_model_device(self._h, ptr(h_in_dev), accepted, ptr(h_out_dev), C.byref(rep), lay))
         return rep, list(lay)
 
+    def set_loopback(self, group: "LoopbackGroup") -> None:
+        check(lib().moespac_ctx_set_loopback(self._h, group._h))
+
     def step_device(self, logits_dev, h_in_dev, accepted: int, h_out_dev):
         rep = StepReport()
         lay = (LayerTiming * self.model.n_layers)()
@@ -648,3 +654,21 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().moespac_nccl_unique_id(buf))
     return buf.raw
+
+
+class LoopbackGroup:
+    """In-process expert-parallel group on one device (moespac_loopback_*):
+    a test harness for the EP device path without NCCL."""
+
+    def __init__(self, device: int, world: int, max_elems: int):
+        h = C.c_void_p()
+        check(lib().moespac_loopback_create(device, world, max_elems, C.byref(h)))
+        self._h = h.value
+
+    def close(self):
+        if self._h:
+            lib().moespac_loopback_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

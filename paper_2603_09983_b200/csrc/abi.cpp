@@ -26,6 +26,10 @@ struct moespac_trace_synth {
   TraceSynth t;
   explicit moespac_trace_synth(const TraceSynthConfig& c) : t(c) {}
 };
+struct moespac_loopback {
+  LoopbackGroup g;
+  moespac_loopback(int dev, int world, size_t n) : g(dev, world, n) {}
+};
 struct moespac_ctx {
   Engine e;
   moespac_ctx(int dev, const moespac_model_desc& m, const moespac_sched_config& c, int r, int w) : e(dev, m, c, r, w) {}
@@ -622,6 +626,23 @@ moespac_status moespac_ctx_set_router(moespac_ctx* c, int layer, const uint16_t*
 moespac_status moespac_step_model(moespac_ctx* c, const uint16_t* h_in, int accepted, uint16_t* h_out,
                                   moespac_step_report* rep, moespac_layer_timing* layers) {
   return guard([&] { c->e.step_model(h_in, true, accepted, h_out, true, rep, layers); });
+}
+
+moespac_status moespac_loopback_create(int device, int world, int64_t max_elems, moespac_loopback** out) {
+  return guard([&] {
+    if (!out || max_elems < 1) throw std::invalid_argument("moespac_loopback_create: arguments");
+    require_device();
+    *out = new moespac_loopback(device, world, static_cast<size_t>(max_elems));
+  });
+}
+
+void moespac_loopback_destroy(moespac_loopback* g) { delete g; }
+
+moespac_status moespac_ctx_set_loopback(moespac_ctx* c, moespac_loopback* g) {
+  return guard([&] {
+    if (!g) throw std::invalid_argument("moespac_ctx_set_loopback: group");
+    c->e.set_loopback(&g->g);
+  });
 }
 
 moespac_status moespac_step_model_device(moespac_ctx* c, const uint16_t* h_in, int accepted, uint16_t* h_out,

@@ -61,6 +61,57 @@ struct NcclUid {
 };
 using CommInitFn = int (*)(void**, int, NcclUid, int);
 
+LoopbackGroup::LoopbackGroup(int device, int world, size_t max_elems) : device_(device), world_(world), max_(max_elems) {
+  if (world < 1 || max_elems < 1) throw std::invalid_argument("moespac_loopback_create: world / size");
+  if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(reinterpret_cast<void**>(&slots_), sizeof(float) * world * max_elems) != cudaSuccess)
+    throw CudaError("moespac_loopback_create: device memory");
+  put_.resize(static_cast<size_t>(world));
+  done_.resize(static_cast<size_t>(world));
+  for (int r = 0; r < world; ++r) {
+    cudaEventCreateWithFlags(&put_[static_cast<size_t>(r)], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&done_[static_cast<size_t>(r)], cudaEventDisableTiming);
+  }
+}
+
+LoopbackGroup::~LoopbackGroup() {
+  cudaSetDevice(device_);
+  cudaDeviceSynchronize();
+  for (auto e : put_) cudaEventDestroy(e);
+  for (auto e : done_) cudaEventDestroy(e);
+  cudaFree(slots_);
+}
+
+void LoopbackGroup::barrier() {
+  std::unique_lock<std::mutex> lk(mu_);
+  const unsigned long long g = gen_;
+  if (++arrived_ == world_) {
+    arrived_ = 0;
+    ++gen_;
+    cv_.notify_all();
+  } else {
+    if (!cv_.wait_for(lk, std::chrono::seconds(60), [&] { return gen_ != g; }))
+      throw std::runtime_error("loopback all_reduce: a rank did not arrive within 60 s");
+  }
+}
+
+void LoopbackGroup::all_reduce(int rank, float* buf, size_t n, cudaStream_t s) {
+  if (n > max_) throw std::invalid_argument("loopback all_reduce: message larger than the group's slots");
+  auto ok = [](cudaError_t e) {
+    if (e != cudaSuccess) throw CudaError(std::string("loopback all_reduce: ") + cudaGetErrorString(e));
+  };
+  // every rank recorded the end of its previous sum before anyone overwrites a slot
+  barrier();
+  for (int q = 0; q < world_; ++q)
+    if (q != rank) ok(cudaStreamWaitEvent(s, done_[static_cast<size_t>(q)], 0));
+  ok(cudaMemcpyAsync(slots_ + static_cast<size_t>(rank) * max_, buf, sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
+  ok(cudaEventRecord(put_[static_cast<size_t>(rank)], s));
+  barrier();
+  for (int q = 0; q < world_; ++q)
+    if (q != rank) ok(cudaStreamWaitEvent(s, put_[static_cast<size_t>(q)], 0));
+  ok(launch_sum_slots(slots_, world_, max_, buf, n, s));
+  ok(cudaEventRecord(done_[static_cast<size_t>(rank)], s));
+}
+
 moespac_status nccl_unique_id(void* out) {
   std::unique_ptr<NcclApi> api(NcclApi::load());
   return api->get_unique_id(out) == 0 ? MOESPAC_OK : MOESPAC_E_NCCL;
@@ -390,7 +441,8 @@ void Engine::step_model(const uint16_t* h_in, bool h_in_host, int accepted, uint
 void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
                   uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers) {
   if (!finalized_) throw std::logic_error("moespac_step: context not finalized");
-  if (world_ > 1 && !comm_) throw std::logic_error("moespac_step: expert-parallel context needs moespac_ctx_set_nccl");
+  if (world_ > 1 && !comm_ && !loop_)
+    throw std::logic_error("moespac_step: expert-parallel context needs moespac_ctx_set_nccl");
   if (accepted < 1 || accepted > T_) throw std::out_of_range("moespac_step: accepted must be in [1, gamma+1]");
   check(cudaSetDevice(device_), "cudaSetDevice");
   const int L = m_.n_layers, N = m_.n_experts, k = m_.top_k, d = m_.d_model;
@@ -598,9 +650,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.hT_out = (world_ == 1 && tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr;
     check(launch_combine(ca, compute_, pdl_ && !timing_ && !y_extra), "combine");
     if (world_ > 1) {
-      const int r = nccl_->all_reduce(yl, yl, static_cast<size_t>(T_) * d, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm_,
-                                      compute_);
-      if (r != 0) throw NcclError("ncclAllReduce failed");
+      if (loop_) {
+        loop_->all_reduce(rank_, yl, static_cast<size_t>(T_) * d, compute_);
+      } else {
+        const int r = nccl_->all_reduce(yl, yl, static_cast<size_t>(T_) * d, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm_,
+                                        compute_);
+        if (r != 0) throw NcclError("ncclAllReduce failed");
+      }
       check(launch_residual(hl, yl, hn, (tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr, d, T_ * d, compute_),
             "residual");
     }

@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <condition_variable>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <vector>
 
@@ -16,6 +18,30 @@
 namespace moespac {
 
 struct NcclApi;  // dlopen'ed libnccl (no link-time dependency)
+
+// In-process stand-in for the per-layer NCCL all-reduce: `world` contexts on
+// one device, each driven by its own host thread, exchange their partial
+// outputs through device slots and CUDA events, and every rank sums the slots
+// in rank order. Test harness for the expert-parallel device path where only
+// one GPU is available (NCCL refuses two ranks on one device).
+class LoopbackGroup {
+ public:
+  LoopbackGroup(int device, int world, size_t max_elems);
+  ~LoopbackGroup();
+  void all_reduce(int rank, float* buf, size_t n, cudaStream_t stream);
+  int world() const { return world_; }
+
+ private:
+  void barrier();
+  int device_, world_;
+  size_t max_;
+  float* slots_ = nullptr;  // [world][max]
+  std::vector<cudaEvent_t> put_, done_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  unsigned long long gen_ = 0;
+};
 class ColdExecutor;
 
 struct CudaError : std::runtime_error {
@@ -42,6 +68,10 @@ class Engine {
   void set_timing(bool on) { timing_ = on; }
   void set_pdl(bool on) { pdl_ = on; }
   void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
+  void set_loopback(LoopbackGroup* g) {
+    if (!g || g->world() != world_) throw std::invalid_argument("moespac_ctx_set_loopback: group size != shard world");
+    loop_ = g;
+  }
   void set_l2_prefetch(int bytes) { l2_prefetch_ = bytes; }
   // host threads for cold (non-resident) experts: -1 auto, 0 = off (misses
   // are then counted but not computed); takes effect at finalize()
@@ -126,6 +156,7 @@ class Engine {
   uint8_t* route_h_ = nullptr;   // pinned ids [L][T][k] | gates [L][T][k]
   std::vector<cudaEvent_t> h_ready_;
   std::unique_ptr<NcclApi> nccl_;
+  LoopbackGroup* loop_ = nullptr;  // test harness instead of NCCL (not owned)
   void* comm_ = nullptr;
 };
 

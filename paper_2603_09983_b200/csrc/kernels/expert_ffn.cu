@@ -689,6 +689,23 @@ cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_ou
                     hT_out, d, n);
 }
 
+namespace dev {
+// out[i] = sum over q = 0..world-1 (in that order) of slots[q * stride + i]
+__global__ void sum_slots_kernel(const float* __restrict__ slots, int world, size_t stride, float* __restrict__ out,
+                                 size_t n) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = slots[i];
+  for (int q = 1; q < world; ++q) s += slots[q * stride + i];
+  out[i] = s;
+}
+}  // namespace dev
+
+cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float* out, size_t n, cudaStream_t stream) {
+  dev::sum_slots_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(slots, world, stride, out, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream) {
   dev::pack_expert_kernel<<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, out);

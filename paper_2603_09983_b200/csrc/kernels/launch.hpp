@@ -111,6 +111,7 @@ cudaError_t launch_pack_expert_tc(const uint16_t* wg, const uint16_t* wu, const 
 cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream, bool pdl = false);
 cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, uint16_t* hT_out, int d, int n,
                             cudaStream_t stream, bool pdl = false);
+cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float* out, size_t n, cudaStream_t stream);
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream);
 cudaError_t launch_fill_synthetic(uint16_t* out, long long n, uint64_t seed, float stdv, cudaStream_t stream);

@@ -292,3 +292,76 @@ def test_model_mode_needs_cold_path_off():
     with pytest.raises(abi.MoespacError) as ei:
         ctx.step_model(h, 1, h.copy())
     assert ei.value.code == "E_LOGIC"
+
+
+@pytest.mark.parametrize("world,cache,kernel,cold", [
+    (2, 1.0, abi.FFN_TENSOR, 0),
+    (2, 0.5, abi.FFN_TENSOR, -1),
+    (3, 0.5, abi.FFN_TENSOR, 0),
+    (2, 0.5, abi.FFN_CUDACORE, 0),
+])
+def test_expert_parallel_device_path(world, cache, kernel, cold):
+    """Expert-parallel mode on one GPU: `world` contexts
+    (expert e on rank e % world, shared units on rank 0), one host thread
+    each, exchanging per-layer partial outputs through the in-process
+    loopback group instead of NCCL. Every rank ends each layer with the same
+    h; every layer's MoE output matches the fp64 oracle over the experts
+    resident on any rank (+ the host cold path when on)."""
+    import threading
+    L, N, k, g, d, ffn, units = 2, 16, 4, 6, 1024, 128, 1
+    rng = np.random.default_rng(world * 10 + int(cache * 10))
+    std, shared = _experts(rng, L, N, d, ffn, units)
+    T = g + 1
+    group = abi.LoopbackGroup(0, world, T * d)
+    ctxs = []
+    for r in range(world):
+        cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache)
+        kern = abi.ffn_resolve(kernel, d, ffn)
+        ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, 0, kern), cfg, r, world)
+        ctx.set_cold_threads(cold)
+        arena = ctx.host_arena(L * N)
+        for (l, e), w in std.items():
+            arena[l * N + e] = _pack(w, kern).cpu().numpy().view(np.uint16)
+        for l in range(L):
+            ctx.set_shared(l, torch.stack([_pack(w, kern) for w in shared[l]]))
+        ctx.finalize()
+        ctx.set_loopback(group)
+        ctxs.append(ctx)
+    gen = O.Generator(L, N, k, g, seed=5)
+    for s in range(5):
+        logits, ids, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        outs = [np.zeros_like(h0) for _ in range(world)]
+        errs = []
+
+        def run(r):
+            try:
+                ctxs[r].step(logits, h0, acc, outs[r])
+            except Exception as exc:  # surfaced below
+                errs.append(exc)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=120)
+        assert not errs, errs
+        for r in range(1, world):
+            assert np.array_equal(outs[r], outs[0]), (s, r)
+        v = ctxs[0].views()
+        hs = abi.fetch(v.h_dev, (L + 1, T, d), np.uint16)
+        ys = abi.fetch(v.y_dev, (L, T, d), np.float32)  # after the all-reduce
+        res = [set() for _ in range(L)]
+        for ctx in ctxs:
+            _, rb, _, _ = ctx.step_tables()
+            for l in range(L):
+                res[l] |= set(_resident(rb, l, N))
+        for l in range(L):
+            _, gates = O.router_topk(logits[l], k, 0)
+            present = range(N) if cold != 0 else sorted(res[l])
+            y_ref = O.moe_layer(hs[l], ids[l], gates, {e: std[(l, e)] for e in present}, shared[l])
+            rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
+            assert rel <= 1e-5, (s, l, rel)
+    for ctx in ctxs:
+        ctx.close()
+    group.close()
