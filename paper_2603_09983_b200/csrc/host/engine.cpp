@@ -242,6 +242,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
     check(cudaEventCreate(&ffn_end_[static_cast<size_t>(l)]), "event");
   }
   for (auto& e : ev_) check(cudaEventCreate(&e), "event");
+  for (auto& e : copy_ev_) check(cudaEventCreate(&e), "event");
   check(cudaEventCreateWithFlags(&k2_done_, cudaEventDisableTiming | cudaEventBlockingSync), "event");
 
   // LayerEstimator ctor state for every layer (utility_estimator.cpp:23-33)
@@ -278,6 +279,8 @@ Engine::~Engine() {
   for (auto e : ffn_beg_) cudaEventDestroy(e);
   for (auto e : ffn_end_) cudaEventDestroy(e);
   for (auto e : ev_)
+    if (e) cudaEventDestroy(e);
+  for (auto e : copy_ev_)
     if (e) cudaEventDestroy(e);
   if (k2_done_) cudaEventDestroy(k2_done_);
   if (compute_) cudaStreamDestroy(compute_);
@@ -474,6 +477,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   // being overwritten is still read by an in-flight FFN (the device-side
   // meaning of the reference's frozen score, execution_engine.cpp:111-118).
   int n_loads = 0;
+  if (timing_) check(cudaEventRecord(copy_ev_[0], copy_), "event");
   {
     size_t i = 0;
     const auto& loads = sched_->loads();
@@ -491,6 +495,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
     }
   }
+  if (timing_) check(cudaEventRecord(copy_ev_[1], copy_), "event");
   // ---- compute stream
   check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
@@ -796,6 +801,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       for (int l = 0; l < L; ++l) f += ms(ffn_beg_[static_cast<size_t>(l)], ffn_end_[static_cast<size_t>(l)]);
       rep->gpu_ms_ffn = f;
       rep->gpu_ms_combine = ms(ev_[3], ev_[4]) - f;
+      rep->gpu_ms_h2d_loads = n_loads > 0 ? ms(copy_ev_[0], copy_ev_[1]) : 0.f;
     }
   }
   if (layers) {

@@ -135,6 +135,7 @@ class Engine {
   cudaStream_t compute_ = nullptr, copy_ = nullptr;
   std::vector<cudaEvent_t> load_done_, ffn_beg_, ffn_end_;
   cudaEvent_t ev_[6] = {};
+  cudaEvent_t copy_ev_[2] = {};  // timing: first / last expert load on the copy stream
   cudaEvent_t k2_done_ = nullptr;
   bool decided_ = false;  // next step's decisions already made
   bool pdl_ = true;                         // programmatic dependent launch between layer kernels
