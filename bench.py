@@ -305,7 +305,7 @@ def run_ours(args, w, rank, world, local_rank):
     loads = sum(r.n_loads for r in reps)
     out = {
         "ms": ms, "ms_e2e": ms_e2e, "ms_timed": ms_t, "tokens": tokens, "ffn_ms": ffn_ms, "ffn_bytes": ffn_bytes,
-        "ffn_launches": args.steps * L, "launches": launches, "hits": hits, "misses": misses, "loads": loads,
+        "ffn_launches": sum(r.ffn_launches for r in reps), "launches": launches, "hits": hits, "misses": misses, "loads": loads,
         "k3_kernel": ctx.k3_kernel(),
         "h2d": float(np.mean([r.h2d_bytes for r in reps_e2e])), "d2h": float(np.mean([r.d2h_bytes for r in reps_e2e])),
         "router_ms": float(np.mean([r.gpu_ms_router for r in reps])),

@@ -93,7 +93,10 @@ typedef struct moespac_step_report {
   /* cold path: (layer, expert) misses computed on the host cores this step
    * and the host time spent on them */
   int32_t cold_experts;
-  float cpu_ms_cold, _pad;
+  float cpu_ms_cold;
+  /* K3 launches this step: n_layers, or 1 when the persistent K3 ran the
+   * whole step (combine included) */
+  int32_t ffn_launches;
 } moespac_step_report;
 
 /* Realized split of one layer (core/src/sim_core.cpp:233-283), as K2 emits it. */
@@ -336,6 +339,12 @@ moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
  * the device, and added by the combine): -1 = all cores (default), 0 = off
  * (misses are counted but not computed). Takes effect at moespac_ctx_finalize. */
 moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
+/* Persistent K3 (tensor-core grouped kernel with the layer loop and the
+ * combine inside, one launch per step, grid barriers between layers;
+ * eligible when d_model <= 2048, one device, no host cold path, trace-driven
+ * routing). Off by default: measured ~15% slower than the per-layer K3 +
+ * combine launches on the Qwen3 shape. */
+moespac_status moespac_ctx_set_persistent(moespac_ctx* c, int enabled);
 /* Programmatic dependent launch between layer kernels (on by default). */
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
 /* Profiling hook: device buffer of [n_layers][grid][32] uint64 that every

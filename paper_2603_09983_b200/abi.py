@@ -60,7 +60,7 @@ class StepReport(C.Structure):
                 ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float),
                 ("ffn_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("kernel_launches", C.c_int32), ("cold_experts", C.c_int32), ("cpu_ms_cold", C.c_float),
-                ("_pad", C.c_float)]
+                ("ffn_launches", C.c_int32)]
 
 
 class LayerOutcome(C.Structure):
@@ -181,6 +181,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_persistent": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
         "moespac_ctx_set_l2_prefetch": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
@@ -516,6 +517,9 @@ class Context:
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))
+
+    def set_persistent(self, on: bool = True):
+        check(lib().moespac_ctx_set_persistent(self._h, int(on)))
 
     def set_l2_prefetch(self, nbytes: int):
         """Per-CTA cross-layer L2 prefetch budget of the tensor-core K3 (0 = off)."""

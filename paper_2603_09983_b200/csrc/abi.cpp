@@ -595,6 +595,10 @@ moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes) {
   });
 }
 
+moespac_status moespac_ctx_set_persistent(moespac_ctx* c, int enabled) {
+  return guard([&] { c->e.set_persistent(enabled != 0); });
+}
+
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_pdl(enabled != 0); });
 }

@@ -215,6 +215,13 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaMemset(hT_d_, 0, sizeof(uint16_t) * 2 * 16 * d), "memset hT");  // token pad rows stay zero
   work_bytes_ = static_cast<size_t>(sms_ + N + m.n_shared_units) * T_ * d * 4;
   dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
+  dmalloc(reinterpret_cast<void**>(&sync_d_), sizeof(unsigned) * 2, "cudaMalloc sync");
+  if (kernel_ == kFfnTensorCore && acc_mode_ == 3 && world_ == 1) {
+    persist_ring_ = ffn_tp_ring_bytes(T_, d, prop.sharedMemPerBlockOptin);
+    persist_smem_ = ffn_tp_smem_bytes(d, persist_ring_);
+    persist_ok_ = persist_ring_ > 0 && ffn_tp_ok(N + m.n_shared_units, m.d_ffn, sms_, sms_);
+  }
+  if (const char* e = std::getenv("MOESPAC_PERSISTENT")) persistent_ = std::atoi(e) != 0;
   dmalloc(reinterpret_cast<void**>(&ycold_d_), sizeof(float) * L * T_ * d, "cudaMalloc ycold");
   check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocDefault),
         "cudaHostAlloc");
@@ -264,7 +271,7 @@ Engine::~Engine() {
                   static_cast<void*>(offsets_d_), static_cast<void*>(perm_d_), static_cast<void*>(hit_list_d_),
                   static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
-                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_)})
+                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sync_d_)})
     if (p) cudaFree(p);
   cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
@@ -681,7 +688,45 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   float cpu_ms_cold = 0.f;
   int cold_experts = 0;
 
-  if (!cold) {
+  const bool persist = !cold && persistent_ && persist_ok_ && !model_mode_;
+  if (persist) {
+    // ---- one persistent K3 for the whole step, combine inside; its layer 0
+    // streams after every load of the step has landed
+    if (n_loads > 0) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(L - 1)], 0), "wait loads");
+    check(cudaMemsetAsync(sync_d_, 0, sizeof(unsigned) * 2, compute_), "memset sync");
+    dev::PersistArgs pa{};
+    pa.T = T_;
+    pa.d = d;
+    pa.ffn = m_.d_ffn;
+    pa.k = k;
+    pa.N = N;
+    pa.L = L;
+    pa.n_shared = m_.n_shared_units;
+    pa.expert_elems = image_elems_;
+    pa.pool_layer_elems = slots_ * image_elems_;
+    pa.pool = pool_;
+    pa.shared_w = shared_;
+    pa.slot_of = slots_d;
+    pa.hit_list = hit_list_d_;
+    pa.hit_ord = hit_ord_d_;
+    pa.counters = counters_d;
+    pa.offsets = offsets_d_;
+    pa.perm = perm_d_;
+    pa.gates = gates_d_;
+    pa.ids = ids_d_;
+    pa.h = h_d_;
+    pa.y = y_d_;
+    pa.hT = hT_d_;
+    pa.partial = work_d_;
+    pa.ring_bytes = persist_ring_;
+    pa.sync = sync_d_;
+    pa.dbg = k3_trace_;
+    if (timing_) check(cudaEventRecord(ffn_beg_[0], compute_), "event");
+    check(launch_expert_ffn_persistent(pa, sms_, persist_smem_, compute_), "K3 persistent");
+    if (timing_) check(cudaEventRecord(ffn_end_[0], compute_), "event");
+    check(cudaEventSynchronize(k2_done_), "sync K2");
+    host_account();
+  } else if (!cold) {
     // ---- all layers on the device back to back; host accounting overlaps
     for (int l = 0; l < L; ++l) {
       if (model_mode_) {
@@ -785,7 +830,10 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
                      (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
     rep->d2h_bytes =
         static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
-    rep->kernel_launches = (model_mode_ ? 4 * L : (replay_ids_ ? 1 : 2) + 2 * L) + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
+    rep->kernel_launches = persist ? (replay_ids_ ? 1 : 2) + 1 + 1
+                                   : (model_mode_ ? 4 * L : (replay_ids_ ? 1 : 2) + 2 * L) + (tc ? 1 : 0) +
+                                         (world_ > 1 ? L : 0);
+    rep->ffn_launches = persist ? 1 : L;
     rep->cold_experts = cold_experts;
     rep->cpu_ms_cold = cpu_ms_cold;
     if (timing_) {
@@ -798,7 +846,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       rep->gpu_ms_router = ms(ev_[1], ev_[2]);
       rep->gpu_ms_hist = ms(ev_[2], ev_[3]);
       float f = 0.f;
-      for (int l = 0; l < L; ++l) f += ms(ffn_beg_[static_cast<size_t>(l)], ffn_end_[static_cast<size_t>(l)]);
+      for (int l = 0; l < (persist ? 1 : L); ++l)
+        f += ms(ffn_beg_[static_cast<size_t>(l)], ffn_end_[static_cast<size_t>(l)]);
       rep->gpu_ms_ffn = f;
       rep->gpu_ms_combine = ms(ev_[3], ev_[4]) - f;
       rep->gpu_ms_h2d_loads = n_loads > 0 ? ms(copy_ev_[0], copy_ev_[1]) : 0.f;

@@ -68,6 +68,7 @@ class Engine {
   void set_timing(bool on) { timing_ = on; }
   void set_pdl(bool on) { pdl_ = on; }
   void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
+  void set_persistent(bool on) { persistent_ = on; }
   void set_loopback(LoopbackGroup* g) {
     if (!g || g->world() != world_) throw std::invalid_argument("moespac_ctx_set_loopback: group size != shard world");
     loop_ = g;
@@ -148,6 +149,11 @@ class Engine {
   uint16_t* wg_d_ = nullptr;      // [L][N][d] bf16 router weights (model mode)
   std::vector<bool> router_set_;
   bool model_mode_ = false;       // set for the duration of step_model()
+  // persistent K3 (expert_ffn_persistent.cu): plan and grid-barrier counters
+  bool persistent_ = false, persist_ok_ = false;  // measured slower than per-layer launches
+  int persist_ring_ = 0;
+  size_t persist_smem_ = 0;
+  unsigned* sync_d_ = nullptr;
   int acc_mode_ = 0;
 
   std::unique_ptr<ColdExecutor> cold_;
