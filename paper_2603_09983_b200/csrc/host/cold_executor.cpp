@@ -4,7 +4,10 @@
 // a miss costs exactly one pass over the expert's bytes in host DRAM.
 #include "cold_executor.hpp"
 
+#include <immintrin.h>
+
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace moespac {
@@ -24,22 +27,34 @@ inline float silu(float x) { return x / (1.f + std::exp(-x)); }
 
 ColdExecutor::ColdExecutor(int threads, int layout, int d, int ffn, int T)
     : layout_(layout), d_(d), ffn_(ffn), T_(T), rows_(layout == 2 ? 64 : 16) {
+  __builtin_cpu_init();
+  bf16_dot_ = __builtin_cpu_supports("avx512bf16") && !std::getenv("MOESPAC_COLD_SCALAR");
   if (threads < 1) threads = 1;
   part_.assign(static_cast<size_t>(threads), std::vector<float>(static_cast<size_t>(T) * d));
   scratch_.assign(static_cast<size_t>(threads), std::vector<float>());
   hf_.assign(static_cast<size_t>(T) * d, 0.f);
+  // Workers spin briefly on the job generation before sleeping: a layer's
+  // cold work arrives every few hundred microseconds, and a condition-
+  // variable wake-up per layer and worker cost tens of microseconds each.
   for (int w = 1; w < threads; ++w) workers_.emplace_back([this, w] {
       int seen = 0;
       for (;;) {
-        {
-          std::unique_lock<std::mutex> lk(mu_);
-          cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-          if (stop_) return;
-          seen = gen_;
+        bool got = false;
+        for (int spin = 0; spin < kSpin && !got; ++spin) {
+          got = gen_a_.load(std::memory_order_acquire) != seen || stop_a_.load(std::memory_order_acquire);
+          if (!got) _mm_pause();
         }
+        if (!got) {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return stop_a_.load() || gen_a_.load() != seen; });
+        }
+        if (stop_a_.load(std::memory_order_acquire)) return;
+        seen = gen_a_.load(std::memory_order_acquire);
         work(w);
-        std::lock_guard<std::mutex> lk(mu_);
-        if (--pending_ == 0) done_cv_.notify_all();
+        if (pending_a_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+          std::lock_guard<std::mutex> lk(mu_);
+          done_cv_.notify_all();
+        }
       }
     });
 }
@@ -47,19 +62,117 @@ ColdExecutor::ColdExecutor(int threads, int layout, int d, int ffn, int T)
 ColdExecutor::~ColdExecutor() {
   {
     std::lock_guard<std::mutex> lk(mu_);
-    stop_ = true;
+    stop_a_.store(true, std::memory_order_release);
   }
   cv_.notify_all();
   for (auto& t : workers_) t.join();
 }
 
+// AVX-512 BF16 path for the tensor-core image (layout 2), chosen at run time
+// when the host has VDPBF16PS: the image's core matrices are 8 rows x 8
+// bf16 = 128 contiguous bytes, i.e. two 512-bit registers of 4 rows x 8 k;
+// one dot-product instruction against a token's 8 h values (16 bytes,
+// broadcast to the four 128-bit lanes) accumulates 32 products. The down
+// projection takes a = silu(g)·u·gate as bf16 hi + lo (two passes), as K3
+// does on the device, so both sides round a the same way.
+__attribute__((target("avx512f,avx512bw,avx512vl,avx512bf16"))) static void chunk_tc_bf16(
+    const ColdItem& it, int c, int d, const uint16_t* hb, float* y, float* acc, uint16_t* abf) {
+  const int R = 64, n = it.n_tok;
+  const uint16_t* base = it.image + static_cast<size_t>(c) * 3 * R * d;
+  const int ktiles = d / 64;
+  // ---- gate|up: acc[row-slot f][i] per token, gate rows then up rows
+  for (int g = 0; g < 16; ++g) {
+    __m512 s0[16], s1[16];
+    for (int i = 0; i < n; ++i) {
+      s0[i] = _mm512_setzero_ps();
+      s1[i] = _mm512_setzero_ps();
+    }
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const uint16_t* gp = base + static_cast<size_t>(kt) * 8192 + g * 512;
+      for (int j = 0; j < 8; ++j) {
+        const __m512bh w0 = reinterpret_cast<__m512bh>(_mm512_loadu_si512(gp + j * 64));
+        const __m512bh w1 = reinterpret_cast<__m512bh>(_mm512_loadu_si512(gp + j * 64 + 32));
+        for (int i = 0; i < n; ++i) {
+          const __m512bh hv = reinterpret_cast<__m512bh>(_mm512_broadcast_i32x4(
+              _mm_loadu_si128(reinterpret_cast<const __m128i*>(hb + static_cast<size_t>(it.tok[i]) * d + kt * 64 + j * 8))));
+          s0[i] = _mm512_dpbf16_ps(s0[i], w0, hv);
+          s1[i] = _mm512_dpbf16_ps(s1[i], w1, hv);
+        }
+      }
+    }
+    for (int i = 0; i < n; ++i) {
+      alignas(64) float v[32];
+      _mm512_store_ps(v, s0[i]);
+      _mm512_store_ps(v + 16, s1[i]);
+      for (int r = 0; r < 8; ++r) {
+        const float tot = (v[4 * r] + v[4 * r + 1]) + (v[4 * r + 2] + v[4 * r + 3]);
+        const int row = g * 8 + r;  // quarter-major, octet-interleaved (see the scalar path)
+        const int qq = row >> 5, sr = row & 31;
+        const int fl = qq * 16 + ((sr >> 4) << 3) + (sr & 7);
+        acc[((((sr >> 3) & 1) ? R + fl : fl)) * 16 + i] = tot;
+      }
+    }
+  }
+  // ---- a = silu(g) u gate as bf16 hi + lo, [i][f]
+  for (int i = 0; i < n; ++i)
+    for (int f = 0; f < R; ++f) {
+      const float gv = acc[f * 16 + i], uv = acc[(R + f) * 16 + i];
+      const float av = gv / (1.f + std::exp(-gv)) * uv * it.gate[i];
+      uint32_t u;
+      std::memcpy(&u, &av, 4);
+      const uint32_t hiu = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;  // round to nearest even
+      float hi;
+      std::memcpy(&hi, &hiu, 4);
+      const float rem = av - hi;
+      uint32_t ru;
+      std::memcpy(&ru, &rem, 4);
+      abf[(i * 2 + 0) * R + f] = static_cast<uint16_t>(hiu >> 16);
+      abf[(i * 2 + 1) * R + f] = static_cast<uint16_t>((ru + 0x7fffu + ((ru >> 16) & 1u)) >> 16);
+    }
+  // ---- down: y[tok][o] += sum_f W[o][f] a[f]
+  const uint16_t* dbase = base + static_cast<size_t>(ktiles) * 8192;
+  for (int mt = 0; mt < d / 128; ++mt) {
+    const uint16_t* tile = dbase + static_cast<size_t>(mt) * 8192;
+    for (int go = 0; go < 16; ++go) {
+      __m512 s0[16], s1[16];
+      for (int i = 0; i < n; ++i) {
+        s0[i] = _mm512_setzero_ps();
+        s1[i] = _mm512_setzero_ps();
+      }
+      for (int j = 0; j < 8; ++j) {
+        const uint16_t* gp = tile + j * 1024 + go * 64;
+        const __m512bh w0 = reinterpret_cast<__m512bh>(_mm512_loadu_si512(gp));
+        const __m512bh w1 = reinterpret_cast<__m512bh>(_mm512_loadu_si512(gp + 32));
+        for (int i = 0; i < n; ++i)
+          for (int part = 0; part < 2; ++part) {
+            const __m512bh av = reinterpret_cast<__m512bh>(_mm512_broadcast_i32x4(
+                _mm_loadu_si128(reinterpret_cast<const __m128i*>(abf + (i * 2 + part) * R + j * 8))));
+            s0[i] = _mm512_dpbf16_ps(s0[i], w0, av);
+            s1[i] = _mm512_dpbf16_ps(s1[i], w1, av);
+          }
+      }
+      for (int i = 0; i < n; ++i) {
+        alignas(64) float v[32];
+        _mm512_store_ps(v, s0[i]);
+        _mm512_store_ps(v + 16, s1[i]);
+        float* yr = y + static_cast<size_t>(it.tok[i]) * d + mt * 128 + go * 8;
+        for (int r = 0; r < 8; ++r) yr[r] += (v[4 * r] + v[4 * r + 1]) + (v[4 * r + 2] + v[4 * r + 3]);
+      }
+    }
+  }
+}
+
 // One chunk of one expert: gate/up rows -> a = silu(g) * u * gate -> down.
 void ColdExecutor::chunk(const ColdItem& it, int c, const float* hf, float* y, std::vector<float>& scr) const {
   const int d = d_, R = rows_, n = it.n_tok;
-  scr.resize(static_cast<size_t>(2 * R) * 16 + static_cast<size_t>(d));
+  scr.resize(static_cast<size_t>(2 * R) * 16 + static_cast<size_t>(d) + static_cast<size_t>(2 * 16 * R));
   float* acc = scr.data();        // [2R][16] gate rows then up rows, per token
   float* wrow = acc + 2 * R * 16;  // one unpacked row [d] (or [64] for layout 2 runs)
   std::memset(acc, 0, sizeof(float) * 2 * R * 16);
+  if (layout_ == 2 && bf16_dot_) {
+    chunk_tc_bf16(it, c, d, hb_, y, acc, reinterpret_cast<uint16_t*>(wrow + d));
+    return;
+  }
   const uint16_t* base = it.image + static_cast<size_t>(c) * 3 * R * d;
   if (layout_ == 2) {
     // gate|up K-tiles [128 rows][64 k]: element (row, kk) at
@@ -154,21 +267,23 @@ void ColdExecutor::work(int w) {
 void ColdExecutor::run(const std::vector<ColdItem>& items, const uint16_t* h, float* y) {
   const size_t TD = static_cast<size_t>(T_) * d_;
   for (size_t i = 0; i < TD; ++i) hf_[i] = bf(h[i]);
+  hb_ = h;
   units_.clear();
   const int cpe = ffn_ / rows_;
   for (size_t i = 0; i < items.size(); ++i)
     for (int c = 0; c < cpe; ++c) units_.emplace_back(static_cast<int>(i), c);
   items_ = &items;
+  pending_a_.store(static_cast<int>(workers_.size()), std::memory_order_relaxed);
   {
     std::lock_guard<std::mutex> lk(mu_);
-    pending_ = static_cast<int>(workers_.size());
-    ++gen_;
+    gen_a_.fetch_add(1, std::memory_order_acq_rel);
   }
   cv_.notify_all();
   work(0);
-  {
+  for (int spin = 0; spin < kSpin && pending_a_.load(std::memory_order_acquire) != 0; ++spin) _mm_pause();
+  if (pending_a_.load(std::memory_order_acquire) != 0) {
     std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [&] { return pending_ == 0; });
+    done_cv_.wait(lk, [&] { return pending_a_.load() == 0; });
   }
   // fixed-order reduction over workers
   std::memcpy(y, part_[0].data(), sizeof(float) * TD);

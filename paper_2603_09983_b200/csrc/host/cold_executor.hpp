@@ -8,6 +8,7 @@
 // layer output by the combine kernel (y_extra).
 #pragma once
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <functional>
@@ -33,19 +34,23 @@ class ColdExecutor {
   // Deterministic: fixed work partition, fixed reduction order.
   void run(const std::vector<ColdItem>& items, const uint16_t* h, float* y);
   int threads() const { return static_cast<int>(workers_.size()) + 1; }
+  bool bf16_dot() const { return bf16_dot_; }
 
  private:
   void work(int w);
   void chunk(const ColdItem& it, int c, const float* hf, float* y, std::vector<float>& scratch) const;
   int layout_, d_, ffn_, T_, rows_;
   std::vector<std::thread> workers_;
+  static constexpr int kSpin = 1 << 16;  // ~100-200 us of _mm_pause before sleeping
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
-  int gen_ = 0, pending_ = 0;
-  bool stop_ = false;
+  std::atomic<int> gen_a_{0}, pending_a_{0};
+  std::atomic<bool> stop_a_{false};
   // current job
   const std::vector<ColdItem>* items_ = nullptr;
   std::vector<float> hf_;                 // [T][d] fp32
+  const uint16_t* hb_ = nullptr;          // [T][d] bf16 (the AVX-512 BF16 path reads it directly)
+  bool bf16_dot_ = false;                 // host has VDPBF16PS (tensor-core image only)
   std::vector<std::vector<float>> part_;  // per worker [T][d]
   std::vector<std::vector<float>> scratch_;
   std::vector<std::pair<int, int>> units_;  // (item, chunk)

@@ -16,6 +16,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <exception>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -222,6 +224,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
     persist_ok_ = persist_ring_ > 0 && ffn_tp_ok(N + m.n_shared_units, m.d_ffn, sms_, sms_);
   }
   if (const char* e = std::getenv("MOESPAC_PERSISTENT")) persistent_ = std::atoi(e) != 0;
+  cold_trace_ = std::getenv("MOESPAC_COLD_TRACE") != nullptr;
   dmalloc(reinterpret_cast<void**>(&ycold_d_), sizeof(float) * L * T_ * d, "cudaMalloc ycold");
   check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocDefault),
         "cudaHostAlloc");
@@ -231,7 +234,9 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
                       cudaHostAllocDefault),
         "cudaHostAlloc");
   h_ready_.resize(static_cast<size_t>(L + 1));
-  for (auto& ev : h_ready_) check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+  // spin-waited: the cold path syncs on every layer's h_l, and a blocking
+  // (interrupt) wake-up per layer costs more than the spin
+  for (auto& ev : h_ready_) check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
   tables_bytes_ = sizeof(uint32_t) * 2 * L * W_ + sizeof(int32_t) * L + sizeof(int32_t) * L * N;
   dmalloc(reinterpret_cast<void**>(&tables_d_), tables_bytes_, "cudaMalloc tables");
   out_bytes_ = sizeof(int32_t) * (L * N + L * 8);
@@ -450,6 +455,7 @@ void Engine::step_model(const uint16_t* h_in, bool h_in_host, int accepted, uint
 
 void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
                   uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers) {
+  const auto t_step0 = std::chrono::steady_clock::now();
   if (!finalized_) throw std::logic_error("moespac_step: context not finalized");
   if (world_ > 1 && !comm_ && !loop_)
     throw std::logic_error("moespac_step: expert-parallel context needs moespac_ctx_set_nccl");
@@ -479,30 +485,6 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   std::vector<int> layer_loads(static_cast<size_t>(L), 0), layer_loads_local(static_cast<size_t>(L), 0);
 
   if (timing_) check(cudaEventRecord(ev_[0], compute_), "event");
-  // ---- copy engine: this step's loads in drain order, one event per layer.
-  // The previous step fully completed before this call returned, so no slot
-  // being overwritten is still read by an in-flight FFN (the device-side
-  // meaning of the reference's frozen score, execution_engine.cpp:111-118).
-  int n_loads = 0;
-  if (timing_) check(cudaEventRecord(copy_ev_[0], copy_), "event");
-  {
-    size_t i = 0;
-    const auto& loads = sched_->loads();
-    for (int l = 0; l < L; ++l) {
-      for (; i < loads.size() && loads[i].layer == l; ++i) {
-        const SlotLoad& ld = loads[i];
-        ++layer_loads[static_cast<size_t>(l)];
-        if (ld.shard != rank_) continue;
-        ++layer_loads_local[static_cast<size_t>(l)];
-        check(cudaMemcpyAsync(slot_ptr(l, ld.slot), arena_h_ + image_of(l, ld.expert) * image_elems_,
-                              image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
-              "H2D expert load");
-        ++n_loads;
-      }
-      check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
-    }
-  }
-  if (timing_) check(cudaEventRecord(copy_ev_[1], copy_), "event");
   // ---- compute stream
   check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
@@ -588,6 +570,34 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   }
   if (!model_mode_) check(cudaEventRecord(k2_done_, compute_), "event");
 
+  // ---- copy engine: this step's loads in drain order, one event per layer,
+  // issued after the compute stream's small H2D copies above: host->device
+  // copies share the copy engines in submission order, so tables / logits /
+  // h queued behind ~10-100 MB of expert loads would hold up K1/K2 by
+  // milliseconds.
+  // The previous step fully completed before this call returned, so no slot
+  // being overwritten is still read by an in-flight FFN (the device-side
+  // meaning of the reference's frozen score, execution_engine.cpp:111-118).
+  int n_loads = 0;
+  if (timing_) check(cudaEventRecord(copy_ev_[0], copy_), "event");
+  {
+    size_t i = 0;
+    const auto& loads = sched_->loads();
+    for (int l = 0; l < L; ++l) {
+      for (; i < loads.size() && loads[i].layer == l; ++i) {
+        const SlotLoad& ld = loads[i];
+        ++layer_loads[static_cast<size_t>(l)];
+        if (ld.shard != rank_) continue;
+        ++layer_loads_local[static_cast<size_t>(l)];
+        check(cudaMemcpyAsync(slot_ptr(l, ld.slot), arena_h_ + image_of(l, ld.expert) * image_elems_,
+                              image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
+              "H2D expert load");
+        ++n_loads;
+      }
+      check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
+    }
+  }
+  if (timing_) check(cudaEventRecord(copy_ev_[1], copy_), "event");
   const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
   const bool tc = kernel_ == kFfnTensorCore;
   uint16_t* hT[2] = {hT_d_, hT_d_ + static_cast<size_t>(16) * d};
@@ -772,11 +782,16 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       }
       cold_experts += static_cast<int>(items[static_cast<size_t>(l)].size());
     }
+
     if (h_in_host) std::memcpy(hcold_h_, h_in, sizeof(uint16_t) * T_ * d);
+    double wait_ms = 0.0;
+    const auto t_loop0 = std::chrono::steady_clock::now();
     for (int l = 0; l < L; ++l) {
       const float* y_extra = nullptr;
       if (!items[static_cast<size_t>(l)].empty()) {
+        const auto w0 = std::chrono::steady_clock::now();
         if (l > 0) check(cudaEventSynchronize(h_ready_[static_cast<size_t>(l)]), "sync h_l");
+        wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
         const auto c0 = std::chrono::steady_clock::now();
         float* yh = ycold_h_ + static_cast<size_t>(l) * T_ * d;
         cold_->run(items[static_cast<size_t>(l)], hcold_h_ + static_cast<size_t>(l) * T_ * d, yh);
@@ -796,7 +811,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         launch_ffn(l + 1);
       }
     }
+    const auto a0 = std::chrono::steady_clock::now();
     host_account();
+    if (cold_trace_)
+      std::fprintf(stderr, "cold-trace: prologue %.3f ms, h waits %.3f ms, cold %.3f ms, loop %.3f ms, account %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(t_loop0 - t_step0).count(), wait_ms, cpu_ms_cold,
+                   std::chrono::duration<double, std::milli>(a0 - t_loop0).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count());
   }
   if (timing_) check(cudaEventRecord(ev_[4], compute_), "event");
   const uint16_t* hfin = h_d_ + static_cast<size_t>(L) * T_ * d;

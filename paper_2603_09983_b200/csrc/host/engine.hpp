@@ -143,6 +143,7 @@ class Engine {
   unsigned long long* k3_trace_ = nullptr;  // profiling: [L][grid][32]
   int l2_prefetch_ = 0;  // per-CTA next-layer L2 prefetch (bytes); measured no gain, off
   int cold_threads_ = -1;
+  bool cold_trace_ = false;  // MOESPAC_COLD_TRACE: per-step host timing of the cold path on stderr
   int ffn_accum_ = 0;
   const int32_t* replay_ids_ = nullptr;  // set for the duration of step_ids()
   const float* replay_gates_ = nullptr;
