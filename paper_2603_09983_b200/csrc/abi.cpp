@@ -510,6 +510,9 @@ moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream) 
       cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
       cuda_ok(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
       c.per_cta = ffn_tc_plan(a->tokens, a->d_model, static_cast<size_t>(optin), a->accum).acc_mode == 3 ? 1 : 0;
+      c.unit_rows = 8;
+    } else {
+      c.unit_rows = 16;
     }
     c.partial = a->workspace_dev;
     c.y_out = a->y_dev;

@@ -664,6 +664,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.n_shared = n_shared_eff;
     ca.grid = sms_;
     ca.per_cta = tc && acc_mode_ == 3 ? 1 : 0;
+    ca.unit_rows = tc ? 8 : 16;
     if (k3_trace_) ca.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
     ca.partial = work_d_;
     float* yl = y_d_ + static_cast<size_t>(l) * T_ * d;

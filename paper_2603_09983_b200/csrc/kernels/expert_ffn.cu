@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.y * 128 + lane * 4;
-  const int qpe = a.per_cta ? a.ffn / 8 : a.ffn / FC;  // work units per entry (grouped K3: 8-row units)
+  const int qpe = a.ffn / (a.per_cta || a.unit_rows == 8 ? 8 : FC);  // work units per entry (tensor-core K3s: 8 rows)
   // The routing (K2 outputs: counters, ids, hit order) was final several
   // kernels ago, so the row list is built before waiting for the K3 launch
   // whose partials it sums: only the partial loads sit on the critical path.

@@ -49,10 +49,10 @@ constexpr int THREADS = 192;
 constexpr int EPI_THREADS = 128;
 constexpr int A_BYTES = 16384;
 constexpr int B_BYTES = 2048;
-constexpr int QBYTES = 4096;     // one 16-row quarter of a 128-row tile (gate|up or down)
+constexpr int UBYTES = 2048;     // one 8-row unit (gate + up octet) of a 128-row gate|up tile, or 8 k of a down tile
 constexpr int NSLOT = 32;        // ring entries in flight (mbarrier pairs)
 constexpr int FCH = 64;  // ffn rows per chunk
-constexpr int QROWS = 16;
+constexpr int UROWS = 8;          // ffn rows per work unit
 constexpr int TMEM_COLS = 512;
 constexpr int D2_COL0 = 256;
 constexpr int ACC_SMEM = 0, ACC_GLOBAL = 1, ACC_TMEM = 2, ACC_GROUP = 3;  // FfnArgs::acc_mode
@@ -70,21 +70,22 @@ struct Ring {
   }
 };
 
-// Iterates the CTA's work as segments (entry, chunk, quarter range).
+// Iterates the CTA's work as segments (entry, chunk, unit range); a unit
+// is 8 ffn rows (image layout v3: one 2 KiB run per tile), 8 per chunk.
 struct Seg {
-  int o, c, qa, qb;  // quarters [qa, qb) of chunk c of entry o
+  int o, c, qa, qb;  // units [qa, qb) of chunk c of entry o
 };
 
 struct SegIter {
   long long q, q1;
-  int qpe;  // quarters per entry = ffn / 16
+  int qpe;  // units per entry = ffn / 8
   __device__ __forceinline__ bool next(Seg& s) {
     if (q >= q1) return false;
     const int o = static_cast<int>(q / qpe);
     const int qi = static_cast<int>(q % qpe);
-    const int c = qi / 4;
-    const int qa = qi % 4;
-    const long long chunk_end = static_cast<long long>(o) * qpe + (c + 1) * 4;
+    const int c = qi / 8;
+    const int qa = qi % 8;
+    const long long chunk_end = static_cast<long long>(o) * qpe + (c + 1) * 8;
     const long long end = chunk_end < q1 ? chunk_end : q1;
     s = {o, c, qa, qa + static_cast<int>(end - q)};
     q = end;
@@ -103,26 +104,28 @@ __device__ __forceinline__ int pow2_divisor(int x, int cap) {
   while (m < cap && x % (2 * m) == 0) m *= 2;
   return m;
 }
-__device__ __forceinline__ int tiles_per_entry(int nq, int cap) {
-  const int t = nq >= 3 ? 2 : (nq == 2 ? 4 : 8);
+__device__ __forceinline__ int tiles_per_entry(int nu, int cap) {
+  const int t = nu >= 6 ? 2 : (nu >= 3 ? 4 : 8);
   return t < cap ? t : cap;
 }
 struct Geom {  // one entry: bytes, tiles, read window (bytes from the entry start)
   uint32_t size, win;
   int m;
 };
-__device__ __forceinline__ Geom gu_geom(int nq, int cap) {
-  const int m = tiles_per_entry(nq, cap);
-  const uint32_t a = static_cast<uint32_t>(nq) * 4096u;
+__device__ __forceinline__ Geom gu_geom(int nu, int cap) {
+  const int m = tiles_per_entry(nu, cap);
+  const uint32_t a = static_cast<uint32_t>(nu) * 2048u;
   const uint32_t size = static_cast<uint32_t>(m) * (a + 2048u);
-  // tile j's A descriptor reads the 16 KiB window at j*a - qa*4096
+  // tile j's A descriptor reads the 16 KiB window at j*a - qa*2048
   const uint32_t w = static_cast<uint32_t>(m - 1) * a + 16384u;
   return {size, size > w ? size : w, m};
 }
-__device__ __forceinline__ Geom dn_geom(int nq, int cap) {
-  const int m = tiles_per_entry(nq, cap);
-  const uint32_t size = static_cast<uint32_t>(m) * static_cast<uint32_t>(nq) * 4096u;
-  return {size, size, m};
+__device__ __forceinline__ Geom dn_geom(int nu, int cap) {
+  const int m = tiles_per_entry(nu, cap);
+  // a down K-step reads two units: one unit past the segment at either end
+  // (its a^T rows are 0)
+  const uint32_t size = static_cast<uint32_t>(m) * static_cast<uint32_t>(nu) * 2048u;
+  return {size, size + 2048u, m};
 }
 __device__ __forceinline__ uint32_t ring_place(uint32_t& head, const Geom& g, uint32_t rb) {
   uint32_t e = head;
@@ -167,7 +170,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
   const int ktiles = d / 64, mtiles = d / 128;
   const int passes = (mtiles + PASS_TILES - 1) / PASS_TILES;
   const long long chunk_elems = 3LL * FCH * d;
-  const int qpe = a.ffn / QROWS;
+  const int qpe = a.ffn / UROWS;
 
   // [a^T 16 KiB][ring][ysum][small]: the a^T buffers sit right before the
   // ring so that a shifted A descriptor of a partial entry (up to 12 KiB
@@ -242,9 +245,14 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
     float4* ys = reinterpret_cast<float4*>(ysum);
     for (int i = tid; i < T * d / 4; i += THREADS) ys[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  {  // a^T columns of tokens >= T stay zero for the whole launch
+  {  // a^T columns of tokens >= T stay zero for the whole launch; the ring
+     // starts zeroed so that the unit a partial down K-step reads past the
+     // segment (a^T = 0 there) is finite even before the ring has wrapped
     uint4* z = reinterpret_cast<uint4*>(aT);
     for (int i = tid; i < 2 * 2 * 4096 / 16; i += THREADS) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    uint4* zr = reinterpret_cast<uint4*>(ring);
+    for (uint32_t i = tid; i < RB / 16; i += THREADS) zr[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async();
   }
   {
     // Stage the routing (token list, per-token gate) of the first ENT_PRE
@@ -351,12 +359,12 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
       // segment is a whole chunk (tiles are contiguous), else one per tile
       auto copy_tiles = [&](const uint8_t* base, int t0, int m, int qa, int nq, uint32_t e, uint64_t* bar) {
         if (!leader) return;
-        if (nq == 4) {
+        if (nq == 8) {
           bulk_g2s(ring + e, base + static_cast<size_t>(t0) * A_BYTES, static_cast<uint32_t>(m) * A_BYTES, bar, pol);
         } else {
-          const uint32_t ab = static_cast<uint32_t>(nq) * QBYTES;
+          const uint32_t ab = static_cast<uint32_t>(nq) * UBYTES;
           for (int j = 0; j < m; ++j)
-            bulk_g2s(ring + e + j * ab, base + static_cast<size_t>(t0 + j) * A_BYTES + qa * QBYTES, ab, bar, pol);
+            bulk_g2s(ring + e + j * ab, base + static_cast<size_t>(t0 + j) * A_BYTES + qa * UBYTES, ab, bar, pol);
         }
       };
       auto seg_base = [&](const Seg& s) {
@@ -385,7 +393,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         }
         pdl_wait();
         // the prefetched entries lie back to back from offset 0 (no wrap)
-        const uint32_t span = (g.size + 1023u) & ~1023u, ab = static_cast<uint32_t>(g.m * nq) * QBYTES;
+        const uint32_t span = (g.size + 1023u) & ~1023u, ab = static_cast<uint32_t>(g.m * nq) * UBYTES;
         for (int j = 0; j < np; ++j)
           if (leader)
             bulk_g2s(ring + j * span + ab, hTb + static_cast<size_t>(j * g.m) * B_BYTES,
@@ -395,7 +403,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         if (more) {
           const int nq = cur.qb - cur.qa;
           const Geom g = gu_geom(nq, kcap);
-          const uint32_t ab = static_cast<uint32_t>(g.m * nq) * QBYTES;
+          const uint32_t ab = static_cast<uint32_t>(g.m * nq) * UBYTES;
           for (int kt = kt0; kt < ktiles; kt += g.m) {
             uint32_t e;
             reserve(g, true, e);
@@ -448,11 +456,11 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
                                        : a.nx_shared_w + static_cast<long long>(s.o - nh) * a.expert_elems;
           const uint8_t* base = reinterpret_cast<const uint8_t*>(w + s.c * chunk_elems);
           const int nq = s.qb - s.qa;
-          const uint32_t run = static_cast<uint32_t>(nq) * QBYTES;
+          const uint32_t run = static_cast<uint32_t>(nq) * UBYTES;
           for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
             if (leader)
               asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * A_BYTES +
-                                                                              s.qa * QBYTES),
+                                                                              s.qa * UBYTES),
                            "r"(run)
                            : "memory");
             budget -= run;
@@ -488,15 +496,15 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
           const int nq = cur.qb - cur.qa;
           const Geom g = gu_geom(nq, kcap);
-          const uint32_t ab = static_cast<uint32_t>(nq) * QBYTES;
+          const uint32_t ab = static_cast<uint32_t>(nq) * UBYTES;
           for (int kt = 0; kt < ktiles; kt += g.m) {
             const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
             wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
             ++idx;
             if (i == 0 && kt == 0 && leader) stamp(a, 2);
             fence_after();
-            // shifted base: rows of quarter qa of tile j land at off + j*ab
-            const uint32_t va = ring_addr + off - static_cast<uint32_t>(cur.qa) * QBYTES;
+            // shifted base: rows of unit qa of tile j land at off + j*ab
+            const uint32_t va = ring_addr + off - static_cast<uint32_t>(cur.qa) * UBYTES;
             const uint32_t vb = ring_addr + off + static_cast<uint32_t>(g.m) * ab;
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
@@ -522,7 +530,9 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           const uint64_t bhi = smem_desc(ahi, 256, 128), blo = smem_desc(ahi + 4096u, 256, 128);
           const int nq = prev.qb - prev.qa;
           const Geom g = dn_geom(nq, mcap);
-          const uint32_t tb = static_cast<uint32_t>(nq) * QBYTES;
+          const uint32_t tb = static_cast<uint32_t>(nq) * UBYTES;
+          // K-steps (16 f = 2 units) overlapping the segment's units
+          const int k0 = prev.qa >> 1, k1 = (prev.qb + 1) >> 1;
           if (mode == ACC_TMEM) {
             // D2[mt] accumulates the whole entry's down projection in TMEM
             // (all M-tiles resident); drained once, at the entry's last
@@ -538,13 +548,13 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
               ++idx;
               if (i == 1 && mt == 0 && leader) stamp(a, 16);
               fence_after();
-              const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * QBYTES;
+              const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * UBYTES;
               if (leader) {
                 for (int j = 0; j < g.m; ++j) {
                   const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>((mt + j) * 16);
                   const uint64_t adn = smem_desc(va + j * tb, 2048, 128);
-                  for (int k = prev.qa; k < prev.qb; ++k) {
-                    mma_bf16(d2, adn + 256 * k, bhi + 32 * k, (first && k == prev.qa) ? 0u : 1u);
+                  for (int k = k0; k < k1; ++k) {
+                    mma_bf16(d2, adn + 256 * k, bhi + 32 * k, (first && k == k0) ? 0u : 1u);
                     mma_bf16(d2, adn + 256 * k, blo + 32 * k, 1u);
                   }
                 }
@@ -571,14 +581,14 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
               ++idx;
               if (i == 1 && mt == 0 && leader) stamp(a, 16);
               fence_after();
-              const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * QBYTES;
+              const uint32_t va = ring_addr + off - static_cast<uint32_t>(prev.qa) * UBYTES;
               if (leader) {
                 for (int j = 0; j < g.m; ++j) {
                   const uint32_t d2 =
                       tmem + D2_COL0 + static_cast<uint32_t>(pb * 128 + (mt + j - ps * PASS_TILES) * 16);
                   const uint64_t adn = smem_desc(va + j * tb, 2048, 128);
-                  for (int k = prev.qa; k < prev.qb; ++k) {  // +4096 B (A) / +512 B (a^T) per K=16 step
-                    mma_bf16(d2, adn + 256 * k, bhi + 32 * k, k == prev.qa ? 0u : 1u);
+                  for (int k = k0; k < k1; ++k) {  // +4096 B (A) / +512 B (a^T) per K=16 step
+                    mma_bf16(d2, adn + 256 * k, bhi + 32 * k, k == k0 ? 0u : 1u);
                     mma_bf16(d2, adn + 256 * k, blo + 32 * k, 1u);
                   }
                 }
@@ -720,7 +730,11 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         // This warp's TMEM lanes are chunk quarter q, octet-interleaved:
         // lanes 8h..8h+7 hold the gate rows f = 16q + 8h + (lane & 7), lanes
         // 8h+8..8h+15 the up rows of the same f (h = lane >> 4).
-        if (q >= cur.qa && q < cur.qb) {
+        if (2 * q + 1 >= cur.qa && 2 * q < cur.qb) {
+          // the quarter overlaps the segment; a unit of it outside the
+          // segment gets a = 0 (a down K-step covers both of its units)
+          const int unit = 2 * q + (lane >> 4);
+          const bool inside = unit >= cur.qa && unit < cur.qb;
           const int f = 16 * q + ((lane >> 4) << 3) + (lane & 7);
           const int up = (lane >> 3) & 1;
           uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
@@ -732,7 +746,8 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
               if ((t & 1) == up) {  // gate lanes even tokens, up lanes odd tokens
                 const float g = up ? pv : v[t];
                 const float u = up ? v[t] : pv;
-                const float av = __fdividef(g, 1.f + __expf(-g)) * u * gs[t];
+                const float gt = inside ? gs[t] : 0.f;
+                const float av = gt != 0.f ? __fdividef(g, 1.f + __expf(-g)) * u * gt : 0.f;
                 const uint16_t h16 = f32_to_bf16_rn(av);
                 const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
                 // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)

@@ -96,6 +96,7 @@ struct CombineArgs {
   int n_shared;
   int grid;                 // K3 grid size
   int per_cta;              // 1: one partial block per K3 CTA (grouped K3), else per (CTA, entry) pair
+  int unit_rows;            // ffn rows per K3 work unit: 8 (tensor-core K3s) or 16 (CUDA-core K3)
   const float* partial;
   float* y_out;             // [T][d] fp32 (may be null)
   uint16_t* h_out;          // [T][d] bf16 (may be null)

@@ -91,7 +91,7 @@ def main():
     lm = L // 2
     x = t[lm]
     n_hit_l = None
-    qpe = ffn // 16
+    qpe = ffn // 8  # work units (8 ffn rows) per entry
     base = np.median(x[:, 22])
     ends = (x[:, 6] - base) / 1e3
     first = (x[:, 2] - base) / 1e3
@@ -105,13 +105,13 @@ def main():
     for b in range(G):
         q, q1, ns = (b * n_units) // G, ((b + 1) * n_units) // G, 0
         while q < q1:
-            q = min((q // 4 + 1) * 4, q1)
+            q = min((q // 8 + 1) * 8, q1)
             ns += 1
         segs.append(ns)
     segs = np.array(segs)
     for nq in sorted(set(quarters.tolist())):
         m = quarters == nq
-        print(json.dumps({"layer": lm, "quarters": nq, "ctas": int(m.sum()),
+        print(json.dumps({"layer": lm, "units": nq, "ctas": int(m.sum()),
                           "end_us_med": round(float(np.median(ends[m])), 2),
                           "end_us_max": round(float(ends[m].max()), 2),
                           "segs_mean": round(float(segs[m].mean()), 2)}))
