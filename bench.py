@@ -377,12 +377,23 @@ def main():
     hbm_peak, peak_kind = load_peaks()
     tps = r["tokens"] / (r["ms"] * 1e-3)
     achieved = r["ffn_bytes"] / (r["ffn_ms"] * 1e-3) / 1e9 if r["ffn_ms"] > 0 else 0.0
-    traffic = None
+    # DRAM traffic of one K3 launch from a committed `ncu --set full`
+    # capture (profiles/ncu_k3_<config>.json), expressed for this run's
+    # average launch: captured DRAM bytes / captured algorithmic bytes x
+    # this run's algorithmic bytes per launch (the capture's launch streams
+    # a different number of experts than the average one)
+    traffic, traffic_capture = None, None
     prof = os.path.join(ROOT, "profiles", f"ncu_k3_{w.name}.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
-        except (ValueError, OSError):
+            cap = json.load(open(prof))
+            ratio = cap.get("traffic_over_algorithmic")
+            bpl = r["ffn_bytes"] / max(1, r["ffn_launches"])
+            traffic = ratio * bpl if ratio else None
+            traffic_capture = {"dram_bytes": cap.get("dram_bytes_per_launch"),
+                               "algorithmic_bytes": cap.get("algorithmic_bytes_of_launch"), "ratio": ratio,
+                               "kernel": cap.get("kernel"), "report": cap.get("report")}
+        except (ValueError, OSError, TypeError):
             traffic = None
     line = dict(base, value=tps, ms_per_step=r["ms"] / args.steps, scaling="strong" if world > 1 else "weak")
     line["e2e"] = {"value": r["tokens"] / (r["ms_e2e"] * 1e-3), "unit": "tokens/s",
@@ -391,6 +402,7 @@ def main():
                         "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)" if peak_kind == "measured"
                         else "fallback 6650 GB/s (B200_PROFILING.md)",
                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                        "traffic_capture": traffic_capture,
                         "bytes_per_launch": r["ffn_bytes"] / max(1, r["ffn_launches"]),
                         "ms_per_launch": r["ffn_ms"] / max(1, r["ffn_launches"])}
     line["gpu_launches"] = int(r["launches"])
