@@ -408,17 +408,31 @@ __global__ void __launch_bounds__(FFN_THREADS, 1) expert_ffn_kernel(FfnArgs a) {
 // experts in ascending id, each over the CTAs that covered it in ascending
 // order) are dealt round-robin to the warps, then the warp sums are added in
 // warp order — a fixed summation tree, so the result is deterministic.
-constexpr int COMBINE_WARPS = 4;  // small footprint: must co-reside with a K3 CTA (PDL)
+// 4 warps next to the per-segment K3 (its 200-register CTA leaves room for
+// no more), 8 next to the grouped K3 (82 registers): twice the partial rows
+// in flight per output column. The row lists and the cross-warp sums share
+// one shared-memory block (lists are dead once the loads are issued).
 constexpr int COMBINE_BATCH = 16;  // partial rows in flight per warp
-constexpr int COMBINE_LIST = 48;  // per-warp row list capacity (else streamed)
+constexpr int COMBINE_ROWS = 192;  // row list capacity over all warps (else streamed)
 
+template <int WARPS>
+struct CombineSmem {
+  union {
+    float4 red[WARPS][32];
+    int rows[WARPS][COMBINE_ROWS / WARPS];
+  };
+};
+
+template <int WARPS>
 __device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, const float4 (*red)[32], int t,
                                               int c, int lane);
 
 // (<= 112 registers: see expert_ffn_tc_kernel)
-__global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs a) {
-  __shared__ float4 red[COMBINE_WARPS][32];
-  __shared__ int rows[COMBINE_WARPS][COMBINE_LIST];
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
+  constexpr int COMBINE_WARPS = WARPS, COMBINE_LIST = COMBINE_ROWS / WARPS;
+  __shared__ CombineSmem<WARPS> sm;
+  auto& rows = sm.rows;
   if (threadIdx.x == 0) pdl_trigger();
   unsigned long long* dbg = a.dbg ? a.dbg + (blockIdx.y * gridDim.x + blockIdx.x) * 32 : nullptr;
   auto stamp = [&](int slot) {
@@ -522,17 +536,19 @@ __global__ void __launch_bounds__(COMBINE_WARPS * 32) combine_kernel(CombineArgs
     }
   }
   if (!(n > 0 && c < a.d)) pdl_wait();  // (no partials to read; still order after K3)
-  red[warp][lane] = acc;
+  __syncthreads();  // every warp is past its row list (the sums reuse that memory)
+  sm.red[warp][lane] = acc;
   __syncthreads();
   stamp(28);
   if (warp != 0 || c >= a.d) return;
-  combine_store(a, acc, red, t, c, lane);
+  combine_store<WARPS>(a, acc, sm.red, t, c, lane);
 }
 
 // warp 0 of a combine CTA: cross-warp sum, y / residual / bf16 / h^T stores
+template <int WARPS>
 __device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, const float4 (*red)[32], int t,
                                               int c, int lane) {
-  for (int w = 1; w < COMBINE_WARPS; ++w) {
+  for (int w = 1; w < WARPS; ++w) {
     const float4 v = red[w][lane];
     acc.x += v.x;
     acc.y += v.y;
@@ -679,7 +695,9 @@ cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cuda
 }
 
 cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream, bool pdl) {
-  return launch_pdl(dev::combine_kernel, dim3(a.T, (a.d + 127) / 128), dim3(dev::COMBINE_WARPS * 32), 0, stream, pdl,
+  if (a.per_cta)
+    return launch_pdl(dev::combine_kernel<8>, dim3(a.T, (a.d + 127) / 128), dim3(8 * 32), 0, stream, pdl, a);
+  return launch_pdl(dev::combine_kernel<4>, dim3(a.T, (a.d + 127) / 128), dim3(4 * 32), 0, stream, pdl,
                     a);
 }
 

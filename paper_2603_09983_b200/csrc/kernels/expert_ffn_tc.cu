@@ -35,6 +35,7 @@
 //            in flight.
 // Warp roles: 0 = TMA producer, 1 = MMA issuer (+ TMEM owner), 2-5 = epilogue
 // (TMEM lane quarters 2,3,0,1).
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -943,7 +944,9 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
   // Leave room on the SM for one combine CTA (3 KiB static + 1 KiB reserve)
   // next to the K3 CTA (+1 KiB reserve) of 228 KiB: programmatic dependent
   // launch only overlaps the two kernels when they can co-reside.
-  constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 3072 + 1024;
+  // (the grouped K3 sits next to the 8-warp combine: 4 KiB static + 1 KiB)
+  constexpr size_t kSmPerSm = 233472, kReserve = 1024, kCombine = 3072 + 1024, kCombine8 = 4096 + 1024 + 256;
+  const size_t limit_grouped = std::min(smem_limit, kSmPerSm - kReserve - kCombine8);
   if (smem_limit > kSmPerSm - kReserve - kCombine) smem_limit = kSmPerSm - kReserve - kCombine;
   auto ring_for = [&](int mode) -> int {
     const size_t fixed = ffn_tc_smem_bytes(T, d, 0, mode);
@@ -958,7 +961,7 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
   const bool tmem_ok = d <= dev::tc::TMEM_ACC_MAX_D;
   if (accum == 4 || (accum == 0 && tmem_ok)) {
     // grouped kernel (expert_ffn_grouped.cu): whole-CTA TMEM accumulator
-    const int rb = ffn_tg_ring_bytes(T, d, smem_limit);
+    const int rb = ffn_tg_ring_bytes(T, d, limit_grouped);
     if (rb > 0) {
       FfnPlan p{rb / 1024, false, ffn_tg_smem_bytes(d, rb)};
       p.acc_mode = dev::tc::ACC_GROUP;

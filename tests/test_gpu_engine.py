@@ -401,9 +401,10 @@ def test_persistent_k3_matches_per_layer_and_oracle(L, N, k, g, d, ffn, units):
             y_ref = O.moe_layer(hs[l], ids[l], gates, {e: std[(l, e)] for e in range(N)}, shared[l])
             rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
             assert rel <= 1e-5, (s, l, rel)
-        # same step through the per-layer path: the outputs agree to bf16
-        # rounding (the two combines add the same partials in another order)
-        diff = np.abs(O.bf16_bits_to_f32(ha).astype(np.float64) - O.bf16_bits_to_f32(hb).astype(np.float64))
-        assert np.all(diff <= 2.0 ** -7 * np.abs(O.bf16_bits_to_f32(hb)) + 1e-6), s
+        # same step through the per-layer path: the two combines add the same
+        # partials in another order, so h differs by bf16 roundings that the
+        # following layers carry along — compare in norm
+        fa, fb = O.bf16_bits_to_f32(ha).astype(np.float64), O.bf16_bits_to_f32(hb).astype(np.float64)
+        assert np.linalg.norm(fa - fb) <= 4e-3 * np.linalg.norm(fb), s
         assert [ra.cache_hits, ra.cache_misses] == [rb_.cache_hits, rb_.cache_misses]
     assert np.array_equal(a.sched_events(), b.sched_events())
