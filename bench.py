@@ -56,6 +56,10 @@ def parse_args():
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--trace-steps", type=int, default=64)
     ap.add_argument("--ffn-kernel", type=int, default=0, help="0 auto (tcgen05), 1 CUDA-core GEMV, 2 tcgen05")
+    ap.add_argument("--draft-window", action="store_true",
+                    help="emulated draft phase: gamma x t_draft_unit (reference default 300 us/token) on the compute "
+                         "stream before each verification step, expert loads overlapping it; TPS then counts "
+                         "draft + verification (the reference's definition)")
     ap.add_argument("--router-gemv", action="store_true",
                     help="model mode: routing from the on-device router GEMV W_g h_l of random-init router weights "
                          "(K0 -> K1 -> K2 per layer) instead of the trace generator's logits; cold path off")
@@ -222,6 +226,8 @@ def run_ours(args, w, rank, world, local_rank):
     if args.router_gemv:
         ctx.set_cold_threads(0)
     ctx.finalize()
+    if args.draft_window:
+        ctx.set_draft_window(True)
     if args.router_gemv:
         gw = torch.Generator().manual_seed(4)
         for l in range(L):
@@ -343,6 +349,8 @@ def main():
                 "parallelism": f"ep{world}" if world > 1 else "single",
                 "routing": "model: on-device router GEMV W_g h_l (random-init router), cold path off"
                 if args.router_gemv else "trace: reference TraceGenerator logits (K1 top-k on device)",
+                "draft": "emulated: gamma x 300 us spin on the compute stream, loads overlapping (reference model)"
+                if args.draft_window else "none: verification step only",
                 "l2": "inputs > L2: every step streams each resident activated expert (>= 9 MB each, "
                       "GBs per step) through HBM; no L2 flush needed"}
     base = {"metric": "decode TPS and expert-FFN HBM GB/s (roofline %) at 1/2/4/8 B200 vs host CPU",

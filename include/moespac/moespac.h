@@ -345,6 +345,12 @@ moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
  * routing). Off by default: measured ~15% slower than the per-layer K3 +
  * combine launches on the Qwen3 shape. */
 moespac_status moespac_ctx_set_persistent(moespac_ctx* c, int enabled);
+/* Emulated draft window (off by default): each step first holds the compute
+ * stream for gamma * t_draft_unit_ns (the reference's modeled draft phase,
+ * sim_core.cpp:167-172) while the copy engine works through the step's
+ * expert loads — the overlap the balancer's draft credit assumes. Steps then
+ * measure draft + verification, the reference's TPS definition. */
+moespac_status moespac_ctx_set_draft_window(moespac_ctx* c, int enabled);
 /* Programmatic dependent launch between layer kernels (on by default). */
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
 /* Profiling hook: device buffer of [n_layers][grid][32] uint64 that every

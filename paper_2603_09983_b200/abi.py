@@ -182,6 +182,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_persistent": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_draft_window": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
         "moespac_ctx_set_l2_prefetch": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
@@ -520,6 +521,9 @@ class Context:
 
     def set_persistent(self, on: bool = True):
         check(lib().moespac_ctx_set_persistent(self._h, int(on)))
+
+    def set_draft_window(self, on: bool = True):
+        check(lib().moespac_ctx_set_draft_window(self._h, int(on)))
 
     def set_l2_prefetch(self, nbytes: int):
         """Per-CTA cross-layer L2 prefetch budget of the tensor-core K3 (0 = off)."""

@@ -598,6 +598,10 @@ moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes) {
   });
 }
 
+moespac_status moespac_ctx_set_draft_window(moespac_ctx* c, int enabled) {
+  return guard([&] { c->e.set_draft_window(enabled != 0); });
+}
+
 moespac_status moespac_ctx_set_persistent(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_persistent(enabled != 0); });
 }

@@ -498,6 +498,11 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   check(cudaMemcpyAsync(h_d_, h_in, sizeof(uint16_t) * T_ * d,
                         h_in_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, compute_),
         "h_in");
+  // emulated draft window: the step's loads (issued below on the copy
+  // stream) overlap it, as the reference's decisions assume (draft credit)
+  if (draft_window_) check(launch_draft_window(static_cast<long long>(T_ - 1) * sched_->config().profile.t_draft_unit_ns,
+                                               compute_),
+                           "draft window");
   if (timing_) check(cudaEventRecord(ev_[1], compute_), "event");
   if (replay_ids_) {
     // recorded routing: ids ascending per token (the order K1 emits and the

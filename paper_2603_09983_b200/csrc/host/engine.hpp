@@ -69,6 +69,7 @@ class Engine {
   void set_pdl(bool on) { pdl_ = on; }
   void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
   void set_persistent(bool on) { persistent_ = on; }
+  void set_draft_window(bool on) { draft_window_ = on; }
   void set_loopback(LoopbackGroup* g) {
     if (!g || g->world() != world_) throw std::invalid_argument("moespac_ctx_set_loopback: group size != shard world");
     loop_ = g;
@@ -151,6 +152,7 @@ class Engine {
   std::vector<bool> router_set_;
   bool model_mode_ = false;       // set for the duration of step_model()
   // persistent K3 (expert_ffn_persistent.cu): plan and grid-barrier counters
+  bool draft_window_ = false;  // emulated γ·t_draft spin on the compute stream before K1
   bool persistent_ = false, persist_ok_ = false;  // measured slower than per-layer launches
   int persist_ring_ = 0;
   size_t persist_smem_ = 0;

@@ -724,6 +724,26 @@ cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float
   return cudaGetLastError();
 }
 
+namespace dev {
+// Emulated draft window (the reference's modeled γ·t_draft, sim_core.cpp:
+// 167-172): one warp holds the compute stream for `ns` nanoseconds of
+// %globaltimer while the copy engine works through the step's expert loads.
+__global__ void draft_window_kernel(long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0)::"memory");
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  } while (static_cast<long long>(t - t0) < ns);
+}
+}  // namespace dev
+
+cudaError_t launch_draft_window(long long ns, cudaStream_t stream) {
+  if (ns <= 0) return cudaSuccess;
+  dev::draft_window_kernel<<<1, 32, 0, stream>>>(ns);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream) {
   dev::pack_expert_kernel<<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, out);

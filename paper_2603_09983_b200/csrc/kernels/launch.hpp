@@ -145,6 +145,7 @@ cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream);
 cudaError_t launch_fill_synthetic(uint16_t* out, long long n, uint64_t seed, float stdv, cudaStream_t stream);
+cudaError_t launch_draft_window(long long ns, cudaStream_t stream);
 
 constexpr int kFfnMaxTokens = 16;
 constexpr int kFfnChunkRows = 16;

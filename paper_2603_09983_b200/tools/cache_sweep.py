@@ -26,7 +26,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 from paper_2603_09983_b200 import abi, configs  # noqa: E402
 
 
-def run_ratio(w, ratio, steps, warmup, cold_threads, profile):
+def run_ratio(w, ratio, steps, warmup, cold_threads, profile, draft=False):
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=ratio, **profile)
     ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode, 0), cfg, 0, 1)
@@ -34,6 +34,7 @@ def run_ratio(w, ratio, steps, warmup, cold_threads, profile):
     ctx.fill_synthetic(seed=3, stdv=0.02)
     ctx.set_cold_threads(cold_threads)
     ctx.finalize()
+    ctx.set_draft_window(draft)
     synth = abi.TraceSynth(cfg)
     S = warmup + 2 * steps
     logits = torch.empty((S, L, T, N), dtype=torch.float64)
@@ -82,7 +83,7 @@ def run_ratio(w, ratio, steps, warmup, cold_threads, profile):
             "cold_experts_per_step": sum(r.cold_experts for r in trep) / len(trep),
             "cold_host_ms_per_step": sum(r.cpu_ms_cold for r in trep) / len(trep),
             "k3_ms_per_step": sum(r.gpu_ms_ffn for r in trep) / len(trep),
-            "cold_threads": cold_threads,
+            "cold_threads": cold_threads, "draft_window": draft,
             "profile_ns": profile or "reference defaults (config.cpp:23-27)"}
     ctx.close()
     return line, summary, series
@@ -99,13 +100,14 @@ def main():
     ap.add_argument("--t-cpu-ns", type=int, default=0, help="HWB profile override: host time per miss token")
     ap.add_argument("--t-gpu-ns", type=int, default=0, help="HWB profile override: device time per hit expert")
     ap.add_argument("--t-io-ns", type=int, default=0, help="HWB profile override: load time per expert")
+    ap.add_argument("--draft-window", action="store_true", help="emulated gamma x t_draft window before each step")
     args = ap.parse_args()
     w = configs.CONFIGS[args.config]
     sums, series = [], []
     profile = {k: v for k, v in (("t_cpu_unit_ns", args.t_cpu_ns), ("t_gpu_unit_ns", args.t_gpu_ns),
                                  ("t_io_unit_ns", args.t_io_ns)) if v > 0}
     for r in [float(x) for x in args.ratios.split(",")]:
-        line, s, ser = run_ratio(w, r, args.steps, args.warmup, args.cold_threads, profile)
+        line, s, ser = run_ratio(w, r, args.steps, args.warmup, args.cold_threads, profile, args.draft_window)
         print(json.dumps(line), flush=True)
         sums.append(s)
         series.append(ser)

@@ -408,3 +408,26 @@ def test_persistent_k3_matches_per_layer_and_oracle(L, N, k, g, d, ffn, units):
         assert np.linalg.norm(fa - fb) <= 4e-3 * np.linalg.norm(fb), s
         assert [ra.cache_hits, ra.cache_misses] == [rb_.cache_hits, rb_.cache_misses]
     assert np.array_equal(a.sched_events(), b.sched_events())
+
+
+def test_draft_window_overlaps_loads_and_changes_nothing_else():
+    """The emulated draft window (γ·t_draft spin on the compute stream) adds
+    its time to the step and leaves every output and decision unchanged."""
+    L, N, k, g, d, ffn = 2, 16, 4, 6, 1024, 128
+    rng = np.random.default_rng(3)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    a, cfg = _make_ctx(L, N, k, g, d, ffn, 0, 0, 0.5, std, shared, abi.FFN_TENSOR, cold=0)
+    b, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, 0.5, std, shared, abi.FFN_TENSOR, cold=0)
+    b.set_draft_window(True)
+    b.set_timing(True)
+    T = g + 1
+    gen = O.Generator(L, N, k, g, seed=4)
+    for s in range(4):
+        logits, _, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        ha, hb = np.zeros_like(h0), np.zeros_like(h0)
+        a.step(logits, h0, acc, ha)
+        rb_, _ = b.step(logits, h0, acc, hb)
+        assert np.array_equal(ha, hb)
+        assert rb_.gpu_ms_total * 1e6 >= g * cfg.t_draft_unit_ns
+    assert np.array_equal(a.sched_events(), b.sched_events())
