@@ -337,7 +337,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     w = workload(args)
-    if world > 1:
+    if world > 1 and args.impl != "reference":  # the CPU reference arm needs no process group
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
