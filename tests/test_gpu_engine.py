@@ -70,6 +70,8 @@ def _resident(rb, l, N):
     (2, 32, 8, 8, 2048, 48, 0, 0, 0.5, abi.FFN_CUDACORE, 2),
     (2, 32, 8, 8, 2048, 128, 0, 0, 0.5, abi.FFN_TENSOR, -1),
     (2, 32, 8, 8, 2048, 128, 0, 0, 1.0, abi.FFN_TENSOR, -1),
+    (2, 16, 8, 15, 1024, 128, 1, 0, 0.5, abi.FFN_TENSOR, -1),  # T = 16 tokens, up to 16 per cold expert
+    (2, 8, 2, 4, 4096, 128, 0, 0, 0.5, abi.FFN_TENSOR, -1),    # per-segment K3 (d > 2048) + cold path
 ])
 def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, cold):
     ref_or_skip()
