@@ -312,7 +312,7 @@ def run_ours(args, w, rank, world, local_rank):
     out = {
         "ms": ms, "ms_e2e": ms_e2e, "ms_timed": ms_t, "tokens": tokens, "ffn_ms": ffn_ms, "ffn_bytes": ffn_bytes,
         "ffn_launches": sum(r.ffn_launches for r in reps), "launches": launches, "hits": hits, "misses": misses, "loads": loads,
-        "k3_kernel": ctx.k3_kernel(),
+        "k3_kernel": ctx.k3_kernel(), "parallel_mode": ctx.parallel_mode(),
         "h2d": float(np.mean([r.h2d_bytes for r in reps_e2e])), "d2h": float(np.mean([r.d2h_bytes for r in reps_e2e])),
         "router_ms": float(np.mean([r.gpu_ms_router for r in reps])),
         "hist_ms": float(np.mean([r.gpu_ms_hist for r in reps])),
@@ -403,6 +403,8 @@ def main():
                                "kernel": cap.get("kernel"), "report": cap.get("report")}
         except (ValueError, OSError, TypeError):
             traffic = None
+    if world > 1:
+        base["config"]["parallelism"] = ("units" if r["parallel_mode"] == "units" else "ep") + str(world)
     line = dict(base, value=tps, ms_per_step=r["ms"] / args.steps, scaling="strong" if world > 1 else "weak")
     line["e2e"] = {"value": r["tokens"] / (r["ms_e2e"] * 1e-3), "unit": "tokens/s",
                    "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])}

@@ -301,7 +301,21 @@ typedef struct moespac_model_desc {
   int32_t n_shared_units; /* shared experts expressed in units of d_ffn rows */
   int32_t gate_mode;      /* see moespac_router_topk */
   int32_t ffn_kernel;     /* MOESPAC_FFN_*; expert images use its layout */
+  int32_t parallel_mode;  /* world > 1 only — MOESPAC_PAR_*; see below */
 } moespac_model_desc;
+
+/* Multi-GPU modes (shard_world > 1 in moespac_ctx_create):
+ * EXPERT: expert e lives on rank e % world (its own slot pool, the
+ *   balancer solves tau on the global scores).
+ * UNITS: every rank holds every expert (the budget must cover all of them:
+ *   cache_ratio 1.0) and each layer's (expert, 8-row unit) work list is cut
+ *   across the ranks' K3 CTAs as one virtual grid, so the per-GPU work is
+ *   balanced whatever the routing; tensor-core K3 only.
+ * AUTO: UNITS when it applies, else EXPERT. Both combine with one
+ *   all-reduce (NCCL) of the per-rank partial outputs per layer. */
+#define MOESPAC_PAR_AUTO 0
+#define MOESPAC_PAR_EXPERT 1
+#define MOESPAC_PAR_UNITS 2
 
 typedef struct moespac_ctx moespac_ctx;
 
@@ -375,6 +389,9 @@ void* moespac_ctx_stream(const moespac_ctx* c);
 #define MOESPAC_K3_TC_TMEM 3
 #define MOESPAC_K3_GROUPED 4
 int moespac_ctx_k3_variant(const moespac_ctx* c);
+/* The multi-GPU mode the context resolved to (MOESPAC_PAR_EXPERT or
+ * MOESPAC_PAR_UNITS; MOESPAC_PAR_EXPERT for a single device). */
+int moespac_ctx_parallel_mode(const moespac_ctx* c);
 
 /* One verification step end to end with HOST buffers: H2D logits [L][T][N]
  * fp64 and h_in [T][d] bf16, run, D2H h_out [T][d] bf16 + the step's

@@ -113,7 +113,7 @@ class RunSummary(C.Structure):
 class ModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("n_shared_units", C.c_int32),
-                ("gate_mode", C.c_int32), ("ffn_kernel", C.c_int32)]
+                ("gate_mode", C.c_int32), ("ffn_kernel", C.c_int32), ("parallel_mode", C.c_int32)]
 
 
 class CtxViews(C.Structure):
@@ -192,6 +192,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_sched": (vp, [vp]),
         "moespac_ctx_stream": (vp, [vp]),
         "moespac_ctx_k3_variant": (C.c_int, [vp]),
+        "moespac_ctx_parallel_mode": (C.c_int, [vp]),
         "moespac_ctx_step_tables": (C.c_int, [vp, vp, vp, vp, vp]),
         "moespac_trace_synth_create": (C.c_int, [C.POINTER(SchedConfig), C.POINTER(vp)]),
         "moespac_trace_synth_next": (C.c_int, [vp, vp, vp]),
@@ -590,6 +591,9 @@ class Context:
     K3_NAMES = {0: "expert_ffn_kernel (K3, CUDA-core GEMV)", 1: "expert_ffn_tc_kernel (K3, smem accumulator)",
                 2: "expert_ffn_tc_kernel (K3, L2 accumulator)", 3: "expert_ffn_tc_kernel (K3, TMEM accumulator)",
                 4: "expert_ffn_tg_kernel (K3, grouped)"}
+
+    def parallel_mode(self) -> str:
+        return {1: "expert", 2: "units"}[lib().moespac_ctx_parallel_mode(self._h)]
 
     def k3_kernel(self) -> str:
         return self.K3_NAMES[lib().moespac_ctx_k3_variant(self._h)]

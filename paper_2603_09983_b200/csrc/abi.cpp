@@ -612,6 +612,10 @@ moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
 
 void* moespac_ctx_stream(const moespac_ctx* c) { return c->e.stream(); }
 
+int moespac_ctx_parallel_mode(const moespac_ctx* c) {
+  return c->e.unit_split() ? MOESPAC_PAR_UNITS : MOESPAC_PAR_EXPERT;
+}
+
 int moespac_ctx_k3_variant(const moespac_ctx* c) {
   if (c->e.ffn_kernel() != kFfnTensorCore) return MOESPAC_K3_CUDACORE;
   switch (c->e.ffn_acc_mode()) {

@@ -164,9 +164,19 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   sc.policy.fixed_down = c.fixed_down;
   sc.cache_ratio = c.cache_ratio;
   sc.ratio_smoothing = c.ratio_smoothing;
-  sc.shard_world = world;
+  // multi-GPU mode (moespac.h MOESPAC_PAR_*): expert-partitioned shards, or
+  // every expert on every rank with each layer's units split across them
+  const bool all_fit = layer_capacity_experts(c.cache_ratio, m.n_experts) >= m.n_experts;
+  const bool units_ok = world > 1 && kernel_ == kFfnTensorCore && all_fit;
+  if (m.parallel_mode == MOESPAC_PAR_UNITS && world > 1 && !units_ok)
+    throw std::invalid_argument("moespac_ctx: unit-split mode needs the tensor-core K3 and a cache budget covering "
+                                "every expert");
+  split_ = units_ok && m.parallel_mode != MOESPAC_PAR_EXPERT;
+  shard_rank_ = split_ ? 0 : rank;
+  shard_world_ = split_ ? 1 : world;
+  sc.shard_world = shard_world_;
   sched_ = std::make_unique<StepScheduler>(sc);
-  slots_ = sched_->slots_per_layer(rank);
+  slots_ = sched_->slots_per_layer(shard_rank_);
 
   int ndev = 0;
   check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -358,7 +368,7 @@ void Engine::finalize() {
   const std::vector<int32_t>& slot = sched_->slot_table();
   const int N = m_.n_experts;
   for (int l = 0; l < m_.n_layers; ++l)
-    for (int e = rank_; e < N; e += world_) {
+    for (int e = shard_rank_; e < N; e += shard_world_) {
       const int s = slot[static_cast<size_t>(l) * N + e];
       if (s < 0) continue;
       if (synthetic_)
@@ -375,7 +385,7 @@ void Engine::finalize() {
   decided_ = false;
   // Misses are possible when a shard holds fewer slots than experts: start
   // the host cold-expert executor (the CPU side of the HWB split).
-  const int shard_size = (m_.n_experts - rank_ + world_ - 1) / world_;
+  const int shard_size = (m_.n_experts - shard_rank_ + shard_world_ - 1) / shard_world_;
   const int threads = cold_threads_ < 0 ? static_cast<int>(std::max(1u, std::thread::hardware_concurrency()))
                                         : cold_threads_;
   if (threads > 0 && slots_ < shard_size)
@@ -543,8 +553,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     a2.adaptive = ec.adaptive_boundaries ? 1 : 0;
     a2.forgetting = ec.forgetting;
   }
-  a2.shard_rank = rank_;
-  a2.shard_world = world_;
+  a2.shard_rank = shard_rank_;
+  a2.shard_world = shard_world_;
   a2.freqs = freqs_d_;
   a2.offsets = offsets_d_;
   a2.perm = perm_d_;
@@ -592,7 +602,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       for (; i < loads.size() && loads[i].layer == l; ++i) {
         const SlotLoad& ld = loads[i];
         ++layer_loads[static_cast<size_t>(l)];
-        if (ld.shard != rank_) continue;
+        if (ld.shard != shard_rank_) continue;
         ++layer_loads_local[static_cast<size_t>(l)];
         check(cudaMemcpyAsync(slot_ptr(l, ld.slot), arena_h_ + image_of(l, ld.expert) * image_elems_,
                               image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
@@ -603,7 +613,9 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     }
   }
   if (timing_) check(cudaEventRecord(copy_ev_[1], copy_), "event");
-  const int n_shared_eff = (world_ > 1 && rank_ != 0) ? 0 : m_.n_shared_units;
+  // shared units: rank 0 in the expert-partitioned mode; in the unit-split
+  // mode they are units of the split work list like any expert's
+  const int n_shared_eff = (world_ > 1 && !split_ && rank_ != 0) ? 0 : m_.n_shared_units;
   const bool tc = kernel_ == kFfnTensorCore;
   uint16_t* hT[2] = {hT_d_, hT_d_ + static_cast<size_t>(16) * d};
   if (tc) check(launch_build_hT(h_d_, T_, d, hT[0], compute_), "build_hT");
@@ -638,6 +650,10 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.global_acc = global_acc_ ? 1 : 0;
     fa.acc_mode = acc_mode_;
     fa.hT = hT[l & 1];
+    if (split_) {
+      fa.cta_base = rank_ * sms_;
+      fa.cta_total = world_ * sms_;
+    }
     if (k3_trace_) fa.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
     if (tc && l + 1 < L && l2_prefetch_ > 0) {
       fa.nx_counters = counters_d + static_cast<size_t>(l + 1) * 8;
@@ -670,6 +686,11 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.grid = sms_;
     ca.per_cta = tc && acc_mode_ == 3 ? 1 : 0;
     ca.unit_rows = tc ? 8 : 16;
+    if (split_) {
+      ca.cta_base = rank_ * sms_;
+      ca.grid = world_ * sms_;
+      ca.grid_local = sms_;
+    }
     if (k3_trace_) ca.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
     ca.partial = work_d_;
     float* yl = y_d_ + static_cast<size_t>(l) * T_ * d;
@@ -773,7 +794,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       const uint32_t* res = rb + static_cast<size_t>(l) * W_;
       const int32_t* il = ids_h + static_cast<size_t>(l) * T_ * k;
       const float* gl = gates_h + static_cast<size_t>(l) * T_ * k;
-      for (int e = rank_; e < N; e += world_) {  // this rank's shard of the misses
+      for (int e = shard_rank_; e < N; e += shard_world_) {  // this rank's shard of the misses
         if ((res[e >> 5] >> (e & 31)) & 1u) continue;
         ColdItem it{};
         it.image = arena_h_ + image_of(l, e) * image_elems_;

@@ -94,6 +94,7 @@ class Engine {
   void step_tables(int32_t* taus, uint32_t* rb, uint32_t* lb, int32_t* slots) const;
   int ffn_kernel() const { return kernel_; }
   int ffn_acc_mode() const { return acc_mode_; }
+  bool unit_split() const { return split_; }
   const StepScheduler& sched() const { return *sched_; }
   void* stream() const { return compute_; }
 
@@ -108,6 +109,10 @@ class Engine {
 
   int kernel_ = 0;
   int device_ = 0, rank_ = 0, world_ = 1, sms_ = 148, T_ = 0, W_ = 1, stages_ = 6;
+  // expert shard of this rank: (rank, world) in the expert-partitioned mode,
+  // (0, 1) in the unit-split mode (every expert on every rank)
+  int shard_rank_ = 0, shard_world_ = 1;
+  bool split_ = false;
   size_t ffn_smem_ = 0;
   moespac_model_desc m_{};
   std::unique_ptr<StepScheduler> sched_;

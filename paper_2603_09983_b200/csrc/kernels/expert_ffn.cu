@@ -458,6 +458,8 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
   const int n_hits = a.counters[7];
   const int n = (n_hits + a.n_shared) * qpe;
   const int G = a.grid;
+  // unit-split mode: only this GPU's K3 CTAs [cb0, cb1) of the virtual grid
+  const int cb0 = a.cta_base, cb1 = a.grid_local > 0 ? a.cta_base + a.grid_local : G;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (n > 0 && c < a.d) {
     // 1) this warp's partial rows, in the fixed order (experts ascending,
@@ -471,13 +473,13 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
       const int hi = (((o + 1) * qpe) * G - 1) / n;
       for (int b = lo; b <= hi; ++b) {
         // with fewer work units than CTAs some CTAs own nothing
-        if ((b * n) / G == ((b + 1) * n) / G) continue;
+        if ((b * n) / G == ((b + 1) * n) / G || b < cb0 || b >= cb1) continue;
         if (a.per_cta) {
           if (b <= last_b) continue;
           last_b = b;
         }
         if ((idx++ % COMBINE_WARPS) != warp) continue;
-        if (lane == 0 && my_n < COMBINE_LIST) rows[warp][my_n] = a.per_cta ? b : b + o;
+        if (lane == 0 && my_n < COMBINE_LIST) rows[warp][my_n] = a.per_cta ? b - cb0 : b - cb0 + o;
         ++my_n;
       }
     };
@@ -515,13 +517,13 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
         const int lo = ((o * qpe + 1) * G - 1) / n;
         const int hi = (((o + 1) * qpe) * G - 1) / n;
         for (int b = lo; b <= hi; ++b) {
-          if ((b * n) / G == ((b + 1) * n) / G) continue;
+          if ((b * n) / G == ((b + 1) * n) / G || b < cb0 || b >= cb1) continue;
           if (a.per_cta) {
             if (b <= last_b) continue;
             last_b = b;
           }
           if ((idx++ % COMBINE_WARPS) != warp) continue;
-          const float4 v = __ldcg(row_ptr(a.per_cta ? b : b + o));
+          const float4 v = __ldcg(row_ptr(a.per_cta ? b - cb0 : b - cb0 + o));
           acc.x += v.x;
           acc.y += v.y;
           acc.z += v.z;

@@ -208,9 +208,13 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   }
   const int n_hits = a.counters[7];
   const long long n = static_cast<long long>(n_hits + a.n_shared) * upe;
-  const int G = gridDim.x, b = blockIdx.x;
-  const long long u0 = n > 0 ? (b * n) / G : 0;
-  const long long u1 = n > 0 ? ((b + 1) * n) / G : 0;
+  // b: this CTA's partial block (local); bg / G: its share of the layer's
+  // units (a virtual grid across GPUs in the unit-split mode)
+  const int b = blockIdx.x;
+  const int G = a.cta_total > 0 ? a.cta_total : static_cast<int>(gridDim.x);
+  const long long bg = a.cta_base + b;
+  const long long u0 = n > 0 ? (bg * n) / G : 0;
+  const long long u1 = n > 0 ? ((bg + 1) * n) / G : 0;
   if (u0 >= u1) return;
   const int o_first = static_cast<int>(u0 / upe);
   const int n_ent = static_cast<int>((u1 - 1) / upe) - o_first + 1;
@@ -352,7 +356,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       // through this launch's tail and the layer handoff)
       const int nh = a.nx_counters[7];
       const long long nn = static_cast<long long>(nh + a.n_shared) * upe;
-      const long long p0 = nn > 0 ? (b * nn) / G : 0, p1 = nn > 0 ? ((b + 1) * nn) / G : 0;
+      const long long p0 = nn > 0 ? (bg * nn) / G : 0, p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
       GroupIt pit{p0, p1, upe};
       Grp pg;
       long long budget = a.pf_bytes;

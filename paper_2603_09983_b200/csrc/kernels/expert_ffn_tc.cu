@@ -217,9 +217,13 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
   }
   const int n_hits = a.counters[7];
   const long long n = static_cast<long long>(n_hits + a.n_shared) * qpe;
-  const int G = gridDim.x, b = blockIdx.x;
-  const long long q0 = n > 0 ? (b * n) / G : 0;
-  const long long q1 = n > 0 ? ((b + 1) * n) / G : 0;
+  // b: this CTA's partial blocks (local); bg / G: its share of the layer's
+  // units (a virtual grid across GPUs in the unit-split mode)
+  const int b = blockIdx.x;
+  const int G = a.cta_total > 0 ? a.cta_total : static_cast<int>(gridDim.x);
+  const long long bg = a.cta_base + b;
+  const long long q0 = n > 0 ? (bg * n) / G : 0;
+  const long long q1 = n > 0 ? ((bg + 1) * n) / G : 0;
   if (q0 >= q1) return;
 
   if (tid == 0) {
@@ -446,8 +450,8 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         // gate/up runs, then their down runs, up to the byte budget.
         const int nh = a.nx_counters[7];
         const long long nn = static_cast<long long>(nh + a.n_shared) * qpe;
-        const long long p0 = nn > 0 ? (static_cast<long long>(blockIdx.x) * nn) / gridDim.x : 0;
-        const long long p1 = nn > 0 ? (static_cast<long long>(blockIdx.x + 1) * nn) / gridDim.x : 0;
+        const long long p0 = nn > 0 ? (bg * nn) / G : 0;
+        const long long p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
         SegIter pit{p0, p1, qpe};
         Seg s;
         long long budget = a.pf_bytes;

@@ -59,6 +59,10 @@ struct FfnArgs {
   const uint16_t* nx_pool;
   const uint16_t* nx_shared_w;
   int pf_bytes;
+  // unit-split multi-GPU mode: this launch's CTAs are [cta_base, cta_base +
+  // grid) of a virtual grid of cta_total CTAs over the layer's work units
+  // (cta_total 0: the launch grid itself)
+  int cta_base, cta_total;
 };
 
 // Persistent grouped K3 (expert_ffn_persistent.cu): every layer of a step in
@@ -97,6 +101,7 @@ struct CombineArgs {
   int grid;                 // K3 grid size
   int per_cta;              // 1: one partial block per K3 CTA (grouped K3), else per (CTA, entry) pair
   int unit_rows;            // ffn rows per K3 work unit: 8 (tensor-core K3s) or 16 (CUDA-core K3)
+  int cta_base, grid_local; // unit-split mode: the K3 launch was CTAs [cta_base, cta_base + grid_local) of `grid`
   const float* partial;
   float* y_out;             // [T][d] fp32 (may be null)
   uint16_t* h_out;          // [T][d] bf16 (may be null)

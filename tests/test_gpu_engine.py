@@ -296,13 +296,16 @@ def test_model_mode_needs_cold_path_off():
     assert ei.value.code == "E_LOGIC"
 
 
-@pytest.mark.parametrize("world,cache,kernel,cold", [
-    (2, 1.0, abi.FFN_TENSOR, 0),
-    (2, 0.5, abi.FFN_TENSOR, -1),
-    (3, 0.5, abi.FFN_TENSOR, 0),
-    (2, 0.5, abi.FFN_CUDACORE, 0),
+@pytest.mark.parametrize("world,cache,kernel,cold,mode", [
+    (2, 1.0, abi.FFN_TENSOR, 0, 1),
+    (2, 0.5, abi.FFN_TENSOR, -1, 0),
+    (3, 0.5, abi.FFN_TENSOR, 0, 0),
+    (2, 0.5, abi.FFN_CUDACORE, 0, 0),
+    (2, 1.0, abi.FFN_TENSOR, 0, 0),     # auto -> unit split (every expert fits)
+    (3, 1.0, abi.FFN_TENSOR, -1, 2),    # unit split, grouped K3
+    (2, 1.0, abi.FFN_TENSOR, 0, 2),     # unit split with d > 2048 (per-segment K3), below
 ])
-def test_expert_parallel_device_path(world, cache, kernel, cold):
+def test_expert_parallel_device_path(world, cache, kernel, cold, mode):
     """Expert-parallel mode on one GPU: `world` contexts
     (expert e on rank e % world, shared units on rank 0), one host thread
     each, exchanging per-layer partial outputs through the in-process
@@ -311,6 +314,8 @@ def test_expert_parallel_device_path(world, cache, kernel, cold):
     resident on any rank (+ the host cold path when on)."""
     import threading
     L, N, k, g, d, ffn, units = 2, 16, 4, 6, 1024, 128, 1
+    if (world, mode) == (2, 2) and cold == 0:
+        d = 4096  # the per-segment K3 in the unit-split mode
     rng = np.random.default_rng(world * 10 + int(cache * 10))
     std, shared = _experts(rng, L, N, d, ffn, units)
     T = g + 1
@@ -319,7 +324,7 @@ def test_expert_parallel_device_path(world, cache, kernel, cold):
     for r in range(world):
         cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache)
         kern = abi.ffn_resolve(kernel, d, ffn)
-        ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, 0, kern), cfg, r, world)
+        ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, 0, kern, mode), cfg, r, world)
         ctx.set_cold_threads(cold)
         arena = ctx.host_arena(L * N)
         for (l, e), w in std.items():
