@@ -7,6 +7,9 @@ Mixtral and Qwen3 renormalise over the top-k (Eq. 3, gate_mode 0);
 Qwen1.5-MoE and DeepSeek-V2-Lite take the softmax over all N (gate_mode 1).
 Shared experts are expressed as units of d_ffn rows (Qwen1.5: one 5632-row
 shared expert = 4 units of 1408; DeepSeek-V2-Lite: 2 x 1408 = 2 units).
+DeepSeek-V2-Lite's first layer is dense in the real model; BASELINE.json
+names 27 layers and all 27 are modeled as MoE layers here (one layer more of
+expert work than the model has).
 """
 from __future__ import annotations
 
