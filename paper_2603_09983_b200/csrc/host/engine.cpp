@@ -186,12 +186,10 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
   if (prop.major != 10) throw CudaError("moespac requires an sm_100 (B200) device");
   sms_ = prop.multiProcessorCount;
-  // profiling knobs: MOESPAC_FFN_ACCUM (accumulator selector, see
-  // moespac_ffn_args::accum), MOESPAC_SMEM_SLACK (bytes kept free per SM)
+  // profiling knob: MOESPAC_FFN_ACCUM (accumulator selector, see
+  // moespac_ffn_args::accum); DESIGN.md §5 lists the others
   if (const char* e = std::getenv("MOESPAC_FFN_ACCUM")) ffn_accum_ = std::atoi(e);
-  size_t smem_optin = prop.sharedMemPerBlockOptin;
-  if (const char* e = std::getenv("MOESPAC_SMEM_SLACK"))
-    smem_optin = std::min<size_t>(smem_optin, 233472 - 1024 - 4096) - static_cast<size_t>(std::atoi(e));
+  const size_t smem_optin = prop.sharedMemPerBlockOptin;
   FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, smem_optin, ffn_accum_)
                                            : ffn_plan(T_, m.d_model, smem_optin);
   if (kernel_ == kFfnTensorCore && plan.acc_mode == 3 &&
