@@ -371,11 +371,12 @@ moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
  * following step's tensor-core K3 launches fill with per-CTA %globaltimer
  * stamps and wait counters (layer l at offset l*grid*32), or NULL to stop. */
 moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf);
-/* Cross-layer L2 prefetch budget per K3 CTA in bytes (tensor-core K3; 0 = off,
- * default 0 = off: measured no gain on the BASELINE shapes): after its last
- * weight copy, each CTA prefetches into L2
- * the start of its next-layer work so HBM stays busy through the launch tail
- * and the layer handoff. */
+/* Cross-layer L2 prefetch budget per K3 CTA in bytes (tensor-core K3; 0 =
+ * off): after its last weight copy, each CTA prefetches into L2 the part of
+ * its next-layer work that follows the next CTA's own ring fill, so HBM
+ * keeps working through the launch tail and the layer handoff. Default: 128
+ * KiB for the grouped K3 (d <= 2048; -2.5 to -3% step time measured), 0 for
+ * the per-segment K3 (no gain on the Mixtral shape). */
 moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a
  * step runs on it, so events recorded there bracket whole steps. */

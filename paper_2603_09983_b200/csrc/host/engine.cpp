@@ -653,13 +653,18 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       fa.cta_total = world_ * sms_;
     }
     if (k3_trace_) fa.dbg = k3_trace_ + static_cast<size_t>(l) * sms_ * 32;
-    if (tc && l + 1 < L && l2_prefetch_ > 0) {
+    // next-layer L2 prefetch (bytes per CTA past the next CTA's own ring
+    // fill): default 128 KiB for the grouped K3, where it measured -2.5 to
+    // -3% step time (Qwen3 / DeepSeek-V2-Lite / Qwen1.5 shapes); 0 for the
+    // per-segment K3 (no gain on the Mixtral shape)
+    const int pf = l2_prefetch_ >= 0 ? l2_prefetch_ : (acc_mode_ == 3 ? 131072 : 0);
+    if (tc && l + 1 < L && pf > 0) {
       fa.nx_counters = counters_d + static_cast<size_t>(l + 1) * 8;
       fa.nx_hit_list = hit_list_d_ + static_cast<size_t>(l + 1) * N;
       fa.nx_slot_of = slots_d + static_cast<size_t>(l + 1) * N;
       fa.nx_pool = pool_ + static_cast<int64_t>(l + 1) * slots_ * image_elems_;
       fa.nx_shared_w = shared_ + static_cast<int64_t>(l + 1) * m_.n_shared_units * image_elems_;
-      fa.pf_bytes = l2_prefetch_;
+      fa.pf_bytes = pf;
     }
     if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
     check(tc ? launch_expert_ffn_tc(fa, sms_, ffn_smem_, compute_, pdl)

@@ -147,7 +147,7 @@ class Engine {
   bool decided_ = false;  // next step's decisions already made
   bool pdl_ = true;                         // programmatic dependent launch between layer kernels
   unsigned long long* k3_trace_ = nullptr;  // profiling: [L][grid][32]
-  int l2_prefetch_ = 0;  // per-CTA next-layer L2 prefetch (bytes); measured no gain, off
+  int l2_prefetch_ = -1;  // per-CTA next-layer L2 prefetch (bytes); -1: per-kernel default
   int cold_threads_ = -1;
   bool cold_trace_ = false;  // MOESPAC_COLD_TRACE: per-step host timing of the cold path on stderr
   int ffn_accum_ = 0;

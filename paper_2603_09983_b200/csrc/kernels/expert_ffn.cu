@@ -425,7 +425,7 @@ struct CombineSmem {
 
 template <int WARPS>
 __device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, const float4 (*red)[32], int t,
-                                              int c, int lane);
+                                              int c, uint2 hv, float4 ex);
 
 // (<= 112 registers: see expert_ffn_tc_kernel)
 template <int WARPS>
@@ -461,6 +461,16 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
   // unit-split mode: only this GPU's K3 CTAs [cb0, cb1) of the virtual grid
   const int cb0 = a.cta_base, cb1 = a.grid_local > 0 ? a.cta_base + a.grid_local : G;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  // warp 0's residual and host-cold inputs, loaded right after the wait
+  // (alongside the partial rows, not after the sums)
+  uint2 hv = make_uint2(0u, 0u);
+  float4 ex = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto preload = [&]() {
+    if (warp != 0 || c >= a.d) return;
+    const size_t off = static_cast<size_t>(t) * a.d + c;
+    if (a.h_out && a.h_in) hv = __ldcg(reinterpret_cast<const uint2*>(a.h_in + off));
+    if (a.y_extra) ex = __ldcg(reinterpret_cast<const float4*>(a.y_extra + off));
+  };
   if (n > 0 && c < a.d) {
     // 1) this warp's partial rows, in the fixed order (experts ascending,
     //    covering CTAs ascending, dealt round-robin to the warps)
@@ -490,6 +500,7 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
     for (int sidx = 0; sidx < a.n_shared; ++sidx) list_entry(n_hits + sidx);
     __syncwarp();
     pdl_wait();  // partials of the K3 launch just before
+    preload();
     stamp(27);
     auto row_ptr = [&](int r) {
       return reinterpret_cast<const float4*>(a.partial + (static_cast<long long>(r) * a.T + t) * a.d + c);
@@ -537,19 +548,24 @@ __global__ void __launch_bounds__(WARPS * 32) combine_kernel(CombineArgs a) {
       for (int sidx = 0; sidx < a.n_shared; ++sidx) add_entry(n_hits + sidx);
     }
   }
-  if (!(n > 0 && c < a.d)) pdl_wait();  // (no partials to read; still order after K3)
+  if (!(n > 0 && c < a.d)) {  // (no partials to read; still order after K3)
+    pdl_wait();
+    preload();
+  }
   __syncthreads();  // every warp is past its row list (the sums reuse that memory)
   sm.red[warp][lane] = acc;
   __syncthreads();
   stamp(28);
   if (warp != 0 || c >= a.d) return;
-  combine_store<WARPS>(a, acc, sm.red, t, c, lane);
+  combine_store<WARPS>(a, acc, sm.red, t, c, hv, ex);
+  if (lane == 0) stamp(30);
 }
 
 // warp 0 of a combine CTA: cross-warp sum, y / residual / bf16 / h^T stores
 template <int WARPS>
 __device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, const float4 (*red)[32], int t,
-                                              int c, int lane) {
+                                              int c, uint2 hv, float4 ex) {
+  const int lane = threadIdx.x & 31;
   for (int w = 1; w < WARPS; ++w) {
     const float4 v = red[w][lane];
     acc.x += v.x;
@@ -559,17 +575,15 @@ __device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, 
   }
   const size_t off = static_cast<size_t>(t) * a.d + c;
   if (a.y_extra) {  // cold experts computed on the host (added after the fixed-order device sum)
-    const float4 e = *reinterpret_cast<const float4*>(a.y_extra + off);
-    acc.x += e.x;
-    acc.y += e.y;
-    acc.z += e.z;
-    acc.w += e.w;
+    acc.x += ex.x;
+    acc.y += ex.y;
+    acc.z += ex.z;
+    acc.w += ex.w;
   }
   if (a.y_out) *reinterpret_cast<float4*>(a.y_out + off) = acc;
   if (a.h_out) {
     float4 r = acc;
     if (a.h_in) {
-      const uint2 hv = *reinterpret_cast<const uint2*>(a.h_in + off);
       r.x += bf_lo(hv.x);
       r.y += bf_hi(hv.x);
       r.z += bf_lo(hv.y);

@@ -359,7 +359,9 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       const long long p0 = nn > 0 ? (bg * nn) / G : 0, p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
       GroupIt pit{p0, p1, upe};
       Grp pg;
-      long long budget = a.pf_bytes;
+      // the next CTA fills its ring with the first ring_bytes itself right
+      // after entry; prefetch what follows (approximately: group order)
+      long long budget = a.pf_bytes, skip = RB;
       while (budget > 0 && pit.next(pg)) {
         for (int i = 0; i < pg.np && budget > 0; ++i) {
           const int o = pg.o[i];
@@ -368,6 +370,10 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           const uint8_t* base = reinterpret_cast<const uint8_t*>(w) + pg.c[i] * chunk_bytes + pg.pa[i] * UB;
           const uint32_t run = static_cast<uint32_t>(pg.n[i]) * UB;
           for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
+            if (skip > 0) {
+              skip -= run;
+              continue;
+            }
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE), "r"(run)
                          : "memory");
             budget -= run;
@@ -519,6 +525,10 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         a.dbg[blockIdx.x * DBG + 10] = static_cast<unsigned long long>(w_at);
         a.dbg[blockIdx.x * DBG + 12] = static_cast<unsigned long long>(w_d1e);
       }
+      named_bar_sync(3, EPI_THREADS + 32);  // the epilogue has drained D2
+      fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+      if (lane == 0) stamp(a, 23);
     } else {
       // ------------------------------------------------ epilogue (4 warps)
       pdl_wait();  // partial blocks are still being read by the previous combine
@@ -614,7 +624,9 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       }
       fence_before();
       fence_proxy_async();
-      named_bar_sync(2, EPI_THREADS);
+      // TMEM is dead past this barrier: warp 1 (also arriving) deallocates it
+      // while the partial rows are stored (it used to wait for CTA exit)
+      named_bar_sync(3, EPI_THREADS + 32);
       if (et == 0) stamp(a, 19);
       if (q == 0 && lane < T) {  // one lane per token row
         if ((tmask >> lane) & 1u)
@@ -630,15 +642,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     }
   }
   __syncwarp();  // bar.sync is warp-aligned: a warp arriving in pieces is counted once per piece
-  fence_before();
   __syncthreads();
   if (tid == 0) stamp(a, 6);
-  if (warp == 1) {
-    fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(static_cast<uint32_t>(misc[1])),
-                 "r"(TMEM_COLS));
-    if (lane == 0) stamp(a, 23);
-  }
 }
 
 }  // namespace tg

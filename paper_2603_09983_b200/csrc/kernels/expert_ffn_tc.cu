@@ -454,7 +454,8 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         const long long p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
         SegIter pit{p0, p1, qpe};
         Seg s;
-        long long budget = a.pf_bytes;
+        // (the next CTA fills its ring with the first ring_bytes itself)
+        long long budget = a.pf_bytes, skip = RB;
         while (budget > 0 && pit.next(s)) {
           const uint16_t* w = s.o < nh ? a.nx_pool + static_cast<long long>(a.nx_slot_of[a.nx_hit_list[s.o]]) *
                                                           a.expert_elems
@@ -463,6 +464,10 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           const int nq = s.qb - s.qa;
           const uint32_t run = static_cast<uint32_t>(nq) * UBYTES;
           for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
+            if (skip > 0) {
+              skip -= run;
+              continue;
+            }
             if (leader)
               asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * A_BYTES +
                                                                               s.qa * UBYTES),

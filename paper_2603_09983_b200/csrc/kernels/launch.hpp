@@ -50,8 +50,9 @@ struct FfnArgs {
   unsigned long long* dbg;  // optional per-CTA profiling record [grid][32]
   int l2_policy;            // weight stream L2 policy: 0 evict_first, 1 evict_normal
   // Next layer (tensor-core kernel): once a CTA has issued its last weight
-  // copy it prefetches into L2 the first pf_bytes of what the same CTA
-  // index will stream in the next layer, so HBM keeps working through this
+  // copy it prefetches into L2 pf_bytes of what the same CTA index will
+  // stream in the next layer — skipping the first ring_bytes, which that CTA
+  // loads into its ring itself on entry — so HBM keeps working through this
   // launch's tail and the layer-to-layer handoff. nx_counters == null: off.
   const int32_t* nx_counters;
   const int32_t* nx_hit_list;

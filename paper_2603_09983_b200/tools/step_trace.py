@@ -119,6 +119,19 @@ def main():
                       "first_data_pct_us": [round(float(np.percentile(first, p)), 2) for p in (0, 50, 100)],
                       "slowest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(-ends)[:8]],
                       "fastest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(ends)[:8]]}))
+    # where the K3 roles waited (clock64 cycles accumulated in debug slots
+    # 8-14) as a fraction of the CTA's lifetime, median over CTAs, plus the
+    # part of the lifetime after the predecessor wait
+    life_ns = x[:, 6] - x[:, 0]
+    cyc = np.maximum(life_ns * 1.965, 1.0)  # ns -> SM cycles at the boost clock
+    act_m = x[:, 0] > 0
+    waits = {nm: round(float(np.median(x[act_m, j] / cyc[act_m])), 3) for j, nm in
+             [(8, "producer_ring_full"), (9, "mma_wait_data"), (10, "mma_wait_aT"), (12, "mma_wait_d1_free"),
+              (13, "epi_wait_d1"), (14, "epi_wait_d2")]}
+    post = (x[act_m, 6] - x[act_m, 22]) / 1e3
+    print(json.dumps({"layer": lm, "wait_frac_of_cta_life": waits,
+                      "cta_life_us_med": round(float(np.median(life_ns[act_m])) / 1e3, 2),
+                      "after_pred_us_pct": [round(float(np.percentile(post, p_)), 2) for p_ in (0, 50, 100)]}))
     # per-SM lateness across layers: is the tail a property of the SM?
     late = {}
     for l in range(L):
@@ -162,10 +175,12 @@ def main():
                                                                 for j in (0, 2, 3, 4, 17, 18, 19, 20, 21, 22, 23, 25) if (xs[:, j] > 0).any()}}))
         dz = t[lm][:, 23] > 0
         if dz.any():
-            print(json.dumps({"layer": lm, "dealloc_minus_end_us_pct": [round(float(np.percentile((t[lm][dz, 23] - t[lm][dz, 6]) / 1e3, p_)), 2) for p_ in (0, 50, 100)],
-                              "predealloc_minus_end_us_pct": [round(float(np.percentile((t[lm][dz, 25] - t[lm][dz, 6]) / 1e3, p_)), 2) for p_ in (0, 50, 100)]}))
+            print(json.dumps({"layer": lm, "dealloc_minus_end_us_pct": [round(float(np.percentile((t[lm][dz, 23] - t[lm][dz, 6]) / 1e3, p_)), 2) for p_ in (0, 50, 100)]}))
+        cs = t[lm][:, 30] > 0
         print(json.dumps({"layer": lm, "combine_ctas": int(cb.sum()), "combine_start_rel_k3_end": rel(26),
-                          "combine_pred_rel_k3_end": rel(27), "combine_end_rel_k3_end": rel(28)}))
+                          "combine_pred_rel_k3_end": rel(27), "combine_sums_rel_k3_end": rel(28),
+                          "combine_stored_rel_k3_end": [round(float(np.percentile((t[lm][cs, 30] - kend) / 1e3, p_)), 2)
+                                                        for p_ in (0, 50, 100)] if cs.any() else None}))
     gaps = [r["gap_to_next_us"] for r in rows if "gap_to_next_us" in r]
     spans = [r["k3_span_us"] for r in rows if "k3_span_us" in r]
     print(json.dumps({"config": args.config, "pf": args.pf, "timed_step_ms": round(step_ms, 4),
