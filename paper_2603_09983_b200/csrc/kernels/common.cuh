@@ -94,6 +94,14 @@ __device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 
+// the same rounding for finite values as f32_to_bf16_rn, one instruction
+// (NaN becomes the canonical 0x7fff)
+__device__ __forceinline__ uint16_t f32_to_bf16_cvt(float f) {
+  uint16_t r;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(f));
+  return r;
+}
+
 }  // namespace dev
 
 // Launch with the programmatic-stream-serialization attribute (kernels call

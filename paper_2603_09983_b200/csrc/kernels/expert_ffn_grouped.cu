@@ -108,7 +108,7 @@ __device__ __forceinline__ int pow2_divisor(int x, int cap) {
 // (capped by the power-of-two divisor of the tile count), so the
 // single-warp producer/MMA bookkeeping per entry is amortised
 __device__ __forceinline__ int tiles_per_entry(int nu, int cap) {
-  const int t = nu >= 8 ? 2 : (nu >= 4 ? 4 : 8);
+  const int t = nu >= 8 ? 2 : (nu >= 4 ? 4 : (nu >= 2 ? 8 : 16));
   return t < cap ? t : cap;
 }
 struct Geom {
@@ -156,9 +156,11 @@ __device__ __forceinline__ void bulk_s2g(void* gmem_dst, const void* smem_src, u
                "r"(smem_u32(smem_src)), "r"(bytes)
                : "memory");
 }
+// (the source reads only: kernel completion makes the writes visible to the
+// dependent combine)
 __device__ __forceinline__ void bulk_commit_wait_all() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // <= 200 registers so a 4-warp combine CTA still fits next to this CTA
@@ -239,7 +241,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   __syncthreads();
   if (tid == 0) pdl_trigger();  // the combine may launch and park on its own wait
 
-  const int kcap = pow2_divisor(ktiles, 8), mcap = pow2_divisor(mtiles, 8);
+  const int kcap = pow2_divisor(ktiles, 16), mcap = pow2_divisor(mtiles, 16);
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     // Starts streaming weights right away (they do not depend on the
@@ -260,9 +262,9 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     bool waited = false;
     auto wait_pred = [&]() {
       pdl_wait();
-      if (leader) {
+      {  // one slice per lane: bulk copies issued by one thread serialise
         const uint8_t* hTb = reinterpret_cast<const uint8_t*>(a.hT);
-        for (int kt = 0; kt < ktiles; ++kt) {
+        for (int kt = lane; kt < ktiles; kt += 32) {
           mbar_arrive_expect_tx(&ht_full[kt], HTS);
           bulk_g2s(hts + kt * HTS, hTb + static_cast<size_t>(kt) * HTS, HTS, &ht_full[kt], pol_h);
         }
@@ -301,14 +303,20 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       pb[1] = reinterpret_cast<const uint8_t*>(b1) + static_cast<long long>(g.np > 1 ? g.c[1] : 0) * chunk_bytes;
     };
     // tiles [t0, t0 + m) (tile index within the chunk: K-tiles then M-tiles)
-    // of every piece, slot-packed: tile j of the entry at j * nu * 2 KiB
+    // of every piece, slot-packed: tile j of the entry at j * nu * 2 KiB.
+    // One copy per lane: a thread's bulk copies issue one after another
+    // (~0.1-0.3 us each, tools/tma_probe.cu), copies from different lanes
+    // overlap — with one issuing lane, split runs capped the stream at
+    // 8-40 GB/s per SM.
     auto copy_entry = [&](const Grp& g, const uint8_t* const (&pb)[2], int t0, int m, uint32_t e, uint64_t* bar) {
-      if (!leader) return;
       const uint32_t ab = static_cast<uint32_t>(g.nu) * UB;
       const uint32_t n0 = static_cast<uint32_t>(g.n[0]) * UB;
-      for (int j = 0; j < m; ++j) {
-        bulk_g2s(ring + e + j * ab, pb[0] + static_cast<size_t>(t0 + j) * TILE + g.pa[0] * UB, n0, bar, pol);
-        if (g.np > 1)
+      __syncwarp();  // after the leader's expect_tx
+      for (int c = lane; c < m * g.np; c += 32) {
+        const int j = g.np > 1 ? c >> 1 : c;
+        if (g.np == 1 || (c & 1) == 0)
+          bulk_g2s(ring + e + j * ab, pb[0] + static_cast<size_t>(t0 + j) * TILE + g.pa[0] * UB, n0, bar, pol);
+        else
           bulk_g2s(ring + e + j * ab + n0, pb[1] + static_cast<size_t>(t0 + j) * TILE,
                    static_cast<uint32_t>(g.n[1]) * UB, bar, pol);
       }
@@ -349,7 +357,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         if (more) piece_bases(cur, cb);
       }
     }
-    if (a.nx_counters && a.pf_bytes > 0 && leader) {
+    if (a.nx_counters && a.pf_bytes > 0) {
       // ---- cross-layer L2 prefetch: the next layer's routing is final (K2
       // ran for all layers), so walk what this CTA index streams next layer,
       // in stream order, and prefetch its runs into L2 (HBM otherwise idles
@@ -362,6 +370,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       // the next CTA fills its ring with the first ring_bytes itself right
       // after entry; prefetch what follows (approximately: group order)
       long long budget = a.pf_bytes, skip = RB;
+      int rc = 0;  // run counter: run r is issued by lane r % 32
       while (budget > 0 && pit.next(pg)) {
         for (int i = 0; i < pg.np && budget > 0; ++i) {
           const int o = pg.o[i];
@@ -374,8 +383,10 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
               skip -= run;
               continue;
             }
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE), "r"(run)
-                         : "memory");
+            if ((rc++ & 31) == lane)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE),
+                           "r"(run)
+                           : "memory");
             budget -= run;
           }
         }
@@ -544,15 +555,22 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         const int b1 = i & 1;
         wait_acc(a, &d1_full[b1], d1f[b1].bit, w_d1f);
         d1f[b1].flip();
+        if (i == 0 && et == 0) stamp(a, 17);
         fence_after();
         float v[16];
         tc::tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b1 * 16), v);
+        if (i == 0 && et == 0 && a.dbg) {  // after the TMEM data is in registers
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt) : "f"(v[0]), "f"(v[15]) : "memory");
+          a.dbg[blockIdx.x * DBG + 25] = tt;
+        }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&d1_empty[b1]);
         const int ab = i & 1;
         mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);  // DN(i-2) done with this buffer
         atf[ab].flip();
+        if (i == 0 && et == 0) stamp(a, 16);
         {
           // this warp's TMEM lanes are group slots 2q (lanes 0-15) and 2q+1
           // (lanes 16-31); in a slot, lanes 0-7 hold the gate rows of
@@ -566,25 +584,37 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           const int up = (lane >> 3) & 1;
           uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
           uint16_t* lo = hi + 2048;
+          float gts[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            if (t < T) {
-              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 8);
-              if ((t & 1) == up) {  // gate lanes even tokens, up lanes odd tokens
-                const float gv = up ? pv : v[t];
-                const float uv = up ? v[t] : pv;
-                const float gt = valid ? gs[t] : 0.f;
-                const float av = gt != 0.f ? __fdividef(gv, 1.f + __expf(-gv)) * uv * gt : 0.f;
-                const uint16_t h16 = f32_to_bf16_rn(av);
-                const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
-                // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
-                const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
-                hi[off] = h16;
-                lo[off] = f32_to_bf16_rn(rem);
-              }
-            }
+          for (int j = 0; j < 4; ++j) {
+            const float4 x = reinterpret_cast<const float4*>(gs)[j];
+            gts[4 * j] = x.x;
+            gts[4 * j + 1] = x.y;
+            gts[4 * j + 2] = x.z;
+            gts[4 * j + 3] = x.w;
+          }
+          // gate lanes take the even tokens, up lanes the odd ones: token
+          // t = 2j + up, its partner value crosses with one xor-8 shuffle.
+          // Branch-free (tokens >= T and unrouted entries select 0) so the
+          // eight independent chains interleave.
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int t = 2 * j + up;
+            const float pv = __shfl_xor_sync(0xffffffffu, up ? v[2 * j] : v[2 * j + 1], 8);
+            const float gv = up ? pv : v[2 * j];
+            const float uv = up ? v[2 * j + 1] : pv;
+            const float gt = up ? gts[2 * j + 1] : gts[2 * j];
+            const float sv = __fdividef(gv, 1.f + __expf(-gv)) * uv * gt;
+            const float av = (valid && t < T && gt != 0.f) ? sv : 0.f;
+            const uint16_t h16 = f32_to_bf16_cvt(av);
+            const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
+            // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
+            const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
+            hi[off] = h16;
+            lo[off] = f32_to_bf16_cvt(rem);
           }
         }
+        if (i == 0 && et == 0) stamp(a, 21);
         fence_proxy_async();
         named_bar_sync(2, EPI_THREADS);
         if (et == 0) {
@@ -603,23 +633,27 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       for (int r = 0; r < n_ent; ++r) tmask |= ent_mask[r];
       const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0);
       float* stg = reinterpret_cast<float*>(ring);
-      for (int mt = 0; mt < mtiles; mt += 2) {
-        uint32_t y0[16], y1[16];
-        const bool two = mt + 1 < mtiles;
-        if (T <= 8) {
-          tc::tmem_ld8_nw(tbase + static_cast<uint32_t>(mt * 16), y0);
-          if (two) tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + 1) * 16), y1);
-        } else {
-          tc::tmem_ld16_nw(tbase + static_cast<uint32_t>(mt * 16), y0);
-          if (two) tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + 1) * 16), y1);
-        }
+      // four M-tiles per tcgen05.wait::ld (mtiles is even; the drain is
+      // load-latency bound: one round trip per wait)
+      for (int mt = 0; mt < mtiles; mt += 4) {
+        uint32_t y[4][16];
+        const int nm = mtiles - mt < 4 ? mtiles - mt : 4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < nm) {
+            if (T <= 8)
+              tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + j) * 16), y[j]);
+            else
+              tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + j) * 16), y[j]);
+          }
         tc::tmem_wait_ld();
         float* r0 = stg + mt * 128 + 32 * q + lane;
 #pragma unroll
-        for (int t = 0; t < 16; ++t)
-          if (t < T) {
-            r0[static_cast<size_t>(t) * d] = __uint_as_float(y0[t]);
-            if (two) r0[static_cast<size_t>(t) * d + 128] = __uint_as_float(y1[t]);
+        for (int j = 0; j < 4; ++j)
+          if (j < nm) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+              if (t < T) r0[static_cast<size_t>(t) * d + 128 * j] = __uint_as_float(y[j][t]);
           }
       }
       fence_before();
@@ -663,13 +697,14 @@ bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid) {
 
 // Grouped mode: d <= 2048 (D2 for all d/128 M-tiles fits in TMEM columns
 // 256-511), the drain's [T][d] fp32 staging fits in the ring, and the ring
-// holds the widest entry window (44 KiB).
+// holds the widest entry window (58 KiB: 3 or 7 units x 8 or 4 tiles, the
+// last tile read as a full 16 KiB A operand).
 int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
   if (d > dev::tg::MAX_KT * 64 || d % 128 || T > 16) return 0;
   const size_t fixed = ffn_tg_smem_bytes(d, 0);
   if (fixed >= smem_limit) return 0;
   const int rb = static_cast<int>(((smem_limit - fixed) / 1024) * 1024);
-  const int need = static_cast<int>(T) * d * 4 > 45056 ? T * d * 4 : 45056;
+  const int need = static_cast<int>(T) * d * 4 > 59392 ? T * d * 4 : 59392;
   return rb >= need ? rb : 0;
 }
 

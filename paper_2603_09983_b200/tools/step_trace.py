@@ -111,10 +111,16 @@ def main():
     segs = np.array(segs)
     for nq in sorted(set(quarters.tolist())):
         m = quarters == nq
+        rel_med = {str(j): round(float(np.median((x[m, j] - base) / 1e3)), 2) for j in (2, 3, 17, 25, 16, 21, 4, 18, 19, 20)
+                   if (x[m, j] > 0).all()}
         print(json.dumps({"layer": lm, "units": nq, "ctas": int(m.sum()),
                           "end_us_med": round(float(np.median(ends[m])), 2),
                           "end_us_max": round(float(ends[m].max()), 2),
-                          "segs_mean": round(float(segs[m].mean()), 2)}))
+                          "segs_mean": round(float(segs[m].mean()), 2),
+                          "stamps_rel_pred_med": rel_med,
+                          "waits_cycles_med": {nm: float(np.median(x[m, j])) for j, nm in
+                                               [(8, "prod_ring_full"), (9, "mma_data"), (10, "mma_aT"),
+                                                (13, "epi_d1"), (14, "epi_d2")]}}))
     print(json.dumps({"layer": lm, "end_pct_us": [round(float(np.percentile(ends, p)), 2) for p in (0, 10, 50, 90, 100)],
                       "first_data_pct_us": [round(float(np.percentile(first, p)), 2) for p in (0, 50, 100)],
                       "slowest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(-ends)[:8]],
