@@ -121,6 +121,15 @@ def main():
                           "waits_cycles_med": {nm: float(np.median(x[m, j])) for j, nm in
                                                [(8, "prod_ring_full"), (9, "mma_data"), (10, "mma_aT"),
                                                 (13, "epi_d1"), (14, "epi_d2")]}}))
+    # end time by the CTA's start offset inside its first chunk (unit % 8)
+    # and its number of chunk pieces
+    by_shape = {}
+    for b in range(G):
+        q0 = (b * n_units) // G
+        key = f"start%8={q0 % 8},pieces={segs[b]}"
+        by_shape.setdefault(key, []).append(float(ends[b]))
+    print(json.dumps({"layer": lm, "end_us_by_shape": {k_: [len(v), round(float(np.median(v)), 2), round(max(v), 2)]
+                                                       for k_, v in sorted(by_shape.items())}}))
     print(json.dumps({"layer": lm, "end_pct_us": [round(float(np.percentile(ends, p)), 2) for p in (0, 10, 50, 90, 100)],
                       "first_data_pct_us": [round(float(np.percentile(first, p)), 2) for p in (0, 50, 100)],
                       "slowest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(-ends)[:8]],
