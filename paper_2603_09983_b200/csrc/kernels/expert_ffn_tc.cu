@@ -528,6 +528,10 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           if (leader) mma_commit(&d1_full[b1]);
           __syncwarp();
           if (i == 0 && leader) stamp(a, 3);
+          if (i < 5 && leader) {  // per-segment trace: GU(i) issued
+            const int gs[5] = {15, 19, 23, 25, 31};
+            stamp(a, gs[i]);
+          }
         }
         if (has_prev) {  // DN(i-1): D2 = W_down x a^T(i-1), hi + lo
           const int ab_ = (i - 1) & 1;
@@ -747,23 +751,33 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           const int up = (lane >> 3) & 1;
           uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
           uint16_t* lo = hi + 2048;
+          float gts[16];
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            if (t < T) {
-              const float pv = __shfl_xor_sync(0xffffffffu, v[t], 8);
-              if ((t & 1) == up) {  // gate lanes even tokens, up lanes odd tokens
-                const float g = up ? pv : v[t];
-                const float u = up ? v[t] : pv;
-                const float gt = inside ? gs[t] : 0.f;
-                const float av = gt != 0.f ? __fdividef(g, 1.f + __expf(-g)) * u * gt : 0.f;
-                const uint16_t h16 = f32_to_bf16_rn(av);
-                const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
-                // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
-                const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
-                hi[off] = h16;
-                lo[off] = f32_to_bf16_rn(rem);
-              }
-            }
+          for (int j = 0; j < 4; ++j) {
+            const float4 x = reinterpret_cast<const float4*>(gs)[j];
+            gts[4 * j] = x.x;
+            gts[4 * j + 1] = x.y;
+            gts[4 * j + 2] = x.z;
+            gts[4 * j + 3] = x.w;
+          }
+          // gate lanes take the even tokens, up lanes the odd ones (t = 2j +
+          // up), one xor-8 shuffle each; branch-free so the eight chains
+          // interleave (a serial branchy token loop took ~2 us per segment)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int t = 2 * j + up;
+            const float pv = __shfl_xor_sync(0xffffffffu, up ? v[2 * j] : v[2 * j + 1], 8);
+            const float g = up ? pv : v[2 * j];
+            const float u = up ? v[2 * j + 1] : pv;
+            const float gt = up ? gts[2 * j + 1] : gts[2 * j];
+            const float sv = __fdividef(g, 1.f + __expf(-g)) * u * gt;
+            const float av = (inside && t < T && gt != 0.f) ? sv : 0.f;
+            const uint16_t h16 = f32_to_bf16_cvt(av);
+            const float rem = av - __uint_as_float(static_cast<uint32_t>(h16) << 16);
+            // byte = j*256 + tg*128 + r*16 + e*2 (token = 8 tg + r, f = 8 j + e)
+            const int off = (f >> 3) * 128 + (t >> 3) * 64 + (t & 7) * 8 + (f & 7);
+            hi[off] = h16;
+            lo[off] = f32_to_bf16_cvt(rem);
           }
         }
         fence_proxy_async();
@@ -822,30 +836,39 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0 + pb * 128);
           float* P = a.partial + static_cast<long long>(b + prev.o) * T * d;
           const float* gsl = gate_s + seg_slot[(i - 1) & 1] * 16;
-          for (int mt = mt0; mt < mt_end; ++mt) {
-            // only the first T token columns matter
-            uint32_t y0[16];
-            if (T <= 8)
-              tmem_ld8_nw(tbase + static_cast<uint32_t>((mt - mt0) * 16), y0);
-            else
-              tmem_ld16_nw(tbase + static_cast<uint32_t>((mt - mt0) * 16), y0);
+          // four M-tiles per tcgen05.wait::ld (the drain is load-latency
+          // bound: one TMEM round trip per wait, ~4x fewer than per tile)
+          for (int mb = mt0; mb < mt_end; mb += 4) {
+            uint32_t y[4][16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (mb + j < mt_end) {  // only the first T token columns matter
+                if (T <= 8)
+                  tmem_ld8_nw(tbase + static_cast<uint32_t>((mb + j - mt0) * 16), y[j]);
+                else
+                  tmem_ld16_nw(tbase + static_cast<uint32_t>((mb + j - mt0) * 16), y[j]);
+              }
             tmem_wait_ld();
-            const int orow = mt * 128 + 32 * q + lane;
-            if (mode == ACC_GLOBAL) {
 #pragma unroll
-              for (int t = 0; t < 16; ++t)
-                if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += __uint_as_float(y0[t]);
-            } else {
-              // all loads, then all stores: the T read-modify-writes of a row
-              // are independent (a += chain would serialise on each LDS)
-              float* r0 = ysum + orow;
-              float o0[16];
+            for (int j = 0; j < 4; ++j) {
+              if (mb + j >= mt_end) break;
+              const int orow = (mb + j) * 128 + 32 * q + lane;
+              if (mode == ACC_GLOBAL) {
 #pragma unroll
-              for (int t = 0; t < 16; ++t)
-                if (t < T) o0[t] = r0[static_cast<size_t>(t) * d];
+                for (int t = 0; t < 16; ++t)
+                  if (t < T && gsl[t] != 0.f) P[static_cast<long long>(t) * d + orow] += __uint_as_float(y[j][t]);
+              } else {
+                // all loads, then all stores: the T read-modify-writes of a
+                // row are independent (a += chain would serialise on each LDS)
+                float* r0 = ysum + orow;
+                float o0[16];
 #pragma unroll
-              for (int t = 0; t < 16; ++t)
-                if (t < T) r0[static_cast<size_t>(t) * d] = o0[t] + __uint_as_float(y0[t]);
+                for (int t = 0; t < 16; ++t)
+                  if (t < T) o0[t] = r0[static_cast<size_t>(t) * d];
+#pragma unroll
+                for (int t = 0; t < 16; ++t)
+                  if (t < T) r0[static_cast<size_t>(t) * d] = o0[t] + __uint_as_float(y[j][t]);
+              }
             }
           }
           fence_before();

@@ -130,6 +130,14 @@ def main():
         by_shape.setdefault(key, []).append(float(ends[b]))
     print(json.dumps({"layer": lm, "end_us_by_shape": {k_: [len(v), round(float(np.median(v)), 2), round(max(v), 2)]
                                                        for k_, v in sorted(by_shape.items())}}))
+    # per-segment GU-issued stamps (per-segment K3 only: slots 15,19,23,25,31)
+    gu = {}
+    for b in range(G):
+        q0 = (b * n_units) // G
+        key = f"start%8={q0 % 8},pieces={segs[b]}"
+        row = [round(float((x[b, j] - base) / 1e3), 2) for j in (15, 19, 23, 25, 31) if x[b, j] > 0]
+        gu.setdefault(key, []).append(row)
+    print(json.dumps({"layer": lm, "gu_issued_us_by_shape_first": {k_: v[0] for k_, v in sorted(gu.items())}}))
     print(json.dumps({"layer": lm, "end_pct_us": [round(float(np.percentile(ends, p)), 2) for p in (0, 10, 50, 90, 100)],
                       "first_data_pct_us": [round(float(np.percentile(first, p)), 2) for p in (0, 50, 100)],
                       "slowest_ctas": [[int(b), int(sm[b]), round(float(ends[b]), 2)] for b in np.argsort(-ends)[:8]],
