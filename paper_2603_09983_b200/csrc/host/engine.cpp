@@ -658,7 +658,9 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     // -3% step time (Qwen3 / DeepSeek-V2-Lite / Qwen1.5 shapes); 0 for the
     // per-segment K3 (no gain on the Mixtral shape)
     const int pf = l2_prefetch_ >= 0 ? l2_prefetch_ : (acc_mode_ == 3 ? 131072 : 0);
-    if (tc && l + 1 < L && pf > 0) {
+    // (model mode routes layer l+1 only after this layer's combine: its
+    // routing tables are not final yet, so nothing to prefetch from)
+    if (tc && l + 1 < L && pf > 0 && !model_mode_) {
       fa.nx_counters = counters_d + static_cast<size_t>(l + 1) * 8;
       fa.nx_hit_list = hit_list_d_ + static_cast<size_t>(l + 1) * N;
       fa.nx_slot_of = slots_d + static_cast<size_t>(l + 1) * N;
