@@ -438,3 +438,30 @@ def test_draft_window_overlaps_loads_and_changes_nothing_else():
         assert np.array_equal(ha, hb)
         assert rb_.gpu_ms_total * 1e6 >= g * cfg.t_draft_unit_ns
     assert np.array_equal(a.sched_events(), b.sched_events())
+
+
+@pytest.mark.parametrize("d,ffn,cache", [(1024, 128, 0.5), (1024, 128, 1.0), (4096, 128, 1.0)])
+def test_l2_prefetch_changes_nothing(d, ffn, cache):
+    """The cross-layer L2 prefetch (default on for the grouped K3, a hint on
+    the per-segment one) only moves bytes into L2: outputs and scheduling
+    are bitwise those of the same engine with it off, including layers whose
+    experts are being loaded while the previous layer prefetches."""
+    L, N, k, g = 3, 16, 4, 6
+    rng = np.random.default_rng(11)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    a, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, cache, std, shared, abi.FFN_TENSOR, cold=0)
+    b, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, cache, std, shared, abi.FFN_TENSOR, cold=0)
+    a.set_l2_prefetch(0)
+    b.set_l2_prefetch(256 * 1024)
+    T = g + 1
+    gen = O.Generator(L, N, k, g, seed=6)
+    for s in range(4):
+        logits, _, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        ha, hb = np.zeros_like(h0), np.zeros_like(h0)
+        a.step(logits, h0, acc, ha)
+        b.step(logits, h0, acc, hb)
+        assert np.array_equal(ha, hb)
+    assert np.array_equal(a.sched_events(), b.sched_events())
+    a.close()
+    b.close()
