@@ -92,7 +92,7 @@ class ClockSampler:
                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.p = None
-        time.sleep(0.3)
+        time.sleep(1.0)  # (nvidia-smi's start-up burns host CPU: keep it out of the first window)
         return self
 
     def __exit__(self, *exc):
