@@ -395,7 +395,7 @@ def main():
                 vals.append(r)
         v = float(np.mean([r["value"] for r in vals]))
         line = dict(base, impl="reference", value=v, ms_per_step=float(np.mean([r["step_ms"] for r in vals])),
-                    scaling="weak" if world == 1 else "strong",
+                    scaling="strong",
                     cpu_baseline={"value": v, "unit": "tokens/s", "cores": vals[0]["cores"], "kind": "port",
                                   "sample": vals[0]["sample"]},
                     e2e={"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -432,7 +432,7 @@ def main():
             traffic = None
     if world > 1:
         base["config"]["parallelism"] = ("units" if r["parallel_mode"] == "units" else "ep") + str(world)
-    line = dict(base, value=tps, ms_per_step=r["ms"] / args.steps, scaling="strong" if world > 1 else "weak")
+    line = dict(base, value=tps, ms_per_step=r["ms"] / args.steps, scaling="strong")
     line["e2e"] = {"value": r["tokens_e2e"] / (r["ms_e2e"] * 1e-3), "unit": "tokens/s",
                    "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])}
     line["roofline"] = {"bound": "hbm", "kernel": r["k3_kernel"], "achieved": achieved, "peak": hbm_peak,
