@@ -215,6 +215,22 @@ def test_expert_ffn_grouped_grids(N, k, T, d, ffn, n_shared, gate_mode, resident
     _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 4, grid=grid, tol=3e-5)
 
 
+@pytest.mark.parametrize("grid", [1, 5, 37, 148, 300])
+@pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
+    (8, 2, 5, 4096, 448, 0, 0, 1.0),      # Mixtral d: chunk pieces split across CTAs at every grid
+    (8, 2, 16, 4096, 192, 1, 0, 0.7),     # T = 16 + shared unit, expert boundaries inside CTA ranges
+    (4, 2, 9, 3072, 320, 0, 1, 1.0),      # d = 3072 (not a power of two), 5 chunks per expert
+])
+def test_expert_ffn_per_segment_grids(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, grid):
+    """Per-segment K3 (d > 2048, shared-memory accumulator): CTA ranges of
+    0..many 8-row units start and end anywhere inside chunks and experts;
+    partial pieces, per-lane tile copies and per-expert flushes against the
+    fp64 oracle."""
+    if abi.FFN_TENSOR not in _kernels(d, ffn):
+        pytest.skip("shape not supported by the tensor-core kernel")
+    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 0, grid=grid)
+
+
 def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum, grid=None, tol=1e-5):
     rng = np.random.default_rng(N * 7 + T)
     experts = _rand_experts(rng, N, d, ffn)
