@@ -113,13 +113,19 @@ struct Geom {  // one entry: bytes, tiles, read window (bytes from the entry sta
   uint32_t size, win;
   int m;
 };
-__device__ __forceinline__ Geom gu_geom(int nu, int cap) {
+// hb: h^T bytes per K-tile carried in the entry — 2 KiB (16 token rows), or
+// 1 KiB when T <= 8: only the first 8-row token group is copied and the
+// descriptor's second group (SBO = 1 KiB) reads whatever follows, which only
+// feeds D1 columns of tokens >= T (the epilogue selects 0 for those).
+__device__ __forceinline__ Geom gu_geom(int nu, int cap, uint32_t hb) {
   const int m = tiles_per_entry(nu, cap);
   const uint32_t a = static_cast<uint32_t>(nu) * 2048u;
-  const uint32_t size = static_cast<uint32_t>(m) * (a + 2048u);
-  // tile j's A descriptor reads the 16 KiB window at j*a - qa*2048
+  const uint32_t size = static_cast<uint32_t>(m) * (a + hb);
+  // tile j's A descriptor reads the 16 KiB window at j*a - qa*2048; the last
+  // h^T slice's second token group reads 1 KiB past the entry when hb = 1 KiB
   const uint32_t w = static_cast<uint32_t>(m - 1) * a + 16384u;
-  return {size, size > w ? size : w, m};
+  const uint32_t ws = size + (hb < 2048u ? 1024u : 0u);
+  return {size, ws > w ? ws : w, m};
 }
 __device__ __forceinline__ Geom dn_geom(int nu, int cap) {
   const int m = tiles_per_entry(nu, cap);
@@ -177,6 +183,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
   // ring so that a shifted A descriptor of a partial entry (up to 12 KiB
   // before the entry) still addresses this CTA's shared memory.
   const uint32_t RB = static_cast<uint32_t>(a.ring_bytes);
+  const uint32_t hb = a.T <= 8 ? 1024u : static_cast<uint32_t>(B_BYTES);  // h^T bytes per K-tile in an entry
   uint8_t* p = smem_raw;
   uint8_t* aT = p;  // [2 buf][2 part][4096]
   p += 2 * 2 * 4096;
@@ -371,8 +378,18 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         for (int j = lane; j < m; j += 32)
           bulk_g2s(ring + e + j * ab, base + static_cast<size_t>(t0 + j) * A_BYTES + qa * UBYTES, ab, bar, pol);
       };
-      auto seg_base = [&](const Seg& s) {
-        return reinterpret_cast<const uint8_t*>(entry_weights(a, s.o, n_hits) + s.c * chunk_elems);
+      // entry image bases, one lane per entry of the CTA's range, looked up
+      // once: a segment change then costs a shuffle instead of two dependent
+      // global loads (hit list -> slot) on the producer's critical path
+      const int o_first = q1 > q0 ? static_cast<int>(q0 / qpe) : 0;
+      const int n_ent = q1 > q0 ? static_cast<int>((q1 - 1) / qpe) - o_first + 1 : 0;
+      unsigned long long my_ent = 0;
+      if (lane < n_ent) my_ent = reinterpret_cast<unsigned long long>(entry_weights(a, o_first + lane, n_hits));
+      auto seg_base = [&](const Seg& s) {  // (warp-uniform)
+        const uint16_t* w =
+            n_ent <= 32 ? reinterpret_cast<const uint16_t*>(__shfl_sync(0xffffffffu, my_ent, (s.o - o_first) & 31))
+                        : entry_weights(a, s.o, n_hits);
+        return reinterpret_cast<const uint8_t*>(w + s.c * chunk_elems);
       };
       SegIter it{q0, q1, qpe};
       Seg cur, prev;
@@ -385,7 +402,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
       int kt0 = 0;
       {
         const int nq = cur.qb - cur.qa;
-        const Geom g = gu_geom(nq, kcap);
+        const Geom g = gu_geom(nq, kcap, hb);
         int np = 0;
         uint32_t e;
         while (kt0 < ktiles && reserve(g, false, e)) {
@@ -398,14 +415,22 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
         pdl_wait();
         // the prefetched entries lie back to back from offset 0 (no wrap)
         const uint32_t span = (g.size + 1023u) & ~1023u, ab = static_cast<uint32_t>(g.m * nq) * UBYTES;
-        for (int j = lane; j < np; j += 32)
-          bulk_g2s(ring + j * span + ab, hTb + static_cast<size_t>(j * g.m) * B_BYTES,
-                   static_cast<uint32_t>(g.m) * B_BYTES, &full[j], pol);
+        if (hb == B_BYTES) {
+          for (int j = lane; j < np; j += 32)
+            bulk_g2s(ring + j * span + ab, hTb + static_cast<size_t>(j * g.m) * B_BYTES,
+                     static_cast<uint32_t>(g.m) * B_BYTES, &full[j], pol);
+        } else {
+          for (int c = lane; c < np * g.m; c += 32) {
+            const int j = c / g.m, jj = c - j * g.m;
+            bulk_g2s(ring + j * span + ab + jj * hb, hTb + static_cast<size_t>(j * g.m + jj) * B_BYTES, hb, &full[j],
+                     pol);
+          }
+        }
       }
       while (more || has_prev) {
         if (more) {
           const int nq = cur.qb - cur.qa;
-          const Geom g = gu_geom(nq, kcap);
+          const Geom g = gu_geom(nq, kcap, hb);
           const uint32_t ab = static_cast<uint32_t>(g.m * nq) * UBYTES;
           for (int kt = kt0; kt < ktiles; kt += g.m) {
             uint32_t e;
@@ -413,9 +438,14 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
             uint64_t* bar = &full[idx % NSLOT];
             if (leader) mbar_arrive_expect_tx(bar, g.size);
             copy_tiles(cur_base, kt, g.m, cur.qa, nq, e, bar);
-            if (lane == 31)  // (m <= 8 < 31: a lane with no tile copy)
-              bulk_g2s(ring + e + ab, hTb + static_cast<size_t>(kt) * B_BYTES, static_cast<uint32_t>(g.m) * B_BYTES,
-                       bar, pol);
+            if (hb == B_BYTES) {
+              if (lane == 31)  // (m <= 8 < 31: a lane with no tile copy)
+                bulk_g2s(ring + e + ab, hTb + static_cast<size_t>(kt) * B_BYTES,
+                         static_cast<uint32_t>(g.m) * B_BYTES, bar, pol);
+            } else if (lane >= 16 && lane < 16 + g.m) {  // one 1 KiB slice per lane
+              const int jj = lane - 16;
+              bulk_g2s(ring + e + ab + jj * hb, hTb + static_cast<size_t>(kt + jj) * B_BYTES, hb, bar, pol);
+            }
             ++idx;
           }
           kt0 = 0;
@@ -503,7 +533,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
           fence_after();
           const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
           const int nq = cur.qb - cur.qa;
-          const Geom g = gu_geom(nq, kcap);
+          const Geom g = gu_geom(nq, kcap, hb);
           const uint32_t ab = static_cast<uint32_t>(nq) * UBYTES;
           for (int kt = 0; kt < ktiles; kt += g.m) {
             const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
@@ -516,7 +546,7 @@ __global__ void __maxnreg__(200) expert_ffn_tc_kernel(FfnArgs a) {
             const uint32_t vb = ring_addr + off + static_cast<uint32_t>(g.m) * ab;
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
-                const uint64_t adesc = smem_desc(va + j * ab, 128, 1024), bdesc = smem_desc(vb + j * B_BYTES, 128, 1024);
+                const uint64_t adesc = smem_desc(va + j * ab, 128, 1024), bdesc = smem_desc(vb + j * hb, 128, 1024);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
                   mma_bf16(d1, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0);

@@ -101,10 +101,12 @@ def main():
                 print(json.dumps({"wait_frac_of_cta_cycles": waits,
                                   "drain_cycles_med": {nm: float(np.median(t[act, j])) for j, nm in
                                                        [(25, "tmem_ld"), (26, "lds"), (27, "sts")]}}), flush=True)
-                # end time vs the CTA's number of segments (chunk pieces)
-                qpe = ffn // 16
+                # end time vs the CTA's number of chunk pieces (8-row units,
+                # 8 units per 64-row chunk) and its start offset in a chunk
+                qpe = ffn // 8
                 n_q = n_hit * qpe
                 by = {}
+                gu_rows = {}
                 ends = (t[:, 6] - t0) / 1e3
                 for b in range(sms):
                     q0, q1 = b * n_q // sms, (b + 1) * n_q // sms
@@ -112,12 +114,18 @@ def main():
                         continue
                     nseg, q = 0, q0
                     while q < q1:
-                        q = min((q // 4 + 1) * 4, q1)
+                        q = min((q // 8 + 1) * 8, q1)
                         nseg += 1
-                    key = f"{nseg}seg_{q1 - q0}q"
+                    key = f"{nseg}pieces_{q1 - q0}u_start%8={q0 % 8}"
                     by.setdefault(key, []).append(float(ends[b]))
+                    # per-segment GU-issued stamps (slots 15, 19, 23, 25, 31)
+                    gu_rows.setdefault(key, []).append([round(float((t[b, j] - t0) / 1e3), 2)
+                                                        for j in (15, 19, 23, 25, 31) if t[b, j] > 0])
                 print(json.dumps({"end_us_by_cta_shape": {k: [len(v), round(float(np.median(v)), 2), round(max(v), 2)]
                                                            for k, v in sorted(by.items())}}), flush=True)
+                print(json.dumps({"gu_issued_us_by_shape": {k: [float(np.median([r[i] for r in v if len(r) > i]))
+                                                                 for i in range(max(len(r) for r in v))]
+                                                             for k, v in sorted(gu_rows.items())}}), flush=True)
 
                 print(json.dumps({"stamps_us_min_med_max": summ, "active_ctas": int(act.sum()),
                                   "cta_clock64_cycles_med_max": [float(np.median(cyc)), float(cyc.max())],
