@@ -107,6 +107,8 @@ def main():
                 n_q = n_hit * qpe
                 by = {}
                 gu_rows = {}
+                waits_by = {}
+                cyc_all = t[:, 7]
                 ends = (t[:, 6] - t0) / 1e3
                 for b in range(sms):
                     q0, q1 = b * n_q // sms, (b + 1) * n_q // sms
@@ -119,10 +121,14 @@ def main():
                     key = f"{nseg}pieces_{q1 - q0}u_start%8={q0 % 8}"
                     by.setdefault(key, []).append(float(ends[b]))
                     # per-segment GU-issued stamps (slots 15, 19, 23, 25, 31)
+                    waits_by.setdefault(key, []).append([float(t[b, j] / max(cyc_all[b], 1.0)) for j in (8, 9, 10, 11, 13, 14)])
                     gu_rows.setdefault(key, []).append([round(float((t[b, j] - t0) / 1e3), 2)
                                                         for j in (15, 19, 23, 25, 31) if t[b, j] > 0])
                 print(json.dumps({"end_us_by_cta_shape": {k: [len(v), round(float(np.median(v)), 2), round(max(v), 2)]
                                                            for k, v in sorted(by.items())}}), flush=True)
+                print(json.dumps({"wait_frac_by_shape[prod_empty,mma_full,mma_at,mma_d2e,epi_d1,epi_d2]": {
+                    k: [round(float(np.median([r[i] for r in v])), 3) for i in range(6)] for k, v in sorted(waits_by.items())}}),
+                    flush=True)
                 print(json.dumps({"gu_issued_us_by_shape": {k: [float(np.median([r[i] for r in v if len(r) > i]))
                                                                  for i in range(max(len(r) for r in v))]
                                                              for k, v in sorted(gu_rows.items())}}), flush=True)
