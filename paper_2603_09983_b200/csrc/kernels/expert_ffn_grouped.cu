@@ -633,6 +633,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       for (int r = 0; r < n_ent; ++r) tmask |= ent_mask[r];
       const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0);
       float* stg = reinterpret_cast<float*>(ring);
+      if (et == 0) stamp(a, 7);
       // four M-tiles per tcgen05.wait::ld (mtiles is even; the drain is
       // load-latency bound: one round trip per wait)
       for (int mt = 0; mt < mtiles; mt += 4) {
@@ -656,6 +657,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
               if (t < T) r0[static_cast<size_t>(t) * d + 128 * j] = __uint_as_float(y[j][t]);
           }
       }
+      if (et == 0) stamp(a, 1);
       fence_before();
       fence_proxy_async();
       // TMEM is dead past this barrier: warp 1 (also arriving) deallocates it
