@@ -15,8 +15,15 @@ accounting. TPS = accepted tokens / device time.
   e2e   : the same through moespac_step with pinned HOST buffers; H2D of
           logits + h_in + decision tables (+ any expert loads) and D2H of
           h_out + scores/counters inside the timed region
-  roofline: K3 (expert_ffn_kernel) algorithmic bytes / its CUDA-event time
+  roofline: K3 algorithmic bytes per launch / its launch duration, from
+          every CTA's %globaltimer stamps in a window run exactly like the
+          timed one (programmatic dependent launch on); the CUDA-event
+          per-launch time (PDL off) is reported beside it
   cpu_baseline: the CPU oracle port of the same step on the box's cores
+  detail.budget: a second workload at a BASELINE cache budget (default
+          Qwen3-30B-A3B at 17%: real expert loads + the host cold path),
+          median / spread of 5 windows for value and e2e, its own roofline
+          and cpu_baseline
 
 --impl reference: the reference's CPU path for the same workload (the
 compiled reference scheduler oracle/_ref + the CPU oracle port of the
@@ -54,11 +61,17 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
-    ap.add_argument("--trace-steps", type=int, default=160)
     ap.add_argument("--settle", type=int, default=20,
                     help="extra untimed steps before the timed windows when the cache budget is < 1 "
                          "(the warm fill holds experts 0..cap-1, not the hot ones)")
     ap.add_argument("--ffn-kernel", type=int, default=0, help="0 auto (tcgen05), 1 CUDA-core GEMV, 2 tcgen05")
+    ap.add_argument("--no-budget", action="store_true",
+                    help="skip the cache-budget leg (detail.budget: a BASELINE budget config, real expert loads "
+                         "and the host cold path, median of windows)")
+    ap.add_argument("--budget-config", default="qwen3")
+    ap.add_argument("--budget-cache", type=float, default=0.17)
+    ap.add_argument("--budget-windows", type=int, default=5)
+    ap.add_argument("--budget-steps", type=int, default=20)
     ap.add_argument("--draft-window", action="store_true",
                     help="emulated draft phase: gamma x t_draft_unit (reference default 300 us/token) on the compute "
                          "stream before each verification step, expert loads overlapping it; TPS then counts "
@@ -122,12 +135,16 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload(args):
+def workload_named(name, cache_ratio=None):
     from paper_2603_09983_b200.configs import CONFIGS
-    w = CONFIGS[args.config]
-    if args.cache_ratio is not None:
-        w = w.with_(cache_ratio=args.cache_ratio)
+    w = CONFIGS[name]
+    if cache_ratio is not None:
+        w = w.with_(cache_ratio=cache_ratio)
     return w
+
+
+def workload(args):
+    return workload_named(args.config, args.cache_ratio)
 
 
 # ------------------------------------------------------------------ CPU leg
@@ -213,7 +230,47 @@ def cpu_path_sample(w, budget_s: float, use_ref_sched: bool):
 
 
 # ------------------------------------------------------------------ GPU leg
-def run_ours(args, w, rank, world, local_rank):
+def golden_path(w):
+    """The committed reference fixture (tests/golden, made from the compiled
+    reference) for this workload at this budget, if there is one: its trace is
+    the bench's (reference defaults, seed 1), so the warm-up steps' decisions
+    must equal it record for record."""
+    name = {("mixtral", 1.0): "mixtral_c100", ("mixtral", 0.17): "mixtral", ("tiny", 0.17): "tiny",
+            ("tiny", 1.0): "tiny_c100", ("qwen15", 0.5): "qwen15", ("dsv2", 0.17): "dsv2"}.get(
+        (w.name, round(w.cache_ratio, 2)))
+    if w.name == "qwen3":
+        name = "qwen3_c%03d" % round(w.cache_ratio * 100)
+    p = os.path.join(ROOT, "tests", "golden", f"sim_{name}.npz") if name else None
+    return p if p and os.path.exists(p) else None
+
+
+def check_decisions(ctx, w, n_steps):
+    """SimEvent log of the first n_steps equals the reference's (golden)."""
+    p = golden_path(w)
+    if not p:
+        return None
+    z = np.load(p)
+    n = min(n_steps, len(z["accepted"]))
+    ev = z["events"]
+    got = ctx.sched_events()
+    ok = np.array_equal(got[got[:, 1] < n], ev[ev[:, 1] < n])
+    if not ok:
+        raise SystemExit(f"bench: decision parity FAILED against {os.path.relpath(p, ROOT)} over {n} steps")
+    return {"golden": os.path.relpath(p, ROOT), "steps": int(n), "events": int((ev[:, 1] < n).sum()), "equal": True}
+
+
+def n_images_for(w):
+    """Pinned master-copy images: expert (l, e) -> image (l*N + e) % n. At a
+    partial budget the host cold path reads them, so use >= 8 GiB of distinct
+    images (beyond any LLC) and n = N + 1 at least, so the same expert id in
+    consecutive layers never maps to the same image."""
+    n = w.n_experts + 1
+    if w.cache_ratio < 1.0:
+        n = max(n, -(-(8 << 30) // w.expert_bytes))
+    return min(w.n_layers * w.n_experts, n)
+
+
+def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", steps=None):
     import torch
 
     from paper_2603_09983_b200 import abi
@@ -221,11 +278,11 @@ def run_ours(args, w, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=w.cache_ratio)
-    model = abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode, args.ffn_kernel)
+    model = w.model_desc(args.ffn_kernel)
 
     def make_ctx():
         c = abi.Context(local_rank, model, cfg, rank, world)
-        c.host_arena(min(L * N, max(N, 8)))
+        c.host_arena(n_images_for(w))
         c.fill_synthetic(seed=3, stdv=0.02)
         if args.router_gemv:
             c.set_cold_threads(0)
@@ -244,17 +301,17 @@ def run_ours(args, w, rank, world, local_rank):
         return c
 
     ctx = make_ctx()
-    # synthetic inputs: routing from the trace synthesizer (reference
-    # TraceGenerator semantics), hidden states ~ N(0, 1) bf16.
-    # Trace steps: W warm-up (+ settle steps when the cache budget is < 1),
-    # then one window of K steps that the device-resident value, the
-    # end-to-end run and the per-kernel timing run all use. Below a full
-    # cache the end-to-end run gets a fresh context driven through the same
-    # warm-up, so it starts from the same cache and estimator state instead
-    # of replaying routing the cache has already adapted to.
+    # Synthetic inputs: routing from the trace synthesizer (reference
+    # TraceGenerator semantics, seed 1), hidden states ~ N(0, 1) bf16.
+    # Trace steps: W warm-up (+ settle steps below a full cache), then
+    # `windows` windows of K steps for `value`, one more window with the K3
+    # globaltimer stamps (PDL on) and one with per-K3 CUDA events (PDL off).
+    # The end-to-end run uses a fresh context through the same warm-up and
+    # the same `windows` windows, so both start from the same cache state.
     settle = args.settle if w.cache_ratio < 1.0 else 0
     w0 = args.warmup + settle
-    S = min(args.trace_steps, w0 + args.steps)
+    K = steps or args.steps
+    S = w0 + (windows + 2) * K
     synth = abi.TraceSynth(cfg)
     logits_h = torch.empty((S, L, T, N), dtype=torch.float64).pin_memory()
     accepted = []
@@ -275,23 +332,27 @@ def run_ours(args, w, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(fn, n, offset):
+    def max_over_ranks(x):
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([x], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    def timed(fn, n, offset, per_step=None):
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         stream = torch.cuda.ExternalStream(ctx.stream())
         reps = []
         e0.record(stream)
         for i in range(n):
-            reps.append(fn((offset + i) % S))
+            reps.append(fn(offset + i))
+            if per_step:
+                per_step(reps[-1])
         e1.record(stream)
         barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, reps
+        return max_over_ranks(e0.elapsed_time(e1)), reps
 
     dev_step = lambda s: ctx.step_device(logits_d[s], h_d[s], accepted[s], h_out_d)[0]  # noqa: E731
     host_step = lambda s: ctx.step(logits_h[s].numpy(), h_h[s].view(torch.int16).numpy(), accepted[s],  # noqa: E731
@@ -301,58 +362,125 @@ def run_ours(args, w, rank, world, local_rank):
         host_step = lambda s: ctx.step_model(h_h[s].view(torch.int16).numpy(), accepted[s],  # noqa: E731
                                              h_out_h.view(torch.int16).numpy())[0]
     for i in range(w0):
-        dev_step(i % S)
-    K = args.steps
+        dev_step(i)
+    parity = None if args.router_gemv else check_decisions(ctx, w, w0)
+    tok = lambda o, n: float(sum(accepted[o + i] for i in range(n)))  # noqa: E731
+    sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    stamps = torch.zeros((L, sms, 32), dtype=torch.int64, device="cuda")
+    spans = []
+
+    def read_stamps(_rep):
+        # K3 launch durations of this step from its CTAs' %globaltimer
+        # stamps (first CTA start -> last CTA end, per layer): the kernels ran
+        # with programmatic dependent launch, as in the timed windows
+        st = stamps.cpu().numpy()
+        for l in range(L):
+            beg, end = st[l, :, 0], st[l, :, 6]
+            if (end > 0).any():
+                spans.append((end[end > 0].max() - beg[beg > 0].min()) * 1e-6)
+        stamps.zero_()
+        torch.cuda.synchronize()
+
     with ClockSampler(local_rank) as clk:
-        # (1) headline: whole steps, no per-kernel events (layer kernels use
-        #     programmatic dependent launch)
         ctx.set_timing(False)
-        ms, reps = timed(dev_step, K, w0)
-        # (2) end to end through the host API, same window
-        if settle:
-            ctx.close()
-            ctx = make_ctx()  # (the step lambdas look ctx up at call time)
-            for i in range(w0):
-                host_step(i % S)
-        else:
-            for i in range(max(1, args.warmup // 2)):
-                host_step(i % S)
-        ms_e2e, reps_e2e = timed(host_step, K, w0)
-        # (3) roofline: the window again with a CUDA-event pair around every
-        #     K3 launch (PDL off so each pair brackets exactly one kernel)
+        win = []  # (ms, tokens, reps) per window
+        for j in range(windows):
+            ms, reps = timed(dev_step, K, w0 + j * K)
+            win.append((ms, tok(w0 + j * K, K), reps))
+        o = w0 + windows * K
+        # K3 stamps, PDL on (the timed windows' launch mode)
+        ctx.set_k3_trace(abi.ptr(stamps))
+        ms_st, reps_st = timed(dev_step, K, o, per_step=read_stamps)
+        ctx.set_k3_trace(None)
+        # per-K3 CUDA events (PDL off so each pair brackets one kernel)
         ctx.set_timing(True)
-        ms_t, reps_t = timed(dev_step, K, w0)
-    reps_tok = reps
-    reps = reps_t
-    tokens = float(sum(accepted[(w0 + i) % S] for i in range(K)))
-    tokens_e2e = tokens
-    ffn_ms = sum(r.gpu_ms_ffn for r in reps)
-    ffn_bytes = sum(r.ffn_bytes for r in reps)
-    launches = sum(r.kernel_launches for r in reps_tok)
-    hits = sum(r.cache_hits for r in reps)
-    misses = sum(r.cache_misses for r in reps)
-    loads = sum(r.n_loads for r in reps)
+        ms_ev, reps_ev = timed(dev_step, K, o + K)
+        ctx.set_timing(False)
+        # end to end through the host API: fresh context through the same
+        # warm-up, the same windows
+        ctx.close()
+        ctx = make_ctx()  # (the step lambdas look ctx up at call time)
+        for i in range(w0):
+            host_step(i)
+        win_e2e = []
+        for j in range(windows):
+            ms, reps = timed(host_step, K, w0 + j * K)
+            win_e2e.append((ms, tok(w0 + j * K, K), reps))
+    ffn_bytes_st = sum(r.ffn_bytes for r in reps_st)
+    n_launch_st = sum(r.ffn_launches for r in reps_st)
     out = {
-        "ms": ms, "ms_e2e": ms_e2e, "ms_timed": ms_t, "tokens": tokens, "tokens_e2e": tokens_e2e,
-        "settle": settle, "ffn_ms": ffn_ms, "ffn_bytes": ffn_bytes,
-        "ffn_launches": sum(r.ffn_launches for r in reps), "launches": launches, "hits": hits, "misses": misses, "loads": loads,
+        "label": label, "w0": w0, "settle": settle, "windows": windows,
+        "win": [(m, t) for m, t, _ in win], "win_e2e": [(m, t) for m, t, _ in win_e2e],
+        "ms": win[0][0], "tokens": win[0][1], "ms_e2e": win_e2e[0][0], "tokens_e2e": win_e2e[0][1],
+        "k3_span_ms": spans, "ffn_bytes_st": ffn_bytes_st, "ffn_launches_st": n_launch_st,
+        "ffn_ms_ev": sum(r.gpu_ms_ffn for r in reps_ev), "ffn_bytes_ev": sum(r.ffn_bytes for r in reps_ev),
+        "ffn_launches_ev": sum(r.ffn_launches for r in reps_ev),
+        "launches": sum(r.kernel_launches for r in win[0][2]),
+        "hits": sum(r.cache_hits for _, _, rs in win for r in rs),
+        "misses": sum(r.cache_misses for _, _, rs in win for r in rs),
+        "loads": sum(r.n_loads for _, _, rs in win for r in rs),
+        "cold_experts": sum(r.cold_experts for _, _, rs in win for r in rs),
+        "cpu_ms_cold": sum(r.cpu_ms_cold for _, _, rs in win for r in rs),
         "k3_kernel": ctx.k3_kernel(), "parallel_mode": ctx.parallel_mode(),
-        "h2d": float(np.mean([r.h2d_bytes for r in reps_e2e])), "d2h": float(np.mean([r.d2h_bytes for r in reps_e2e])),
-        "router_ms": float(np.mean([r.gpu_ms_router for r in reps])),
-        "hist_ms": float(np.mean([r.gpu_ms_hist for r in reps])),
-        "gpu_step_ms": float(np.mean([r.gpu_ms_total for r in reps])),
-        "layers_other_ms": float(np.mean([r.gpu_ms_combine for r in reps])),
+        "h2d": float(np.mean([r.h2d_bytes for _, _, rs in win_e2e for r in rs])),
+        "d2h": float(np.mean([r.d2h_bytes for _, _, rs in win_e2e for r in rs])),
+        "router_ms": float(np.mean([r.gpu_ms_router for r in reps_ev])),
+        "hist_ms": float(np.mean([r.gpu_ms_hist for r in reps_ev])),
+        "gpu_step_ms": float(np.mean([r.gpu_ms_total for r in reps_ev])),
+        "layers_other_ms": float(np.mean([r.gpu_ms_combine for r in reps_ev])),
+        "ms_ev": ms_ev, "ms_st": ms_st, "parity": parity, "n_images": n_images_for(w),
         "clocks": clk.summary(),
     }
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ffn_ms, ffn_bytes], dtype=torch.float64, device="cuda")
-        # aggregate K3 bytes and time over ranks (bytes sum, time max)
-        tb = t.clone()
-        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
-        out["ffn_bytes_all"] = float(tb[1].item())
+        # multi-GPU roofline: K3 bytes summed over ranks over the max K3 time
+        t = torch.tensor([ffn_bytes_st, float(np.sum(spans))], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
+        tm = t[1:].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        out["ffn_bytes_st_all"] = float(t[0].item())
+        out["k3_span_ms_max_rank"] = float(tm[0].item())
     ctx.close()
     return out
+
+
+def leg_summary(r, w, args, world, hbm_peak, peak_kind):
+    """value / e2e / roofline of one leg (one workload)."""
+    tps = [t / (m * 1e-3) for m, t in r["win"]]
+    tps_e2e = [t / (m * 1e-3) for m, t in r["win_e2e"]]
+    spans = r["k3_span_ms"]
+    span_ms = float(np.mean(spans)) if spans else 0.0
+    bytes_per_launch = r["ffn_bytes_st"] / max(1, r["ffn_launches_st"])
+    if world > 1 and "ffn_bytes_st_all" in r:
+        achieved = r["ffn_bytes_st_all"] / (r["k3_span_ms_max_rank"] * 1e-3) / 1e9 if r["k3_span_ms_max_rank"] else 0.0
+    else:
+        achieved = bytes_per_launch / (span_ms * 1e-3) / 1e9 if span_ms > 0 else 0.0
+    ev_ms = r["ffn_ms_ev"] / max(1, r["ffn_launches_ev"])
+    ev_achieved = r["ffn_bytes_ev"] / max(1, r["ffn_launches_ev"]) / (ev_ms * 1e-3) / 1e9 if ev_ms > 0 else 0.0
+    traffic, traffic_capture = None, None
+    prof = os.path.join(ROOT, "profiles", f"ncu_k3_{w.name}.json")
+    if os.path.exists(prof):
+        try:
+            cap = json.load(open(prof))
+            ratio = cap.get("traffic_over_algorithmic")
+            traffic = ratio * bytes_per_launch if ratio else None
+            traffic_capture = {"dram_bytes": cap.get("dram_bytes_per_launch"),
+                               "algorithmic_bytes": cap.get("algorithmic_bytes_of_launch"), "ratio": ratio,
+                               "kernel": cap.get("kernel"), "report": cap.get("report")}
+        except (ValueError, OSError, TypeError):
+            traffic = None
+    roof = {"bound": "hbm", "kernel": r["k3_kernel"], "achieved": achieved, "peak": hbm_peak,
+            "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)" if peak_kind == "measured"
+            else "fallback 6650 GB/s (B200_PROFILING.md)",
+            "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic, "traffic_capture": traffic_capture,
+            "bytes_per_launch": bytes_per_launch, "ms_per_launch": span_ms,
+            "timing": "K3 launch duration = first CTA start -> last CTA end (%globaltimer stamps of every CTA), "
+                      "averaged over the L launches of a K-step window run with programmatic dependent launch "
+                      "(the timed windows' mode); bytes = resident activated experts + shared units x image",
+            "cuda_events_pdl_off": {"ms_per_launch": ev_ms, "achieved": ev_achieved, "frac": ev_achieved / hbm_peak}}
+    stat = lambda v: {"median": float(np.median(v)), "min": float(np.min(v)), "max": float(np.max(v)),  # noqa: E731
+                      "spread": float((np.max(v) - np.min(v)) / np.median(v)), "windows": [float(x) for x in v]}
+    return tps, tps_e2e, roof, stat
 
 
 def main():
@@ -377,9 +505,12 @@ def main():
                 if args.draft_window else "none: verification step only",
                 "l2": "inputs > L2: every step streams each resident activated expert (>= 9 MB each, "
                       "GBs per step) through HBM; no L2 flush needed",
-                "windows": "W warm-up steps (+ %d settle steps when cache < 1), then one K-step trace window "
-                           "for value, e2e (below a full cache: a fresh context through the same warm-up) and the "
-                           "per-K3-event timing" % args.settle}
+                "windows": "W warm-up steps (+ %d settle steps when cache < 1; their scheduling decisions checked "
+                           "against the reference's golden fixture), then one K-step trace window for value, the "
+                           "next K steps with K3 %%globaltimer stamps (roofline), the next with per-K3 CUDA events; "
+                           "e2e on a fresh context through the same warm-up and window" % args.settle,
+                "host_arena": "expert (l, e) -> pinned image (l*N + e) %% n_images, n_images >= N + 1 (and >= 8 GiB "
+                              "below a full cache): no image shared by the same expert id in consecutive layers"}
     base = {"metric": "decode TPS and expert-FFN HBM GB/s (roofline %) at 1/2/4/8 B200 vs host CPU",
             "unit": "tokens/s", "higher_is_better": True, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": cfg_json}
@@ -404,54 +535,58 @@ def main():
         return
 
     r = run_ours(args, w, rank, world, local_rank)
+    rb = None
+    if world == 1 and not args.no_budget:
+        wb = workload_named(args.budget_config, args.budget_cache)
+        rb = run_ours(args, wb, rank, world, local_rank, windows=args.budget_windows, label="budget",
+                      steps=args.budget_steps)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
         return
     hbm_peak, peak_kind = load_peaks()
-    tps = r["tokens"] / (r["ms"] * 1e-3)
-    achieved = r["ffn_bytes"] / (r["ffn_ms"] * 1e-3) / 1e9 if r["ffn_ms"] > 0 else 0.0
-    # DRAM traffic of one K3 launch from a committed `ncu --set full`
-    # capture (profiles/ncu_k3_<config>.json), expressed for this run's
-    # average launch: captured DRAM bytes / captured algorithmic bytes x
-    # this run's algorithmic bytes per launch (the capture's launch streams
-    # a different number of experts than the average one)
-    traffic, traffic_capture = None, None
-    prof = os.path.join(ROOT, "profiles", f"ncu_k3_{w.name}.json")
-    if os.path.exists(prof):
-        try:
-            cap = json.load(open(prof))
-            ratio = cap.get("traffic_over_algorithmic")
-            bpl = r["ffn_bytes"] / max(1, r["ffn_launches"])
-            traffic = ratio * bpl if ratio else None
-            traffic_capture = {"dram_bytes": cap.get("dram_bytes_per_launch"),
-                               "algorithmic_bytes": cap.get("algorithmic_bytes_of_launch"), "ratio": ratio,
-                               "kernel": cap.get("kernel"), "report": cap.get("report")}
-        except (ValueError, OSError, TypeError):
-            traffic = None
+    tps, tps_e2e, roof, stat = leg_summary(r, w, args, world, hbm_peak, peak_kind)
     if world > 1:
         base["config"]["parallelism"] = ("units" if r["parallel_mode"] == "units" else "ep") + str(world)
-    line = dict(base, value=tps, ms_per_step=r["ms"] / args.steps, scaling="strong")
-    line["e2e"] = {"value": r["tokens_e2e"] / (r["ms_e2e"] * 1e-3), "unit": "tokens/s",
+    line = dict(base, value=tps[0], ms_per_step=r["ms"] / args.steps, scaling="strong")
+    line["e2e"] = {"value": tps_e2e[0], "unit": "tokens/s",
                    "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])}
-    line["roofline"] = {"bound": "hbm", "kernel": r["k3_kernel"], "achieved": achieved, "peak": hbm_peak,
-                        "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)" if peak_kind == "measured"
-                        else "fallback 6650 GB/s (B200_PROFILING.md)",
-                        "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-                        "traffic_capture": traffic_capture,
-                        "bytes_per_launch": r["ffn_bytes"] / max(1, r["ffn_launches"]),
-                        "ms_per_launch": r["ffn_ms"] / max(1, r["ffn_launches"])}
+    line["roofline"] = roof
     line["gpu_launches"] = int(r["launches"])
     line["clocks"] = r["clocks"]
+    line["decision_parity"] = r["parity"]
     line["detail"] = {"hit_rate": r["hits"] / max(1, r["hits"] + r["misses"]), "loads_per_step": r["loads"] / args.steps,
                       "router_ms": r["router_ms"], "hist_ms": r["hist_ms"], "gpu_step_ms": r["gpu_step_ms"],
-                      "layers_non_ffn_ms": r["layers_other_ms"],
-                      "ffn_ms_per_step": r["ffn_ms"] / args.steps, "tokens_per_step": r["tokens"] / args.steps,
-                      "ms_per_step_with_kernel_events": r["ms_timed"] / args.steps}
+                      "layers_non_ffn_ms": r["layers_other_ms"], "tokens_per_step": r["tokens"] / args.steps,
+                      "ms_per_step_k3_stamps_window": r["ms_st"] / args.steps,
+                      "ms_per_step_kernel_events_window": r["ms_ev"] / args.steps,
+                      "host_arena_images": r["n_images"]}
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_path_sample(w, args.cpu_budget_s, use_ref_sched=True)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rb is not None:
+        wb = workload_named(args.budget_config, args.budget_cache)
+        btps, btps_e2e, broof, _ = leg_summary(rb, wb, args, world, hbm_peak, peak_kind)
+        K = args.budget_steps
+        nwin = len(rb["win"])
+        budget = {"workload": wb.description, "config": wb.name, "cache_ratio": wb.cache_ratio,
+                  "metric": base["metric"], "unit": "tokens/s",
+                  "value": stat(btps), "e2e": stat(btps_e2e),
+                  "e2e_over_value": float(np.median(btps_e2e) / np.median(btps)),
+                  "windows": f"{nwin} windows of {K} consecutive trace steps after {rb['w0']} warm-up + settle steps; "
+                             "value = device-resident inputs, e2e = moespac_step with pinned host buffers on a fresh "
+                             "context driven through the same warm-up (same cache state, same windows)",
+                  "roofline": broof, "decision_parity": rb["parity"], "clocks": rb["clocks"],
+                  "hit_rate": rb["hits"] / max(1, rb["hits"] + rb["misses"]),
+                  "loads_per_step": rb["loads"] / (nwin * K), "cold_experts_per_step": rb["cold_experts"] / (nwin * K),
+                  "host_cold_ms_per_step": rb["cpu_ms_cold"] / (nwin * K),
+                  "gpu_step_ms": rb["gpu_step_ms"], "host_arena_images": rb["n_images"],
+                  "e2e_bytes": {"h2d_bytes_per_step": int(rb["h2d"]), "d2h_bytes_per_step": int(rb["d2h"])}}
+        if not args.no_cpu_baseline:
+            cbb = cpu_path_sample(wb, args.cpu_budget_s, use_ref_sched=True)
+            budget["cpu_baseline"] = {k: cbb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["detail"]["budget"] = budget
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

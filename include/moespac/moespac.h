@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define MOESPAC_ABI_VERSION 1
+#define MOESPAC_ABI_VERSION 2
 
 typedef enum moespac_status {
   MOESPAC_OK = 0,
@@ -94,8 +94,7 @@ typedef struct moespac_step_report {
    * and the host time spent on them */
   int32_t cold_experts;
   float cpu_ms_cold;
-  /* K3 launches this step: n_layers, or 1 when the persistent K3 ran the
-   * whole step (combine included) */
+  /* K3 launches this step (one per layer) */
   int32_t ffn_launches;
 } moespac_step_report;
 
@@ -286,6 +285,10 @@ moespac_status moespac_ffn_combine(const moespac_combine_args* a, void* stream);
 moespac_status moespac_pack_expert(const uint16_t* w_gate_dev, const uint16_t* w_up_dev,
                                    const uint16_t* w_down_dev, int d_model, int d_ffn, int kernel,
                                    uint16_t* image_dev, void* stream);
+/* Inverse of moespac_pack_expert: tiled image -> standard layouts (export /
+ * checkpointing of the resident pool; parity checks on synthetic images). */
+moespac_status moespac_unpack_expert(const uint16_t* image_dev, int d_model, int d_ffn, int kernel,
+                                     uint16_t* w_gate_dev, uint16_t* w_up_dev, uint16_t* w_down_dev, void* stream);
 moespac_status moespac_fill_synthetic(uint16_t* dev, int64_t n_elems, uint64_t seed, float stdv, void* stream);
 
 /* ------------------------------------------------------------------ engine context
@@ -302,7 +305,16 @@ typedef struct moespac_model_desc {
   int32_t gate_mode;      /* see moespac_router_topk */
   int32_t ffn_kernel;     /* MOESPAC_FFN_*; expert images use its layout */
   int32_t parallel_mode;  /* world > 1 only — MOESPAC_PAR_*; see below */
+  int32_t shared_gate;    /* MOESPAC_SHARED_GATE_*: how shared units enter the layer output */
 } moespac_model_desc;
+
+/* Shared-expert gate (SURVEY.md §8 gate flags): NONE adds the shared units
+ * with weight 1 (DeepSeek-V2-Lite); SIGMOID scales them per token by
+ * sigmoid(w_sg . h_t) with a per-layer gate vector w_sg [d_model]
+ * (Qwen1.5-MoE's shared_expert_gate; set with moespac_ctx_set_shared_gate;
+ * grouped tensor-core K3 only: d_model <= 2048). */
+#define MOESPAC_SHARED_GATE_NONE 0
+#define MOESPAC_SHARED_GATE_SIGMOID 1
 
 /* Multi-GPU modes (shard_world > 1 in moespac_ctx_create):
  * EXPERT: expert e lives on rank e % world (its own slot pool, the
@@ -330,6 +342,10 @@ moespac_status moespac_ctx_host_arena(moespac_ctx* c, int64_t n_images, uint16_t
 moespac_status moespac_ctx_fill_synthetic(moespac_ctx* c, uint64_t seed, float stdv);
 /* Shared units of layer l from a device buffer [n_shared_units][image]. */
 moespac_status moespac_ctx_set_shared(moespac_ctx* c, int layer, const uint16_t* units_dev);
+/* Shared-expert gate vector of layer l, [d_model] bf16 (host or device
+ * pointer), for MOESPAC_SHARED_GATE_SIGMOID (filled synthetically by
+ * moespac_ctx_fill_synthetic otherwise). */
+moespac_status moespac_ctx_set_shared_gate(moespac_ctx* c, int layer, const uint16_t* w_sg);
 /* Upload the warm-fill residents (sim_core.cpp:108-111) from the arena. */
 moespac_status moespac_ctx_finalize(moespac_ctx* c);
 /* Expert-parallel combine over NCCL: 128-byte ncclUniqueId from rank 0. */
@@ -353,12 +369,6 @@ moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
  * the device, and added by the combine): -1 = all cores (default), 0 = off
  * (misses are counted but not computed). Takes effect at moespac_ctx_finalize. */
 moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
-/* Persistent K3 (tensor-core grouped kernel with the layer loop and the
- * combine inside, one launch per step, grid barriers between layers;
- * eligible when d_model <= 2048, one device, no host cold path, trace-driven
- * routing). Off by default: measured ~15% slower than the per-layer K3 +
- * combine launches on the Qwen3 shape. */
-moespac_status moespac_ctx_set_persistent(moespac_ctx* c, int enabled);
 /* Emulated draft window (off by default): each step first holds the compute
  * stream for gamma * t_draft_unit_ns (the reference's modeled draft phase,
  * sim_core.cpp:167-172) while the copy engine works through the step's
@@ -437,6 +447,8 @@ typedef struct moespac_ctx_views {
   const uint16_t* pool_dev;     /* [L][slots][image] */
   const double* logits_dev;     /* [L][T][N] router logits (trace input, or K0's output in model mode) */
   int64_t slots_per_layer, image_elems;
+  const uint16_t* shared_dev;   /* [L][n_shared_units][image] shared-expert units */
+  const uint16_t* shared_gate_dev; /* [L][d] bf16 shared-expert gate vectors (SIGMOID), else NULL */
 } moespac_ctx_views;
 moespac_status moespac_ctx_get_views(const moespac_ctx* c, moespac_ctx_views* out);
 /* Decision tables the last executed step ran with (the context's scheduler

@@ -176,13 +176,23 @@ def expert_apply(h_bits, tok, gate, wg, wu, wd, y, n_threads=0):
                            wg.ctypes.data, wu.ctypes.data, wd.ctypes.data, y, n_threads)
 
 
-def moe_layer(h_bits, ids, gates, experts, shared=(), n_threads=0):
+def shared_gate(h_bits, w_sg_bits):
+    """Qwen1.5-MoE shared-expert gate (public HF config `shared_expert_gate`,
+    SURVEY.md §8 gate flags; not in the reference): g_t = sigmoid(w_sg . h_t)
+    in fp64, one value per token."""
+    h = bf16_bits_to_f32(h_bits).astype(np.float64)
+    w = bf16_bits_to_f32(w_sg_bits).astype(np.float64)
+    return 1.0 / (1.0 + np.exp(-(h @ w)))
+
+
+def moe_layer(h_bits, ids, gates, experts, shared=(), n_threads=0, shared_gates=None):
     """Eq. 3 MoE layer output y (fp64 [T][d]) over the given experts.
 
     experts: dict expert_id -> (wg[ffn][d], wu[ffn][d], wd[d][ffn]) bf16 bits;
              activations whose expert is absent from the dict are skipped
              (cold / other-shard experts).
-    shared:  sequence of (wg, wu, wd) applied to every token with gate 1.
+    shared:  sequence of (wg, wu, wd) applied to every token with gate 1, or
+             with gate shared_gates[t] when given (see shared_gate()).
     """
     T, d = h_bits.shape
     y = np.zeros((T, d), np.float64)
@@ -193,8 +203,9 @@ def moe_layer(h_bits, ids, gates, experts, shared=(), n_threads=0):
         if toks:
             wg, wu, wd = experts[e]
             expert_apply(h_bits, toks, g, wg, wu, wd, y, n_threads)
+    sg = [1.0] * T if shared_gates is None else [float(x) for x in shared_gates]
     for wg, wu, wd in shared:
-        expert_apply(h_bits, list(range(T)), [1.0] * T, wg, wu, wd, y, n_threads)
+        expert_apply(h_bits, list(range(T)), sg, wg, wu, wd, y, n_threads)
     return y
 
 
@@ -305,10 +316,12 @@ EV_DRAFT, EV_CPU, EV_GPU, EV_STALL, EV_LOAD, EV_EVICT = range(6)
 def ref_sim_run(cfg: RefSimConfig, ids: np.ndarray, accepted: np.ndarray) -> RefRun:
     S = len(accepted)
     L = cfg.n_layers
-    lr = np.zeros((S, L, 10), np.int64)
-    sr = np.zeros((S, 8), np.int64)
-    acc = np.zeros(S, np.float64)
-    cap = S * (1 + L * (4 + 2 * cfg.n_experts))
+    # AR mode runs one simulated step per accepted token (sim_core.cpp:306-313)
+    R = int(np.sum(accepted)) if cfg.policy == POLICIES.index("ar_mode") else S
+    lr = np.zeros((R, L, 10), np.int64)
+    sr = np.zeros((R, 8), np.int64)
+    acc = np.zeros(R, np.float64)
+    cap = R * (1 + L * (4 + 2 * cfg.n_experts))
     ev = np.zeros((cap, 6), np.int64)
     nev = np.zeros(1, np.int64)
     tot = np.zeros(1, np.int64)

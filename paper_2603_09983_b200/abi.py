@@ -113,7 +113,8 @@ class RunSummary(C.Structure):
 class ModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32), ("gamma", C.c_int32),
                 ("d_model", C.c_int32), ("d_ffn", C.c_int32), ("n_shared_units", C.c_int32),
-                ("gate_mode", C.c_int32), ("ffn_kernel", C.c_int32), ("parallel_mode", C.c_int32)]
+                ("gate_mode", C.c_int32), ("ffn_kernel", C.c_int32), ("parallel_mode", C.c_int32),
+                ("shared_gate", C.c_int32)]
 
 
 class CtxViews(C.Structure):
@@ -121,7 +122,7 @@ class CtxViews(C.Structure):
                 ("offsets_dev", C.c_void_p), ("perm_dev", C.c_void_p), ("counters_dev", C.c_void_p),
                 ("est_state_dev", C.c_void_p), ("h_dev", C.c_void_p), ("y_dev", C.c_void_p),
                 ("pool_dev", C.c_void_p), ("logits_dev", C.c_void_p), ("slots_per_layer", C.c_int64),
-                ("image_elems", C.c_int64)]
+                ("image_elems", C.c_int64), ("shared_dev", C.c_void_p), ("shared_gate_dev", C.c_void_p)]
 
 
 POLICIES = ["moe_spac", "on_demand_gpu", "lru_cache", "static_split", "ar_mode",
@@ -170,6 +171,8 @@ def lib() -> C.CDLL:
         "moespac_ffn_resolve": (C.c_int, [C.c_int, C.c_int, C.c_int]),
         "moespac_build_hT": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
         "moespac_fill_synthetic": (C.c_int, [vp, i64, C.c_uint64, C.c_float, vp]),
+        "moespac_unpack_expert": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
+        "moespac_ctx_set_shared_gate": (C.c_int, [vp, C.c_int, vp]),
         "moespac_ctx_create": (C.c_int, [C.c_int, C.POINTER(ModelDesc), C.POINTER(SchedConfig), C.c_int, C.c_int,
                                          C.POINTER(vp)]),
         "moespac_ctx_destroy": (None, [vp]),
@@ -181,7 +184,6 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
-        "moespac_ctx_set_persistent": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_draft_window": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
         "moespac_ctx_set_l2_prefetch": (C.c_int, [vp, C.c_int]),
@@ -468,6 +470,20 @@ def pack_expert(wg, wu, wd, kernel: int = FFN_AUTO, stream=None):
     return out
 
 
+def unpack_expert(image, d: int, ffn: int, kernel: int = FFN_AUTO, stream=None):
+    """Tiled image (device tensor) -> (w_gate [ffn][d], w_up [ffn][d], w_down [d][ffn]) int16 views."""
+    import torch
+    dev = image.device
+    wg = torch.empty((ffn, d), dtype=torch.int16, device=dev)
+    wu = torch.empty((ffn, d), dtype=torch.int16, device=dev)
+    wd = torch.empty((d, ffn), dtype=torch.int16, device=dev)
+    check(lib().moespac_unpack_expert(ptr(image), d, ffn, kernel, ptr(wg), ptr(wu), ptr(wd), _stream(stream)))
+    return wg, wu, wd
+
+
+SHARED_GATE_NONE, SHARED_GATE_SIGMOID = 0, 1
+
+
 def build_hT(h, stream=None):
     """[T][d] bf16 (int16 view) -> h^T UMMA image for the tensor-core K3."""
     import torch
@@ -486,7 +502,8 @@ class Context:
         h = C.c_void_p()
         check(lib().moespac_ctx_create(device, C.byref(model), C.byref(cfg), rank, world, C.byref(h)))
         self._h = h
-        self.T = model.gamma + 1
+        # AR policy: one token per step (the context runs at T = 1)
+        self.T = 1 if cfg.policy == POLICIES.index("ar_mode") else model.gamma + 1
         self.image_elems = expert_image_elems(model.d_model, model.d_ffn)
 
     def close(self):
@@ -508,6 +525,12 @@ class Context:
     def set_shared(self, layer: int, units_dev):
         check(lib().moespac_ctx_set_shared(self._h, layer, ptr(units_dev)))
 
+    def set_shared_gate(self, layer: int, w) -> None:
+        """Shared-expert gate vector w_sg of a layer, [d_model] bf16 (host array or device tensor)."""
+        if isinstance(w, np.ndarray):
+            w = np.ascontiguousarray(w.view(np.uint16))
+        check(lib().moespac_ctx_set_shared_gate(self._h, layer, ptr(w)))
+
     def finalize(self):
         check(lib().moespac_ctx_finalize(self._h))
 
@@ -519,9 +542,6 @@ class Context:
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))
-
-    def set_persistent(self, on: bool = True):
-        check(lib().moespac_ctx_set_persistent(self._h, int(on)))
 
     def set_draft_window(self, on: bool = True):
         check(lib().moespac_ctx_set_draft_window(self._h, int(on)))

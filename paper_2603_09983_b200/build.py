@@ -29,7 +29,6 @@ SOURCES = [
     "kernels/expert_ffn.cu",
     "kernels/expert_ffn_tc.cu",
     "kernels/expert_ffn_grouped.cu",
-    "kernels/expert_ffn_persistent.cu",
     "host/scheduler.cpp",
     "host/step_scheduler.cpp",
     "host/engine.cpp",

@@ -7,6 +7,9 @@ Mixtral and Qwen3 renormalise over the top-k (Eq. 3, gate_mode 0);
 Qwen1.5-MoE and DeepSeek-V2-Lite take the softmax over all N (gate_mode 1).
 Shared experts are expressed as units of d_ffn rows (Qwen1.5: one 5632-row
 shared expert = 4 units of 1408; DeepSeek-V2-Lite: 2 x 1408 = 2 units).
+Qwen1.5-MoE scales its shared expert per token by sigmoid(w_sg . h_t)
+(`shared_expert_gate`, shared_gate=1); DeepSeek-V2-Lite adds its shared
+experts with weight 1.
 DeepSeek-V2-Lite's first layer is dense in the real model; BASELINE.json
 names 27 layers and all 27 are modeled as MoE layers here (one layer more of
 expert work than the model has).
@@ -29,6 +32,7 @@ class WorkloadConfig:
     gate_mode: int = 0
     cache_ratio: float = 0.17
     description: str = ""
+    shared_gate: int = 0  # MOESPAC_SHARED_GATE_*: 1 = per-token sigmoid(w_sg . h) (Qwen1.5-MoE)
 
     @property
     def tokens(self) -> int:
@@ -41,6 +45,11 @@ class WorkloadConfig:
     def with_(self, **kw) -> "WorkloadConfig":
         return replace(self, **kw)
 
+    def model_desc(self, ffn_kernel: int = 0, parallel_mode: int = 0):
+        from . import abi
+        return abi.ModelDesc(self.n_layers, self.n_experts, self.top_k, self.gamma, self.d_model, self.d_ffn,
+                             self.n_shared_units, self.gate_mode, ffn_kernel, parallel_mode, self.shared_gate)
+
 
 CONFIGS = {
     "tiny": WorkloadConfig("tiny", 1, 8, 2, 4, 512, 1024, 0, 0, 0.17,
@@ -48,7 +57,8 @@ CONFIGS = {
     "mixtral": WorkloadConfig("mixtral", 32, 8, 2, 4, 4096, 14336, 0, 0, 1.0,
                               "Mixtral-8x7B-shaped MoE layer: 8 experts top-2, d=4096, ffn=14336, draft_len=4, bf16"),
     "qwen15": WorkloadConfig("qwen15", 24, 60, 4, 6, 2048, 1408, 4, 1, 0.5,
-                             "Qwen1.5-MoE-A2.7B shape: 60 experts top-4 + shared expert, draft_len=6, 50% cache"),
+                             "Qwen1.5-MoE-A2.7B shape: 60 experts top-4 + shared expert, draft_len=6, 50% cache",
+                             shared_gate=1),
     "dsv2": WorkloadConfig("dsv2", 27, 64, 6, 8, 2048, 1408, 2, 1, 0.17,
                            "DeepSeek-V2-Lite shape: 64 routed experts top-6, 27 layers, draft_len=8"),
     "qwen3": WorkloadConfig("qwen3", 48, 128, 8, 8, 2048, 768, 0, 0, 0.17,

@@ -534,6 +534,19 @@ moespac_status moespac_pack_expert(const uint16_t* wg, const uint16_t* wu, const
   });
 }
 
+moespac_status moespac_unpack_expert(const uint16_t* image, int d, int ffn, int kernel, uint16_t* wg, uint16_t* wu,
+                                     uint16_t* wd, void* stream) {
+  return guard([&] {
+    const int kern = ffn_resolve(kernel, d, ffn);
+    if (!ffn_shape_ok(kern, d, ffn)) throw std::invalid_argument("moespac_unpack_expert: shape");
+    require_device();
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_ok(kern == kFfnTensorCore ? launch_unpack_expert_tc(image, d, ffn, wg, wu, wd, st)
+                                   : launch_unpack_expert(image, d, ffn, wg, wu, wd, st),
+            "unpack_expert");
+  });
+}
+
 moespac_status moespac_fill_synthetic(uint16_t* dst, int64_t n, uint64_t seed, float stdv, void* stream) {
   return guard([&] {
     if (n < 0) throw std::invalid_argument("moespac_fill_synthetic: n");
@@ -559,6 +572,10 @@ moespac_status moespac_ctx_host_arena(moespac_ctx* c, int64_t n_images, uint16_t
 
 moespac_status moespac_ctx_fill_synthetic(moespac_ctx* c, uint64_t seed, float stdv) {
   return guard([&] { c->e.fill_synthetic(seed, stdv); });
+}
+
+moespac_status moespac_ctx_set_shared_gate(moespac_ctx* c, int layer, const uint16_t* w_sg) {
+  return guard([&] { c->e.set_shared_gate(layer, w_sg); });
 }
 
 moespac_status moespac_ctx_set_shared(moespac_ctx* c, int layer, const uint16_t* units) {
@@ -600,10 +617,6 @@ moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes) {
 
 moespac_status moespac_ctx_set_draft_window(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_draft_window(enabled != 0); });
-}
-
-moespac_status moespac_ctx_set_persistent(moespac_ctx* c, int enabled) {
-  return guard([&] { c->e.set_persistent(enabled != 0); });
 }
 
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {

@@ -136,9 +136,17 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   if (m.gamma + 1 > kFfnMaxTokens) throw std::invalid_argument("moespac_model_desc: gamma + 1 must be <= 16");
   if (m.n_experts > 1024) throw std::invalid_argument("moespac_model_desc: n_experts must be <= 1024");
   if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("moespac_ctx: bad shard rank/world");
+  if (m.shared_gate != MOESPAC_SHARED_GATE_NONE && m.shared_gate != MOESPAC_SHARED_GATE_SIGMOID)
+    throw std::invalid_argument("moespac_model_desc: shared_gate");
   if (m.n_layers != c.n_layers || m.n_experts != c.n_experts || m.top_k != c.top_k || m.gamma != c.gamma)
     throw std::invalid_argument("moespac_ctx: model desc and sched config disagree on the workload shape");
-  T_ = m.gamma + 1;
+  // AR mode (policies.hpp ar_mode; sim_core.cpp:148-152, 306-313): every
+  // step verifies ONE token — the reference feeds one token's frequencies per
+  // simulated step and advances a token cursor through the trace step — so
+  // the context runs the whole step (K1 .. combine) at T = 1; the driver
+  // passes that token's logits [L][1][N] and hidden state [1][d].
+  ar_ = static_cast<PolicyKind>(c.policy) == PolicyKind::ar_mode;
+  T_ = ar_ ? 1 : m.gamma + 1;
   W_ = (m.n_experts + 31) / 32;
   image_elems_ = 3LL * m.d_ffn * m.d_model;
 
@@ -196,6 +204,10 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
       !ffn_tg_grid_ok(m.n_experts + m.n_shared_units, m.d_ffn, sms_))  // (not at 148 SMs)
     plan = ffn_tc_plan(T_, m.d_model, smem_optin, 3);
   if (plan.n_stages == 0) throw std::invalid_argument("moespac_ctx: (gamma+1) x d_model too large for shared memory");
+  if (m.shared_gate == MOESPAC_SHARED_GATE_SIGMOID && m.n_shared_units > 0 &&
+      !(kernel_ == kFfnTensorCore && plan.acc_mode == 3))
+    throw std::invalid_argument("moespac_model_desc: the sigmoid shared-expert gate needs the grouped tensor-core K3 "
+                                "(d_model <= 2048)");
   stages_ = plan.n_stages;
   global_acc_ = plan.global_acc;
   acc_mode_ = plan.acc_mode;
@@ -210,6 +222,10 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
           "cudaMalloc shared");
   if (m.n_shared_units > 0)
     check(cudaMemset(shared_, 0, static_cast<size_t>(L) * m.n_shared_units * image_elems_ * 2), "memset");
+  if (m.shared_gate == MOESPAC_SHARED_GATE_SIGMOID && m.n_shared_units > 0) {
+    dmalloc(reinterpret_cast<void**>(&sg_w_), sizeof(uint16_t) * L * d, "cudaMalloc shared gate");
+    check(cudaMemset(sg_w_, 0, sizeof(uint16_t) * L * d), "memset");
+  }
   dmalloc(reinterpret_cast<void**>(&logits_d_), sizeof(double) * L * T_ * N, "cudaMalloc logits");
   dmalloc(reinterpret_cast<void**>(&ids_d_), sizeof(int32_t) * L * T_ * k, "cudaMalloc ids");
   dmalloc(reinterpret_cast<void**>(&gates_d_), sizeof(float) * L * T_ * k, "cudaMalloc gates");
@@ -225,13 +241,6 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   check(cudaMemset(hT_d_, 0, sizeof(uint16_t) * 2 * 16 * d), "memset hT");  // token pad rows stay zero
   work_bytes_ = static_cast<size_t>(sms_ + N + m.n_shared_units) * T_ * d * 4;
   dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
-  dmalloc(reinterpret_cast<void**>(&sync_d_), sizeof(unsigned) * 2, "cudaMalloc sync");
-  if (kernel_ == kFfnTensorCore && acc_mode_ == 3 && world_ == 1) {
-    persist_ring_ = ffn_tp_ring_bytes(T_, d, prop.sharedMemPerBlockOptin);
-    persist_smem_ = ffn_tp_smem_bytes(d, persist_ring_);
-    persist_ok_ = persist_ring_ > 0 && ffn_tp_ok(N + m.n_shared_units, m.d_ffn, sms_, sms_);
-  }
-  if (const char* e = std::getenv("MOESPAC_PERSISTENT")) persistent_ = std::atoi(e) != 0;
   cold_trace_ = std::getenv("MOESPAC_COLD_TRACE") != nullptr;
   dmalloc(reinterpret_cast<void**>(&ycold_d_), sizeof(float) * L * T_ * d, "cudaMalloc ycold");
   check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocDefault),
@@ -284,7 +293,7 @@ Engine::~Engine() {
                   static_cast<void*>(offsets_d_), static_cast<void*>(perm_d_), static_cast<void*>(hit_list_d_),
                   static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
-                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sync_d_)})
+                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sg_w_)})
     if (p) cudaFree(p);
   cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
@@ -343,6 +352,10 @@ void Engine::fill_synthetic(uint64_t seed, float stdv) {
       check(launch_fill_synthetic(shared_ + (static_cast<int64_t>(l) * m_.n_shared_units + u) * image_elems_,
                                   image_elems_, image_seed(seed ^ 0x5bd1e995ULL, l * 64 + u), stdv, compute_),
             "fill shared");
+  if (sg_w_)
+    check(launch_fill_synthetic(sg_w_, static_cast<long long>(m_.n_layers) * m_.d_model,
+                                image_seed(seed ^ 0x27d4eb2fULL, 0), stdv, compute_),
+          "fill shared gate");
   check(cudaStreamSynchronize(compute_), "sync");
   cudaFree(tmp);
   synthetic_ = true;
@@ -356,6 +369,15 @@ void Engine::set_shared(int layer, const uint16_t* units_dev) {
                         static_cast<size_t>(m_.n_shared_units) * image_elems_ * 2, cudaMemcpyDeviceToDevice, compute_),
         "copy shared");
   check(cudaStreamSynchronize(compute_), "sync");
+}
+
+void Engine::set_shared_gate(int layer, const uint16_t* w) {
+  if (layer < 0 || layer >= m_.n_layers) throw std::out_of_range("moespac_ctx_set_shared_gate: layer out of range");
+  if (!sg_w_) throw std::logic_error("moespac_ctx_set_shared_gate: model has no sigmoid shared-expert gate");
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  check(cudaMemcpy(sg_w_ + static_cast<size_t>(layer) * m_.d_model, w, sizeof(uint16_t) * m_.d_model,
+                   cudaMemcpyDefault),
+        "shared gate");
 }
 
 // Warm fill (sim_core.cpp:108-111): the residents the scheduler placed at
@@ -624,7 +646,10 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     // so its prologue and first weight copies overlap that kernel's tail.
     const bool has_loads = layer_loads_local[static_cast<size_t>(l)] > 0;
     if (has_loads) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
-    const bool pdl = pdl_ && !has_loads && !timing_;
+    // (model mode: K3 follows route_layer, whose routing tables its prologue
+    // reads before griddepcontrol.wait — only a full dependency makes them
+    // visible, so no programmatic launch there)
+    const bool pdl = pdl_ && !has_loads && !timing_ && !model_mode_;
     dev::FfnArgs fa{};
     fa.h = h_d_ + static_cast<size_t>(l) * T_ * d;
     fa.T = T_;
@@ -641,6 +666,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.pool = pool_ + static_cast<int64_t>(l) * slots_ * image_elems_;
     fa.shared_w = shared_ + static_cast<int64_t>(l) * m_.n_shared_units * image_elems_;
     fa.n_shared = n_shared_eff;  // expert-parallel: shared units are computed once, on rank 0
+    fa.shared_gate_w = sg_w_ ? sg_w_ + static_cast<size_t>(l) * d : nullptr;
     fa.expert_elems = image_elems_;
     fa.partial = work_d_;
     fa.n_stages = stages_;
@@ -730,45 +756,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   float cpu_ms_cold = 0.f;
   int cold_experts = 0;
 
-  const bool persist = !cold && persistent_ && persist_ok_ && !model_mode_;
-  if (persist) {
-    // ---- one persistent K3 for the whole step, combine inside; its layer 0
-    // streams after every load of the step has landed
-    if (n_loads > 0) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(L - 1)], 0), "wait loads");
-    check(cudaMemsetAsync(sync_d_, 0, sizeof(unsigned) * 2, compute_), "memset sync");
-    dev::PersistArgs pa{};
-    pa.T = T_;
-    pa.d = d;
-    pa.ffn = m_.d_ffn;
-    pa.k = k;
-    pa.N = N;
-    pa.L = L;
-    pa.n_shared = m_.n_shared_units;
-    pa.expert_elems = image_elems_;
-    pa.pool_layer_elems = slots_ * image_elems_;
-    pa.pool = pool_;
-    pa.shared_w = shared_;
-    pa.slot_of = slots_d;
-    pa.hit_list = hit_list_d_;
-    pa.hit_ord = hit_ord_d_;
-    pa.counters = counters_d;
-    pa.offsets = offsets_d_;
-    pa.perm = perm_d_;
-    pa.gates = gates_d_;
-    pa.ids = ids_d_;
-    pa.h = h_d_;
-    pa.y = y_d_;
-    pa.hT = hT_d_;
-    pa.partial = work_d_;
-    pa.ring_bytes = persist_ring_;
-    pa.sync = sync_d_;
-    pa.dbg = k3_trace_;
-    if (timing_) check(cudaEventRecord(ffn_beg_[0], compute_), "event");
-    check(launch_expert_ffn_persistent(pa, sms_, persist_smem_, compute_), "K3 persistent");
-    if (timing_) check(cudaEventRecord(ffn_end_[0], compute_), "event");
-    check(cudaEventSynchronize(k2_done_), "sync K2");
-    host_account();
-  } else if (!cold) {
+  if (!cold) {
     // ---- all layers on the device back to back; host accounting overlaps
     for (int l = 0; l < L; ++l) {
       if (model_mode_) {
@@ -874,19 +862,30 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     rep->n_experts = N;
     rep->n_layers = L;
     rep->n_loads = n_loads;
-    int64_t units = 0;
-    for (int l = 0; l < L; ++l) units += oc[static_cast<size_t>(l)].n_local_hits + n_shared_eff;
-    rep->ffn_bytes = units * image_elems_ * 2;
+    // K3 bytes this rank streamed: its (hit experts + shared units) x image;
+    // in the unit-split mode only its CTAs' slice [rank, rank+1) * sms of the
+    // virtual grid's units (8 ffn rows each)
+    int64_t bytes = 0;
+    for (int l = 0; l < L; ++l) {
+      const int64_t ent = oc[static_cast<size_t>(l)].n_local_hits + n_shared_eff;
+      if (!split_) {
+        bytes += ent * image_elems_ * 2;
+      } else {
+        const int64_t upe = m_.d_ffn / 8, n = ent * upe, G = static_cast<int64_t>(world_) * sms_;
+        const int64_t u0 = static_cast<int64_t>(rank_) * sms_ * n / G, u1 = static_cast<int64_t>(rank_ + 1) * sms_ * n / G;
+        bytes += (u1 - u0) * (image_elems_ * 2 / upe);
+      }
+    }
+    rep->ffn_bytes = bytes;
     rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads) * image_elems_ * 2 +
                      (logits_host && !replay_ids_ && !model_mode_ ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
                      (replay_ids_ ? static_cast<int64_t>(sizeof(int32_t) + sizeof(float)) * L * T_ * k : 0) +
                      (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
     rep->d2h_bytes =
         static_cast<int64_t>(out_bytes_) + (h_out && h_out_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
-    rep->kernel_launches = persist ? (replay_ids_ ? 1 : 2) + 1 + 1
-                                   : (model_mode_ ? 4 * L : (replay_ids_ ? 1 : 2) + 2 * L) + (tc ? 1 : 0) +
-                                         (world_ > 1 ? L : 0);
-    rep->ffn_launches = persist ? 1 : L;
+    rep->kernel_launches =
+        (model_mode_ ? 4 * L : (replay_ids_ ? 1 : 2) + 2 * L) + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
+    rep->ffn_launches = L;
     rep->cold_experts = cold_experts;
     rep->cpu_ms_cold = cpu_ms_cold;
     if (timing_) {
@@ -899,7 +898,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       rep->gpu_ms_router = ms(ev_[1], ev_[2]);
       rep->gpu_ms_hist = ms(ev_[2], ev_[3]);
       float f = 0.f;
-      for (int l = 0; l < (persist ? 1 : L); ++l)
+      for (int l = 0; l < L; ++l)
         f += ms(ffn_beg_[static_cast<size_t>(l)], ffn_end_[static_cast<size_t>(l)]);
       rep->gpu_ms_ffn = f;
       rep->gpu_ms_combine = ms(ev_[3], ev_[4]) - f;
@@ -951,6 +950,8 @@ void Engine::views(moespac_ctx_views* v) const {
   v->logits_dev = logits_d_;
   v->slots_per_layer = slots_;
   v->image_elems = image_elems_;
+  v->shared_dev = shared_;
+  v->shared_gate_dev = sg_w_;
 }
 
 }  // namespace moespac

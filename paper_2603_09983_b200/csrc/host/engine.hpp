@@ -63,12 +63,12 @@ class Engine {
   uint16_t* host_arena(int64_t n_images);
   void fill_synthetic(uint64_t seed, float stdv);
   void set_shared(int layer, const uint16_t* units_dev);
+  void set_shared_gate(int layer, const uint16_t* w_sg);
   void finalize();
   void set_nccl(const void* uid, int nranks, int rank);
   void set_timing(bool on) { timing_ = on; }
   void set_pdl(bool on) { pdl_ = on; }
   void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
-  void set_persistent(bool on) { persistent_ = on; }
   void set_draft_window(bool on) { draft_window_ = on; }
   void set_loopback(LoopbackGroup* g) {
     if (!g || g->world() != world_) throw std::invalid_argument("moespac_ctx_set_loopback: group size != shard world");
@@ -113,6 +113,7 @@ class Engine {
   // (0, 1) in the unit-split mode (every expert on every rank)
   int shard_rank_ = 0, shard_world_ = 1;
   bool split_ = false;
+  bool ar_ = false;  // AR policy: T = 1 token per step
   size_t ffn_smem_ = 0;
   moespac_model_desc m_{};
   std::unique_ptr<StepScheduler> sched_;
@@ -124,6 +125,7 @@ class Engine {
   // HBM
   uint16_t* pool_ = nullptr;    // [L][slots][image]
   uint16_t* shared_ = nullptr;  // [L][n_shared][image]
+  uint16_t* sg_w_ = nullptr;    // [L][d] bf16 shared-expert gate vectors (MOESPAC_SHARED_GATE_SIGMOID)
   double* logits_d_ = nullptr;
   int32_t *ids_d_ = nullptr, *freqs_d_ = nullptr, *offsets_d_ = nullptr, *perm_d_ = nullptr;
   int32_t *hit_list_d_ = nullptr, *hit_ord_d_ = nullptr, *est_d_ = nullptr;
@@ -156,12 +158,7 @@ class Engine {
   uint16_t* wg_d_ = nullptr;      // [L][N][d] bf16 router weights (model mode)
   std::vector<bool> router_set_;
   bool model_mode_ = false;       // set for the duration of step_model()
-  // persistent K3 (expert_ffn_persistent.cu): plan and grid-barrier counters
   bool draft_window_ = false;  // emulated γ·t_draft spin on the compute stream before K1
-  bool persistent_ = false, persist_ok_ = false;  // measured slower than per-layer launches
-  int persist_ring_ = 0;
-  size_t persist_smem_ = 0;
-  unsigned* sync_d_ = nullptr;
   int acc_mode_ = 0;
 
   std::unique_ptr<ColdExecutor> cold_;

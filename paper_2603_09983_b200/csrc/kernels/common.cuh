@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <utility>
 
 namespace moespac {
@@ -86,6 +87,10 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // bf16x2 word -> two fp32 (exact).
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 v, float (&o)[8]) {
+  o[0] = bf_lo(v.x), o[1] = bf_hi(v.x), o[2] = bf_lo(v.y), o[3] = bf_hi(v.y);
+  o[4] = bf_lo(v.z), o[5] = bf_hi(v.z), o[6] = bf_lo(v.w), o[7] = bf_hi(v.w);
+}
 
 __device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
   uint32_t u = __float_as_uint(f);
@@ -103,6 +108,22 @@ __device__ __forceinline__ uint16_t f32_to_bf16_cvt(float f) {
 }
 
 }  // namespace dev
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set it once
+// per (kernel, device), thread-safe (loopback ranks drive contexts from
+// several host threads).
+template <auto Kernel>
+inline cudaError_t smem_optin_once(int bytes) {
+  constexpr int kMaxDev = 64;
+  static std::once_flag once[kMaxDev];
+  static cudaError_t err[kMaxDev];
+  int dev = 0;
+  const cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDev) return cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  std::call_once(once[dev], [&] { err[dev] = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); });
+  return err[dev];
+}
 
 // Launch with the programmatic-stream-serialization attribute (kernels call
 // pdl_wait() before touching their predecessor's outputs).

@@ -622,9 +622,12 @@ __global__ void residual_kernel(const uint16_t* h_in, const float* y, uint16_t* 
 }
 
 // ---------------------------------------------------------------- packing
-// Standard layouts (wg, wu: [ffn][d], wd: [d][ffn]) -> tiled expert image.
-__global__ void pack_expert_kernel(const uint16_t* __restrict__ wg, const uint16_t* __restrict__ wu,
-                                   const uint16_t* __restrict__ wd, int d, int ffn, uint16_t* __restrict__ out) {
+// Standard layouts (wg, wu: [ffn][d], wd: [d][ffn]) <-> tiled expert image:
+// kUnpack = false packs (image element idx gathers its source element), true
+// unpacks (the same index map, scattered back).
+template <bool kUnpack>
+__global__ void pack_expert_kernel(uint16_t* __restrict__ wg, uint16_t* __restrict__ wu, uint16_t* __restrict__ wd,
+                                   int d, int ffn, uint16_t* __restrict__ out) {
   const long long total = 3LL * ffn * d;
   const long long chunk = 3LL * FC * d;
   const long long gu = 2LL * FC * d;
@@ -635,21 +638,24 @@ __global__ void pack_expert_kernel(const uint16_t* __restrict__ wg, const uint16
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long c = idx / chunk;
     const long long r = idx % chunk;
-    uint16_t v;
+    uint16_t* src;
     if (r < gu) {
       const long long tile = r / TILE_ELEMS, within = r % TILE_ELEMS;
       const int row = static_cast<int>(within / 256), col = static_cast<int>(within % 256);
       const long long src_col = tile * 256 + col;
-      v = row < FC ? wg[(c * FC + row) * d + src_col] : wu[(c * FC + row - FC) * d + src_col];
+      src = row < FC ? &wg[(c * FC + row) * d + src_col] : &wu[(c * FC + row - FC) * d + src_col];
     } else {
       const long long r2 = r - gu;
       const long long tile = r2 / TILE_ELEMS, within = r2 % TILE_ELEMS;
       const int row = static_cast<int>(within / DW), col = static_cast<int>(within % DW);
       const long long ct2 = tile / nrg, fg = tile % nrg;
       const long long f = c * FC + fg * DR + row;
-      v = wd[(ct2 * DW + col) * ffn + f];
+      src = &wd[(ct2 * DW + col) * ffn + f];
     }
-    out[idx] = v;
+    if (kUnpack)
+      *src = out[idx];
+    else
+      out[idx] = *src;
   }
 }
 
@@ -701,12 +707,7 @@ FfnPlan ffn_plan(int T, int d, size_t smem_limit) {
 }
 
 cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(dev::expert_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (const cudaError_t e = smem_optin_once<dev::expert_ffn_kernel>(232448); e != cudaSuccess) return e;
   return launch_pdl(dev::expert_ffn_kernel, dim3(grid), dim3(dev::FFN_THREADS), smem, stream, pdl, a);
 }
 
@@ -762,7 +763,14 @@ cudaError_t launch_draft_window(long long ns, cudaStream_t stream) {
 
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream) {
-  dev::pack_expert_kernel<<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, out);
+  dev::pack_expert_kernel<false><<<1184, 256, 0, stream>>>(const_cast<uint16_t*>(wg), const_cast<uint16_t*>(wu),
+                                                           const_cast<uint16_t*>(wd), d, ffn, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_expert(const uint16_t* image, int d, int ffn, uint16_t* wg, uint16_t* wu, uint16_t* wd,
+                                 cudaStream_t stream) {
+  dev::pack_expert_kernel<true><<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, const_cast<uint16_t*>(image));
   return cudaGetLastError();
 }
 

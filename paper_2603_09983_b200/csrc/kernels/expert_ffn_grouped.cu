@@ -189,6 +189,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   p += ENT_MAX * 4;
   int* misc = reinterpret_cast<int*>(p);  // [1] TMEM base
   p += 16;
+  float* sg_part = reinterpret_cast<float*>(p);  // [4 warps][16 tokens] shared-gate partial dots
+  p += 4 * 16 * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(p) + 7) & ~uintptr_t(7));
   uint64_t* full = bars;
   uint64_t* empty = full + NSLOT;
@@ -545,6 +547,48 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       pdl_wait();  // partial blocks are still being read by the previous combine
       const int q = warp & 3;   // TMEM lane quarter = group slot
       const int et = tid - 64;  // 0..127
+      if (a.shared_gate_w && o_first + n_ent - 1 >= n_hits) {
+        // ---- sigmoid shared-expert gate (Qwen1.5-MoE): g_t = sigmoid(w_sg . h_t)
+        // from the resident h^T slices, one fixed order for every CTA (thread
+        // et: 8-k chunks et, et + 128, ...; xor butterfly; warps in order);
+        // it replaces the weight-1 gates the staging gave the shared entries
+        for (int kt = 0; kt < ktiles; ++kt) mbar_wait(&ht_full[kt], 0);
+        float acc[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) acc[t] = 0.f;
+        const uint16_t* ht16 = reinterpret_cast<const uint16_t*>(hts);
+        for (int c8 = et; c8 < d / 8; c8 += EPI_THREADS) {
+          const int kt = c8 >> 3, j = c8 & 7;
+          const uint4 wv = *reinterpret_cast<const uint4*>(a.shared_gate_w + static_cast<size_t>(c8) * 8);
+          float w8[8];
+          bf16x8_to_f32(wv, w8);
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            if (t < T) {
+              const uint4 hv = *reinterpret_cast<const uint4*>(ht16 + kt * 1024 + (t >> 3) * 512 + j * 64 + (t & 7) * 8);
+              float h8[8];
+              bf16x8_to_f32(hv, h8);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[t] = fmaf(w8[e], h8[e], acc[t]);
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) sg_part[q * 16 + t] = acc[t];
+        }
+        named_bar_sync(2, EPI_THREADS);
+        const float z = lane < T ? ((sg_part[lane] + sg_part[16 + lane]) + sg_part[32 + lane]) + sg_part[48 + lane] : 0.f;
+        const float sg = lane < T ? 1.f / (1.f + expf(-z)) : 0.f;
+        for (int r = warp - 2; r < n_ent; r += 4)
+          if (o_first + r >= n_hits && lane < 16) ent_gate[r * 16 + lane] = sg;
+        named_bar_sync(2, EPI_THREADS);
+      }
       Phase d1f[2], atf[2];
       long long w_d1f = 0, w_d2f = 0;
       GroupIt it{u0, u1, upe};
@@ -687,7 +731,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 
 size_t ffn_tg_smem_bytes(int d, int ring_bytes) {
   return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * dev::tg::HTS + static_cast<size_t>(ring_bytes) + dev::tg::UB +
-         dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
+         dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 4 * 16 * 4 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
 }
 
 // Every CTA's range must touch <= ENT_MAX entries (one producer lane each).
@@ -711,13 +755,7 @@ int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
 }
 
 cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(dev::tg::expert_ffn_tg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (const cudaError_t e = smem_optin_once<dev::tg::expert_ffn_tg_kernel>(232448); e != cudaSuccess) return e;
   return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, a);
 }
 

@@ -950,16 +950,18 @@ __global__ void build_hT_kernel(const uint16_t* __restrict__ h, int T, int d, ui
   }
 }
 
-// Standard layouts -> v2 tiled image (see file header).
-__global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uint16_t* __restrict__ wu,
-                                      const uint16_t* __restrict__ wd, int d, int ffn, uint16_t* __restrict__ out) {
+// Standard layouts <-> v2 tiled image (see file header); kUnpack scatters
+// the image back through the same index map.
+template <bool kUnpack>
+__global__ void pack_expert_tc_kernel(uint16_t* __restrict__ wg, uint16_t* __restrict__ wu, uint16_t* __restrict__ wd,
+                                      int d, int ffn, uint16_t* __restrict__ out) {
   const long long total = 3LL * ffn * d;
   const long long chunk = 3LL * FCH * d;
   const long long gu = 2LL * FCH * d;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long c = idx / chunk, r0 = idx % chunk;
-    uint16_t v;
+    uint16_t* src;
     if (r0 < gu) {
       const long long kt = r0 / 8192;
       const int w = static_cast<int>(r0 % 8192);
@@ -969,7 +971,7 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
       const int qq = row >> 5, s = row & 31;
       const long long f = c * FCH + qq * 16 + ((s >> 4) << 3) + (s & 7);
       const long long k = kt * 64 + j * 8 + e;
-      v = ((s >> 3) & 1) ? wu[f * d + k] : wg[f * d + k];
+      src = ((s >> 3) & 1) ? &wu[f * d + k] : &wg[f * d + k];
     } else {
       const long long r2 = r0 - gu;
       const long long mt = r2 / 8192;
@@ -977,9 +979,12 @@ __global__ void pack_expert_tc_kernel(const uint16_t* __restrict__ wg, const uin
       const int j = w >> 10, g = (w >> 6) & 15, r = (w >> 3) & 7, e = w & 7;
       const long long orow = mt * 128 + g * 8 + r;
       const long long f = c * FCH + j * 8 + e;
-      v = wd[orow * ffn + f];
+      src = &wd[orow * ffn + f];
     }
-    out[idx] = v;
+    if (kUnpack)
+      *src = out[idx];
+    else
+      out[idx] = *src;
   }
 }
 
@@ -1046,13 +1051,7 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
 
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
   if (a.acc_mode == dev::tc::ACC_GROUP) return launch_expert_ffn_tg(a, grid, smem, stream, pdl);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(dev::tc::expert_ffn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (const cudaError_t e = smem_optin_once<dev::tc::expert_ffn_tc_kernel>(232448); e != cudaSuccess) return e;
   return launch_pdl(dev::tc::expert_ffn_tc_kernel, dim3(grid), dim3(dev::tc::THREADS), smem, stream, pdl, a);
 }
 
@@ -1063,7 +1062,14 @@ cudaError_t launch_build_hT(const uint16_t* h, int T, int d, uint16_t* out, cuda
 
 cudaError_t launch_pack_expert_tc(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                   uint16_t* out, cudaStream_t stream) {
-  dev::tc::pack_expert_tc_kernel<<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, out);
+  dev::tc::pack_expert_tc_kernel<false><<<1184, 256, 0, stream>>>(
+      const_cast<uint16_t*>(wg), const_cast<uint16_t*>(wu), const_cast<uint16_t*>(wd), d, ffn, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_expert_tc(const uint16_t* image, int d, int ffn, uint16_t* wg, uint16_t* wu, uint16_t* wd,
+                                    cudaStream_t stream) {
+  dev::tc::pack_expert_tc_kernel<true><<<1184, 256, 0, stream>>>(wg, wu, wd, d, ffn, const_cast<uint16_t*>(image));
   return cudaGetLastError();
 }
 

@@ -39,6 +39,7 @@ struct FfnArgs {
   const uint16_t* pool;     // tiled expert images, stride expert_elems
   const uint16_t* shared_w; // tiled shared-expert units, stride expert_elems
   int n_shared;
+  const uint16_t* shared_gate_w;  // [d] bf16: shared units weighted by sigmoid(w . h_t) (null: weight 1)
   long long expert_elems;   // 3*ffn*d
   float* partial;           // [(grid + N + n_shared)][T][d]
   int n_stages;             // CUDA-core kernel: ring stages
@@ -64,31 +65,6 @@ struct FfnArgs {
   // grid) of a virtual grid of cta_total CTAs over the layer's work units
   // (cta_total 0: the launch grid itself)
   int cta_base, cta_total;
-};
-
-// Persistent grouped K3 (expert_ffn_persistent.cu): every layer of a step in
-// one launch, combine included. Per-layer tables are [L]-major.
-struct PersistArgs {
-  int T, d, ffn, k, N, L, n_shared;
-  long long expert_elems;       // 3*ffn*d
-  long long pool_layer_elems;   // slots * expert_elems (layer stride of `pool`)
-  const uint16_t* pool;         // [L][slots][image]
-  const uint16_t* shared_w;     // [L][n_shared][image]
-  const int32_t* slot_of;       // [L][N]
-  const int32_t* hit_list;      // [L][N]
-  const int32_t* hit_ord;       // [L][N]
-  const int32_t* counters;      // [L][8]
-  const int32_t* offsets;       // [L][N+1]
-  const int32_t* perm;          // [L][T*k]
-  const float* gates;           // [L][T*k]
-  const int32_t* ids;           // [L][T*k]
-  uint16_t* h;                  // [L+1][T][d] bf16: h[0] input, h[l+1] written per layer
-  float* y;                     // [L][T][d] fp32 MoE outputs
-  uint16_t* hT;                 // [2][16*d] h^T images (layer parity); hT[0] = layer 0's, built before launch
-  float* partial;               // [grid][T][d]
-  int ring_bytes;
-  unsigned* sync;               // [2] grid-barrier counters, zeroed before launch
-  unsigned long long* dbg;      // optional [L][grid][32] stamps
 };
 
 struct CombineArgs {
@@ -133,10 +109,6 @@ cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cuda
 size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, int acc_mode);
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum = 0);
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
-size_t ffn_tp_smem_bytes(int d, int ring_bytes);
-int ffn_tp_ring_bytes(int T, int d, size_t smem_limit);
-bool ffn_tp_ok(int n_entries, int d_ffn, int grid, int sms);
-cudaError_t launch_expert_ffn_persistent(const dev::PersistArgs& a, int grid, size_t smem, cudaStream_t stream);
 size_t ffn_tg_smem_bytes(int d, int ring_bytes);
 int ffn_tg_ring_bytes(int T, int d, size_t smem_limit);
 bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid);
@@ -150,6 +122,10 @@ cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_ou
 cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float* out, size_t n, cudaStream_t stream);
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream);
+cudaError_t launch_unpack_expert(const uint16_t* image, int d, int ffn, uint16_t* wg, uint16_t* wu, uint16_t* wd,
+                                 cudaStream_t stream);
+cudaError_t launch_unpack_expert_tc(const uint16_t* image, int d, int ffn, uint16_t* wg, uint16_t* wu, uint16_t* wd,
+                                    cudaStream_t stream);
 cudaError_t launch_fill_synthetic(uint16_t* out, long long n, uint64_t seed, float stdv, cudaStream_t stream);
 cudaError_t launch_draft_window(long long ns, cudaStream_t stream);
 

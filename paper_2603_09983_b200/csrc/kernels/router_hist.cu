@@ -361,13 +361,7 @@ cudaError_t launch_router_gemv(const uint16_t* wg, const uint16_t* h, int T, int
                                cudaStream_t stream, bool pdl) {
   if (d % 256 || T < 1 || T > 16) return cudaErrorInvalidValue;
   const size_t smem = static_cast<size_t>(T) * d * 2;
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(dev::router_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               16 * 4096 * 2);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (const cudaError_t e = smem_optin_once<dev::router_gemv_kernel>(16 * 4096 * 2); e != cudaSuccess) return e;
   return launch_pdl(dev::router_gemv_kernel, dim3((N + dev::K0_WARPS - 1) / dev::K0_WARPS),
                     dim3(dev::K0_WARPS * 32), smem, stream, pdl, wg, h, T, N, d, logits);
 }

@@ -39,6 +39,9 @@ SIM_CASES = [
     ("fixed_boundaries", 4, 32, 8, 8, 0.17, "fixed_boundaries", 60),
     ("binary_utility", 4, 32, 8, 8, 0.17, "binary_utility", 60),
     ("shift_regime", 6, 64, 6, 8, 0.25, "moe_spac", 60),
+    ("mixtral_c100", 32, 8, 2, 4, 1.00, "moe_spac", 60),   # the bench headline's budget
+    ("ar_mode", 4, 32, 8, 8, 0.17, "ar_mode", 30),         # one simulated step per accepted token
+    ("tiny_c100", 1, 8, 2, 4, 1.00, "moe_spac", 200),
 ]
 
 
@@ -53,16 +56,20 @@ def sim_case(name, L, N, k, g, cache, policy, steps, **extra):
                 total_time_ns=run.total_time_ns)
 
 
-def main():
+def main(only=None):
     if not O.ref_available():
         O.build()
     assert O.ref_available(), "needs /root/reference to build oracle/_ref"
     for case in SIM_CASES:
+        if only and case[0] not in only:
+            continue
         name = case[0]
         extra = {"shift_period": 7, "drift_scale": 0.5} if name == "shift_regime" else {}
         d = sim_case(*case, **extra)
         np.savez_compressed(os.path.join(HERE, f"sim_{name}.npz"), **d)
         print(name, d["ids"].shape, d["events"].shape)
+    if only:
+        return
 
     # estimator fuzz (acceptance C4 style; seed 777)
     rng = np.random.default_rng(777)
@@ -115,4 +122,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    # `make_golden.py name ...` regenerates only those sim cases
+    if len(sys.argv) > 1:
+        main(set(sys.argv[1:]))
+    else:
+        main()

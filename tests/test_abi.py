@@ -21,7 +21,7 @@ def test_library_exports_every_header_function():
 
 
 def test_abi_version_and_defaults():
-    assert abi.lib().moespac_abi_version() == 1
+    assert abi.lib().moespac_abi_version() == 2
     c = abi.default_config()
     # default_sim_config(), core/src/config.cpp:11-39
     assert (c.n_layers, c.n_experts, c.top_k, c.gamma) == (48, 128, 8, 8)

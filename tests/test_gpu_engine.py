@@ -374,49 +374,6 @@ def test_expert_parallel_device_path(world, cache, kernel, cold, mode):
     group.close()
 
 
-@pytest.mark.parametrize("L,N,k,g,d,ffn,units", [
-    (6, 4, 2, 4, 512, 64, 0),      # most CTAs idle in every layer (few units)
-    (4, 32, 8, 8, 2048, 128, 0),   # Qwen3-like routing density
-    (3, 16, 4, 6, 1024, 256, 2),   # shared units
-    (2, 128, 8, 15, 2048, 64, 0),  # T = 16
-])
-def test_persistent_k3_matches_per_layer_and_oracle(L, N, k, g, d, ffn, units):
-    """The persistent K3 (all layers + the combine in one launch, grid
-    barriers between layers) against the per-layer K3 + combine path and the
-    fp64 oracle, over several steps."""
-    rng = np.random.default_rng(L * 7 + N)
-    std, shared = _experts(rng, L, N, d, ffn, units)
-    a, _ = _make_ctx(L, N, k, g, d, ffn, units, 0, 1.0, std, shared, abi.FFN_TENSOR, cold=0)
-    b, _ = _make_ctx(L, N, k, g, d, ffn, units, 0, 1.0, std, shared, abi.FFN_TENSOR, cold=0)
-    a.set_persistent(True)
-    b.set_persistent(False)
-    T = g + 1
-    gen = O.Generator(L, N, k, g, seed=9)
-    for s in range(4):
-        logits, ids, acc = gen.next_step()
-        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
-        ha, hb = np.zeros_like(h0), np.zeros_like(h0)
-        ra, _ = a.step(logits, h0, acc, ha)
-        rb_, _ = b.step(logits, h0, acc, hb)
-        assert ra.ffn_launches == 1 and rb_.ffn_launches == L
-        va = a.views()
-        hs = abi.fetch(va.h_dev, (L + 1, T, d), np.uint16)
-        ys = abi.fetch(va.y_dev, (L, T, d), np.float32)
-        assert np.array_equal(hs[0], h0) and np.array_equal(hs[L], ha)
-        for l in range(L):
-            _, gates = O.router_topk(logits[l], k, 0)
-            y_ref = O.moe_layer(hs[l], ids[l], gates, {e: std[(l, e)] for e in range(N)}, shared[l])
-            rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
-            assert rel <= 1e-5, (s, l, rel)
-        # same step through the per-layer path: the two combines add the same
-        # partials in another order, so h differs by bf16 roundings that the
-        # following layers carry along — compare in norm
-        fa, fb = O.bf16_bits_to_f32(ha).astype(np.float64), O.bf16_bits_to_f32(hb).astype(np.float64)
-        assert np.linalg.norm(fa - fb) <= 4e-3 * np.linalg.norm(fb), s
-        assert [ra.cache_hits, ra.cache_misses] == [rb_.cache_hits, rb_.cache_misses]
-    assert np.array_equal(a.sched_events(), b.sched_events())
-
-
 def test_draft_window_overlaps_loads_and_changes_nothing_else():
     """The emulated draft window (γ·t_draft spin on the compute stream) adds
     its time to the step and leaves every output and decision unchanged."""

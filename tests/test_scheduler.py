@@ -31,10 +31,16 @@ def replay(cfg, ids, accepted, shard_world=1, cap=None):
     est = [O.estimator_init(N, g, init_up, init_down) for _ in range(L)]
     scores = np.zeros((L, N), np.int32)
     recs, steps = [], []
-    for st in range(len(accepted)):
+    # AR mode: one scheduler step per accepted token of a trace step, fed that
+    # token's frequencies (sim_core.cpp:148-152, 181-183, 306-313)
+    if pol == "ar_mode":
+        windows = [(st, slice(c, c + 1), 1) for st in range(len(accepted)) for c in range(int(accepted[st]))]
+    else:
+        windows = [(st, slice(None), int(accepted[st])) for st in range(len(accepted))]
+    for st, tok, acc in windows:
         s.decide(scores)
-        freqs = np.stack([O.hist_scan(ids[st, l], N)[0] for l in range(L)])
-        rep, lay = s.observe_freqs(freqs, int(accepted[st]))
+        freqs = np.stack([O.hist_scan(ids[st, l][tok], N)[0] for l in range(L)])
+        rep, lay = s.observe_freqs(freqs, acc)
         recs.append([[x.tau, x.fallback, x.n_prefetch, x.t_cpu_ns, x.t_gpu_ns, x.t_io_used_ns, x.stall_ns,
                       x.wall_ns, x.bubble_ns] for x in lay])
         steps.append(rep)
