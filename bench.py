@@ -274,6 +274,7 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
     import torch
 
     from paper_2603_09983_b200 import abi
+    from paper_2603_09983_b200.configs import SYNTH_STD
 
     torch.cuda.set_device(local_rank)
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
@@ -283,7 +284,7 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
     def make_ctx():
         c = abi.Context(local_rank, model, cfg, rank, world)
         c.host_arena(n_images_for(w))
-        c.fill_synthetic(seed=3, stdv=0.02)
+        c.fill_synthetic(seed=3, stdv=SYNTH_STD)
         if args.router_gemv:
             c.set_cold_threads(0)
         c.finalize()

@@ -519,7 +519,7 @@ class Context:
         arr = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint16)), shape=(n_images, self.image_elems))
         return arr
 
-    def fill_synthetic(self, seed: int = 3, stdv: float = 0.02):
+    def fill_synthetic(self, seed: int = 3, stdv: float = 0.006):
         check(lib().moespac_ctx_fill_synthetic(self._h, seed, stdv))
 
     def set_shared(self, layer: int, units_dev):

@@ -19,6 +19,15 @@ from __future__ import annotations
 from dataclasses import dataclass, replace
 
 
+# Synthetic weight scale: bf16 ~ N(0, SYNTH_STD^2) for every gate/up/down
+# entry. The layers have no norms, so the residual stream h_{l+1} = h_l + y_l
+# must not blow up over 24-48 layers: a SwiGLU expert scales as |h|^2, and at
+# std 0.02 the Mixtral shape (d = 4096, ffn = 14336) overflows to inf by
+# layer ~16. At 0.006 every BASELINE shape keeps |y| << |h| (values stay
+# finite and parity-checkable; timing does not depend on the values).
+SYNTH_STD = 0.006
+
+
 @dataclass(frozen=True)
 class WorkloadConfig:
     name: str

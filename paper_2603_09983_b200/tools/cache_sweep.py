@@ -24,6 +24,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2603_09983_b200 import abi, configs  # noqa: E402
+from paper_2603_09983_b200.configs import SYNTH_STD  # noqa: E402
 
 
 def run_ratio(w, ratio, steps, warmup, cold_threads, profile, draft=False):
@@ -31,7 +32,7 @@ def run_ratio(w, ratio, steps, warmup, cold_threads, profile, draft=False):
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=ratio, **profile)
     ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode, 0), cfg, 0, 1)
     ctx.host_arena(min(L * N, max(N, 8)))
-    ctx.fill_synthetic(seed=3, stdv=0.02)
+    ctx.fill_synthetic(seed=3, stdv=SYNTH_STD)
     ctx.set_cold_threads(cold_threads)
     ctx.finalize()
     ctx.set_draft_window(draft)

@@ -30,7 +30,7 @@ import torch
 
 import oracle as O
 from paper_2603_09983_b200 import abi
-from paper_2603_09983_b200.configs import CONFIGS
+from paper_2603_09983_b200.configs import CONFIGS, SYNTH_STD
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -87,7 +87,7 @@ def _build(w, n_images, cold=-1):
     ctx = abi.Context(0, w.model_desc(), cfg)
     ctx.set_cold_threads(cold)
     arena = ctx.host_arena(n_images)
-    ctx.fill_synthetic(seed=3, stdv=0.02)
+    ctx.fill_synthetic(seed=3, stdv=SYNTH_STD)
     ctx.finalize()
     kernel = abi.ffn_resolve(abi.FFN_AUTO, w.d_model, w.d_ffn)
     return ctx, arena, Weights(ctx, arena, w, n_images, kernel)
@@ -99,6 +99,7 @@ def _check_layer(W, w, logits_l, ids_l, hs, ys, l, tag):
     sg = W.shared_gate(l)
     sgt = None if sg is None else O.shared_gate(hs[l], sg)
     y_ref = O.moe_layer(hs[l], ids_l, gates, experts, W.shared(l), shared_gates=sgt)
+    assert np.isfinite(ys[l]).all() and np.isfinite(y_ref).all(), (tag, l)
     rel = np.linalg.norm(ys[l] - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
     assert rel <= 1e-5, (tag, l, rel)
     exact = O.bf16_bits_to_f32(hs[l]).astype(np.float64) + y_ref
