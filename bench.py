@@ -65,6 +65,11 @@ def parse_args():
                     help="extra untimed steps before the timed windows when the cache budget is < 1 "
                          "(the warm fill holds experts 0..cap-1, not the hot ones)")
     ap.add_argument("--ffn-kernel", type=int, default=0, help="0 auto (tcgen05), 1 CUDA-core GEMV, 2 tcgen05")
+    ap.add_argument("--draft-params", type=float, default=2e9,
+                    help="detail.draft_verify leg: a dense bf16 draft model of this many parameters (2e9 bf16 = the "
+                         "~4 GB a Qwen3-4B-FP8 draft token streams) drafting gamma tokens before each verification "
+                         "step on the same GPU; 0 skips the leg")
+    ap.add_argument("--draft-d", type=int, default=2560)
     ap.add_argument("--no-budget", action="store_true",
                     help="skip the cache-budget leg (detail.budget: a BASELINE budget config, real expert loads "
                          "and the host cold path, median of windows)")
@@ -270,7 +275,7 @@ def n_images_for(w):
     return min(w.n_layers * w.n_experts, n)
 
 
-def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", steps=None):
+def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", steps=None, draft_params=0):
     import torch
 
     from paper_2603_09983_b200 import abi
@@ -290,6 +295,8 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
         c.finalize()
         if args.draft_window:
             c.set_draft_window(True)
+        if draft_params > 0:
+            c.set_draft_model(int(draft_params), args.draft_d)
         if args.router_gemv:
             gw = torch.Generator().manual_seed(4)
             for l in range(L):
@@ -430,6 +437,7 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
         "gpu_step_ms": float(np.mean([r.gpu_ms_total for r in reps_ev])),
         "layers_other_ms": float(np.mean([r.gpu_ms_combine for r in reps_ev])),
         "ms_ev": ms_ev, "ms_st": ms_st, "parity": parity, "n_images": n_images_for(w),
+        "draft_ms_ev": sum(r.gpu_ms_draft for r in reps_ev), "draft_bytes": sum(r.draft_bytes for r in reps_ev),
         "clocks": clk.summary(),
     }
     if world > 1:
@@ -536,6 +544,9 @@ def main():
         return
 
     r = run_ours(args, w, rank, world, local_rank)
+    rd = None
+    if args.draft_params > 0 and not args.router_gemv and not args.draft_window:
+        rd = run_ours(args, w, rank, world, local_rank, label="draft_verify", draft_params=args.draft_params)
     rb = None
     if world == 1 and not args.no_budget:
         wb = workload_named(args.budget_config, args.budget_cache)
@@ -566,6 +577,20 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_path_sample(w, args.cpu_budget_s, use_ref_sched=True)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rd is not None:
+        dtps, dtps_e2e, droof, _ = leg_summary(rd, w, args, world, hbm_peak, peak_kind)
+        dms = rd["draft_ms_ev"] / args.steps
+        dbytes = rd["draft_bytes"] / args.steps
+        line["detail"]["draft_verify"] = {
+            "value": dtps[0], "e2e": dtps_e2e[0], "unit": "tokens/s", "ms_per_step": rd["ms"] / args.steps,
+            "verify_only_value": tps[0],
+            "draft": f"dense bf16 draft model, {args.draft_params:.3g} parameters (rows of {args.draft_d}), gamma = "
+                     f"{w.gamma} autoregressive passes per step, each one weight-streaming GEMV over all of it, "
+                     "on the compute stream before the verification step, expert loads overlapping",
+            "draft_ms_per_step": dms, "draft_bytes_per_step": dbytes,
+            "draft_gbs": dbytes / (dms * 1e-3) / 1e9 if dms > 0 else None,
+            "draft_frac_of_peak": (dbytes / (dms * 1e-3) / 1e9) / hbm_peak if dms > 0 else None,
+            "k3_roofline_frac": droof["frac"], "decision_parity": rd["parity"]}
     if rb is not None:
         wb = workload_named(args.budget_config, args.budget_cache)
         btps, btps_e2e, broof, _ = leg_summary(rb, wb, args, world, hbm_peak, peak_kind)

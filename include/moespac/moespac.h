@@ -96,6 +96,10 @@ typedef struct moespac_step_report {
   float cpu_ms_cold;
   /* K3 launches this step (one per layer) */
   int32_t ffn_launches;
+  /* draft phase this step: device time (timing on) and draft-model weight
+   * bytes streamed (moespac_ctx_set_draft_model; 0 for the emulated window) */
+  float gpu_ms_draft;
+  int64_t draft_bytes;
 } moespac_step_report;
 
 /* Realized split of one layer (core/src/sim_core.cpp:233-283), as K2 emits it. */
@@ -375,6 +379,38 @@ moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
  * expert loads — the overlap the balancer's draft credit assumes. Steps then
  * measure draft + verification, the reference's TPS definition. */
 moespac_status moespac_ctx_set_draft_window(moespac_ctx* c, int enabled);
+/* Real draft phase (replaces the modeled window of
+ * sim_core.cpp:167-172): a dense draft model of n_params bf16 weights (rows
+ * of d_draft) on the same GPU; each step first runs gamma autoregressive
+ * draft passes — one weight-streaming GEMV over all n_params per draft token,
+ * each fed by the previous pass's output — on the compute stream, while the
+ * copy engine works through the step's expert loads. Steps then measure
+ * draft + verification. n_params = 0 turns it off. (Qwen3-4B-FP8, the
+ * paper's draft, streams ~4 GB per token: n_params 2e9 bf16, d_draft 2560.) */
+moespac_status moespac_ctx_set_draft_model(moespac_ctx* c, int64_t n_params, int d_draft);
+/* One draft pass as a stateless kernel (the draft model's building block):
+ * y [R] fp32 = W [R][D] bf16 . x, x = bf16(scale * y_prev[0:D]) or x0 [D]
+ * bf16 when y_prev is NULL. D as moespac_ctx_set_draft_model's d_draft. */
+moespac_status moespac_draft_gemv(const uint16_t* w_dev, int64_t rows, int d, const float* y_prev_dev,
+                                  const uint16_t* x0_dev, float scale, float* y_dev, void* stream);
+/* Measured timeline: while on, every step appends
+ * device-measured records in the reference's SimEvent schema
+ * (sim_core.hpp:65-73): [n][6] = kind (0 draft, 1 cpu, 2 gpu, 3 stall,
+ * 4 load, 5 evict), step, layer, expert, start_ns, duration_ns — gpu = K3 +
+ * combine of the layer on the compute stream, stall = the compute stream's
+ * wait for the layer's loads, load = one H2D copy on the copy stream, cpu =
+ * the host cold path of the layer (host clock; start = the layer's K3
+ * start), draft = the draft phase. Starts are on the context's measured
+ * clock (sum of earlier steps' totals). Implies per-kernel events (PDL off).
+ * timeline_layers: measured moespac_layer_timing per (step, layer) (ns;
+ * wall = previous layer's end -> this layer's end). timeline_steps:
+ * [n][6] = total, draft, prologue (H2D + K1 + K2), sum of layer walls,
+ * epilogue (D2H), step index — total == draft + prologue + walls + epilogue.
+ * Each getter returns the record count (out may be NULL). */
+moespac_status moespac_ctx_set_timeline(moespac_ctx* c, int enabled);
+int64_t moespac_ctx_timeline_events(const moespac_ctx* c, int64_t* out, int64_t cap);
+int64_t moespac_ctx_timeline_layers(const moespac_ctx* c, moespac_layer_timing* out, int64_t cap);
+int64_t moespac_ctx_timeline_steps(const moespac_ctx* c, int64_t* out, int64_t cap);
 /* Programmatic dependent launch between layer kernels (on by default). */
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
 /* Profiling hook: device buffer of [n_layers][grid][32] uint64 that every

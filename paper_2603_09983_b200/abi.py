@@ -60,7 +60,7 @@ class StepReport(C.Structure):
                 ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float),
                 ("ffn_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("kernel_launches", C.c_int32), ("cold_experts", C.c_int32), ("cpu_ms_cold", C.c_float),
-                ("ffn_launches", C.c_int32)]
+                ("ffn_launches", C.c_int32), ("gpu_ms_draft", C.c_float), ("draft_bytes", C.c_int64)]
 
 
 class LayerOutcome(C.Structure):
@@ -185,6 +185,12 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_draft_window": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_draft_model": (C.c_int, [vp, i64, C.c_int]),
+        "moespac_ctx_set_timeline": (C.c_int, [vp, C.c_int]),
+        "moespac_draft_gemv": (C.c_int, [vp, i64, C.c_int, vp, vp, C.c_float, vp, vp]),
+        "moespac_ctx_timeline_events": (i64, [vp, vp, i64]),
+        "moespac_ctx_timeline_layers": (i64, [vp, vp, i64]),
+        "moespac_ctx_timeline_steps": (i64, [vp, vp, i64]),
         "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
         "moespac_ctx_set_l2_prefetch": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
@@ -484,6 +490,15 @@ def unpack_expert(image, d: int, ffn: int, kernel: int = FFN_AUTO, stream=None):
 SHARED_GATE_NONE, SHARED_GATE_SIGMOID = 0, 1
 
 
+def draft_gemv(w, x0=None, y_prev=None, scale: float = 1.0, stream=None):
+    """One draft pass: y [R] fp32 = w [R][D] (bf16, int16 view) . x."""
+    import torch
+    R, D = w.shape
+    y = torch.empty(R, dtype=torch.float32, device=w.device)
+    check(lib().moespac_draft_gemv(ptr(w), R, D, ptr(y_prev), ptr(x0), scale, ptr(y), _stream(stream)))
+    return y
+
+
 def build_hT(h, stream=None):
     """[T][d] bf16 (int16 view) -> h^T UMMA image for the tensor-core K3."""
     import torch
@@ -545,6 +560,28 @@ class Context:
 
     def set_draft_window(self, on: bool = True):
         check(lib().moespac_ctx_set_draft_window(self._h, int(on)))
+
+    def set_draft_model(self, n_params: int, d_draft: int = 2560):
+        """Real draft phase: gamma weight-streaming GEMV passes over n_params bf16 weights per step (0: off)."""
+        check(lib().moespac_ctx_set_draft_model(self._h, int(n_params), int(d_draft)))
+
+    def set_timeline(self, on: bool = True):
+        """Measured SimEvent-shaped timeline (clears the previous one)."""
+        check(lib().moespac_ctx_set_timeline(self._h, int(on)))
+
+    def timeline(self):
+        """(events [n][6], measured LayerTiming rows [steps*L], steps [n][6])."""
+        f = lib()
+        n = f.moespac_ctx_timeline_events(self._h, None, 0)
+        ev = np.zeros((max(n, 1), 6), np.int64)
+        f.moespac_ctx_timeline_events(self._h, ev.ctypes.data, n)
+        nl = f.moespac_ctx_timeline_layers(self._h, None, 0)
+        lay = (LayerTiming * max(nl, 1))()
+        f.moespac_ctx_timeline_layers(self._h, lay, nl)
+        ns = f.moespac_ctx_timeline_steps(self._h, None, 0)
+        st = np.zeros((max(ns, 1), 6), np.int64)
+        f.moespac_ctx_timeline_steps(self._h, st.ctypes.data, ns)
+        return ev[:n], list(lay)[:nl], st[:ns]
 
     def set_l2_prefetch(self, nbytes: int):
         """Per-CTA cross-layer L2 prefetch budget of the tensor-core K3 (0 = off)."""

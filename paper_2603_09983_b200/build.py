@@ -29,6 +29,7 @@ SOURCES = [
     "kernels/expert_ffn.cu",
     "kernels/expert_ffn_tc.cu",
     "kernels/expert_ffn_grouped.cu",
+    "kernels/draft.cu",
     "host/scheduler.cpp",
     "host/step_scheduler.cpp",
     "host/engine.cpp",

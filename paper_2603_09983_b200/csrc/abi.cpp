@@ -619,6 +619,46 @@ moespac_status moespac_ctx_set_draft_window(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_draft_window(enabled != 0); });
 }
 
+moespac_status moespac_ctx_set_draft_model(moespac_ctx* c, int64_t n_params, int d_draft) {
+  return guard([&] {
+    if (n_params < 0) throw std::invalid_argument("moespac_ctx_set_draft_model: n_params must be >= 0");
+    c->e.set_draft_model(n_params, d_draft);
+  });
+}
+
+moespac_status moespac_draft_gemv(const uint16_t* w, int64_t rows, int d, const float* y_prev, const uint16_t* x0,
+                                  float scale, float* y, void* stream) {
+  return guard([&] {
+    if (!draft_d_ok(d) || rows < 1) throw std::invalid_argument("moespac_draft_gemv: shape");
+    if (!y_prev && !x0) throw std::invalid_argument("moespac_draft_gemv: y_prev or x0 required");
+    require_device();
+    int dev = 0, sms = 148;
+    cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_ok(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    cuda_ok(launch_draft_gemv(w, rows, d, y_prev, x0, scale, y, sms, static_cast<cudaStream_t>(stream)),
+            "draft_gemv");
+  });
+}
+
+moespac_status moespac_ctx_set_timeline(moespac_ctx* c, int enabled) {
+  return guard([&] {
+    c->e.timeline_clear();
+    c->e.set_timeline(enabled != 0);
+  });
+}
+
+int64_t moespac_ctx_timeline_events(const moespac_ctx* c, int64_t* out, int64_t cap) {
+  return c->e.timeline_events(out, cap);
+}
+
+int64_t moespac_ctx_timeline_layers(const moespac_ctx* c, moespac_layer_timing* out, int64_t cap) {
+  return c->e.timeline_layers(out, cap);
+}
+
+int64_t moespac_ctx_timeline_steps(const moespac_ctx* c, int64_t* out, int64_t cap) {
+  return c->e.timeline_steps(out, cap);
+}
+
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_pdl(enabled != 0); });
 }

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <exception>
 #include <cstdio>
 #include <cstdlib>
@@ -265,7 +266,11 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   load_done_.resize(static_cast<size_t>(L));
   ffn_beg_.resize(static_cast<size_t>(L));
   ffn_end_.resize(static_cast<size_t>(L));
+  wait_beg_.resize(static_cast<size_t>(L));
+  layer_end_.resize(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
+    check(cudaEventCreate(&wait_beg_[static_cast<size_t>(l)]), "event");
+    check(cudaEventCreate(&layer_end_[static_cast<size_t>(l)]), "event");
     check(cudaEventCreateWithFlags(&load_done_[static_cast<size_t>(l)], cudaEventDisableTiming), "event");
     check(cudaEventCreate(&ffn_beg_[static_cast<size_t>(l)]), "event");
     check(cudaEventCreate(&ffn_end_[static_cast<size_t>(l)]), "event");
@@ -293,7 +298,8 @@ Engine::~Engine() {
                   static_cast<void*>(offsets_d_), static_cast<void*>(perm_d_), static_cast<void*>(hit_list_d_),
                   static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
-                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sg_w_)})
+                  static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sg_w_),
+                  static_cast<void*>(draft_w_), static_cast<void*>(draft_y_), static_cast<void*>(draft_x0_)})
     if (p) cudaFree(p);
   cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
@@ -305,6 +311,8 @@ Engine::~Engine() {
   if (tables_h_) cudaFreeHost(tables_h_);
   if (out_h_) cudaFreeHost(out_h_);
   for (auto e : load_done_) cudaEventDestroy(e);
+  for (auto* v : {&wait_beg_, &layer_end_, &ld_beg_, &ld_end_})
+    for (auto e : *v) cudaEventDestroy(e);
   for (auto e : ffn_beg_) cudaEventDestroy(e);
   for (auto e : ffn_end_) cudaEventDestroy(e);
   for (auto e : ev_)
@@ -369,6 +377,50 @@ void Engine::set_shared(int layer, const uint16_t* units_dev) {
                         static_cast<size_t>(m_.n_shared_units) * image_elems_ * 2, cudaMemcpyDeviceToDevice, compute_),
         "copy shared");
   check(cudaStreamSynchronize(compute_), "sync");
+}
+
+void Engine::set_draft_model(int64_t n_params, int d_draft) {
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  for (void* p : {static_cast<void*>(draft_w_), static_cast<void*>(draft_y_), static_cast<void*>(draft_x0_)})
+    if (p) cudaFree(p);
+  draft_w_ = nullptr;
+  draft_y_ = nullptr;
+  draft_x0_ = nullptr;
+  draft_R_ = 0;
+  if (n_params == 0) return;  // off
+  if (!draft_d_ok(d_draft)) throw std::invalid_argument("moespac_ctx_set_draft_model: d_draft must be a multiple of 256 "
+                                                        "with d_draft / 256 in {1, 2, 4, 6, 8, 10, 12, 16}");
+  if (n_params < d_draft) throw std::invalid_argument("moespac_ctx_set_draft_model: n_params < d_draft");
+  draft_R_ = n_params / d_draft;
+  draft_D_ = d_draft;
+  constexpr float kStd = 0.006f;
+  draft_scale_ = 1.f / (kStd * std::sqrt(static_cast<float>(d_draft)));  // keeps x ~ N(0, 1) pass after pass
+  check(cudaMalloc(reinterpret_cast<void**>(&draft_w_), sizeof(uint16_t) * draft_R_ * d_draft), "cudaMalloc draft");
+  check(cudaMalloc(reinterpret_cast<void**>(&draft_y_), sizeof(float) * 2 * draft_R_), "cudaMalloc draft y");
+  check(cudaMalloc(reinterpret_cast<void**>(&draft_x0_), sizeof(uint16_t) * d_draft), "cudaMalloc draft x");
+  check(launch_fill_synthetic(draft_w_, draft_R_ * d_draft, 0xd4afULL, kStd, compute_), "fill draft");
+  check(launch_fill_synthetic(draft_x0_, d_draft, 0xd4b0ULL, 1.f, compute_), "fill draft x");
+  check(cudaStreamSynchronize(compute_), "sync");
+}
+
+int64_t Engine::timeline_events(int64_t* out, int64_t cap) const {
+  const int64_t n = static_cast<int64_t>(tl_events_.size());
+  for (int64_t i = 0; out && i < std::min(n, cap); ++i)
+    std::memcpy(out + 6 * i, tl_events_[static_cast<size_t>(i)].data(), sizeof(int64_t) * 6);
+  return n;
+}
+
+int64_t Engine::timeline_layers(moespac_layer_timing* out, int64_t cap) const {
+  const int64_t n = static_cast<int64_t>(tl_layers_.size());
+  for (int64_t i = 0; out && i < std::min(n, cap); ++i) out[i] = tl_layers_[static_cast<size_t>(i)];
+  return n;
+}
+
+int64_t Engine::timeline_steps(int64_t* out, int64_t cap) const {
+  const int64_t n = static_cast<int64_t>(tl_steps_.size());
+  for (int64_t i = 0; out && i < std::min(n, cap); ++i)
+    std::memcpy(out + 6 * i, tl_steps_[static_cast<size_t>(i)].data(), sizeof(int64_t) * 6);
+  return n;
 }
 
 void Engine::set_shared_gate(int layer, const uint16_t* w) {
@@ -513,8 +565,17 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   const int32_t* taus_d = reinterpret_cast<const int32_t*>(lb_d + static_cast<size_t>(L) * W_);
   const int32_t* slots_d = taus_d + L;
   std::vector<int> layer_loads(static_cast<size_t>(L), 0), layer_loads_local(static_cast<size_t>(L), 0);
+  // per-kernel CUDA events (set_timing) — also for the measured timeline
+  const bool timing = timing_ || timeline_;
+  std::vector<std::vector<int>> tl_evicts;
+  std::vector<int> tl_load_expert, tl_load_layer;
+  std::vector<float> tl_cpu_ms(static_cast<size_t>(L), 0.f);
+  if (timeline_) {
+    for (int l = 0; l < L; ++l) tl_evicts.push_back(sched_->evicted(l));
+    sched_decisions_ = sched_->decisions();
+  }
 
-  if (timing_) check(cudaEventRecord(ev_[0], compute_), "event");
+  if (timing) check(cudaEventRecord(ev_[0], compute_), "event");
   // ---- compute stream
   check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
@@ -528,12 +589,25 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   check(cudaMemcpyAsync(h_d_, h_in, sizeof(uint16_t) * T_ * d,
                         h_in_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, compute_),
         "h_in");
-  // emulated draft window: the step's loads (issued below on the copy
-  // stream) overlap it, as the reference's decisions assume (draft credit)
-  if (draft_window_) check(launch_draft_window(static_cast<long long>(T_ - 1) * sched_->config().profile.t_draft_unit_ns,
-                                               compute_),
-                           "draft window");
-  if (timing_) check(cudaEventRecord(ev_[1], compute_), "event");
+  // Draft phase before the verification: the step's loads (issued below on
+  // the copy stream) overlap it, as the reference's decisions assume (draft
+  // credit, sim_core.cpp:167-172). Draft model: gamma weight-streaming GEMV
+  // passes, each fed by the previous one (real HBM / SM contention);
+  // otherwise the emulated window holds the stream for gamma * t_draft.
+  if (timing) check(cudaEventRecord(ev_[6], compute_), "event");
+  const int n_draft = T_ - 1;  // gamma (0 in AR mode)
+  const bool drafted = n_draft > 0 && (draft_R_ > 0 || draft_window_);
+  if (draft_R_ > 0) {
+    for (int i = 0; i < n_draft; ++i)
+      check(launch_draft_gemv(draft_w_, draft_R_, draft_D_, i == 0 ? nullptr : draft_y_ + ((i - 1) & 1) * draft_R_,
+                              draft_x0_, draft_scale_, draft_y_ + (i & 1) * draft_R_, sms_, compute_,
+                              pdl_ && !timing && i > 0),
+            "draft pass");
+  } else if (draft_window_) {
+    check(launch_draft_window(static_cast<long long>(n_draft) * sched_->config().profile.t_draft_unit_ns, compute_),
+          "draft window");
+  }
+  if (timing) check(cudaEventRecord(ev_[1], compute_), "event");
   if (replay_ids_) {
     // recorded routing: ids ascending per token (the order K1 emits and the
     // combine's row lists rely on), gates carried along
@@ -556,7 +630,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   } else if (!model_mode_) {
     check(launch_router_topk(lg, L * T_, N, k, m_.gate_mode, ids_d_, gates_d_, compute_), "K1 router");
   }
-  if (timing_) check(cudaEventRecord(ev_[2], compute_), "event");
+  if (timing) check(cudaEventRecord(ev_[2], compute_), "event");
   dev::K2Args a2{};
   a2.ids = ids_d_;
   a2.L = L;
@@ -586,7 +660,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   a2.scores_out = scores_out_d;
   a2.gates = gates_d_;
   if (!model_mode_) check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
-  if (timing_) check(cudaEventRecord(ev_[3], compute_), "event");
+  if (timing) check(cudaEventRecord(ev_[3], compute_), "event");
   // scores + counters (+ routing for the cold path) back to the host right
   // away: the host scheduler works on them while the device runs the layers
   // (model mode: each layer's routing is known only after the layer before
@@ -614,7 +688,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   // being overwritten is still read by an in-flight FFN (the device-side
   // meaning of the reference's frozen score, execution_engine.cpp:111-118).
   int n_loads = 0;
-  if (timing_) check(cudaEventRecord(copy_ev_[0], copy_), "event");
+  if (timing) check(cudaEventRecord(copy_ev_[0], copy_), "event");
   {
     size_t i = 0;
     const auto& loads = sched_->loads();
@@ -624,15 +698,27 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         ++layer_loads[static_cast<size_t>(l)];
         if (ld.shard != shard_rank_) continue;
         ++layer_loads_local[static_cast<size_t>(l)];
+        if (timeline_) {
+          while (ld_beg_.size() <= static_cast<size_t>(n_loads)) {
+            ld_beg_.emplace_back();
+            ld_end_.emplace_back();
+            check(cudaEventCreate(&ld_beg_.back()), "event");
+            check(cudaEventCreate(&ld_end_.back()), "event");
+          }
+          check(cudaEventRecord(ld_beg_[static_cast<size_t>(n_loads)], copy_), "event");
+          tl_load_expert.push_back(ld.expert);
+          tl_load_layer.push_back(l);
+        }
         check(cudaMemcpyAsync(slot_ptr(l, ld.slot), arena_h_ + image_of(l, ld.expert) * image_elems_,
                               image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
               "H2D expert load");
+        if (timeline_) check(cudaEventRecord(ld_end_[static_cast<size_t>(n_loads)], copy_), "event");
         ++n_loads;
       }
       check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
     }
   }
-  if (timing_) check(cudaEventRecord(copy_ev_[1], copy_), "event");
+  if (timing) check(cudaEventRecord(copy_ev_[1], copy_), "event");
   // shared units: rank 0 in the expert-partitioned mode; in the unit-split
   // mode they are units of the split work list like any expert's
   const int n_shared_eff = (world_ > 1 && !split_ && rank_ != 0) ? 0 : m_.n_shared_units;
@@ -645,11 +731,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     // other K3 is launched programmatically-dependent on the previous kernel
     // so its prologue and first weight copies overlap that kernel's tail.
     const bool has_loads = layer_loads_local[static_cast<size_t>(l)] > 0;
+    if (timeline_) check(cudaEventRecord(wait_beg_[static_cast<size_t>(l)], compute_), "event");
     if (has_loads) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
     // (model mode: K3 follows route_layer, whose routing tables its prologue
     // reads before griddepcontrol.wait — only a full dependency makes them
     // visible, so no programmatic launch there)
-    const bool pdl = pdl_ && !has_loads && !timing_ && !model_mode_;
+    const bool pdl = pdl_ && !has_loads && !timing && !model_mode_;
     dev::FfnArgs fa{};
     fa.h = h_d_ + static_cast<size_t>(l) * T_ * d;
     fa.T = T_;
@@ -694,11 +781,11 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       fa.nx_shared_w = shared_ + static_cast<int64_t>(l + 1) * m_.n_shared_units * image_elems_;
       fa.pf_bytes = pf;
     }
-    if (timing_) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
+    if (timing) check(cudaEventRecord(ffn_beg_[static_cast<size_t>(l)], compute_), "event");
     check(tc ? launch_expert_ffn_tc(fa, sms_, ffn_smem_, compute_, pdl)
              : launch_expert_ffn(fa, sms_, ffn_smem_, compute_, pdl),
           "K3 expert FFN");
-    if (timing_) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
+    if (timing) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
   };
   auto launch_combine_layer = [&](int l, const float* y_extra) {
     const uint16_t* hl = h_d_ + static_cast<size_t>(l) * T_ * d;
@@ -728,7 +815,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.y_out = yl;
     ca.h_out = world_ > 1 ? nullptr : hn;
     ca.hT_out = (world_ == 1 && tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr;
-    check(launch_combine(ca, compute_, pdl_ && !timing_ && !y_extra), "combine");
+    check(launch_combine(ca, compute_, pdl_ && !timing && !y_extra), "combine");
     if (world_ > 1) {
       if (loop_) {
         loop_->all_reduce(rank_, yl, static_cast<size_t>(T_) * d, compute_);
@@ -740,6 +827,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       check(launch_residual(hl, yl, hn, (tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr, d, T_ * d, compute_),
             "residual");
     }
+    if (timeline_) check(cudaEventRecord(layer_end_[static_cast<size_t>(l)], compute_), "event");
   };
 
   StepReport sr;
@@ -761,7 +849,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     for (int l = 0; l < L; ++l) {
       if (model_mode_) {
         // K0 router GEMV on h_l, then K1 + K2 for layer l
-        const bool pdl = pdl_ && !timing_;
+        const bool pdl = pdl_ && !timing;
         check(launch_router_gemv(wg_d_ + static_cast<size_t>(l) * N * d, h_d_ + static_cast<size_t>(l) * T_ * d, T_, N,
                                  d, logits_d_ + static_cast<size_t>(l) * T_ * N, compute_, pdl),
               "K0 router GEMV");
@@ -815,7 +903,9 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         const auto c0 = std::chrono::steady_clock::now();
         float* yh = ycold_h_ + static_cast<size_t>(l) * T_ * d;
         cold_->run(items[static_cast<size_t>(l)], hcold_h_ + static_cast<size_t>(l) * T_ * d, yh);
-        cpu_ms_cold += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        const float cms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        cpu_ms_cold += cms;
+        tl_cpu_ms[static_cast<size_t>(l)] = cms;
         float* yd = ycold_d_ + static_cast<size_t>(l) * T_ * d;
         check(cudaMemcpyAsync(yd, yh, sizeof(float) * T_ * d, cudaMemcpyHostToDevice, compute_), "H2D cold y");
         y_extra = yd;
@@ -839,15 +929,70 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
                    std::chrono::duration<double, std::milli>(a0 - t_loop0).count(),
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count());
   }
-  if (timing_) check(cudaEventRecord(ev_[4], compute_), "event");
+  if (timing) check(cudaEventRecord(ev_[4], compute_), "event");
   const uint16_t* hfin = h_d_ + static_cast<size_t>(L) * T_ * d;
   if (h_out)
     check(cudaMemcpyAsync(h_out, hfin, sizeof(uint16_t) * T_ * d,
                           h_out_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, compute_),
           "h_out");
-  if (timing_) check(cudaEventRecord(ev_[5], compute_), "event");
+  if (timing) check(cudaEventRecord(ev_[5], compute_), "event");
   check(cudaStreamSynchronize(compute_), "sync compute");
   check(cudaStreamSynchronize(copy_), "sync copy");
+
+  if (timeline_) {
+    // ---- measured SimEvent-shaped records of this step (sim_core.hpp:65-73
+    // kinds; start = the context's measured clock). Every device time is an
+    // integer ns offset from the step's first event, so the step identity
+    // total == draft + prologue + sum(layer walls) + epilogue telescopes.
+    auto t = [&](cudaEvent_t e) {
+      float v = 0.f;
+      check(cudaEventElapsedTime(&v, ev_[0], e), "event time");
+      return static_cast<int64_t>(std::llround(static_cast<double>(v) * 1e6));
+    };
+    const int64_t c0 = tl_clock_ns_, step_no = static_cast<int64_t>(tl_steps_.size());
+    enum { kDraft = 0, kCpu = 1, kGpu = 2, kStall = 3, kLoad = 4, kEvict = 5 };
+    const int64_t d0 = t(ev_[6]), d1 = t(ev_[1]), pro_end = t(ev_[3]);
+    const int64_t draft = drafted ? d1 - d0 : 0;
+    if (drafted) tl_events_.push_back({kDraft, step_no, -1, -1, c0 + d0, draft});
+    int64_t prev = pro_end, walls = 0;
+    size_t li = 0;
+    for (int l = 0; l < L; ++l) {
+      const int64_t wb = t(wait_beg_[static_cast<size_t>(l)]), kb = t(ffn_beg_[static_cast<size_t>(l)]),
+                    le = t(layer_end_[static_cast<size_t>(l)]);
+      for (int e : tl_evicts[static_cast<size_t>(l)])
+        if (e % shard_world_ == shard_rank_) tl_events_.push_back({kEvict, step_no, l, e, c0 + prev, 0});
+      int64_t io_first = -1, io_last = -1;
+      for (; li < tl_load_layer.size() && tl_load_layer[li] == l; ++li) {
+        const int64_t lb_ = t(ld_beg_[li]), le_ = t(ld_end_[li]);
+        tl_events_.push_back({kLoad, step_no, l, tl_load_expert[li], c0 + lb_, le_ - lb_});
+        if (io_first < 0) io_first = lb_;
+        io_last = le_;
+      }
+      const int64_t cpu = static_cast<int64_t>(std::llround(static_cast<double>(tl_cpu_ms[static_cast<size_t>(l)]) * 1e6));
+      const int64_t gpu = le - kb, stall = layer_loads_local[static_cast<size_t>(l)] > 0 ? kb - wb : 0;
+      if (cpu > 0) tl_events_.push_back({kCpu, step_no, l, -1, c0 + kb, cpu});
+      tl_events_.push_back({kGpu, step_no, l, -1, c0 + kb, gpu});
+      if (stall > 0) tl_events_.push_back({kStall, step_no, l, -1, c0 + wb, stall});
+      moespac_layer_timing m{};
+      m.t_cpu_ns = cpu;
+      m.t_gpu_ns = gpu;
+      m.t_io_used_ns = io_first >= 0 ? io_last - io_first : 0;
+      m.stall_ns = stall;
+      m.wall_ns = le - prev;
+      m.bubble_ns = std::llabs(cpu - gpu) + stall;
+      const ThresholdDecision& dec = sched_decisions_[static_cast<size_t>(l)];
+      m.tau = dec.tau;
+      m.fallback = dec.fallback ? 1 : 0;
+      m.n_prefetch = dec.n_prefetch;
+      m.n_loads = layer_loads[static_cast<size_t>(l)];
+      tl_layers_.push_back(m);
+      walls += le - prev;
+      prev = le;
+    }
+    const int64_t total = t(ev_[5]);
+    tl_steps_.push_back({total, draft, pro_end - draft, walls, total - prev, step_no});
+    tl_clock_ns_ += total;
+  }
 
   if (rep) {
     std::memset(rep, 0, sizeof(*rep));
@@ -888,7 +1033,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     rep->ffn_launches = L;
     rep->cold_experts = cold_experts;
     rep->cpu_ms_cold = cpu_ms_cold;
-    if (timing_) {
+    rep->draft_bytes = draft_R_ > 0 ? static_cast<int64_t>(n_draft) * draft_R_ * draft_D_ * 2 : 0;
+    if (timing) {
       auto ms = [](cudaEvent_t a, cudaEvent_t b) {
         float v = 0.f;
         cudaEventElapsedTime(&v, a, b);
@@ -903,6 +1049,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       rep->gpu_ms_ffn = f;
       rep->gpu_ms_combine = ms(ev_[3], ev_[4]) - f;
       rep->gpu_ms_h2d_loads = n_loads > 0 ? ms(copy_ev_[0], copy_ev_[1]) : 0.f;
+      rep->gpu_ms_draft = drafted ? ms(ev_[6], ev_[1]) : 0.f;
     }
   }
   if (layers) {

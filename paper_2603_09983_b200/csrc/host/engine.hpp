@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <array>
 #include <condition_variable>
 #include <memory>
 #include <mutex>
@@ -70,6 +71,20 @@ class Engine {
   void set_pdl(bool on) { pdl_ = on; }
   void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
   void set_draft_window(bool on) { draft_window_ = on; }
+  // real draft phase: gamma weight-streaming GEMV passes over n_params bf16
+  // draft weights (rows of d_draft) before each verification step
+  void set_draft_model(int64_t n_params, int d_draft);
+  // measured SimEvent-shaped timeline (implies per-kernel events, PDL off)
+  void set_timeline(bool on) { timeline_ = on; }
+  int64_t timeline_events(int64_t* out, int64_t cap) const;
+  int64_t timeline_layers(moespac_layer_timing* out, int64_t cap) const;
+  int64_t timeline_steps(int64_t* out, int64_t cap) const;
+  void timeline_clear() {
+    tl_events_.clear();
+    tl_layers_.clear();
+    tl_steps_.clear();
+    tl_clock_ns_ = 0;
+  }
   void set_loopback(LoopbackGroup* g) {
     if (!g || g->world() != world_) throw std::invalid_argument("moespac_ctx_set_loopback: group size != shard world");
     loop_ = g;
@@ -143,7 +158,7 @@ class Engine {
 
   cudaStream_t compute_ = nullptr, copy_ = nullptr;
   std::vector<cudaEvent_t> load_done_, ffn_beg_, ffn_end_;
-  cudaEvent_t ev_[6] = {};
+  cudaEvent_t ev_[7] = {};  // step begin, draft end, K1 end, K2 end, layers end, step end, draft begin
   cudaEvent_t copy_ev_[2] = {};  // timing: first / last expert load on the copy stream
   cudaEvent_t k2_done_ = nullptr;
   bool decided_ = false;  // next step's decisions already made
@@ -159,6 +174,21 @@ class Engine {
   std::vector<bool> router_set_;
   bool model_mode_ = false;       // set for the duration of step_model()
   bool draft_window_ = false;  // emulated γ·t_draft spin on the compute stream before K1
+  // draft model (draft.cu): weights [R][D] bf16, y ping-pong [2][R] fp32, x0 [D]
+  uint16_t* draft_w_ = nullptr;
+  float* draft_y_ = nullptr;
+  uint16_t* draft_x0_ = nullptr;
+  int64_t draft_R_ = 0;
+  int draft_D_ = 0;
+  float draft_scale_ = 1.f;
+  // measured timeline
+  bool timeline_ = false;
+  std::vector<cudaEvent_t> wait_beg_, layer_end_, ld_beg_, ld_end_;
+  std::vector<std::array<int64_t, 6>> tl_events_;
+  std::vector<ThresholdDecision> sched_decisions_;  // decisions of the step being executed
+  std::vector<moespac_layer_timing> tl_layers_;
+  std::vector<std::array<int64_t, 6>> tl_steps_;  // total, draft, prologue, sum of layer walls, epilogue, step
+  int64_t tl_clock_ns_ = 0;
   int acc_mode_ = 0;
 
   std::unique_ptr<ColdExecutor> cold_;

@@ -102,6 +102,8 @@ class StepScheduler {
   const std::vector<std::int32_t>& taus() const { return taus_; }                     // [L]
   const std::vector<SlotLoad>& loads() const { return loads_; }  // ordered as drained
   const std::vector<ThresholdDecision>& decisions() const { return decisions_; }
+  // experts evicted from layer l's pools by the last decide(), in order
+  const std::vector<int>& evicted(int layer) const { return layers_[static_cast<std::size_t>(layer)].evicted; }
   // slot of expert e of layer l within its shard pool, -1 if not resident.
   const std::vector<std::int32_t>& slot_table() const { return slot_of_; }  // [L][N]
   int slots_per_layer(int shard) const { return shard_slots_[static_cast<std::size_t>(shard)]; }

@@ -128,6 +128,10 @@ cudaError_t launch_unpack_expert_tc(const uint16_t* image, int d, int ffn, uint1
                                     cudaStream_t stream);
 cudaError_t launch_fill_synthetic(uint16_t* out, long long n, uint64_t seed, float stdv, cudaStream_t stream);
 cudaError_t launch_draft_window(long long ns, cudaStream_t stream);
+// draft model (draft.cu): one weight-streaming GEMV pass per draft token
+bool draft_d_ok(int D);  // D % 256 == 0, D / 256 in {1, 2, 4, 6, 8, 10, 12, 16}
+cudaError_t launch_draft_gemv(const uint16_t* W, long long R, int D, const float* y_prev, const uint16_t* x0,
+                              float scale, float* y, int grid, cudaStream_t stream, bool pdl = false);
 
 constexpr int kFfnMaxTokens = 16;
 constexpr int kFfnChunkRows = 16;

@@ -422,3 +422,73 @@ def test_l2_prefetch_changes_nothing(d, ffn, cache):
     assert np.array_equal(a.sched_events(), b.sched_events())
     a.close()
     b.close()
+
+
+def test_draft_gemv_matches_torch():
+    """One draft pass (the draft model's weight-streaming GEMV) against a
+    plain PyTorch fp32 reference, first pass (x0) and chained (y_prev)."""
+    R, D = 5000, 2560
+    g = torch.Generator(device="cuda").manual_seed(7)
+    w = (torch.randn((R, D), device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    x0 = torch.randn(D, device="cuda", generator=g).to(torch.bfloat16)
+    y = abi.draft_gemv(w.view(torch.int16), x0=x0.view(torch.int16))
+    ref = w.float() @ x0.float()
+    assert torch.allclose(y, ref, rtol=1e-4, atol=1e-4 * ref.abs().max().item())
+    scale = 0.7
+    y2 = abi.draft_gemv(w.view(torch.int16), y_prev=y, scale=scale)
+    x1 = (y[:D] * scale).to(torch.bfloat16).float()
+    ref2 = w.float() @ x1
+    assert torch.allclose(y2, ref2, rtol=1e-4, atol=1e-4 * ref2.abs().max().item())
+
+
+def test_draft_model_and_measured_timeline():
+    """Real draft phase + measured SimEvent timeline
+    (row 1): the draft passes stream gamma x n_params x 2 bytes per step and
+    leave outputs / decisions bitwise unchanged; the measured log has one gpu
+    record per layer, the load / evict records of the modeled log (same
+    experts, same order), and every step conserves time:
+    total == draft + prologue + sum(layer walls) + epilogue, with
+    gpu + stall <= wall per layer."""
+    L, N, k, g, d, ffn = 3, 16, 4, 6, 1024, 128
+    rng = np.random.default_rng(13)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    a, cfg = _make_ctx(L, N, k, g, d, ffn, 0, 0, 0.5, std, shared, abi.FFN_TENSOR, cold=-1)
+    b, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, 0.5, std, shared, abi.FFN_TENSOR, cold=-1)
+    n_params, dd = 64 << 20, 2560
+    b.set_draft_model(n_params, dd)
+    b.set_timeline(True)
+    T = g + 1
+    gen = O.Generator(L, N, k, g, seed=4)
+    loads = 0
+    for s in range(5):
+        logits, _, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        ha, hb = np.zeros_like(h0), np.zeros_like(h0)
+        a.step(logits, h0, acc, ha)
+        rb_, _ = b.step(logits, h0, acc, hb)
+        loads += rb_.n_loads
+        assert np.array_equal(ha, hb)
+        assert rb_.draft_bytes == g * (n_params // dd) * dd * 2 and rb_.gpu_ms_draft > 0
+    assert loads > 0
+    modeled = a.sched_events()
+    assert np.array_equal(modeled, b.sched_events())
+    ev, lay, steps = b.timeline()
+    assert len(steps) == 5 and len(lay) == 5 * L
+    for st in steps:
+        total, draft, pro, walls, epi, _ = st
+        assert total == draft + pro + walls + epi and draft > 0 and pro > 0 and walls > 0
+    for m in lay:
+        assert m.t_gpu_ns > 0 and m.t_gpu_ns + m.stall_ns <= m.wall_ns
+    for kind in (O.EV_LOAD, O.EV_EVICT):
+        got = ev[ev[:, 0] == kind][:, 1:4]
+        want = modeled[modeled[:, 0] == kind][:, 1:4]
+        assert np.array_equal(got, want), kind
+    gpu = ev[ev[:, 0] == O.EV_GPU]
+    assert len(gpu) == 5 * L and (gpu[:, 5] > 0).all()
+    assert (ev[ev[:, 0] == O.EV_DRAFT][:, 5] > 0).sum() == 5
+    # starts are on one monotone measured clock
+    starts = ev[ev[:, 0] == O.EV_GPU][:, 4]
+    assert (np.diff(starts) > 0).all()
+    b.set_draft_model(0)
+    a.close()
+    b.close()
