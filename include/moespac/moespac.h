@@ -297,7 +297,7 @@ moespac_status moespac_fill_synthetic(uint16_t* dev, int64_t n_elems, uint64_t s
 
 /* ------------------------------------------------------------------ engine context
  * The full verification step on one device: K1 -> K2 -> per layer
- * [wait own loads] K3 -> combine (-> NCCL all-reduce in expert-parallel mode),
+ * [wait own loads] K3 -> combine (-> NCCL all-gather + ordered sum in the multi-GPU modes),
  * with the host scheduler deciding every layer's tau and loads during the
  * draft window and the Asynchronous Execution Engine issuing each load as a
  * pinned-host -> HBM cudaMemcpyAsync on a copy stream. Replaces
@@ -328,7 +328,9 @@ typedef struct moespac_model_desc {
  *   across the ranks' K3 CTAs as one virtual grid, so the per-GPU work is
  *   balanced whatever the routing; tensor-core K3 only.
  * AUTO: UNITS when it applies, else EXPERT. Both combine with one
- *   all-reduce (NCCL) of the per-rank partial outputs per layer. */
+ *   all-gather (NCCL) of the per-rank fp32 partial outputs per layer, then
+ *   every rank sums them in rank order (deterministic; the loopback group
+ *   runs the same ordered-sum kernel, so it pins the NCCL path's bits). */
 #define MOESPAC_PAR_AUTO 0
 #define MOESPAC_PAR_EXPERT 1
 #define MOESPAC_PAR_UNITS 2
@@ -355,7 +357,7 @@ moespac_status moespac_ctx_finalize(moespac_ctx* c);
 /* Expert-parallel combine over NCCL: 128-byte ncclUniqueId from rank 0. */
 moespac_status moespac_nccl_unique_id(void* out128);
 moespac_status moespac_ctx_set_nccl(moespac_ctx* c, const void* unique_id128, int nranks, int rank);
-/* In-process stand-in for the expert-parallel all-reduce: `world` contexts on
+/* In-process stand-in for the expert-parallel all-gather: `world` contexts on
  * ONE device (one host thread each) exchange their per-layer partial outputs
  * through device slots instead of NCCL (which refuses two ranks on one GPU).
  * Test harness for the expert-parallel device path on a single GPU;
@@ -479,7 +481,7 @@ typedef struct moespac_ctx_views {
   const int32_t* counters_dev;  /* [L][8] */
   const int32_t* est_state_dev; /* [L][N][4] */
   const uint16_t* h_dev;        /* [L+1][T][d] bf16 layer inputs / final output */
-  const float* y_dev;           /* [L][T][d] fp32 MoE outputs (expert-parallel: after the all-reduce) */
+  const float* y_dev;           /* [L][T][d] fp32 MoE outputs (multi-GPU: the ordered sum over ranks) */
   const uint16_t* pool_dev;     /* [L][slots][image] */
   const double* logits_dev;     /* [L][T][N] router logits (trace input, or K0's output in model mode) */
   int64_t slots_per_layer, image_elems;

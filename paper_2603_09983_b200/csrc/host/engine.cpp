@@ -34,7 +34,7 @@ namespace moespac {
 struct NcclApi {
   void* so = nullptr;
   int (*get_unique_id)(void*) = nullptr;
-  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   int (*comm_destroy)(void*) = nullptr;
   const char* (*error_string)(int) = nullptr;
   static NcclApi* load() {
@@ -47,11 +47,11 @@ struct NcclApi {
       throw NcclError("libnccl.so.2 not loadable");
     }
     a->get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(a->so, "ncclGetUniqueId"));
-    a->all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
-        dlsym(a->so, "ncclAllReduce"));
+    a->all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+        dlsym(a->so, "ncclAllGather"));
     a->comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(a->so, "ncclCommDestroy"));
     a->error_string = reinterpret_cast<const char* (*)(int)>(dlsym(a->so, "ncclGetErrorString"));
-    if (!a->get_unique_id || !a->all_reduce || !a->comm_destroy) {
+    if (!a->get_unique_id || !a->all_gather || !a->comm_destroy) {
       delete a;
       throw NcclError("libnccl missing symbols");
     }
@@ -97,12 +97,16 @@ void LoopbackGroup::barrier() {
   }
 }
 
-void LoopbackGroup::all_reduce(int rank, float* buf, size_t n, cudaStream_t s) {
-  if (n > max_) throw std::invalid_argument("loopback all_reduce: message larger than the group's slots");
+// All-gather of the ranks' partials into the shared device slots: after it,
+// slot q holds rank q's partial for every rank's stream. release() marks the
+// end of this rank's reads (the ordered sum), so the next layer's put waits
+// for every reader of the slot it overwrites.
+const float* LoopbackGroup::all_gather(int rank, const float* buf, size_t n, cudaStream_t s) {
+  if (n > max_) throw std::invalid_argument("loopback all_gather: message larger than the group's slots");
   auto ok = [](cudaError_t e) {
-    if (e != cudaSuccess) throw CudaError(std::string("loopback all_reduce: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw CudaError(std::string("loopback all_gather: ") + cudaGetErrorString(e));
   };
-  // every rank recorded the end of its previous sum before anyone overwrites a slot
+  // every rank recorded the end of its previous reads before anyone overwrites a slot
   barrier();
   for (int q = 0; q < world_; ++q)
     if (q != rank) ok(cudaStreamWaitEvent(s, done_[static_cast<size_t>(q)], 0));
@@ -111,8 +115,11 @@ void LoopbackGroup::all_reduce(int rank, float* buf, size_t n, cudaStream_t s) {
   barrier();
   for (int q = 0; q < world_; ++q)
     if (q != rank) ok(cudaStreamWaitEvent(s, put_[static_cast<size_t>(q)], 0));
-  ok(launch_sum_slots(slots_, world_, max_, buf, n, s));
-  ok(cudaEventRecord(done_[static_cast<size_t>(rank)], s));
+  return slots_;
+}
+
+void LoopbackGroup::release(int rank, cudaStream_t s) {
+  if (cudaEventRecord(done_[static_cast<size_t>(rank)], s) != cudaSuccess) throw CudaError("loopback release");
 }
 
 moespac_status nccl_unique_id(void* out) {
@@ -299,7 +306,8 @@ Engine::~Engine() {
                   static_cast<void*>(hit_ord_d_), static_cast<void*>(est_d_), static_cast<void*>(y_d_),
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
                   static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sg_w_),
-                  static_cast<void*>(draft_w_), static_cast<void*>(draft_y_), static_cast<void*>(draft_x0_)})
+                  static_cast<void*>(draft_w_), static_cast<void*>(draft_y_), static_cast<void*>(draft_x0_),
+                  static_cast<void*>(gather_d_)})
     if (p) cudaFree(p);
   cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
@@ -470,6 +478,8 @@ void Engine::set_nccl(const void* uid, int nranks, int rank) {
   if (nranks != world_ || rank != rank_) throw std::invalid_argument("set_nccl: ranks disagree with the shard layout");
   check(cudaSetDevice(device_), "cudaSetDevice");
   nccl_.reset(NcclApi::load());
+  if (!gather_d_)
+    check(cudaMalloc(reinterpret_cast<void**>(&gather_d_), sizeof(float) * world_ * T_ * m_.d_model), "cudaMalloc gather");
   auto init = reinterpret_cast<CommInitFn>(dlsym(nccl_->so, "ncclCommInitRank"));
   if (!init) throw NcclError("ncclCommInitRank missing");
   NcclUid id;
@@ -817,15 +827,24 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.hT_out = (world_ == 1 && tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr;
     check(launch_combine(ca, compute_, pdl_ && !timing && !y_extra), "combine");
     if (world_ > 1) {
+      // deterministic combine: all-gather the ranks' fp32
+      // partials, then every rank sums them in rank order (+ residual, h^T)
+      // — the same kernel and the same bits for NCCL and the loopback group
+      const size_t n = static_cast<size_t>(T_) * d;
+      const float* parts;
+      size_t stride = n;
       if (loop_) {
-        loop_->all_reduce(rank_, yl, static_cast<size_t>(T_) * d, compute_);
+        parts = loop_->all_gather(rank_, yl, n, compute_);
+        stride = loop_->stride();
       } else {
-        const int r = nccl_->all_reduce(yl, yl, static_cast<size_t>(T_) * d, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm_,
-                                        compute_);
-        if (r != 0) throw NcclError("ncclAllReduce failed");
+        const int r = nccl_->all_gather(yl, gather_d_, n, /*ncclFloat32*/ 7, comm_, compute_);
+        if (r != 0) throw NcclError("ncclAllGather failed");
+        parts = gather_d_;
       }
-      check(launch_residual(hl, yl, hn, (tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr, d, T_ * d, compute_),
-            "residual");
+      check(launch_gather_sum_residual(parts, world_, stride, hl, yl, hn, (tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr,
+                                       d, static_cast<int>(n), compute_),
+            "ordered sum + residual");
+      if (loop_) loop_->release(rank_, compute_);
     }
     if (timeline_) check(cudaEventRecord(layer_end_[static_cast<size_t>(l)], compute_), "event");
   };

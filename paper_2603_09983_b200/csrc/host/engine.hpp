@@ -20,16 +20,19 @@ namespace moespac {
 
 struct NcclApi;  // dlopen'ed libnccl (no link-time dependency)
 
-// In-process stand-in for the per-layer NCCL all-reduce: `world` contexts on
+// In-process stand-in for the per-layer NCCL all-gather: `world` contexts on
 // one device, each driven by its own host thread, exchange their partial
-// outputs through device slots and CUDA events, and every rank sums the slots
-// in rank order. Test harness for the expert-parallel device path where only
+// outputs through device slots and CUDA events; every rank then sums the
+// slots in rank order with the same kernel the NCCL path uses. Test harness for the expert-parallel device path where only
 // one GPU is available (NCCL refuses two ranks on one device).
 class LoopbackGroup {
  public:
   LoopbackGroup(int device, int world, size_t max_elems);
   ~LoopbackGroup();
-  void all_reduce(int rank, float* buf, size_t n, cudaStream_t stream);
+  // buf [n] -> slots [world][stride()] (rank order); release() after reading them
+  const float* all_gather(int rank, const float* buf, size_t n, cudaStream_t stream);
+  void release(int rank, cudaStream_t stream);
+  size_t stride() const { return max_; }
   int world() const { return world_; }
 
  private:
@@ -145,6 +148,7 @@ class Engine {
   int32_t *ids_d_ = nullptr, *freqs_d_ = nullptr, *offsets_d_ = nullptr, *perm_d_ = nullptr;
   int32_t *hit_list_d_ = nullptr, *hit_ord_d_ = nullptr, *est_d_ = nullptr;
   float *gates_d_ = nullptr, *y_d_ = nullptr, *work_d_ = nullptr;
+  float* gather_d_ = nullptr;   // [world][T][d] all-gathered rank partials (NCCL)
   uint16_t* h_d_ = nullptr;     // [L+1][T][d]
   uint16_t* hT_d_ = nullptr;    // h^T UMMA image of the current layer input (tensor-core K3)
   uint8_t* tables_d_ = nullptr; // resident bits | loaded bits | taus | slot table

@@ -31,7 +31,7 @@
 //  * Combine: y_t = sum over the token's experts (ascending id) and over the
 //    CTAs that covered them (ascending), fixed order => deterministic; fused
 //    with the residual add + bf16 round, or fp32 partial out for the
-//    expert-parallel all-reduce.
+//    multi-GPU all-gather + ordered sum.
 #include <cstdint>
 
 #include "common.cuh"
@@ -738,6 +738,42 @@ __global__ void sum_slots_kernel(const float* __restrict__ slots, int world, siz
 
 cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float* out, size_t n, cudaStream_t stream) {
   dev::sum_slots_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(slots, world, stride, out, n);
+  return cudaGetLastError();
+}
+
+namespace dev {
+// Expert-parallel combine after the all-gather of the ranks' fp32 partial
+// outputs ([world][stride], rank order): y = sum over ranks 0..world-1 in
+// that order (the same bits on every rank, for NCCL and the in-process
+// loopback alike), h_out = bf16(h_in + y), and the next layer's h^T image.
+__global__ void gather_sum_residual_kernel(const float* __restrict__ parts, int world, size_t stride,
+                                           const uint16_t* __restrict__ h_in, float* __restrict__ y_out,
+                                           uint16_t* __restrict__ h_out, uint16_t* __restrict__ hT_out, int d, int n) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (i >= n) return;
+  float2 y = *reinterpret_cast<const float2*>(parts + i);
+  for (int q = 1; q < world; ++q) {
+    const float2 p = *reinterpret_cast<const float2*>(parts + q * stride + i);
+    y.x += p.x;
+    y.y += p.y;
+  }
+  *reinterpret_cast<float2*>(y_out + i) = y;
+  const uint32_t hv = *reinterpret_cast<const uint32_t*>(h_in + i);
+  const uint32_t o = static_cast<uint32_t>(f32_to_bf16_rn(bf_lo(hv) + y.x)) |
+                     (static_cast<uint32_t>(f32_to_bf16_rn(bf_hi(hv) + y.y)) << 16);
+  *reinterpret_cast<uint32_t*>(h_out + i) = o;
+  if (hT_out) {
+    const int t = i / d, c = i % d;
+    const int kt = c >> 6, j = (c >> 3) & 7, e = c & 7;
+    *reinterpret_cast<uint32_t*>(hT_out + kt * 1024 + (t >> 3) * 512 + j * 64 + (t & 7) * 8 + e) = o;
+  }
+}
+}  // namespace dev
+
+cudaError_t launch_gather_sum_residual(const float* parts, int world, size_t stride, const uint16_t* h_in, float* y_out,
+                                       uint16_t* h_out, uint16_t* hT_out, int d, int n, cudaStream_t stream) {
+  dev::gather_sum_residual_kernel<<<static_cast<unsigned>((n / 2 + 255) / 256), 256, 0, stream>>>(
+      parts, world, stride, h_in, y_out, h_out, hT_out, d, n);
   return cudaGetLastError();
 }
 

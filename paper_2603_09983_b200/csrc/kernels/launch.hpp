@@ -120,6 +120,9 @@ cudaError_t launch_combine(const dev::CombineArgs& a, cudaStream_t stream, bool 
 cudaError_t launch_residual(const uint16_t* h_in, const float* y, uint16_t* h_out, uint16_t* hT_out, int d, int n,
                             cudaStream_t stream, bool pdl = false);
 cudaError_t launch_sum_slots(const float* slots, int world, size_t stride, float* out, size_t n, cudaStream_t stream);
+// expert-parallel combine: ordered sum of the all-gathered rank partials + residual + h^T (n = T*d, even)
+cudaError_t launch_gather_sum_residual(const float* parts, int world, size_t stride, const uint16_t* h_in, float* y_out,
+                                       uint16_t* h_out, uint16_t* hT_out, int d, int n, cudaStream_t stream);
 cudaError_t launch_pack_expert(const uint16_t* wg, const uint16_t* wu, const uint16_t* wd, int d, int ffn,
                                uint16_t* out, cudaStream_t stream);
 cudaError_t launch_unpack_expert(const uint16_t* image, int d, int ffn, uint16_t* wg, uint16_t* wu, uint16_t* wd,
