@@ -509,7 +509,9 @@ def test_expert_parallel_combine_is_deterministic():
         group = abi.LoopbackGroup(0, world, T * d) if world > 1 else None
         ctxs = []
         for r in range(world):
-            cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=0.5)
+            # cache 1.0: every expert resident at any world size (the same experts
+            # contribute; only the work split and the summation order change)
+            cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=1.0)
             ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, 0, abi.FFN_TENSOR, 1), cfg, r, world)
             ctx.set_cold_threads(0)
             arena = ctx.host_arena(L * N)
