@@ -375,17 +375,25 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
     tok = lambda o, n: float(sum(accepted[o + i] for i in range(n)))  # noqa: E731
     sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
     stamps = torch.zeros((L, sms, 32), dtype=torch.int64, device="cuda")
-    spans = []
+    spans, spans_raw = [], []
 
     def read_stamps(_rep):
         # K3 launch durations of this step from its CTAs' %globaltimer
-        # stamps (first CTA start -> last CTA end, per layer): the kernels ran
-        # with programmatic dependent launch, as in the timed windows
+        # stamps. The kernels ran with programmatic dependent launch, as in
+        # the timed windows, so a K3's first CTAs start while the previous
+        # layer still runs: the duration is counted from the later of its
+        # first CTA start and the previous K3's last CTA end (the overlap is
+        # not counted twice: the spans of a step sum to less than the step)
+        # to its last CTA end.
         st = stamps.cpu().numpy()
+        prev_end = None
         for l in range(L):
             beg, end = st[l, :, 0], st[l, :, 6]
             if (end > 0).any():
-                spans.append((end[end > 0].max() - beg[beg > 0].min()) * 1e-6)
+                b0, e1 = beg[beg > 0].min(), end[end > 0].max()
+                spans_raw.append((e1 - b0) * 1e-6)
+                spans.append((e1 - (b0 if prev_end is None else max(b0, prev_end))) * 1e-6)
+                prev_end = e1
         stamps.zero_()
         torch.cuda.synchronize()
 
@@ -417,10 +425,10 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
     ffn_bytes_st = sum(r.ffn_bytes for r in reps_st)
     n_launch_st = sum(r.ffn_launches for r in reps_st)
     out = {
-        "label": label, "w0": w0, "settle": settle, "windows": windows,
+        "label": label, "w0": w0, "settle": settle, "windows": windows, "K": K,
         "win": [(m, t) for m, t, _ in win], "win_e2e": [(m, t) for m, t, _ in win_e2e],
         "ms": win[0][0], "tokens": win[0][1], "ms_e2e": win_e2e[0][0], "tokens_e2e": win_e2e[0][1],
-        "k3_span_ms": spans, "ffn_bytes_st": ffn_bytes_st, "ffn_launches_st": n_launch_st,
+        "k3_span_ms": spans, "k3_span_raw_ms": spans_raw, "ffn_bytes_st": ffn_bytes_st, "ffn_launches_st": n_launch_st,
         "ffn_ms_ev": sum(r.gpu_ms_ffn for r in reps_ev), "ffn_bytes_ev": sum(r.ffn_bytes for r in reps_ev),
         "ffn_launches_ev": sum(r.ffn_launches for r in reps_ev),
         "launches": sum(r.kernel_launches for r in win[0][2]),
@@ -453,6 +461,14 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
     return out
 
 
+def L_layers(w):
+    return w.n_layers
+
+
+def args_steps(args, r):
+    return r.get("K", args.steps)
+
+
 def leg_summary(r, w, args, world, hbm_peak, peak_kind):
     """value / e2e / roofline of one leg (one workload)."""
     tps = [t / (m * 1e-3) for m, t in r["win"]]
@@ -483,9 +499,15 @@ def leg_summary(r, w, args, world, hbm_peak, peak_kind):
             else "fallback 6650 GB/s (B200_PROFILING.md)",
             "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic, "traffic_capture": traffic_capture,
             "bytes_per_launch": bytes_per_launch, "ms_per_launch": span_ms,
-            "timing": "K3 launch duration = first CTA start -> last CTA end (%globaltimer stamps of every CTA), "
-                      "averaged over the L launches of a K-step window run with programmatic dependent launch "
-                      "(the timed windows' mode); bytes = resident activated experts + shared units x image",
+            "timing": "K3 launch duration from every CTA's %globaltimer stamps in a K-step window run with "
+                      "programmatic dependent launch (the timed windows' mode): max(first CTA start, previous K3's "
+                      "last CTA end) -> last CTA end, so overlapping launches are not double counted (the spans "
+                      "sum to less than the step time); bytes = resident activated experts + shared units x image",
+            "first_cta_start_span": {"ms_per_launch": float(np.mean(r["k3_span_raw_ms"])) if r["k3_span_raw_ms"] else 0.0,
+                                     "frac": (bytes_per_launch / (np.mean(r["k3_span_raw_ms"]) * 1e-3) / 1e9 / hbm_peak)
+                                     if r["k3_span_raw_ms"] else 0.0},
+            "step_level": {"frac": (r["ffn_bytes_st"] / max(1, r["ffn_launches_st"]) * L_layers(w)
+                                    / (r["ms"] / args_steps(args, r) * 1e-3) / 1e9 / hbm_peak)},
             "cuda_events_pdl_off": {"ms_per_launch": ev_ms, "achieved": ev_achieved, "frac": ev_achieved / hbm_peak}}
     stat = lambda v: {"median": float(np.median(v)), "min": float(np.min(v)), "max": float(np.max(v)),  # noqa: E731
                       "spread": float((np.max(v) - np.min(v)) / np.median(v)), "windows": [float(x) for x in v]}

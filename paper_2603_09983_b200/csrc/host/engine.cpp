@@ -205,6 +205,8 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   // profiling knob: MOESPAC_FFN_ACCUM (accumulator selector, see
   // moespac_ffn_args::accum); DESIGN.md §5 lists the others
   if (const char* e = std::getenv("MOESPAC_FFN_ACCUM")) ffn_accum_ = std::atoi(e);
+  if (const char* e = std::getenv("MOESPAC_GROUP_UNITS")) group_units_ = std::atoi(e);
+  if (const char* e = std::getenv("MOESPAC_L2_PF")) l2_prefetch_ = std::atoi(e);
   const size_t smem_optin = prop.sharedMemPerBlockOptin;
   FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, smem_optin, ffn_accum_)
                                            : ffn_plan(T_, m.d_model, smem_optin);
@@ -771,6 +773,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.global_acc = global_acc_ ? 1 : 0;
     fa.acc_mode = acc_mode_;
     fa.hT = hT[l & 1];
+    fa.group_units = group_units_;
     if (split_) {
       fa.cta_base = rank_ * sms_;
       fa.cta_total = world_ * sms_;

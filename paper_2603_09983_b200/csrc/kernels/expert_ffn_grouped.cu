@@ -53,7 +53,7 @@ constexpr int NSLOT = 32;      // ring entries in flight (mbarrier pairs)
 constexpr int TILE = 16384;    // one gate|up K-tile or down M-tile of a 64-row chunk
 constexpr int UB = 2048;       // one 8-row unit (gate + up octet) of a gate|up tile, or 8 k of a down tile
 constexpr int UPC = 8;         // units per 64-row chunk
-constexpr int GMAX = 8;        // units per group (one M = 128 gate|up tile)
+constexpr int GMAX = 16;       // units per group: up to two M = 128 gate|up tiles (8 units each)
 constexpr int HTS = 2048;      // h^T slice of one K-tile (16 tokens x 64 k)
 constexpr int ENT_MAX = 32;    // entries one CTA may touch (one producer lane each)
 constexpr int MAX_KT = 32;     // d <= 2048
@@ -63,10 +63,13 @@ constexpr int DBG = 32;
 
 // ---------------------------------------------------------------- groups
 // Work unit = 8 ffn rows of one expert (its 8 gate + 8 up rows: one 2 KiB
-// run per gate|up K-tile, one 2 KiB k-chunk per down M-tile). A group is <= 8
-// consecutive units of the CTA's range; it spans at most two chunk pieces
-// (chunks are 8 units and entry boundaries are chunk boundaries because
-// ffn % 64 == 0).
+// run per gate|up K-tile, one 2 KiB k-chunk per down M-tile). A group is <=
+// gmax (8 or 16) consecutive units of the CTA's range — one or two M = 128
+// gate|up tiles — cut so that it spans at most two chunk pieces (chunks are
+// 8 units and entry boundaries are chunk boundaries because ffn % 64 == 0):
+// a 16-unit group starting mid-chunk ends at the end of the next chunk. (A
+// CTA's 9 units always fit one group; measured, a third piece per group
+// made the producer's per-copy bookkeeping ~4% slower on the Qwen3 shape.)
 struct Grp {
   long long us;                 // first unit (global order)
   int nu, np;
@@ -75,15 +78,17 @@ struct Grp {
 
 struct GroupIt {
   long long u, u1;
-  int upe;  // units per entry = ffn / 8
+  int upe;   // units per entry = ffn / 8
+  int gmax;  // units per group (8 or 16)
   __device__ __forceinline__ bool next(Grp& g) {
     if (u >= u1) return false;
-    const long long ue = u + GMAX < u1 ? u + GMAX : u1;
+    const int o = static_cast<int>(u / upe), ui = static_cast<int>(u % upe);
+    // end of u's chunk, and of the chunk after it (a group has <= 2 pieces)
+    const long long cend = static_cast<long long>(o) * upe + (ui / UPC + 1) * UPC;
+    long long ue = u + gmax < u1 ? u + gmax : u1;
+    if (ue > cend + UPC) ue = cend + UPC;
     g.us = u;
     g.nu = static_cast<int>(ue - u);
-    // piece 0: up to the end of u's chunk; piece 1: the rest (next chunk)
-    const int o = static_cast<int>(u / upe), ui = static_cast<int>(u % upe);
-    const long long cend = static_cast<long long>(o) * upe + (ui / UPC + 1) * UPC;
     const long long e = cend < ue ? cend : ue;
     g.o[0] = o;
     g.c[0] = ui / UPC;
@@ -104,11 +109,11 @@ __device__ __forceinline__ int pow2_divisor(int x, int cap) {
   while (m < cap && x % (2 * m) == 0) m *= 2;
   return m;
 }
-// tiles per ring entry: >= 32 KiB of weights per entry whatever the width
+// tiles per ring entry: >= 24-32 KiB of weights per entry whatever the width
 // (capped by the power-of-two divisor of the tile count), so the
 // single-warp producer/MMA bookkeeping per entry is amortised
 __device__ __forceinline__ int tiles_per_entry(int nu, int cap) {
-  const int t = nu >= 8 ? 2 : (nu >= 4 ? 4 : (nu >= 2 ? 8 : 16));
+  const int t = nu >= 12 ? 1 : (nu >= 8 ? 2 : (nu >= 4 ? 4 : (nu >= 2 ? 8 : 16)));
   return t < cap ? t : cap;
 }
 struct Geom {
@@ -119,7 +124,8 @@ __device__ __forceinline__ Geom gu_geom(int nu, int cap) {
   const int m = tiles_per_entry(nu, cap);
   const uint32_t a = static_cast<uint32_t>(nu) * UB;
   const uint32_t size = static_cast<uint32_t>(m) * a;
-  const uint32_t w = static_cast<uint32_t>(m - 1) * a + TILE;  // an M = 128 A operand reads 16 KiB
+  // the last tile's M = 128 A operands read 16 KiB each (one or two of them)
+  const uint32_t w = static_cast<uint32_t>(m - 1) * a + static_cast<uint32_t>((nu + 7) / 8) * TILE;
   return {size, size > w ? size : w, m};
 }
 __device__ __forceinline__ Geom dn_geom(int nu, int cap) {
@@ -171,6 +177,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   const int ktiles = d / 64, mtiles = d / 128;
   const long long chunk_bytes = 3LL * 64 * d * 2;
   const int upe = a.ffn / 8;
+  const int gmax = a.group_units == 16 ? 16 : 8;  // measured: 8 (one tile per group round) is faster
   const uint32_t RB = static_cast<uint32_t>(a.ring_bytes);
 
   // [a^T 2 x (hi, lo) x 4 KiB][h^T ktiles x 2 KiB][ring][2 KiB zeros][entry gates][entry masks][misc][mbarriers]
@@ -261,7 +268,41 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
                                      : a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
       my_base = reinterpret_cast<unsigned long long>(w);
     }
+    // L2 prefetch of a layer's stream for this CTA index, in stream order
+    // (approximately: group order), skipping the first `skip` bytes; run r
+    // is issued by lane r % 32
+    auto prefetch_l2 = [&](int nh, const int32_t* hit_list, const int32_t* slot_of, const uint16_t* pool,
+                           const uint16_t* shared_w, long long skip, long long budget) {
+      const long long nn = static_cast<long long>(nh + a.n_shared) * upe;
+      const long long p0 = nn > 0 ? (bg * nn) / G : 0, p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
+      GroupIt pit{p0, p1, upe, gmax};
+      Grp pg;
+      int rc = 0;
+      while (budget > 0 && pit.next(pg)) {
+        for (int i = 0; i < pg.np && budget > 0; ++i) {
+          const int o = pg.o[i];
+          const uint16_t* w = o < nh ? pool + static_cast<long long>(slot_of[hit_list[o]]) * a.expert_elems
+                                     : shared_w + static_cast<long long>(o - nh) * a.expert_elems;
+          const uint8_t* base = reinterpret_cast<const uint8_t*>(w) + pg.c[i] * chunk_bytes + pg.pa[i] * UB;
+          const uint32_t run = static_cast<uint32_t>(pg.n[i]) * UB;
+          for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
+            if (skip > 0) {
+              skip -= run;
+              continue;
+            }
+            if ((rc++ & 31) == lane)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE),
+                           "r"(run)
+                           : "memory");
+            budget -= run;
+          }
+        }
+      }
+    };
     bool waited = false;
+    // (Measured: an own-stream L2 prefetch issued here, at the first full
+    // ring before the input wait, made the layer 7-15% slower for 128-384
+    // KiB per CTA on the Qwen3 / DeepSeek-V2-Lite shapes; not used.)
     auto wait_pred = [&]() {
       pdl_wait();
       {  // one slice per lane: bulk copies issued by one thread serialise
@@ -323,7 +364,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
                    static_cast<uint32_t>(g.n[1]) * UB, bar, pol);
       }
     };
-    GroupIt it{u0, u1, upe};
+    GroupIt it{u0, u1, upe, gmax};
     Grp cur, prev;
     bool more = it.next(cur), has_prev = false;
     const uint8_t* cb[2];
@@ -361,38 +402,11 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     }
     if (a.nx_counters && a.pf_bytes > 0) {
       // ---- cross-layer L2 prefetch: the next layer's routing is final (K2
-      // ran for all layers), so walk what this CTA index streams next layer,
-      // in stream order, and prefetch its runs into L2 (HBM otherwise idles
-      // through this launch's tail and the layer handoff)
-      const int nh = a.nx_counters[7];
-      const long long nn = static_cast<long long>(nh + a.n_shared) * upe;
-      const long long p0 = nn > 0 ? (bg * nn) / G : 0, p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
-      GroupIt pit{p0, p1, upe};
-      Grp pg;
-      // the next CTA fills its ring with the first ring_bytes itself right
-      // after entry; prefetch what follows (approximately: group order)
-      long long budget = a.pf_bytes, skip = RB;
-      int rc = 0;  // run counter: run r is issued by lane r % 32
-      while (budget > 0 && pit.next(pg)) {
-        for (int i = 0; i < pg.np && budget > 0; ++i) {
-          const int o = pg.o[i];
-          const uint16_t* w = o < nh ? a.nx_pool + static_cast<long long>(a.nx_slot_of[a.nx_hit_list[o]]) * a.expert_elems
-                                     : a.nx_shared_w + static_cast<long long>(o - nh) * a.expert_elems;
-          const uint8_t* base = reinterpret_cast<const uint8_t*>(w) + pg.c[i] * chunk_bytes + pg.pa[i] * UB;
-          const uint32_t run = static_cast<uint32_t>(pg.n[i]) * UB;
-          for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
-            if (skip > 0) {
-              skip -= run;
-              continue;
-            }
-            if ((rc++ & 31) == lane)
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE),
-                           "r"(run)
-                           : "memory");
-            budget -= run;
-          }
-        }
-      }
+      // ran for all layers), so walk what this CTA index streams next layer
+      // and prefetch its runs into L2 (HBM otherwise idles through this
+      // launch's tail and the layer handoff); the next CTA fills its ring
+      // with the first ring_bytes itself right after entry
+      prefetch_l2(a.nx_counters[7], a.nx_hit_list, a.nx_slot_of, a.nx_pool, a.nx_shared_w, RB, a.pf_bytes);
     }
     if (!waited) wait_pred();
     if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
@@ -453,17 +467,18 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       int ht_ok = 0;  // h^T slices [0, ht_ok) known to have landed
       const uint32_t ring_addr = smem_u32(ring), at_addr = smem_u32(aT), ht_addr = smem_u32(hts);
       const uint32_t zero_addr = smem_u32(zeros);
-      GroupIt it{u0, u1, upe};
+      GroupIt it{u0, u1, upe, gmax};
       Grp cur, prev;
       bool more = it.next(cur), has_prev = false;
       int i = 0;
       while (more || has_prev) {
-        if (more) {  // GU(i): D1[i & 1] = W_gu(group) x h^T
+        if (more) {  // GU(i): D1[i & 1] = W_gu(group) x h^T, one or two M = 128 tiles
           const int b1 = i & 1;
           wait_acc(a, &d1_empty[b1], d1e[b1].bit ^ 1u, w_d1e);
           d1e[b1].flip();
           fence_after();
-          const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 16);
+          const uint32_t d1 = tmem + static_cast<uint32_t>(b1 * 32);
+          const int nt = (cur.nu + 7) / 8;
           const Geom g = gu_geom(cur.nu, kcap);
           const uint32_t ab = static_cast<uint32_t>(cur.nu) * UB;
           for (int kt = 0; kt < ktiles; kt += g.m) {
@@ -475,11 +490,13 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
             fence_after();
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
-                const uint64_t adesc = smem_desc(ring_addr + off + j * ab, 128, 1024);
                 const uint64_t bdesc = smem_desc(ht_addr + (kt + j) * HTS, 128, 1024);
+                for (int t = 0; t < nt; ++t) {
+                  const uint64_t adesc = smem_desc(ring_addr + off + j * ab + t * TILE, 128, 1024);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
-                  mma_bf16(d1, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0);
+                  for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
+                    mma_bf16(d1 + 16 * t, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0);
+                }
               }
               mma_commit(&empty[slot]);
             }
@@ -591,7 +608,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       }
       Phase d1f[2], atf[2];
       long long w_d1f = 0, w_d2f = 0;
-      GroupIt it{u0, u1, upe};
+      GroupIt it{u0, u1, upe, gmax};
       Grp g;
       int i = 0;
       while (it.next(g)) {
@@ -601,11 +618,13 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         d1f[b1].flip();
         if (i == 0 && et == 0) stamp(a, 17);
         fence_after();
-        float v[16];
-        tc::tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b1 * 16), v);
+        const int nt = (g.nu + 7) / 8;
+        float v[2][16];
+        tc::tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b1 * 32), v[0]);
+        if (nt > 1) tc::tmem_ld16(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(b1 * 32 + 16), v[1]);
         if (i == 0 && et == 0 && a.dbg) {  // after the TMEM data is in registers
           unsigned long long tt;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt) : "f"(v[0]), "f"(v[15]) : "memory");
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt) : "f"(v[0][0]), "f"(v[0][15]) : "memory");
           a.dbg[blockIdx.x * DBG + 25] = tt;
         }
         fence_before();
@@ -615,19 +634,21 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         mbar_wait(&at_empty[ab], atf[ab].bit ^ 1u);  // DN(i-2) done with this buffer
         atf[ab].flip();
         if (i == 0 && et == 0) stamp(a, 16);
-        {
-          // this warp's TMEM lanes are group slots 2q (lanes 0-15) and 2q+1
-          // (lanes 16-31); in a slot, lanes 0-7 hold the gate rows of
-          // f = 8 slot + (lane & 7), lanes 8-15 the up rows of the same f.
-          // Slots past the group's last unit get a = 0 (an odd group's last
-          // down K-step reads them).
-          const int slot = 2 * q + (lane >> 4);
+        uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
+        uint16_t* lo = hi + 2048;
+        const int up = (lane >> 3) & 1;
+#pragma unroll
+        for (int t16 = 0; t16 < 2; ++t16) {
+          if (t16 >= nt) break;
+          // this warp's TMEM lanes of tile t16 are group slots 8 t16 + 2q
+          // (lanes 0-15) and 8 t16 + 2q + 1 (lanes 16-31); in a slot, lanes
+          // 0-7 hold the gate rows of f = 8 slot + (lane & 7), lanes 8-15
+          // the up rows of the same f. Slots past the group's last unit get
+          // a = 0 (an odd group's last down K-step reads them).
+          const int slot = 8 * t16 + 2 * q + (lane >> 4);
           const bool valid = slot < g.nu;
           const float* gs = ent_gate + (valid ? static_cast<int>((g.us + slot) / upe) - o_first : 0) * 16;
           const int f = 8 * slot + (lane & 7);
-          const int up = (lane >> 3) & 1;
-          uint16_t* hi = reinterpret_cast<uint16_t*>(aT + static_cast<size_t>(ab) * 8192);
-          uint16_t* lo = hi + 2048;
           float gts[16];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -644,9 +665,9 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int t = 2 * j + up;
-            const float pv = __shfl_xor_sync(0xffffffffu, up ? v[2 * j] : v[2 * j + 1], 8);
-            const float gv = up ? pv : v[2 * j];
-            const float uv = up ? v[2 * j + 1] : pv;
+            const float pv = __shfl_xor_sync(0xffffffffu, up ? v[t16][2 * j] : v[t16][2 * j + 1], 8);
+            const float gv = up ? pv : v[t16][2 * j];
+            const float uv = up ? v[t16][2 * j + 1] : pv;
             const float gt = up ? gts[2 * j + 1] : gts[2 * j];
             const float sv = __fdividef(gv, 1.f + __expf(-gv)) * uv * gt;
             const float av = (valid && t < T && gt != 0.f) ? sv : 0.f;

@@ -65,6 +65,9 @@ struct FfnArgs {
   // grid) of a virtual grid of cta_total CTAs over the layer's work units
   // (cta_total 0: the launch grid itself)
   int cta_base, cta_total;
+  // grouped K3: units per group (8: one M = 128 gate|up tile per group
+  // round; 0 / 16: up to two tiles, one round for CTAs with <= 16 units)
+  int group_units;
 };
 
 struct CombineArgs {
