@@ -157,6 +157,12 @@ int moespac_layer_capacity_experts(double cache_ratio, int n_experts);
  * the latent random walk and per-token Gumbel noise from the same
  * mt19937_64 stream, emitted as noisy fp64 logits [L][gamma+1][N] for K1 (the
  * top-k selection itself runs on the device). Uses the trace fields of cfg. */
+/* The whole generator on the host (TraceGenerator::next_step, trace_model.cpp:
+ * 73-109, incl. its top-k): ids [n_steps][L][gamma+1][k] ascending per
+ * token, accepted [n_steps] (either may be NULL). The operator for trace
+ * export; the device path takes logits (below) and selects with K1. */
+moespac_status moespac_trace_generate(const moespac_sched_config* cfg, int64_t n_steps, int32_t* ids,
+                                      int32_t* accepted);
 typedef struct moespac_trace_synth moespac_trace_synth;
 moespac_status moespac_trace_synth_create(const moespac_sched_config* cfg, moespac_trace_synth** out);
 moespac_status moespac_trace_synth_next(moespac_trace_synth* s, double* logits_host, int32_t* accepted);
@@ -352,6 +358,16 @@ moespac_status moespac_ctx_set_shared(moespac_ctx* c, int layer, const uint16_t*
  * pointer), for MOESPAC_SHARED_GATE_SIGMOID (filled synthetically by
  * moespac_ctx_fill_synthetic otherwise). */
 moespac_status moespac_ctx_set_shared_gate(moespac_ctx* c, int layer, const uint16_t* w_sg);
+/* Estimator checkpoint (LayerEstimator::dump / load, utility_estimator.cpp:
+ * 81-107): the device estimator state of every layer in the reference's text
+ * format, layer after layer, one line "<layer> <expert> <score> <up> <down>
+ * <last_freq>" per expert. load parses every layer before changing anything
+ * (MOESPAC_E_IO with the reference's message on a truncated / malformed
+ * checkpoint), uploads it, and the next step decides from its scores. The
+ * residency pools, queues and ratio estimates are not part of it (the
+ * reference does not serialise them either). */
+moespac_status moespac_ctx_estimator_dump(moespac_ctx* c, const char* path);
+moespac_status moespac_ctx_estimator_load(moespac_ctx* c, const char* path);
 /* Upload the warm-fill residents (sim_core.cpp:108-111) from the arena. */
 moespac_status moespac_ctx_finalize(moespac_ctx* c);
 /* Expert-parallel combine over NCCL: 128-byte ncclUniqueId from rank 0. */

@@ -173,6 +173,8 @@ def lib() -> C.CDLL:
         "moespac_fill_synthetic": (C.c_int, [vp, i64, C.c_uint64, C.c_float, vp]),
         "moespac_unpack_expert": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp, vp]),
         "moespac_ctx_set_shared_gate": (C.c_int, [vp, C.c_int, vp]),
+        "moespac_ctx_estimator_dump": (C.c_int, [vp, C.c_char_p]),
+        "moespac_ctx_estimator_load": (C.c_int, [vp, C.c_char_p]),
         "moespac_ctx_create": (C.c_int, [C.c_int, C.POINTER(ModelDesc), C.POINTER(SchedConfig), C.c_int, C.c_int,
                                          C.POINTER(vp)]),
         "moespac_ctx_destroy": (None, [vp]),
@@ -203,6 +205,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_parallel_mode": (C.c_int, [vp]),
         "moespac_ctx_step_tables": (C.c_int, [vp, vp, vp, vp, vp]),
         "moespac_trace_synth_create": (C.c_int, [C.POINTER(SchedConfig), C.POINTER(vp)]),
+        "moespac_trace_generate": (C.c_int, [C.POINTER(SchedConfig), i64, vp, vp]),
         "moespac_trace_synth_next": (C.c_int, [vp, vp, vp]),
         "moespac_trace_synth_destroy": (None, [vp]),
         "moespac_trace_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, i64, vp, vp]),
@@ -345,6 +348,14 @@ def solve_threshold(scores, resident, gamma, top_k, b_est, rc, rg, t_cpu, t_gpu,
                                         rg.ctypes.data, len(rc), t_cpu, t_gpu, t_io, expert_bytes, vram_left,
                                         draft_credit, out.ctypes.data))
     return out
+
+
+def trace_generate(cfg: SchedConfig, n_steps: int):
+    """Host TraceGenerator (incl. top-k): ids [S][L][gamma+1][k], accepted [S]."""
+    ids = np.zeros((n_steps, cfg.n_layers, cfg.gamma + 1, cfg.top_k), np.int32)
+    acc = np.zeros(n_steps, np.int32)
+    check(lib().moespac_trace_generate(C.byref(cfg), n_steps, ids.ctypes.data, acc.ctypes.data))
+    return ids, acc
 
 
 class TraceSynth:
@@ -545,6 +556,13 @@ class Context:
         if isinstance(w, np.ndarray):
             w = np.ascontiguousarray(w.view(np.uint16))
         check(lib().moespac_ctx_set_shared_gate(self._h, layer, ptr(w)))
+
+    def estimator_dump(self, path: str):
+        """Device estimator state -> the reference's checkpoint text format."""
+        check(lib().moespac_ctx_estimator_dump(self._h, path.encode()))
+
+    def estimator_load(self, path: str):
+        check(lib().moespac_ctx_estimator_load(self._h, path.encode()))
 
     def finalize(self):
         check(lib().moespac_ctx_finalize(self._h))

@@ -36,12 +36,15 @@ SOURCES = [
     "host/trace_synth.cpp",
     "host/cold_executor.cpp",
     "host/trace_io.cpp",
+    "host/estimator.cpp",
+    "host/trace_model.cpp",
     "host/metrics.cpp",
     "abi.cpp",
 ]
 HEADERS = [
     "kernels/common.cuh", "kernels/tcgen05.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
     "host/engine.hpp", "host/trace_synth.hpp", "host/cold_executor.hpp", "host/trace_io.hpp", "host/metrics.hpp",
+    "host/estimator.hpp", "host/trace_model.hpp",
 ]
 
 

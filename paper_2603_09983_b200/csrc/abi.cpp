@@ -13,6 +13,7 @@
 #include "host/metrics.hpp"
 #include "host/trace_io.hpp"
 #include "host/step_scheduler.hpp"
+#include "host/trace_model.hpp"
 #include "host/trace_synth.hpp"
 #include "kernels/launch.hpp"
 
@@ -340,6 +341,39 @@ int moespac_layer_capacity_experts(double cache_ratio, int n_experts) {
 }
 
 // ------------------------------------------------------------ workload
+static TraceSynthConfig synth_config(const moespac_sched_config* cfg) {
+  TraceSynthConfig c;
+  c.n_layers = cfg->n_layers;
+  c.n_experts = cfg->n_experts;
+  c.top_k = cfg->top_k;
+  c.gamma = cfg->gamma;
+  c.alpha = cfg->alpha;
+  c.drift_scale = cfg->drift_scale;
+  c.route_noise = cfg->route_noise;
+  c.shift_period = cfg->shift_period;
+  c.seed = cfg->seed;
+  return c;
+}
+
+moespac_status moespac_trace_generate(const moespac_sched_config* cfg, int64_t n_steps, int32_t* ids,
+                                      int32_t* accepted) {
+  return guard([&] {
+    if (!cfg || n_steps < 0) throw std::invalid_argument("moespac_trace_generate: arguments");
+    TraceGenerator gen(synth_config(cfg));
+    const int L = cfg->n_layers, T = cfg->gamma + 1, k = cfg->top_k;
+    for (int64_t s = 0; s < n_steps; ++s) {
+      const StepActivations a = gen.next_step();
+      if (accepted) accepted[s] = a.accepted_count;
+      if (ids)
+        for (int l = 0; l < L; ++l)
+          for (int t = 0; t < T; ++t)
+            std::copy(a.experts[static_cast<size_t>(l)][static_cast<size_t>(t)].begin(),
+                      a.experts[static_cast<size_t>(l)][static_cast<size_t>(t)].end(),
+                      ids + ((s * L + l) * T + t) * k);
+    }
+  });
+}
+
 moespac_status moespac_trace_synth_create(const moespac_sched_config* cfg, moespac_trace_synth** out) {
   return guard([&] {
     if (!cfg || !out) throw std::invalid_argument("moespac_trace_synth_create: null argument");
@@ -572,6 +606,20 @@ moespac_status moespac_ctx_host_arena(moespac_ctx* c, int64_t n_images, uint16_t
 
 moespac_status moespac_ctx_fill_synthetic(moespac_ctx* c, uint64_t seed, float stdv) {
   return guard([&] { c->e.fill_synthetic(seed, stdv); });
+}
+
+moespac_status moespac_ctx_estimator_dump(moespac_ctx* c, const char* path) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("moespac_ctx_estimator_dump: path");
+    c->e.estimator_dump(path);
+  });
+}
+
+moespac_status moespac_ctx_estimator_load(moespac_ctx* c, const char* path) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("moespac_ctx_estimator_load: path");
+    c->e.estimator_load(path);
+  });
 }
 
 moespac_status moespac_ctx_set_shared_gate(moespac_ctx* c, int layer, const uint16_t* w_sg) {

@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <exception>
+#include <fstream>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +28,7 @@
 
 #include "../kernels/launch.hpp"
 #include "cold_executor.hpp"
+#include "estimator.hpp"
 
 namespace moespac {
 
@@ -431,6 +433,39 @@ int64_t Engine::timeline_steps(int64_t* out, int64_t cap) const {
   for (int64_t i = 0; out && i < std::min(n, cap); ++i)
     std::memcpy(out + 6 * i, tl_steps_[static_cast<size_t>(i)].data(), sizeof(int64_t) * 6);
   return n;
+}
+
+void Engine::estimator_dump(const char* path) {
+  const int L = m_.n_layers, N = m_.n_experts;
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  check(cudaStreamSynchronize(compute_), "sync");
+  std::vector<int32_t> st(static_cast<size_t>(L) * N * 4);
+  check(cudaMemcpy(st.data(), est_d_, sizeof(int32_t) * st.size(), cudaMemcpyDeviceToHost), "D2H estimator");
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error(std::string("estimator_dump: cannot open ") + path);
+  const EstimatorConfig ec = estimator_config_for(sched_->config().policy, sched_->config().estimator);
+  for (int l = 0; l < L; ++l) {
+    LayerEstimator est(N, ec);
+    est.from_device_layout(st.data() + static_cast<size_t>(l) * N * 4);
+    est.dump(out, l);
+  }
+  if (!out) throw std::runtime_error(std::string("estimator_dump: write failed: ") + path);
+}
+
+void Engine::estimator_load(const char* path) {
+  const int L = m_.n_layers, N = m_.n_experts;
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error(std::string("estimator_load: cannot open ") + path);
+  const EstimatorConfig ec = estimator_config_for(sched_->config().policy, sched_->config().estimator);
+  std::vector<int32_t> st(static_cast<size_t>(L) * N * 4);
+  for (int l = 0; l < L; ++l)  // all layers parse before any state changes
+    LayerEstimator::load(in, N, ec).to_device_layout(st.data() + static_cast<size_t>(l) * N * 4);
+  check(cudaSetDevice(device_), "cudaSetDevice");
+  check(cudaStreamSynchronize(compute_), "sync");
+  check(cudaMemcpy(est_d_, st.data(), sizeof(int32_t) * st.size(), cudaMemcpyHostToDevice), "H2D estimator");
+  // the next step decides from the loaded scores
+  for (size_t i = 0; i < scores_.size(); ++i) scores_[i] = st[4 * i];
+  decided_ = false;
 }
 
 void Engine::set_shared_gate(int layer, const uint16_t* w) {

@@ -68,6 +68,10 @@ class Engine {
   void fill_synthetic(uint64_t seed, float stdv);
   void set_shared(int layer, const uint16_t* units_dev);
   void set_shared_gate(int layer, const uint16_t* w_sg);
+  // estimator checkpoint in the reference's text format (one
+  // LayerEstimator::dump per layer, utility_estimator.cpp:81-107)
+  void estimator_dump(const char* path);
+  void estimator_load(const char* path);
   void finalize();
   void set_nccl(const void* uid, int nranks, int rank);
   void set_timing(bool on) { timing_ = on; }

@@ -67,3 +67,18 @@ def test_trace_synth_matches_reference_golden():
             assert acc == z["accepted"][s]
             ids, _ = O.router_topk(logits, int(z["k"]))
             assert np.array_equal(ids, z["ids"][s])
+
+
+def test_host_trace_generator_matches_reference_golden():
+    """moespac_trace_generate (host TraceGenerator mirror, incl. its top-k)
+    reproduces the reference's ids and accepted counts of every committed
+    golden trace (seed 1, reference defaults)."""
+    import glob
+    import os
+    for p in sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "sim_*.npz"))):
+        z = np.load(p)
+        cfg = abi.default_config(n_layers=int(z["L"]), n_experts=int(z["N"]), top_k=int(z["k"]),
+                                 gamma=int(z["gamma"]), shift_period=int(z["shift_period"]),
+                                 drift_scale=float(z["drift_scale"]))
+        ids, acc = abi.trace_generate(cfg, len(z["accepted"]))
+        assert np.array_equal(ids, z["ids"]) and np.array_equal(acc, z["accepted"]), p

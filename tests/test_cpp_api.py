@@ -16,3 +16,17 @@ def test_operator_api_scenarios(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failures" in r.stdout
+
+
+def test_estimator_and_trace_model_scenarios(tmp_path):
+    """utility_estimator_test.cpp / trace_model_test.cpp scenarios against
+    the host LayerEstimator and TraceGenerator mirrors."""
+    exe = tmp_path / "test_estimator_trace_api"
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-ffp-contract=off", "-I", HOST,
+                           os.path.join(ROOT, "tests", "cpp", "test_estimator_trace_api.cpp"),
+                           *(os.path.join(HOST, f) for f in ("estimator.cpp", "scheduler.cpp", "trace_model.cpp",
+                                                             "trace_synth.cpp", "trace_io.cpp")),
+                           "-o", str(exe)])
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 failures" in r.stdout

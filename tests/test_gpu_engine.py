@@ -549,3 +549,51 @@ def test_expert_parallel_combine_is_deterministic():
     one = run(1)
     fa, f1 = O.bf16_bits_to_f32(a).astype(np.float64), O.bf16_bits_to_f32(one).astype(np.float64)
     assert np.linalg.norm(fa - f1) <= 4e-3 * np.linalg.norm(f1)
+
+
+def test_estimator_checkpoint_round_trip(tmp_path):
+    """moespac_ctx_estimator_dump / _load: the device estimator state in the
+    reference's checkpoint format (utility_estimator.cpp:81-107) equals the
+    oracle estimator run over the same routing; a fresh context loaded from it
+    continues bit-identically (outputs and the next checkpoint); malformed
+    checkpoints fail with the reference's error class and change nothing."""
+    L, N, k, g, d, ffn = 2, 16, 4, 6, 1024, 64
+    rng = np.random.default_rng(17)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    a, cfg = _make_ctx(L, N, k, g, d, ffn, 0, 0, 1.0, std, shared, abi.FFN_TENSOR, cold=0)
+    T = g + 1
+    gen = O.Generator(L, N, k, g, seed=21)
+    steps = [gen.next_step() for _ in range(6)]
+    hs = [O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32)) for _ in range(6)]
+    est = [O.estimator_init(N, g) for _ in range(L)]
+    for s in range(5):
+        logits, ids, acc = steps[s]
+        a.step(logits, hs[s], acc, np.zeros_like(hs[s]))
+        for l in range(L):
+            est[l] = O.estimator_observe(est[l], O.hist_scan(ids[l], N)[0], cfg.utility_cap, cfg.forgetting)
+    p1 = str(tmp_path / "est1.txt")
+    a.estimator_dump(p1)
+    rows = np.loadtxt(p1, dtype=np.int64)
+    assert rows.shape == (L * N, 6)
+    for l in range(L):
+        blk = rows[l * N:(l + 1) * N]
+        assert (blk[:, 0] == l).all() and (blk[:, 1] == np.arange(N)).all()
+        assert np.array_equal(blk[:, 2:], est[l])
+    b, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, 1.0, std, shared, abi.FFN_TENSOR, cold=0)
+    bad = tmp_path / "bad.txt"
+    bad.write_text("0 0 1 2 3\n")
+    with pytest.raises(abi.MoespacError) as ei:
+        b.estimator_load(str(bad))
+    assert ei.value.code == "E_IO"
+    b.estimator_load(p1)
+    logits, ids, acc = steps[5]
+    ha, hb = np.zeros_like(hs[5]), np.zeros_like(hs[5])
+    a.step(logits, hs[5], acc, ha)
+    b.step(logits, hs[5], acc, hb)
+    assert np.array_equal(ha, hb)
+    p2a, p2b = str(tmp_path / "a2.txt"), str(tmp_path / "b2.txt")
+    a.estimator_dump(p2a)
+    b.estimator_dump(p2b)
+    assert open(p2a).read() == open(p2b).read()
+    a.close()
+    b.close()
