@@ -5,6 +5,8 @@
 #include "cold_executor.hpp"
 
 #include <immintrin.h>
+#include <pthread.h>
+#include <sched.h>
 
 #include <cmath>
 #include <cstdlib>
@@ -30,13 +32,33 @@ ColdExecutor::ColdExecutor(int threads, int layout, int d, int ffn, int T)
   __builtin_cpu_init();
   bf16_dot_ = __builtin_cpu_supports("avx512bf16") && !std::getenv("MOESPAC_COLD_SCALAR");
   if (threads < 1) threads = 1;
+  // Worker w >= 1 is pinned to its own CPU of the process's allowed set,
+  // skipping the first one, which is left to the driver thread (worker 0,
+  // which also issues the layer's CUDA work): a static chunk partition waits
+  // for its slowest worker, so a worker preempted or migrated mid-layer
+  // stalls the layer (measured: 17-65% window-to-window spread unpinned).
+  // MOESPAC_COLD_PIN=0 disables it.
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  std::vector<int> cpus;
+  if (sched_getaffinity(0, sizeof(allowed), &allowed) == 0)
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+      if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
+  const char* pin_env = std::getenv("MOESPAC_COLD_PIN");
+  pin_ = !(pin_env && pin_env[0] == '0') && static_cast<int>(cpus.size()) >= threads;
   part_.assign(static_cast<size_t>(threads), std::vector<float>(static_cast<size_t>(T) * d));
   scratch_.assign(static_cast<size_t>(threads), std::vector<float>());
   hf_.assign(static_cast<size_t>(T) * d, 0.f);
   // Workers spin briefly on the job generation before sleeping: a layer's
   // cold work arrives every few hundred microseconds, and a condition-
   // variable wake-up per layer and worker cost tens of microseconds each.
-  for (int w = 1; w < threads; ++w) workers_.emplace_back([this, w] {
+  for (int w = 1; w < threads; ++w) workers_.emplace_back([this, w, cpu = pin_ ? cpus[static_cast<size_t>(w)] : -1] {
+      if (cpu >= 0) {
+        cpu_set_t one;
+        CPU_ZERO(&one);
+        CPU_SET(cpu, &one);
+        pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
+      }
       int seen = 0;
       for (;;) {
         bool got = false;

@@ -35,6 +35,7 @@ class ColdExecutor {
   void run(const std::vector<ColdItem>& items, const uint16_t* h, float* y);
   int threads() const { return static_cast<int>(workers_.size()) + 1; }
   bool bf16_dot() const { return bf16_dot_; }
+  bool pinned() const { return pin_; }
 
  private:
   void work(int w);
@@ -51,6 +52,7 @@ class ColdExecutor {
   std::vector<float> hf_;                 // [T][d] fp32
   const uint16_t* hb_ = nullptr;          // [T][d] bf16 (the AVX-512 BF16 path reads it directly)
   bool bf16_dot_ = false;                 // host has VDPBF16PS (tensor-core image only)
+  bool pin_ = false;                      // workers pinned one per CPU
   std::vector<std::vector<float>> part_;  // per worker [T][d]
   std::vector<std::vector<float>> scratch_;
   std::vector<std::pair<int, int>> units_;  // (item, chunk)

@@ -277,6 +277,10 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   load_done_.resize(static_cast<size_t>(L));
   ffn_beg_.resize(static_cast<size_t>(L));
   ffn_end_.resize(static_cast<size_t>(L));
+  xload_ev_.resize(static_cast<size_t>(L));
+  for (auto& e : xload_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  preloaded_.assign(static_cast<size_t>(L), 0);
+  if (const char* e = std::getenv("MOESPAC_CROSS_STEP")) cross_step_ = std::atoi(e) != 0;
   wait_beg_.resize(static_cast<size_t>(L));
   layer_end_.resize(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
@@ -323,7 +327,7 @@ Engine::~Engine() {
   if (tables_h_) cudaFreeHost(tables_h_);
   if (out_h_) cudaFreeHost(out_h_);
   for (auto e : load_done_) cudaEventDestroy(e);
-  for (auto* v : {&wait_beg_, &layer_end_, &ld_beg_, &ld_end_})
+  for (auto* v : {&wait_beg_, &layer_end_, &ld_beg_, &ld_end_, &xload_ev_})
     for (auto e : *v) cudaEventDestroy(e);
   for (auto e : ffn_beg_) cudaEventDestroy(e);
   for (auto e : ffn_end_) cudaEventDestroy(e);
@@ -463,7 +467,10 @@ void Engine::estimator_load(const char* path) {
   check(cudaSetDevice(device_), "cudaSetDevice");
   check(cudaStreamSynchronize(compute_), "sync");
   check(cudaMemcpy(est_d_, st.data(), sizeof(int32_t) * st.size(), cudaMemcpyHostToDevice), "H2D estimator");
-  // the next step decides from the loaded scores
+  // the next step decides from the loaded scores; loads issued for the
+  // superseded decision land first (the pools already account for them)
+  check(cudaStreamSynchronize(copy_), "sync copy");
+  std::fill(preloaded_.begin(), preloaded_.end(), 0);
   for (size_t i = 0; i < scores_.size(); ++i) scores_[i] = st[4 * i];
   decided_ = false;
 }
@@ -500,6 +507,7 @@ void Engine::finalize() {
   check(cudaStreamSynchronize(compute_), "sync");
   finalized_ = true;
   decided_ = false;
+  std::fill(preloaded_.begin(), preloaded_.end(), 0);
   // Misses are possible when a shard holds fewer slots than experts: start
   // the host cold-expert executor (the CPU side of the HWB split).
   const int shard_size = (m_.n_experts - shard_rank_ + shard_world_ - 1) / shard_world_;
@@ -740,11 +748,16 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     size_t i = 0;
     const auto& loads = sched_->loads();
     for (int l = 0; l < L; ++l) {
+      const bool pre = preloaded_[static_cast<size_t>(l)] != 0;  // issued during the previous step
       for (; i < loads.size() && loads[i].layer == l; ++i) {
         const SlotLoad& ld = loads[i];
         ++layer_loads[static_cast<size_t>(l)];
         if (ld.shard != shard_rank_) continue;
         ++layer_loads_local[static_cast<size_t>(l)];
+        if (pre) {
+          ++n_loads;
+          continue;
+        }
         if (timeline_) {
           while (ld_beg_.size() <= static_cast<size_t>(n_loads)) {
             ld_beg_.emplace_back();
@@ -762,7 +775,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         if (timeline_) check(cudaEventRecord(ld_end_[static_cast<size_t>(n_loads)], copy_), "event");
         ++n_loads;
       }
-      check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
+      if (!pre) check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
+      preloaded_[static_cast<size_t>(l)] = 0;
     }
   }
   if (timing) check(cudaEventRecord(copy_ev_[1], copy_), "event");
@@ -949,6 +963,21 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     }
 
     if (h_in_host) std::memcpy(hcold_h_, h_in, sizeof(uint16_t) * T_ * d);
+    // Cross-step loads (the device meaning of freeze / thaw_and_recycle,
+    // execution_engine.cpp:111-126): this step is accounted and the next one
+    // decided right away (the K2 counters are all that needs), and the next
+    // step's loads into layer l are issued on the copy stream as soon as this
+    // step's last reader of layer l's slots (its K3, behind the layer's
+    // combine) is done — they overlap this step's remaining layers and host
+    // cold path instead of waiting for the next step to start.
+    const bool xstep = cross_step_ && !timeline_;
+    std::vector<std::vector<const SlotLoad*>> next_loads;
+    if (xstep) {
+      host_account();
+      next_loads.resize(static_cast<size_t>(L));
+      for (const SlotLoad& ld : sched_->loads())
+        if (ld.shard == shard_rank_) next_loads[static_cast<size_t>(ld.layer)].push_back(&ld);
+    }
     double wait_ms = 0.0;
     const auto t_loop0 = std::chrono::steady_clock::now();
     for (int l = 0; l < L; ++l) {
@@ -968,6 +997,16 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         y_extra = yd;
       }
       launch_combine_layer(l, y_extra);
+      if (xstep && !next_loads[static_cast<size_t>(l)].empty()) {
+        check(cudaEventRecord(xload_ev_[static_cast<size_t>(l)], compute_), "event");
+        check(cudaStreamWaitEvent(copy_, xload_ev_[static_cast<size_t>(l)], 0), "wait last reader");
+        for (const SlotLoad* ld : next_loads[static_cast<size_t>(l)])
+          check(cudaMemcpyAsync(slot_ptr(l, ld->slot), arena_h_ + image_of(l, ld->expert) * image_elems_,
+                                image_elems_ * 2, cudaMemcpyHostToDevice, copy_),
+                "H2D expert load (next step)");
+        check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
+        preloaded_[static_cast<size_t>(l)] = 1;
+      }
       if (l + 1 < L) {
         if (!items[static_cast<size_t>(l + 1)].empty()) {
           check(cudaMemcpyAsync(hcold_h_ + static_cast<size_t>(l + 1) * T_ * d, h_d_ + static_cast<size_t>(l + 1) * T_ * d,
@@ -979,7 +1018,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       }
     }
     const auto a0 = std::chrono::steady_clock::now();
-    host_account();
+    if (!xstep) host_account();
     if (cold_trace_)
       std::fprintf(stderr, "cold-trace: prologue %.3f ms, h waits %.3f ms, cold %.3f ms, loop %.3f ms, account %.3f ms\n",
                    std::chrono::duration<double, std::milli>(t_loop0 - t_step0).count(), wait_ms, cpu_ms_cold,

@@ -194,6 +194,11 @@ class Engine {
   // measured timeline
   bool timeline_ = false;
   std::vector<cudaEvent_t> wait_beg_, layer_end_, ld_beg_, ld_end_;
+  // cross-step loads: next step's loads of layer l issued during this step
+  // after its last reader of the layer's slots (xload_ev_[l])
+  std::vector<cudaEvent_t> xload_ev_;
+  std::vector<uint8_t> preloaded_;  // [L] loads of the coming step already on the copy stream
+  bool cross_step_ = true;          // MOESPAC_CROSS_STEP=0 disables
   std::vector<std::array<int64_t, 6>> tl_events_;
   std::vector<ThresholdDecision> sched_decisions_;  // decisions of the step being executed
   std::vector<moespac_layer_timing> tl_layers_;
