@@ -353,12 +353,17 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         stream = torch.cuda.ExternalStream((c or ctx).stream())
         reps = []
+        nvtx = os.environ.get("MOESPAC_NVTX") == "1"  # profiling: ncu --nvtx --nvtx-include "timed/"
+        if nvtx:
+            torch.cuda.nvtx.range_push("timed")
         e0.record(stream)
         for i in range(n):
             reps.append(fn(offset + i))
             if per_step:
                 per_step(reps[-1])
         e1.record(stream)
+        if nvtx:
+            torch.cuda.nvtx.range_pop()
         barrier()
         return max_over_ranks(e0.elapsed_time(e1)), reps
 

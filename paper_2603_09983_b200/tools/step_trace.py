@@ -31,8 +31,8 @@ def main():
     w = configs.CONFIGS[args.config]
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=args.cache_ratio)
-    ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, w.n_shared_units, w.gate_mode, 0), cfg, 0, 1)
-    ctx.host_arena(min(L * N, max(N, 8)))
+    ctx = abi.Context(0, w.model_desc(), cfg, 0, 1)
+    ctx.host_arena(min(L * N, N + 1))
     ctx.fill_synthetic(seed=3, stdv=SYNTH_STD)
     ctx.finalize()
     ctx.set_pdl(bool(args.pdl))
