@@ -30,3 +30,16 @@ def test_estimator_and_trace_model_scenarios(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 failures" in r.stdout
+
+
+REF_INCLUDE = "/root/reference/proj/core/include"
+
+
+def test_reference_side_binding_compiles():
+    """INTEGRATION.md's B200Backend (tests/cpp/b200_backend.cpp) compiles
+    against the reference's own headers and include/moespac/moespac.h."""
+    import pytest
+    if not os.path.isdir(REF_INCLUDE):
+        pytest.skip("/root/reference not mounted")
+    subprocess.check_call(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Werror", "-I", REF_INCLUDE,
+                           "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "cpp", "b200_backend.cpp")])
