@@ -429,6 +429,11 @@ moespac_status moespac_ctx_set_timeline(moespac_ctx* c, int enabled);
 int64_t moespac_ctx_timeline_events(const moespac_ctx* c, int64_t* out, int64_t cap);
 int64_t moespac_ctx_timeline_layers(const moespac_ctx* c, moespac_layer_timing* out, int64_t cap);
 int64_t moespac_ctx_timeline_steps(const moespac_ctx* c, int64_t* out, int64_t cap);
+/* Launch-latency path (on by default): a step with no expert loads, no host
+ * cold path, no draft phase and no per-kernel timing enqueues the same device
+ * work every time, so the context captures it once into a CUDA graph
+ * (programmatic dependencies included) and replays it with one launch. */
+moespac_status moespac_ctx_set_graph(moespac_ctx* c, int enabled);
 /* Programmatic dependent launch between layer kernels (on by default). */
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled);
 /* Profiling hook: device buffer of [n_layers][grid][32] uint64 that every

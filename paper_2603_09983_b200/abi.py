@@ -186,6 +186,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_nccl": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "moespac_ctx_set_timing": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_pdl": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_graph": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_draft_window": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_draft_model": (C.c_int, [vp, i64, C.c_int]),
         "moespac_ctx_set_timeline": (C.c_int, [vp, C.c_int]),
@@ -575,6 +576,10 @@ class Context:
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))
+
+    def set_graph(self, on: bool = True):
+        """Launch-latency path: replay a captured CUDA graph of load-free steps."""
+        check(lib().moespac_ctx_set_graph(self._h, int(on)))
 
     def set_draft_window(self, on: bool = True):
         check(lib().moespac_ctx_set_draft_window(self._h, int(on)))

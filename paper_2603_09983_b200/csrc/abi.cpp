@@ -707,6 +707,10 @@ int64_t moespac_ctx_timeline_steps(const moespac_ctx* c, int64_t* out, int64_t c
   return c->e.timeline_steps(out, cap);
 }
 
+moespac_status moespac_ctx_set_graph(moespac_ctx* c, int enabled) {
+  return guard([&] { c->e.set_graph(enabled != 0); });
+}
+
 moespac_status moespac_ctx_set_pdl(moespac_ctx* c, int enabled) {
   return guard([&] { c->e.set_pdl(enabled != 0); });
 }

@@ -281,6 +281,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   for (auto& e : xload_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   preloaded_.assign(static_cast<size_t>(L), 0);
   if (const char* e = std::getenv("MOESPAC_CROSS_STEP")) cross_step_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("MOESPAC_GRAPH")) use_graph_ = std::atoi(e) != 0;
   wait_beg_.resize(static_cast<size_t>(L));
   layer_end_.resize(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
@@ -303,8 +304,15 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   scores_.assign(static_cast<size_t>(L) * N, 0);
 }
 
+void Engine::drop_graph() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  graph_exec_ = nullptr;
+  graph_warm_ = 0;
+}
+
 Engine::~Engine() {
   cudaSetDevice(device_);
+  drop_graph();
   if (compute_) cudaStreamSynchronize(compute_);
   if (copy_) cudaStreamSynchronize(copy_);
   if (comm_ && nccl_) nccl_->comm_destroy(comm_);
@@ -508,6 +516,7 @@ void Engine::finalize() {
   finalized_ = true;
   decided_ = false;
   std::fill(preloaded_.begin(), preloaded_.end(), 0);
+  drop_graph();
   // Misses are possible when a shard holds fewer slots than experts: start
   // the host cold-expert executor (the CPU side of the HWB split).
   const int shard_size = (m_.n_experts - shard_rank_ + shard_world_ - 1) / shard_world_;
@@ -632,18 +641,44 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
 
   if (timing) check(cudaEventRecord(ev_[0], compute_), "event");
   // ---- compute stream
-  check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   const double* lg = logits;
   if (replay_ids_ || model_mode_) {
     lg = nullptr;
-  } else if (logits_host) {
-    check(cudaMemcpyAsync(logits_d_, logits, sizeof(double) * L * T_ * N, cudaMemcpyHostToDevice, compute_),
-          "H2D logits");
+  } else if (logits_host || (use_graph_ && world_ == 1 && !cold_)) {
+    // (device logits are copied too when a captured graph may run the step:
+    // its K1 reads the context's own buffer)
+    check(cudaMemcpyAsync(logits_d_, logits, sizeof(double) * L * T_ * N,
+                          logits_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, compute_),
+          "logits");
     lg = logits_d_;
   }
   check(cudaMemcpyAsync(h_d_, h_in, sizeof(uint16_t) * T_ * d,
                         h_in_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, compute_),
         "h_in");
+  // Launch-latency path (SURVEY.md §7 hard part (iii)): a step without
+  // loads, host cold path, draft phase or per-kernel events enqueues the
+  // same device work every time — tables H2D, K1, K2, scores D2H, h^T, and
+  // L x (K3 + combine) from fixed buffers — so it is captured once into a
+  // CUDA graph (programmatic dependencies included) and replayed with one
+  // launch. The caller's logits / h_in are copied into the graph's input
+  // buffers just above; only the tables' contents change between replays.
+  bool graph_replay = false, graph_capture = false;
+  if (use_graph_ && world_ == 1 && !cold_ && !replay_ids_ && !model_mode_ && !timing && !drafted_any() && !k3_trace_ &&
+      lg == logits_d_) {
+    bool local_loads = false;
+    for (const SlotLoad& ld : sched_->loads()) local_loads = local_loads || ld.shard == shard_rank_;
+    if (!local_loads) {
+      if (graph_exec_) {
+        graph_replay = true;
+      } else if (++graph_warm_ >= 2) {  // capture after the kernels' first launches (attributes set)
+        graph_capture = true;
+        check(cudaStreamBeginCapture(compute_, cudaStreamCaptureModeThreadLocal), "begin capture");
+      }
+    }
+  }
+  const bool enq = !graph_replay;  // enqueue the device work (or capture it)
+  if (enq)
+    check(cudaMemcpyAsync(tables_d_, tables_h_, tables_bytes_, cudaMemcpyHostToDevice, compute_), "H2D tables");
   // Draft phase before the verification: the step's loads (issued below on
   // the copy stream) overlap it, as the reference's decisions assume (draft
   // credit, sim_core.cpp:167-172). Draft model: gamma weight-streaming GEMV
@@ -682,7 +717,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     }
     check(cudaMemcpyAsync(ids_d_, ih, sizeof(int32_t) * L * T_ * k, cudaMemcpyHostToDevice, compute_), "H2D ids");
     check(cudaMemcpyAsync(gates_d_, gh, sizeof(float) * L * T_ * k, cudaMemcpyHostToDevice, compute_), "H2D gates");
-  } else if (!model_mode_) {
+  } else if (!model_mode_ && enq) {
     check(launch_router_topk(lg, L * T_, N, k, m_.gate_mode, ids_d_, gates_d_, compute_), "K1 router");
   }
   if (timing) check(cudaEventRecord(ev_[2], compute_), "event");
@@ -714,13 +749,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   a2.counters = counters_d;
   a2.scores_out = scores_out_d;
   a2.gates = gates_d_;
-  if (!model_mode_) check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
+  if (!model_mode_ && enq) check(launch_hist_scan_observe(a2, compute_), "K2 hist/scan/observe");
   if (timing) check(cudaEventRecord(ev_[3], compute_), "event");
   // scores + counters (+ routing for the cold path) back to the host right
   // away: the host scheduler works on them while the device runs the layers
   // (model mode: each layer's routing is known only after the layer before
   // it, so the copy follows the last layer)
-  if (!model_mode_)
+  if (!model_mode_ && enq)
     check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
   const bool cold = static_cast<bool>(cold_);
   int32_t* ids_h = reinterpret_cast<int32_t*>(route_h_);
@@ -732,7 +767,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     if (!h_in_host)
       check(cudaMemcpyAsync(hcold_h_, h_d_, sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_), "D2H h0");
   }
-  if (!model_mode_) check(cudaEventRecord(k2_done_, compute_), "event");
+  if (!model_mode_ && enq) check(cudaEventRecord(k2_done_, compute_), "event");
 
   // ---- copy engine: this step's loads in drain order, one event per layer,
   // issued after the compute stream's small H2D copies above: host->device
@@ -775,7 +810,8 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         if (timeline_) check(cudaEventRecord(ld_end_[static_cast<size_t>(n_loads)], copy_), "event");
         ++n_loads;
       }
-      if (!pre) check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
+      if (!pre && layer_loads_local[static_cast<size_t>(l)] > 0)
+        check(cudaEventRecord(load_done_[static_cast<size_t>(l)], copy_), "event");
       preloaded_[static_cast<size_t>(l)] = 0;
     }
   }
@@ -785,7 +821,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   const int n_shared_eff = (world_ > 1 && !split_ && rank_ != 0) ? 0 : m_.n_shared_units;
   const bool tc = kernel_ == kFfnTensorCore;
   uint16_t* hT[2] = {hT_d_, hT_d_ + static_cast<size_t>(16) * d};
-  if (tc) check(launch_build_hT(h_d_, T_, d, hT[0], compute_), "build_hT");
+  if (tc && enq) check(launch_build_hT(h_d_, T_, d, hT[0], compute_), "build_hT");
 
   auto launch_ffn = [&](int l) {
     // Only a layer with this-rank loads needs the copy-stream event; every
@@ -917,7 +953,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
 
   if (!cold) {
     // ---- all layers on the device back to back; host accounting overlaps
-    for (int l = 0; l < L; ++l) {
+    for (int l = 0; l < L && enq; ++l) {
       if (model_mode_) {
         // K0 router GEMV on h_l, then K1 + K2 for layer l
         const bool pdl = pdl_ && !timing;
@@ -934,6 +970,14 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       check(cudaMemcpyAsync(out_h_, out_d_, out_bytes_, cudaMemcpyDeviceToHost, compute_), "D2H scores/counters");
       check(cudaEventRecord(k2_done_, compute_), "event");
     }
+    if (graph_capture) {
+      cudaGraph_t g = nullptr;
+      check(cudaStreamEndCapture(compute_, &g), "end capture");
+      const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+      cudaGraphDestroy(g);
+      check(e, "graph instantiate");
+    }
+    if (graph_capture || graph_replay) check(cudaGraphLaunch(graph_exec_, compute_), "graph launch");
     check(cudaEventSynchronize(k2_done_), "sync K2");
     host_account();
   } else {

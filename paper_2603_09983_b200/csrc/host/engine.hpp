@@ -75,8 +75,14 @@ class Engine {
   void finalize();
   void set_nccl(const void* uid, int nranks, int rank);
   void set_timing(bool on) { timing_ = on; }
-  void set_pdl(bool on) { pdl_ = on; }
-  void set_k3_trace(unsigned long long* buf) { k3_trace_ = buf; }
+  void set_pdl(bool on) {
+    pdl_ = on;
+    drop_graph();
+  }
+  void set_k3_trace(unsigned long long* buf) {
+    k3_trace_ = buf;
+    drop_graph();
+  }
   void set_draft_window(bool on) { draft_window_ = on; }
   // real draft phase: gamma weight-streaming GEMV passes over n_params bf16
   // draft weights (rows of d_draft) before each verification step
@@ -96,7 +102,16 @@ class Engine {
     if (!g || g->world() != world_) throw std::invalid_argument("moespac_ctx_set_loopback: group size != shard world");
     loop_ = g;
   }
-  void set_l2_prefetch(int bytes) { l2_prefetch_ = bytes; }
+  void set_l2_prefetch(int bytes) {
+    l2_prefetch_ = bytes;
+    drop_graph();
+  }
+  // launch-latency path: replay a captured CUDA graph of steps without loads
+  // or host work (on by default; MOESPAC_GRAPH=0)
+  void set_graph(bool on) {
+    use_graph_ = on;
+    drop_graph();
+  }
   // host threads for cold (non-resident) experts: -1 auto, 0 = off (misses
   // are then counted but not computed); takes effect at finalize()
   void set_cold_threads(int n) { cold_threads_ = n; }
@@ -199,6 +214,12 @@ class Engine {
   std::vector<cudaEvent_t> xload_ev_;
   std::vector<uint8_t> preloaded_;  // [L] loads of the coming step already on the copy stream
   bool cross_step_ = true;          // MOESPAC_CROSS_STEP=0 disables
+  // captured step graph (launch-latency path)
+  void drop_graph();
+  bool drafted_any() const { return T_ > 1 && (draft_R_ > 0 || draft_window_); }
+  bool use_graph_ = true;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int graph_warm_ = 0;
   std::vector<std::array<int64_t, 6>> tl_events_;
   std::vector<ThresholdDecision> sched_decisions_;  // decisions of the step being executed
   std::vector<moespac_layer_timing> tl_layers_;

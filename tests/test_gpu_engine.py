@@ -597,3 +597,46 @@ def test_estimator_checkpoint_round_trip(tmp_path):
     assert open(p2a).read() == open(p2b).read()
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("d,ffn,kernel", [(1024, 128, abi.FFN_TENSOR), (4096, 128, abi.FFN_TENSOR),
+                                          (1024, 64, abi.FFN_CUDACORE)])
+def test_graph_replay_bitwise_equal(d, ffn, kernel):
+    """The launch-latency path (a captured CUDA graph replayed for load-free
+    steps) gives the bits of the launch-by-launch path: h_out, K3 outputs,
+    reports and the SimEvent log, host and device inputs alike, across a
+    toggle of programmatic dependent launch (which re-captures)."""
+    L, N, k, g = 3, 16, 4, 6
+    rng = np.random.default_rng(d + ffn)
+    std, shared = _experts(rng, L, N, d, ffn, 0)
+    a, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, 1.0, std, shared, kernel, cold=0)
+    b, _ = _make_ctx(L, N, k, g, d, ffn, 0, 0, 1.0, std, shared, kernel, cold=0)
+    a.set_graph(False)
+    b.set_graph(True)
+    T = g + 1
+    gen = O.Generator(L, N, k, g, seed=8)
+    for s in range(8):
+        logits, _, acc = gen.next_step()
+        h0 = O.f32_to_bf16_bits(rng.normal(0, 1, (T, d)).astype(np.float32))
+        if s == 5:
+            a.set_pdl(False)
+            b.set_pdl(False)
+        outs = []
+        for c in (a, b):
+            if s % 2:
+                ho = torch.zeros((T, d), dtype=torch.int16, device="cuda")
+                rep, lay = c.step_device(torch.from_numpy(logits).cuda(), torch.from_numpy(h0.view(np.int16)).cuda(),
+                                         acc, ho)
+                torch.cuda.synchronize()
+                h_out = ho.cpu().numpy().view(np.uint16)
+            else:
+                h_out = np.zeros_like(h0)
+                rep, lay = c.step(logits, h0, acc, h_out)
+            v = c.views()
+            outs.append((h_out, abi.fetch(v.y_dev, (L, T, d), np.float32), rep.cache_hits, rep.kernel_launches,
+                         [(x.tau, x.n_prefetch) for x in lay]))
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1]), s
+        assert outs[0][2:] == outs[1][2:], s
+    assert np.array_equal(a.sched_events(), b.sched_events())
+    a.close()
+    b.close()
