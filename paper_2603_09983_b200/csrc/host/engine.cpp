@@ -767,7 +767,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     if (!h_in_host)
       check(cudaMemcpyAsync(hcold_h_, h_d_, sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_), "D2H h0");
   }
-  if (!model_mode_ && enq) check(cudaEventRecord(k2_done_, compute_), "event");
+  // (inside a graph capture the record becomes an event-record node, so the
+  // replayed graph still signals the host as soon as K2's copy is back)
+  if (!model_mode_ && enq)
+    check(graph_capture ? cudaEventRecordWithFlags(k2_done_, compute_, cudaEventRecordExternal)
+                        : cudaEventRecord(k2_done_, compute_),
+          "event");
 
   // ---- copy engine: this step's loads in drain order, one event per layer,
   // issued after the compute stream's small H2D copies above: host->device
