@@ -42,7 +42,7 @@ SOURCES = [
     "abi.cpp",
 ]
 HEADERS = [
-    "kernels/common.cuh", "kernels/tcgen05.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
+    "kernels/common.cuh", "kernels/k3_stream.cuh", "kernels/tcgen05.cuh", "kernels/launch.hpp", "host/scheduler.hpp", "host/step_scheduler.hpp",
     "host/engine.hpp", "host/trace_synth.hpp", "host/cold_executor.hpp", "host/trace_io.hpp", "host/metrics.hpp",
     "host/estimator.hpp", "host/trace_model.hpp",
 ]

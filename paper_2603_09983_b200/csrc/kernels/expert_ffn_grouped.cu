@@ -28,9 +28,17 @@
 //
 // Warp roles (192 threads): 0 TMA producer, 1 MMA issuer (TMEM owner),
 // 2-5 epilogue (TMEM lane quarters 2, 3, 0, 1 = group slots).
+#include <cuda.h>
+
 #include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "common.cuh"
+#include "k3_stream.cuh"
 #include "launch.hpp"
 #include "tcgen05.cuh"
 
@@ -50,9 +58,8 @@ using tc::smem_desc;
 constexpr int THREADS = 192;
 constexpr int EPI_THREADS = 128;
 constexpr int NSLOT = 32;      // ring entries in flight (mbarrier pairs)
-constexpr int TILE = 16384;    // one gate|up K-tile or down M-tile of a 64-row chunk
-constexpr int UB = 2048;       // one 8-row unit (gate + up octet) of a gate|up tile, or 8 k of a down tile
-constexpr int UPC = 8;         // units per 64-row chunk
+constexpr int TILE = k3s::TILE;  // one gate|up K-tile or down M-tile of a 64-row chunk
+constexpr int UB = k3s::UB;      // one 8-row unit (gate + up octet) of a gate|up tile, or 8 k of a down tile
 constexpr int GMAX = 16;       // units per group: up to two M = 128 gate|up tiles (8 units each)
 constexpr int HTS = 2048;      // h^T slice of one K-tile (16 tokens x 64 k)
 constexpr int ENT_MAX = 32;    // entries one CTA may touch (one producer lane each)
@@ -62,47 +69,12 @@ constexpr int TMEM_COLS = 512;
 constexpr int DBG = 32;
 
 // ---------------------------------------------------------------- groups
-// Work unit = 8 ffn rows of one expert (its 8 gate + 8 up rows: one 2 KiB
-// run per gate|up K-tile, one 2 KiB k-chunk per down M-tile). A group is <=
-// gmax (8 or 16) consecutive units of the CTA's range — one or two M = 128
-// gate|up tiles — cut so that it spans at most two chunk pieces (chunks are
-// 8 units and entry boundaries are chunk boundaries because ffn % 64 == 0):
-// a 16-unit group starting mid-chunk ends at the end of the next chunk. (A
-// CTA's 9 units always fit one group; measured, a third piece per group
-// made the producer's per-copy bookkeeping ~4% slower on the Qwen3 shape.)
-struct Grp {
-  long long us;                 // first unit (global order)
-  int nu, np;
-  int o[2], c[2], pa[2], n[2];  // piece p: units [pa, pa + n) of chunk c of entry o
-};
-
-struct GroupIt {
-  long long u, u1;
-  int upe;   // units per entry = ffn / 8
-  int gmax;  // units per group (8 or 16)
-  __device__ __forceinline__ bool next(Grp& g) {
-    if (u >= u1) return false;
-    const int o = static_cast<int>(u / upe), ui = static_cast<int>(u % upe);
-    // end of u's chunk, and of the chunk after it (a group has <= 2 pieces)
-    const long long cend = static_cast<long long>(o) * upe + (ui / UPC + 1) * UPC;
-    long long ue = u + gmax < u1 ? u + gmax : u1;
-    if (ue > cend + UPC) ue = cend + UPC;
-    g.us = u;
-    g.nu = static_cast<int>(ue - u);
-    const long long e = cend < ue ? cend : ue;
-    g.o[0] = o;
-    g.c[0] = ui / UPC;
-    g.pa[0] = ui % UPC;
-    g.n[0] = static_cast<int>(e - u);
-    g.np = e < ue ? 2 : 1;
-    g.o[1] = static_cast<int>(e / upe);
-    g.c[1] = static_cast<int>(e % upe) / UPC;
-    g.pa[1] = 0;
-    g.n[1] = static_cast<int>(ue - e);
-    u = ue;
-    return true;
-  }
-};
+// Work unit = 8 ffn rows of one expert; groups of <= gmax (8 or 16) units,
+// at most two chunk pieces each (k3_stream.cuh). (A CTA's 9 units always fit
+// one 16-unit group; measured, a third piece per group made the producer's
+// per-copy bookkeeping ~4% slower on the Qwen3 shape.)
+using k3s::Grp;
+using k3s::GroupIt;
 
 __device__ __forceinline__ int pow2_divisor(int x, int cap) {
   int m = 1;
@@ -260,45 +232,16 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     long long w_empty = 0;
     const uint64_t pol = a.l2_policy == 1 ? l2_evict_normal_policy() : l2_evict_first_policy();
     const uint64_t pol_h = l2_evict_normal_policy();
-    // entry image bases, one lane per entry of this CTA's range
+    // entry image bases (and image index in its buffer), one lane per entry
+    // of this CTA's range
     unsigned long long my_base = 0;
+    int my_img = 0;
     if (lane < n_ent) {
       const int o = o_first + lane;
-      const uint16_t* w = o < n_hits ? a.pool + static_cast<long long>(a.slot_of[a.hit_list[o]]) * a.expert_elems
-                                     : a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
+      my_img = o < n_hits ? a.slot_of[a.hit_list[o]] : o - n_hits;
+      const uint16_t* w = (o < n_hits ? a.pool : a.shared_w) + static_cast<long long>(my_img) * a.expert_elems;
       my_base = reinterpret_cast<unsigned long long>(w);
     }
-    // L2 prefetch of a layer's stream for this CTA index, in stream order
-    // (approximately: group order), skipping the first `skip` bytes; run r
-    // is issued by lane r % 32
-    auto prefetch_l2 = [&](int nh, const int32_t* hit_list, const int32_t* slot_of, const uint16_t* pool,
-                           const uint16_t* shared_w, long long skip, long long budget) {
-      const long long nn = static_cast<long long>(nh + a.n_shared) * upe;
-      const long long p0 = nn > 0 ? (bg * nn) / G : 0, p1 = nn > 0 ? ((bg + 1) * nn) / G : 0;
-      GroupIt pit{p0, p1, upe, gmax};
-      Grp pg;
-      int rc = 0;
-      while (budget > 0 && pit.next(pg)) {
-        for (int i = 0; i < pg.np && budget > 0; ++i) {
-          const int o = pg.o[i];
-          const uint16_t* w = o < nh ? pool + static_cast<long long>(slot_of[hit_list[o]]) * a.expert_elems
-                                     : shared_w + static_cast<long long>(o - nh) * a.expert_elems;
-          const uint8_t* base = reinterpret_cast<const uint8_t*>(w) + pg.c[i] * chunk_bytes + pg.pa[i] * UB;
-          const uint32_t run = static_cast<uint32_t>(pg.n[i]) * UB;
-          for (int t = 0; t < ktiles + mtiles && budget > 0; ++t) {
-            if (skip > 0) {
-              skip -= run;
-              continue;
-            }
-            if ((rc++ & 31) == lane)
-              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + static_cast<size_t>(t) * TILE),
-                           "r"(run)
-                           : "memory");
-            budget -= run;
-          }
-        }
-      }
-    };
     bool waited = false;
     // (Measured: an own-stream L2 prefetch issued here, at the first full
     // ring before the input wait, made the layer 7-15% slower for 128-384
@@ -347,14 +290,27 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     };
     // tiles [t0, t0 + m) (tile index within the chunk: K-tiles then M-tiles)
     // of every piece, slot-packed: tile j of the entry at j * nu * 2 KiB.
-    // One copy per lane: a thread's bulk copies issue one after another
+    // A one-piece group's entry is ONE tensor copy (box: n runs of 2 KiB x m
+    // tiles, landing in exactly that order). Two-piece groups interleave the
+    // pieces inside every tile, so they take one bulk copy per (tile, piece),
+    // one copy per lane: a thread's bulk copies issue one after another
     // (~0.1-0.3 us each, tools/tma_probe.cu), copies from different lanes
-    // overlap — with one issuing lane, split runs capped the stream at
-    // 8-40 GB/s per SM.
+    // overlap. (Measured: a 1-unit group's 2 KiB bulk copies streamed at
+    // ~17 GB/s per SM — the second group round of a 9-unit CTA took 4 us.)
     auto copy_entry = [&](const Grp& g, const uint8_t* const (&pb)[2], int t0, int m, uint32_t e, uint64_t* bar) {
       const uint32_t ab = static_cast<uint32_t>(g.nu) * UB;
       const uint32_t n0 = static_cast<uint32_t>(g.n[0]) * UB;
       __syncwarp();  // after the leader's expect_tx
+      if (g.np == 1) {
+        const int img = __shfl_sync(0xffffffffu, my_img, g.o[0] - o_first);
+        const uint8_t* tm = reinterpret_cast<const uint8_t*>(g.o[0] < n_hits ? a.tm_pool : a.tm_shared);
+        if (tm != nullptr) {
+          if (lane == 0)
+            tma_load_5d(ring + e, tm + (static_cast<size_t>(g.n[0] - 1) * 5 + (31 - __clz(m))) * 128, 0, g.pa[0], t0,
+                        g.c[0], img, bar, pol);
+          return;
+        }
+      }
       for (int c = lane; c < m * g.np; c += 32) {
         const int j = g.np > 1 ? c >> 1 : c;
         if (g.np == 1 || (c & 1) == 0)
@@ -389,6 +345,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           if (leader) mbar_arrive_expect_tx(bar, g.size);
           copy_entry(prev, pbs, ktiles + mt, g.m, e, bar);
           ++idx;
+          if (mt == 0 && !more && leader) stamp(a, 11);  // last round's DN: first entry issued
         }
       }
       has_prev = more;
@@ -400,13 +357,16 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         if (more) piece_bases(cur, cb);
       }
     }
+    if (leader) stamp(a, 15);  // last weight copy issued
     if (a.nx_counters && a.pf_bytes > 0) {
       // ---- cross-layer L2 prefetch: the next layer's routing is final (K2
       // ran for all layers), so walk what this CTA index streams next layer
       // and prefetch its runs into L2 (HBM otherwise idles through this
       // launch's tail and the layer handoff); the next CTA fills its ring
       // with the first ring_bytes itself right after entry
-      prefetch_l2(a.nx_counters[7], a.nx_hit_list, a.nx_slot_of, a.nx_pool, a.nx_shared_w, RB, a.pf_bytes);
+      const k3s::StreamSrc nx{a.nx_counters, a.nx_hit_list, a.nx_slot_of, a.nx_pool, a.nx_shared_w,
+                              a.n_shared,    a.expert_elems, d,            a.ffn};
+      k3s::prefetch_stream_l2(nx, bg, G, gmax, RB, a.pf_bytes, lane);
     }
     if (!waited) wait_pred();
     if (a.dbg && leader) a.dbg[blockIdx.x * DBG + 8] = static_cast<unsigned long long>(w_empty);
@@ -505,6 +465,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           if (leader) mma_commit(&d1_full[b1]);
           __syncwarp();
           if (i == 0 && leader) stamp(a, 3);
+          if (i == 1 && leader) stamp(a, 5);  // GU(1) issued
         }
         if (has_prev) {  // DN(i-1): D2 += W_down(group) x a^T(i-1), hi + lo
           const int ab_ = (i - 1) & 1;
@@ -775,9 +736,85 @@ int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
   return rb >= need ? rb : 0;
 }
 
+namespace {
+
+// TMA tensor maps over a buffer of expert images (layout: see
+// expert_ffn_tc.cu): 5-D view of 8-byte elements
+//   dim0 = 256 (one 2 KiB run: 8 gate + 8 up rows of a K-tile, or 8 k of a down M-tile)
+//   dim1 = 8 runs per tile, dim2 = tiles per 64-row chunk (d/64 + d/128),
+//   dim3 = chunks (ffn/64), dim4 = image index in the buffer,
+// one map per box [256, n, m, 1, 1] (n = 1..8 runs, m = 1, 2, 4, 8, 16
+// tiles) so an entry of a one-piece group is a single copy. Built once per
+// (device, buffer, shape) with synchronous copies — the engine's first step
+// runs them before any graph capture — and cached for the process.
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t weight_tmaps(const void* buf, int d, int ffn, const void** out) {
+  *out = nullptr;
+  if (!buf) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, int>, void*> cache;
+  static EncodeTiled encode = nullptr;
+  int dev = 0;
+  if (const cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, buf, d, ffn);
+  if (const auto it = cache.find(key); it != cache.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        e != cudaSuccess || !fn)
+      return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<EncodeTiled>(fn);
+  }
+  const int tiles = d / 64 + d / 128;
+  const cuuint64_t chunk = static_cast<cuuint64_t>(tiles) * dev::tg::TILE;
+  const cuuint64_t dims[5] = {256, 8, static_cast<cuuint64_t>(tiles), static_cast<cuuint64_t>(ffn / 64), 4096};
+  const cuuint64_t strides[4] = {dev::tg::UB, dev::tg::TILE, chunk, chunk * static_cast<cuuint64_t>(ffn / 64)};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  std::vector<CUtensorMap> maps(40);
+  std::memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
+  for (int n = 1; n <= 8; ++n)
+    for (int mi = 0; mi < 5; ++mi) {
+      const cuuint32_t m = 1u << mi;
+      // never used: m divides d/64 or d/128, and entries stay <= 64 KiB (the
+      // driver rejects a 256 KiB box)
+      if (m > static_cast<cuuint32_t>(tiles) || n * m > 32) continue;
+      const cuuint32_t box[5] = {256, static_cast<cuuint32_t>(n), m, 1, 1};
+      const CUresult r = encode(&maps[static_cast<size_t>((n - 1) * 5 + mi)], CU_TENSOR_MAP_DATA_TYPE_UINT64, 5,
+                                const_cast<void*>(buf), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  void* d_maps = nullptr;
+  if (const cudaError_t e = cudaMalloc(&d_maps, maps.size() * sizeof(CUtensorMap)); e != cudaSuccess) return e;
+  if (const cudaError_t e = cudaMemcpy(d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+      e != cudaSuccess)
+    return e;
+  cache.emplace(key, d_maps);
+  *out = d_maps;
+  return cudaSuccess;
+}
+
+}  // namespace
+
 cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
   if (const cudaError_t e = smem_optin_once<dev::tg::expert_ffn_tg_kernel>(232448); e != cudaSuccess) return e;
-  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, a);
+  dev::FfnArgs b = a;
+  if (!b.tm_pool && b.counters) {
+    if (const cudaError_t e = weight_tmaps(b.pool, b.d, b.ffn, &b.tm_pool); e != cudaSuccess) return e;
+    if (const cudaError_t e = weight_tmaps(b.n_shared > 0 ? b.shared_w : nullptr, b.d, b.ffn, &b.tm_shared);
+        e != cudaSuccess)
+      return e;
+  }
+  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, b);
 }
 
 }  // namespace moespac

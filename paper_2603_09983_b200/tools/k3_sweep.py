@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--l2", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0, help="CTAs (0: one per SM)")
     ap.add_argument("--stamps", action="store_true", help="dump per-CTA timeline (tensor-core kernel)")
+    ap.add_argument("--dump", default="", help="save the raw per-CTA stamp array (.npy prefix)")
     args = ap.parse_args()
     d, ffn, T, k, N = args.d, args.ffn, args.T, args.k, args.N
     dev = torch.device("cuda")
@@ -84,6 +85,8 @@ def main():
                 abi.check(abi.lib().moespac_expert_ffn(ctypes.byref(fa), abi._stream(None)))
                 torch.cuda.synchronize()
                 fa.debug_ts_dev = None
+                if args.dump:
+                    np.save(f"{args.dump}_e{n_hit}.npy", dbg.cpu().numpy())
                 t = dbg.cpu().numpy().astype("float64")
                 act = t[:, 1] > 0
                 t0 = t[act, 0].min()
