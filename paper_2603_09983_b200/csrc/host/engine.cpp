@@ -254,6 +254,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   work_bytes_ = static_cast<size_t>(sms_ + N + m.n_shared_units) * T_ * d * 4;
   dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
   cold_trace_ = std::getenv("MOESPAC_COLD_TRACE") != nullptr;
+  step_trace_ = std::getenv("MOESPAC_STEP_TRACE") != nullptr;
   dmalloc(reinterpret_cast<void**>(&ycold_d_), sizeof(float) * L * T_ * d, "cudaMalloc ycold");
   check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocDefault),
         "cudaHostAlloc");
@@ -983,8 +984,17 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       check(e, "graph instantiate");
     }
     if (graph_capture || graph_replay) check(cudaGraphLaunch(graph_exec_, compute_), "graph launch");
+    const auto t_enq = std::chrono::steady_clock::now();
     check(cudaEventSynchronize(k2_done_), "sync K2");
+    const auto t_k2 = std::chrono::steady_clock::now();
     host_account();
+    if (step_trace_) {
+      const auto t_acc = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      std::fprintf(stderr, "step-trace: %s enqueue %.1f us, K2 wait %.1f us, account+decide %.1f us\n",
+                   graph_replay ? "graph" : (graph_capture ? "capture" : "eager"), us(t_step0, t_enq), us(t_enq, t_k2),
+                   us(t_k2, t_acc));
+    }
   } else {
     // ---- heterogeneous split: per layer, the device runs the resident
     // experts while the host cores run the missed ones on the same h_l.
@@ -1081,8 +1091,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
                           h_out_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, compute_),
           "h_out");
   if (timing) check(cudaEventRecord(ev_[5], compute_), "event");
+  const auto t_sync0 = std::chrono::steady_clock::now();
   check(cudaStreamSynchronize(compute_), "sync compute");
   check(cudaStreamSynchronize(copy_), "sync copy");
+  if (step_trace_)
+    std::fprintf(stderr, "step-trace: final sync %.1f us, step total %.1f us\n",
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_sync0).count(),
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_step0).count());
 
   if (timeline_) {
     // ---- measured SimEvent-shaped records of this step (sim_core.hpp:65-73

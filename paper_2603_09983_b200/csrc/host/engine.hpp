@@ -190,6 +190,7 @@ class Engine {
   int l2_prefetch_ = -1;  // per-CTA next-layer L2 prefetch (bytes); -1: per-kernel default
   int cold_threads_ = -1;
   bool cold_trace_ = false;  // MOESPAC_COLD_TRACE: per-step host timing of the cold path on stderr
+  bool step_trace_ = false;  // MOESPAC_STEP_TRACE: per-step host timing of the device-only path on stderr
   int ffn_accum_ = 0;
   int group_units_ = 0;
   int self_pf_ = 0;      // grouped K3 own-stream L2 prefetch at the input wait (MOESPAC_SELF_PF)  // grouped K3 group size (MOESPAC_GROUP_UNITS profiling knob; 0 = 16)

@@ -61,17 +61,6 @@ __device__ __forceinline__ uint64_t l2_evict_normal_policy() {
   return pol;
 }
 
-// 5-D TMA tensor copy global -> shared (SASS UTMALDG): one instruction moves
-// a whole box (e.g. n 2 KiB weight runs x m tiles), completion on an mbarrier.
-__device__ __forceinline__ void tma_load_5d(void* smem_dst, const void* tmap, int c0, int c1, int c2, int c3, int c4,
-                                            uint64_t* bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-      "%3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(smem_dst)),
-      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
 // 1-D bulk async copy global -> shared (TMA engine, SASS UBLKCP), completion
 // signalled on an mbarrier via complete_tx.
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,

@@ -28,14 +28,7 @@
 //
 // Warp roles (192 threads): 0 TMA producer, 1 MMA issuer (TMEM owner),
 // 2-5 epilogue (TMEM lane quarters 2, 3, 0, 1 = group slots).
-#include <cuda.h>
-
 #include <cstdint>
-#include <cstring>
-#include <map>
-#include <mutex>
-#include <tuple>
-#include <vector>
 
 #include "common.cuh"
 #include "k3_stream.cuh"
@@ -232,14 +225,12 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     long long w_empty = 0;
     const uint64_t pol = a.l2_policy == 1 ? l2_evict_normal_policy() : l2_evict_first_policy();
     const uint64_t pol_h = l2_evict_normal_policy();
-    // entry image bases (and image index in its buffer), one lane per entry
-    // of this CTA's range
+    // entry image bases, one lane per entry of this CTA's range
     unsigned long long my_base = 0;
-    int my_img = 0;
     if (lane < n_ent) {
       const int o = o_first + lane;
-      my_img = o < n_hits ? a.slot_of[a.hit_list[o]] : o - n_hits;
-      const uint16_t* w = (o < n_hits ? a.pool : a.shared_w) + static_cast<long long>(my_img) * a.expert_elems;
+      const uint16_t* w = o < n_hits ? a.pool + static_cast<long long>(a.slot_of[a.hit_list[o]]) * a.expert_elems
+                                     : a.shared_w + static_cast<long long>(o - n_hits) * a.expert_elems;
       my_base = reinterpret_cast<unsigned long long>(w);
     }
     bool waited = false;
@@ -290,27 +281,16 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
     };
     // tiles [t0, t0 + m) (tile index within the chunk: K-tiles then M-tiles)
     // of every piece, slot-packed: tile j of the entry at j * nu * 2 KiB.
-    // A one-piece group's entry is ONE tensor copy (box: n runs of 2 KiB x m
-    // tiles, landing in exactly that order). Two-piece groups interleave the
-    // pieces inside every tile, so they take one bulk copy per (tile, piece),
-    // one copy per lane: a thread's bulk copies issue one after another
-    // (~0.1-0.3 us each, tools/tma_probe.cu), copies from different lanes
-    // overlap. (Measured: a 1-unit group's 2 KiB bulk copies streamed at
-    // ~17 GB/s per SM — the second group round of a 9-unit CTA took 4 us.)
+    // One bulk copy per (tile, piece), one copy per lane: a thread's bulk
+    // copies issue one after another (~0.1-0.3 us each, tools/tma_probe.cu),
+    // copies from different lanes overlap — with one issuing lane, split runs
+    // capped the stream at 8-40 GB/s per SM. (Measured: issuing a one-piece
+    // group's entry as ONE 5-D TMA tensor copy instead — n runs x m tiles —
+    // changed nothing on Qwen3 / DeepSeek-V2-Lite step time; removed.)
     auto copy_entry = [&](const Grp& g, const uint8_t* const (&pb)[2], int t0, int m, uint32_t e, uint64_t* bar) {
       const uint32_t ab = static_cast<uint32_t>(g.nu) * UB;
       const uint32_t n0 = static_cast<uint32_t>(g.n[0]) * UB;
       __syncwarp();  // after the leader's expect_tx
-      if (g.np == 1) {
-        const int img = __shfl_sync(0xffffffffu, my_img, g.o[0] - o_first);
-        const uint8_t* tm = reinterpret_cast<const uint8_t*>(g.o[0] < n_hits ? a.tm_pool : a.tm_shared);
-        if (tm != nullptr) {
-          if (lane == 0)
-            tma_load_5d(ring + e, tm + (static_cast<size_t>(g.n[0] - 1) * 5 + (31 - __clz(m))) * 128, 0, g.pa[0], t0,
-                        g.c[0], img, bar, pol);
-          return;
-        }
-      }
       for (int c = lane; c < m * g.np; c += 32) {
         const int j = g.np > 1 ? c >> 1 : c;
         if (g.np == 1 || (c & 1) == 0)
@@ -736,85 +716,9 @@ int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
   return rb >= need ? rb : 0;
 }
 
-namespace {
-
-// TMA tensor maps over a buffer of expert images (layout: see
-// expert_ffn_tc.cu): 5-D view of 8-byte elements
-//   dim0 = 256 (one 2 KiB run: 8 gate + 8 up rows of a K-tile, or 8 k of a down M-tile)
-//   dim1 = 8 runs per tile, dim2 = tiles per 64-row chunk (d/64 + d/128),
-//   dim3 = chunks (ffn/64), dim4 = image index in the buffer,
-// one map per box [256, n, m, 1, 1] (n = 1..8 runs, m = 1, 2, 4, 8, 16
-// tiles) so an entry of a one-piece group is a single copy. Built once per
-// (device, buffer, shape) with synchronous copies — the engine's first step
-// runs them before any graph capture — and cached for the process.
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-cudaError_t weight_tmaps(const void* buf, int d, int ffn, const void** out) {
-  *out = nullptr;
-  if (!buf) return cudaSuccess;
-  static std::mutex mu;
-  static std::map<std::tuple<int, const void*, int, int>, void*> cache;
-  static EncodeTiled encode = nullptr;
-  int dev = 0;
-  if (const cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> lk(mu);
-  const auto key = std::make_tuple(dev, buf, d, ffn);
-  if (const auto it = cache.find(key); it != cache.end()) {
-    *out = it->second;
-    return cudaSuccess;
-  }
-  if (!encode) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (const cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-        e != cudaSuccess || !fn)
-      return e != cudaSuccess ? e : cudaErrorNotSupported;
-    encode = reinterpret_cast<EncodeTiled>(fn);
-  }
-  const int tiles = d / 64 + d / 128;
-  const cuuint64_t chunk = static_cast<cuuint64_t>(tiles) * dev::tg::TILE;
-  const cuuint64_t dims[5] = {256, 8, static_cast<cuuint64_t>(tiles), static_cast<cuuint64_t>(ffn / 64), 4096};
-  const cuuint64_t strides[4] = {dev::tg::UB, dev::tg::TILE, chunk, chunk * static_cast<cuuint64_t>(ffn / 64)};
-  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  std::vector<CUtensorMap> maps(40);
-  std::memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
-  for (int n = 1; n <= 8; ++n)
-    for (int mi = 0; mi < 5; ++mi) {
-      const cuuint32_t m = 1u << mi;
-      // never used: m divides d/64 or d/128, and entries stay <= 64 KiB (the
-      // driver rejects a 256 KiB box)
-      if (m > static_cast<cuuint32_t>(tiles) || n * m > 32) continue;
-      const cuuint32_t box[5] = {256, static_cast<cuuint32_t>(n), m, 1, 1};
-      const CUresult r = encode(&maps[static_cast<size_t>((n - 1) * 5 + mi)], CU_TENSOR_MAP_DATA_TYPE_UINT64, 5,
-                                const_cast<void*>(buf), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    }
-  void* d_maps = nullptr;
-  if (const cudaError_t e = cudaMalloc(&d_maps, maps.size() * sizeof(CUtensorMap)); e != cudaSuccess) return e;
-  if (const cudaError_t e = cudaMemcpy(d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
-      e != cudaSuccess)
-    return e;
-  cache.emplace(key, d_maps);
-  *out = d_maps;
-  return cudaSuccess;
-}
-
-}  // namespace
-
 cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
   if (const cudaError_t e = smem_optin_once<dev::tg::expert_ffn_tg_kernel>(232448); e != cudaSuccess) return e;
-  dev::FfnArgs b = a;
-  if (!b.tm_pool && b.counters) {
-    if (const cudaError_t e = weight_tmaps(b.pool, b.d, b.ffn, &b.tm_pool); e != cudaSuccess) return e;
-    if (const cudaError_t e = weight_tmaps(b.n_shared > 0 ? b.shared_w : nullptr, b.d, b.ffn, &b.tm_shared);
-        e != cudaSuccess)
-      return e;
-  }
-  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, b);
+  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, a);
 }
 
 }  // namespace moespac

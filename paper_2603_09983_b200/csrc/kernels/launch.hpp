@@ -68,11 +68,6 @@ struct FfnArgs {
   // grouped K3: units per group (8: one M = 128 gate|up tile per group
   // round; 0 / 16: up to two tiles, one round for CTAs with <= 16 units)
   int group_units;
-  // grouped K3: TMA tensor maps over the weight images of `pool` and
-  // `shared_w` ([8 piece widths][5 entry depths] each, device memory; null:
-  // built and cached by the launcher)
-  const void* tm_pool;
-  const void* tm_shared;
 };
 
 struct CombineArgs {
