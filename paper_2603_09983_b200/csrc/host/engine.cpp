@@ -294,7 +294,10 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   }
   for (auto& e : ev_) check(cudaEventCreate(&e), "event");
   for (auto& e : copy_ev_) check(cudaEventCreate(&e), "event");
-  check(cudaEventCreateWithFlags(&k2_done_, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+  // spin-waited too: the host decides the next step as soon as K2's outputs
+  // land; a blocking (interrupt) wake-up cost ~100 us per step on the tiny
+  // shape (MOESPAC_STEP_TRACE), more than the whole device step
+  check(cudaEventCreateWithFlags(&k2_done_, cudaEventDisableTiming), "event");
 
   // LayerEstimator ctor state for every layer (utility_estimator.cpp:23-33)
   const EstimatorConfig ec = estimator_config_for(sched_->config().policy, sched_->config().estimator);

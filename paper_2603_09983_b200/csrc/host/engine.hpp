@@ -192,8 +192,7 @@ class Engine {
   bool cold_trace_ = false;  // MOESPAC_COLD_TRACE: per-step host timing of the cold path on stderr
   bool step_trace_ = false;  // MOESPAC_STEP_TRACE: per-step host timing of the device-only path on stderr
   int ffn_accum_ = 0;
-  int group_units_ = 0;
-  int self_pf_ = 0;      // grouped K3 own-stream L2 prefetch at the input wait (MOESPAC_SELF_PF)  // grouped K3 group size (MOESPAC_GROUP_UNITS profiling knob; 0 = 16)
+  int group_units_ = 0;  // grouped K3 units per group (MOESPAC_GROUP_UNITS profiling knob; 0 = 8)
   const int32_t* replay_ids_ = nullptr;  // set for the duration of step_ids()
   const float* replay_gates_ = nullptr;
   uint16_t* wg_d_ = nullptr;      // [L][N][d] bf16 router weights (model mode)
