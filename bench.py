@@ -77,6 +77,11 @@ def parse_args():
     ap.add_argument("--budget-cache", type=float, default=0.17)
     ap.add_argument("--budget-windows", type=int, default=7)
     ap.add_argument("--budget-steps", type=int, default=20)
+    ap.add_argument("--stage-slots", type=int, default=16,
+                    help="cold-expert staging ring below a full cache (HBM images; 0 = off): --stage-frac of each "
+                         "layer's misses is copied over PCIe and run by K3 instead of on the host cores (decisions "
+                         "unchanged; measured on Qwen3 @ 0.17: 0.2 -> +16%% TPS, host DRAM is the shared bound)")
+    ap.add_argument("--stage-frac", type=float, default=0.2)
     ap.add_argument("--draft-window", action="store_true",
                     help="emulated draft phase: gamma x t_draft_unit (reference default 300 us/token) on the compute "
                          "stream before each verification step, expert loads overlapping it; TPS then counts "
@@ -288,6 +293,8 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
 
     def make_ctx():
         c = abi.Context(local_rank, model, cfg, rank, world)
+        if args.stage_slots > 0 and w.cache_ratio < 1.0:
+            c.set_cold_staging(args.stage_slots, args.stage_frac)
         c.host_arena(n_images_for(w))
         c.fill_synthetic(seed=3, stdv=SYNTH_STD)
         if args.router_gemv:
@@ -460,6 +467,7 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
         "misses": sum(r.cache_misses for _, _, rs in win for r in rs),
         "loads": sum(r.n_loads for _, _, rs in win for r in rs),
         "cold_experts": sum(r.cold_experts for _, _, rs in win for r in rs),
+        "staged_experts": sum(r.staged_experts for _, _, rs in win for r in rs),
         "cpu_ms_cold": sum(r.cpu_ms_cold for _, _, rs in win for r in rs),
         "k3_kernel": ctx.k3_kernel(), "parallel_mode": ctx.parallel_mode(),
         "h2d": float(np.mean([r.h2d_bytes for _, _, rs in win_e2e for r in rs])),
@@ -656,6 +664,8 @@ def main():
                   "roofline": broof, "decision_parity": rb["parity"], "clocks": rb["clocks"],
                   "hit_rate": rb["hits"] / max(1, rb["hits"] + rb["misses"]),
                   "loads_per_step": rb["loads"] / (nwin * K), "cold_experts_per_step": rb["cold_experts"] / (nwin * K),
+                  "staged_experts_per_step": rb["staged_experts"] / (nwin * K),
+                  "staging": {"slots": args.stage_slots, "fraction": args.stage_frac},
                   "host_cold_ms_per_step": rb["cpu_ms_cold"] / (nwin * K),
                   "gpu_step_ms": rb["gpu_step_ms"], "host_arena_images": rb["n_images"],
                   "e2e_bytes": {"h2d_bytes_per_step": int(rb["h2d"]), "d2h_bytes_per_step": int(rb["d2h"])}}

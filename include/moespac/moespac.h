@@ -100,6 +100,9 @@ typedef struct moespac_step_report {
    * bytes streamed (moespac_ctx_set_draft_model; 0 for the emulated window) */
   float gpu_ms_draft;
   int64_t draft_bytes;
+  /* cold experts of this step run on the device from the staging ring
+   * (moespac_ctx_set_cold_staging); cold_experts counts the host-run ones */
+  int32_t staged_experts;
 } moespac_step_report;
 
 /* Realized split of one layer (core/src/sim_core.cpp:233-283), as K2 emits it. */
@@ -391,6 +394,18 @@ moespac_status moespac_ctx_set_timing(moespac_ctx* c, int enabled);
  * the device, and added by the combine): -1 = all cores (default), 0 = off
  * (misses are counted but not computed). Takes effect at moespac_ctx_finalize. */
 moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads);
+/* Cold experts staged through HBM: of each layer's misses, a fixed fraction
+ * (spread evenly over the misses in expert order, at most slots/2 per layer)
+ * is copied pinned host -> a staging ring of `slots` expert images (two
+ * layers in flight, outside the cache budget's slots) on a side stream and
+ * run by that layer's K3 with the resident experts; the rest stay on the
+ * host cores. The misses' decisions and accounting are unchanged (the
+ * reference's HWB decides residency; this only chooses where a miss is
+ * computed: host DRAM -> cores, or host DRAM -> PCIe -> tensor cores).
+ * slots even, >= 0 (0 = off, the default); fraction in [0, 1]. Takes effect
+ * at moespac_ctx_finalize. Replaces nothing in the reference (its misses are
+ * modeled as CPU time, core/src/sim_core.cpp:253-254). */
+moespac_status moespac_ctx_set_cold_staging(moespac_ctx* c, int slots, double fraction);
 /* Emulated draft window (off by default): each step first holds the compute
  * stream for gamma * t_draft_unit_ns (the reference's modeled draft phase,
  * sim_core.cpp:167-172) while the copy engine works through the step's

@@ -60,7 +60,8 @@ class StepReport(C.Structure):
                 ("gpu_ms_ffn", C.c_float), ("gpu_ms_combine", C.c_float), ("gpu_ms_h2d_loads", C.c_float),
                 ("ffn_bytes", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("kernel_launches", C.c_int32), ("cold_experts", C.c_int32), ("cpu_ms_cold", C.c_float),
-                ("ffn_launches", C.c_int32), ("gpu_ms_draft", C.c_float), ("draft_bytes", C.c_int64)]
+                ("ffn_launches", C.c_int32), ("gpu_ms_draft", C.c_float), ("draft_bytes", C.c_int64),
+                ("staged_experts", C.c_int32)]
 
 
 class LayerOutcome(C.Structure):
@@ -197,6 +198,7 @@ def lib() -> C.CDLL:
         "moespac_ctx_set_k3_trace": (C.c_int, [vp, vp]),
         "moespac_ctx_set_l2_prefetch": (C.c_int, [vp, C.c_int]),
         "moespac_ctx_set_cold_threads": (C.c_int, [vp, C.c_int]),
+        "moespac_ctx_set_cold_staging": (C.c_int, [vp, C.c_int, C.c_double]),
         "moespac_step": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_step_device": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp]),
         "moespac_ctx_get_views": (C.c_int, [vp, C.POINTER(CtxViews)]),
@@ -573,6 +575,11 @@ class Context:
 
     def set_cold_threads(self, n: int = -1):
         check(lib().moespac_ctx_set_cold_threads(self._h, n))
+
+    def set_cold_staging(self, slots: int, fraction: float):
+        """Run `fraction` of each layer's misses on the device from a staging
+        ring of `slots` HBM images (before finalize; 0 slots = off)."""
+        check(lib().moespac_ctx_set_cold_staging(self._h, slots, fraction))
 
     def set_pdl(self, on: bool = True):
         check(lib().moespac_ctx_set_pdl(self._h, int(on)))

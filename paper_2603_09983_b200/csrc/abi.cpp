@@ -652,6 +652,10 @@ moespac_status moespac_ctx_set_cold_threads(moespac_ctx* c, int threads) {
   return guard([&] { c->e.set_cold_threads(threads); });
 }
 
+moespac_status moespac_ctx_set_cold_staging(moespac_ctx* c, int slots, double fraction) {
+  return guard([&] { c->e.set_cold_staging(slots, fraction); });
+}
+
 moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf) {
   return guard([&] { c->e.set_k3_trace(static_cast<unsigned long long*>(dev_buf)); });
 }

@@ -230,6 +230,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
     check(cudaMalloc(p, bytes ? bytes : 16), what);
   };
   dmalloc(reinterpret_cast<void**>(&pool_), static_cast<size_t>(L) * slots_ * image_elems_ * 2, "cudaMalloc pool");
+  pool_images_ = static_cast<int64_t>(L) * slots_;
   dmalloc(reinterpret_cast<void**>(&shared_), static_cast<size_t>(L) * m.n_shared_units * image_elems_ * 2,
           "cudaMalloc shared");
   if (m.n_shared_units > 0)
@@ -255,11 +256,15 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   dmalloc(reinterpret_cast<void**>(&work_d_), work_bytes_, "cudaMalloc workspace");
   cold_trace_ = std::getenv("MOESPAC_COLD_TRACE") != nullptr;
   step_trace_ = std::getenv("MOESPAC_STEP_TRACE") != nullptr;
-  dmalloc(reinterpret_cast<void**>(&ycold_d_), sizeof(float) * L * T_ * d, "cudaMalloc ycold");
-  check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocDefault),
+  // cold-path exchange buffers, mapped: the combine reads the host-computed
+  // y and writes h_{l+1} straight over PCIe (no per-layer copy that would
+  // queue on a copy engine behind megabytes of expert loads)
+  check(cudaHostAlloc(reinterpret_cast<void**>(&ycold_h_), sizeof(float) * L * T_ * d, cudaHostAllocMapped),
         "cudaHostAlloc");
-  check(cudaHostAlloc(reinterpret_cast<void**>(&hcold_h_), sizeof(uint16_t) * (L + 1) * T_ * d, cudaHostAllocDefault),
+  check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ycold_d_), ycold_h_, 0), "mapped y");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&hcold_h_), sizeof(uint16_t) * (L + 1) * T_ * d, cudaHostAllocMapped),
         "cudaHostAlloc");
+  check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hcold_d_), hcold_h_, 0), "mapped h");
   check(cudaHostAlloc(reinterpret_cast<void**>(&route_h_), (sizeof(int32_t) + sizeof(float)) * L * T_ * k,
                       cudaHostAllocDefault),
         "cudaHostAlloc");
@@ -327,14 +332,17 @@ Engine::~Engine() {
                   static_cast<void*>(h_d_), static_cast<void*>(hT_d_), static_cast<void*>(work_d_), static_cast<void*>(tables_d_),
                   static_cast<void*>(out_d_), static_cast<void*>(wg_d_), static_cast<void*>(sg_w_),
                   static_cast<void*>(draft_w_), static_cast<void*>(draft_y_), static_cast<void*>(draft_x0_),
-                  static_cast<void*>(gather_d_)})
+                  static_cast<void*>(gather_d_), static_cast<void*>(xt_d_)})
     if (p) cudaFree(p);
   cold_.reset();
   if (arena_h_) cudaFreeHost(arena_h_);
   if (ycold_h_) cudaFreeHost(ycold_h_);
+  if (xt_h_) cudaFreeHost(xt_h_);
+  for (auto* v : {&stage_ev_, &stage_done_})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  if (stage_) cudaStreamDestroy(stage_);
   if (hcold_h_) cudaFreeHost(hcold_h_);
   if (route_h_) cudaFreeHost(route_h_);
-  if (ycold_d_) cudaFree(ycold_d_);
   for (auto ev : h_ready_) cudaEventDestroy(ev);
   if (tables_h_) cudaFreeHost(tables_h_);
   if (out_h_) cudaFreeHost(out_h_);
@@ -501,6 +509,28 @@ void Engine::set_shared_gate(int layer, const uint16_t* w) {
 void Engine::finalize() {
   if (!arena_h_) throw std::logic_error("finalize: no host arena");
   check(cudaSetDevice(device_), "cudaSetDevice");
+  const int64_t want = static_cast<int64_t>(m_.n_layers) * slots_ + stage_slots_;
+  if (want > pool_images_) {
+    // the staging ring lives right after the pool so a staged expert is a
+    // K3 entry like any resident one (slot index past the layer's slots)
+    check(cudaFree(pool_), "cudaFree pool");
+    pool_ = nullptr;
+    check(cudaMalloc(reinterpret_cast<void**>(&pool_), static_cast<size_t>(want) * image_elems_ * 2),
+          "cudaMalloc pool + staging ring");
+    pool_images_ = want;
+    drop_graph();
+  }
+  if (stage_slots_ > 0 && !stage_) {
+    const int L = m_.n_layers, N = m_.n_experts;
+    check(cudaStreamCreateWithFlags(&stage_, cudaStreamNonBlocking), "stream");
+    stage_ev_.resize(static_cast<size_t>(L));
+    stage_done_.resize(static_cast<size_t>(L));
+    for (auto* v : {&stage_ev_, &stage_done_})
+      for (auto& e : *v) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    const size_t xt = sizeof(int32_t) * L * (3 * N + 8);
+    check(cudaMalloc(reinterpret_cast<void**>(&xt_d_), xt), "cudaMalloc staged tables");
+    check(cudaHostAlloc(reinterpret_cast<void**>(&xt_h_), xt, cudaHostAllocDefault), "cudaHostAlloc");
+  }
   const std::vector<int32_t>& slot = sched_->slot_table();
   const int N = m_.n_experts;
   for (int l = 0; l < m_.n_layers; ++l)
@@ -633,6 +663,10 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   const int32_t* taus_d = reinterpret_cast<const int32_t*>(lb_d + static_cast<size_t>(L) * W_);
   const int32_t* slots_d = taus_d + L;
   std::vector<int> layer_loads(static_cast<size_t>(L), 0), layer_loads_local(static_cast<size_t>(L), 0);
+  // cold experts of layer l run by its K3 from the staging ring (routing
+  // tables then from xt_d_, which lists them with the resident hits)
+  std::vector<int> stage_n(static_cast<size_t>(L), 0);
+  const int XS = 3 * N + 8;
   // per-kernel CUDA events (set_timing) — also for the measured timeline
   const bool timing = timing_ || timeline_;
   std::vector<std::vector<int>> tl_evicts;
@@ -836,9 +870,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     // Only a layer with this-rank loads needs the copy-stream event; every
     // other K3 is launched programmatically-dependent on the previous kernel
     // so its prologue and first weight copies overlap that kernel's tail.
-    const bool has_loads = layer_loads_local[static_cast<size_t>(l)] > 0;
+    const bool staged = stage_n[static_cast<size_t>(l)] > 0;
+    const bool has_loads = layer_loads_local[static_cast<size_t>(l)] > 0 || staged;
     if (timeline_) check(cudaEventRecord(wait_beg_[static_cast<size_t>(l)], compute_), "event");
-    if (has_loads) check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
+    if (layer_loads_local[static_cast<size_t>(l)] > 0)
+      check(cudaStreamWaitEvent(compute_, load_done_[static_cast<size_t>(l)], 0), "wait loads");
+    if (staged) check(cudaStreamWaitEvent(compute_, stage_done_[static_cast<size_t>(l)], 0), "wait staged");
     // (model mode: K3 follows route_layer, whose routing tables its prologue
     // reads before griddepcontrol.wait — only a full dependency makes them
     // visible, so no programmatic launch there)
@@ -856,6 +893,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.hit_list = hit_list_d_ + static_cast<size_t>(l) * N;
     fa.counters = counters_d + static_cast<size_t>(l) * 8;
     fa.slot_of = slots_d + static_cast<size_t>(l) * N;
+    if (staged) {
+      const int32_t* x = xt_d_ + static_cast<size_t>(l) * XS;
+      fa.hit_list = x;
+      fa.slot_of = x + 2 * N;
+      fa.counters = x + 3 * N;
+    }
     fa.pool = pool_ + static_cast<int64_t>(l) * slots_ * image_elems_;
     fa.shared_w = shared_ + static_cast<int64_t>(l) * m_.n_shared_units * image_elems_;
     fa.n_shared = n_shared_eff;  // expert-parallel: shared units are computed once, on rank 0
@@ -884,6 +927,12 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       fa.nx_counters = counters_d + static_cast<size_t>(l + 1) * 8;
       fa.nx_hit_list = hit_list_d_ + static_cast<size_t>(l + 1) * N;
       fa.nx_slot_of = slots_d + static_cast<size_t>(l + 1) * N;
+      if (stage_n[static_cast<size_t>(l + 1)] > 0) {
+        const int32_t* x = xt_d_ + static_cast<size_t>(l + 1) * XS;
+        fa.nx_hit_list = x;
+        fa.nx_slot_of = x + 2 * N;
+        fa.nx_counters = x + 3 * N;
+      }
       fa.nx_pool = pool_ + static_cast<int64_t>(l + 1) * slots_ * image_elems_;
       fa.nx_shared_w = shared_ + static_cast<int64_t>(l + 1) * m_.n_shared_units * image_elems_;
       fa.pf_bytes = pf;
@@ -894,7 +943,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
           "K3 expert FFN");
     if (timing) check(cudaEventRecord(ffn_end_[static_cast<size_t>(l)], compute_), "event");
   };
-  auto launch_combine_layer = [&](int l, const float* y_extra) {
+  auto launch_combine_layer = [&](int l, const float* y_extra, uint16_t* h_host = nullptr) {
     const uint16_t* hl = h_d_ + static_cast<size_t>(l) * T_ * d;
     uint16_t* hn = h_d_ + static_cast<size_t>(l + 1) * T_ * d;
     dev::CombineArgs ca{};
@@ -907,6 +956,10 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     ca.ids = ids_d_ + static_cast<size_t>(l) * T_ * k;
     ca.hit_ord = hit_ord_d_ + static_cast<size_t>(l) * N;
     ca.counters = counters_d + static_cast<size_t>(l) * 8;
+    if (stage_n[static_cast<size_t>(l)] > 0) {
+      ca.hit_ord = xt_d_ + static_cast<size_t>(l) * XS + N;
+      ca.counters = xt_d_ + static_cast<size_t>(l) * XS + 3 * N;
+    }
     ca.n_shared = n_shared_eff;
     ca.grid = sms_;
     ca.per_cta = tc && acc_mode_ == 3 ? 1 : 0;
@@ -921,6 +974,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     float* yl = y_d_ + static_cast<size_t>(l) * T_ * d;
     ca.y_out = yl;
     ca.h_out = world_ > 1 ? nullptr : hn;
+    ca.h_host = h_host;
     ca.hT_out = (world_ == 1 && tc && l + 1 < L) ? hT[(l + 1) & 1] : nullptr;
     check(launch_combine(ca, compute_, pdl_ && !timing && !y_extra), "combine");
     if (world_ > 1) {
@@ -958,7 +1012,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     sched_->decide(scores_.data());
   };
   float cpu_ms_cold = 0.f;
-  int cold_experts = 0;
+  int cold_experts = 0, staged_experts = 0;
 
   if (!cold) {
     // ---- all layers on the device back to back; host accounting overlaps
@@ -1001,13 +1055,21 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   } else {
     // ---- heterogeneous split: per layer, the device runs the resident
     // experts while the host cores run the missed ones on the same h_l.
-    launch_ffn(0);
+    // (with the staging ring, K3 of layer 0 may run staged misses: it waits
+    // for their routing tables, built below from K2's outputs)
+    const bool staging = stage_slots_ > 0;
+    if (!staging) launch_ffn(0);
     check(cudaEventSynchronize(k2_done_), "sync K2");
     std::vector<std::vector<ColdItem>> items(static_cast<size_t>(L));
+    std::vector<std::vector<int>> staged(static_cast<size_t>(L));
+    const int half = stage_slots_ / 2;  // staging slots per layer (two layers in flight)
+    double carry = 0.0;
     for (int l = 0; l < L; ++l) {
       const uint32_t* res = rb + static_cast<size_t>(l) * W_;
       const int32_t* il = ids_h + static_cast<size_t>(l) * T_ * k;
       const float* gl = gates_h + static_cast<size_t>(l) * T_ * k;
+      std::vector<ColdItem> miss;
+      std::vector<int> miss_e;
       for (int e = shard_rank_; e < N; e += shard_world_) {  // this rank's shard of the misses
         if ((res[e >> 5] >> (e & 31)) & 1u) continue;
         ColdItem it{};
@@ -1019,9 +1081,83 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
               it.gate[it.n_tok] = gl[t * k + j];
               ++it.n_tok;
             }
-        if (it.n_tok) items[static_cast<size_t>(l)].push_back(it);
+        if (it.n_tok) {
+          miss.push_back(it);
+          miss_e.push_back(e);
+        }
       }
+      // staged share: fraction x misses (carried across layers), at most a
+      // ring half, spread evenly over the misses in expert order
+      int ns = 0;
+      const int nm = static_cast<int>(miss.size());
+      if (staging && nm > 0) {
+        carry += stage_frac_ * nm;
+        const int want = static_cast<int>(carry);
+        carry -= want;
+        ns = std::min(want, half);
+      }
+      for (int i = 0; i < nm; ++i) {
+        if (ns > 0 && ((i + 1) * ns) / nm > (i * ns) / nm)
+          staged[static_cast<size_t>(l)].push_back(miss_e[static_cast<size_t>(i)]);
+        else
+          items[static_cast<size_t>(l)].push_back(miss[static_cast<size_t>(i)]);
+      }
+      stage_n[static_cast<size_t>(l)] = static_cast<int>(staged[static_cast<size_t>(l)].size());
       cold_experts += static_cast<int>(items[static_cast<size_t>(l)].size());
+      staged_experts += stage_n[static_cast<size_t>(l)];
+    }
+    // staged copies of layer l: ring half l & 1, behind the combine of layer
+    // l - 2 (the last reader of that half); issued two layers ahead
+    auto issue_staged = [&](int l) {
+      if (l >= L || staged[static_cast<size_t>(l)].empty()) return;
+      if (l >= 2) check(cudaStreamWaitEvent(stage_, stage_ev_[static_cast<size_t>(l - 2)], 0), "wait ring half");
+      const int64_t base = static_cast<int64_t>(L) * slots_ + (l & 1) * half;
+      for (size_t j = 0; j < staged[static_cast<size_t>(l)].size(); ++j)
+        check(cudaMemcpyAsync(pool_ + (base + static_cast<int64_t>(j)) * image_elems_,
+                              arena_h_ + image_of(l, staged[static_cast<size_t>(l)][j]) * image_elems_, image_elems_ * 2,
+                              cudaMemcpyHostToDevice, stage_),
+              "H2D staged cold expert");
+      check(cudaEventRecord(stage_done_[static_cast<size_t>(l)], stage_), "event");
+    };
+    if (staging) {
+      // routing tables of the layers with staged misses: K2's hit list
+      // (resident activated experts of this shard) merged with the staged
+      // ones, ascending; staged slots index past the layer's own slots
+      const int32_t* cnt_h = out_h_ + static_cast<size_t>(L) * N;
+      for (int l = 0; l < L; ++l) {
+        if (staged[static_cast<size_t>(l)].empty()) continue;
+        int32_t* x = xt_h_ + static_cast<size_t>(l) * XS;
+        std::fill(x + N, x + 3 * N, -1);
+        const uint32_t* res = rb + static_cast<size_t>(l) * W_;
+        const int32_t* il = ids_h + static_cast<size_t>(l) * T_ * k;
+        std::vector<uint8_t> act(static_cast<size_t>(N), 0);
+        for (int i = 0; i < T_ * k; ++i) act[static_cast<size_t>(il[i])] = 1;
+        const std::vector<int>& st = staged[static_cast<size_t>(l)];
+        const int64_t base = static_cast<int64_t>(L) * slots_ + (l & 1) * half - static_cast<int64_t>(l) * slots_;
+        int n = 0;
+        size_t si = 0;
+        for (int e = shard_rank_; e < N; e += shard_world_) {
+          int32_t slot = -1;
+          if (si < st.size() && st[si] == e) {
+            slot = static_cast<int32_t>(base + static_cast<int64_t>(si));
+            ++si;
+          } else if (act[static_cast<size_t>(e)] && ((res[e >> 5] >> (e & 31)) & 1u)) {
+            slot = slots[static_cast<size_t>(l) * N + e];
+          }
+          if (slot < 0) continue;
+          x[n] = e;
+          x[N + e] = n;
+          x[2 * N + e] = slot;
+          ++n;
+        }
+        std::memcpy(x + 3 * N, cnt_h + static_cast<size_t>(l) * 8, sizeof(int32_t) * 8);
+        x[3 * N + 7] = n;
+      }
+      check(cudaMemcpyAsync(xt_d_, xt_h_, sizeof(int32_t) * L * XS, cudaMemcpyHostToDevice, compute_),
+            "H2D staged routing tables");
+      issue_staged(0);
+      issue_staged(1);
+      launch_ffn(0);
     }
 
     if (h_in_host) std::memcpy(hcold_h_, h_in, sizeof(uint16_t) * T_ * d);
@@ -1054,11 +1190,16 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         const float cms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - c0).count();
         cpu_ms_cold += cms;
         tl_cpu_ms[static_cast<size_t>(l)] = cms;
-        float* yd = ycold_d_ + static_cast<size_t>(l) * T_ * d;
-        check(cudaMemcpyAsync(yd, yh, sizeof(float) * T_ * d, cudaMemcpyHostToDevice, compute_), "H2D cold y");
-        y_extra = yd;
+        y_extra = ycold_d_ + static_cast<size_t>(l) * T_ * d;  // mapped: read by the combine
       }
-      launch_combine_layer(l, y_extra);
+      // (single GPU: the combine also writes h_{l+1} into the mapped host
+      // buffer when the next layer has host work)
+      const bool h_mapped = world_ == 1 && l + 1 < L && !items[static_cast<size_t>(l + 1)].empty();
+      launch_combine_layer(l, y_extra, h_mapped ? hcold_d_ + static_cast<size_t>(l + 1) * T_ * d : nullptr);
+      if (staging) {
+        check(cudaEventRecord(stage_ev_[static_cast<size_t>(l)], compute_), "event");
+        issue_staged(l + 2);
+      }
       if (xstep && !next_loads[static_cast<size_t>(l)].empty()) {
         check(cudaEventRecord(xload_ev_[static_cast<size_t>(l)], compute_), "event");
         check(cudaStreamWaitEvent(copy_, xload_ev_[static_cast<size_t>(l)], 0), "wait last reader");
@@ -1071,9 +1212,10 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       }
       if (l + 1 < L) {
         if (!items[static_cast<size_t>(l + 1)].empty()) {
-          check(cudaMemcpyAsync(hcold_h_ + static_cast<size_t>(l + 1) * T_ * d, h_d_ + static_cast<size_t>(l + 1) * T_ * d,
-                                sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_),
-                "D2H h_l");
+          if (world_ > 1)  // (the ordered-sum kernel writes h_{l+1} on the device only)
+            check(cudaMemcpyAsync(hcold_h_ + static_cast<size_t>(l + 1) * T_ * d, h_d_ + static_cast<size_t>(l + 1) * T_ * d,
+                                  sizeof(uint16_t) * T_ * d, cudaMemcpyDeviceToHost, compute_),
+                  "D2H h_l");
           check(cudaEventRecord(h_ready_[static_cast<size_t>(l + 1)], compute_), "event");
         }
         launch_ffn(l + 1);
@@ -1097,6 +1239,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
   const auto t_sync0 = std::chrono::steady_clock::now();
   check(cudaStreamSynchronize(compute_), "sync compute");
   check(cudaStreamSynchronize(copy_), "sync copy");
+  if (stage_) check(cudaStreamSynchronize(stage_), "sync staging");
   if (step_trace_)
     std::fprintf(stderr, "step-trace: final sync %.1f us, step total %.1f us\n",
                  std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_sync0).count(),
@@ -1175,7 +1318,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     // virtual grid's units (8 ffn rows each)
     int64_t bytes = 0;
     for (int l = 0; l < L; ++l) {
-      const int64_t ent = oc[static_cast<size_t>(l)].n_local_hits + n_shared_eff;
+      const int64_t ent = oc[static_cast<size_t>(l)].n_local_hits + stage_n[static_cast<size_t>(l)] + n_shared_eff;
       if (!split_) {
         bytes += ent * image_elems_ * 2;
       } else {
@@ -1185,7 +1328,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
       }
     }
     rep->ffn_bytes = bytes;
-    rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads) * image_elems_ * 2 +
+    rep->h2d_bytes = static_cast<int64_t>(tables_bytes_) + static_cast<int64_t>(n_loads + staged_experts) * image_elems_ * 2 +
                      (logits_host && !replay_ids_ && !model_mode_ ? static_cast<int64_t>(sizeof(double)) * L * T_ * N : 0) +
                      (replay_ids_ ? static_cast<int64_t>(sizeof(int32_t) + sizeof(float)) * L * T_ * k : 0) +
                      (h_in_host ? static_cast<int64_t>(sizeof(uint16_t)) * T_ * d : 0);
@@ -1195,6 +1338,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
         (model_mode_ ? 4 * L : (replay_ids_ ? 1 : 2) + 2 * L) + (tc ? 1 : 0) + (world_ > 1 ? L : 0);
     rep->ffn_launches = L;
     rep->cold_experts = cold_experts;
+    rep->staged_experts = staged_experts;
     rep->cpu_ms_cold = cpu_ms_cold;
     rep->draft_bytes = draft_R_ > 0 ? static_cast<int64_t>(n_draft) * draft_R_ * draft_D_ * 2 : 0;
     if (timing) {

@@ -115,6 +115,14 @@ class Engine {
   // host threads for cold (non-resident) experts: -1 auto, 0 = off (misses
   // are then counted but not computed); takes effect at finalize()
   void set_cold_threads(int n) { cold_threads_ = n; }
+  // cold experts staged through HBM (moespac_ctx_set_cold_staging); before finalize()
+  void set_cold_staging(int slots, double fraction) {
+    if (finalized_) throw std::logic_error("moespac_ctx_set_cold_staging: context already finalized");
+    if (slots < 0 || slots % 2 || !(fraction >= 0.0 && fraction <= 1.0))
+      throw std::invalid_argument("moespac_ctx_set_cold_staging: slots must be even and >= 0, fraction in [0, 1]");
+    stage_slots_ = slots;
+    stage_frac_ = fraction;
+  }
   void step(const double* logits, bool logits_host, const uint16_t* h_in, bool h_in_host, int accepted,
             uint16_t* h_out, bool h_out_host, moespac_step_report* rep, moespac_layer_timing* layers);
   // Trace replay (#moetrace v1, trace_io.hpp): routing ids [L][T][k] (and
@@ -228,9 +236,20 @@ class Engine {
   int acc_mode_ = 0;
 
   std::unique_ptr<ColdExecutor> cold_;
-  float* ycold_d_ = nullptr;   // [L][T][d] host-computed cold-expert outputs
-  float* ycold_h_ = nullptr;   // pinned staging of the same
-  uint16_t* hcold_h_ = nullptr;  // pinned [L+1][T][d] layer inputs for the cold path
+  // cold-expert staging ring: stage_slots_ images after the pool's L x slots_
+  // (two halves, layers alternating), filled on stage_ behind the event of
+  // the combine two layers back (its last reader)
+  int stage_slots_ = 0;
+  double stage_frac_ = 0.0;
+  int64_t pool_images_ = 0;       // images allocated in pool_ (L x slots_ + staging)
+  cudaStream_t stage_ = nullptr;
+  std::vector<cudaEvent_t> stage_ev_, stage_done_;  // [L] combine(l) done / layer l's staged copies landed
+  int32_t* xt_d_ = nullptr;       // [L][3N + 8] routing tables incl. staged experts: hit_list | hit_ord | slot_of | counters
+  int32_t* xt_h_ = nullptr;       // pinned host copy
+  float* ycold_h_ = nullptr;   // pinned, mapped [L][T][d] host-computed cold-expert outputs
+  float* ycold_d_ = nullptr;   // device alias of ycold_h_ (read by the combine)
+  uint16_t* hcold_h_ = nullptr;  // pinned, mapped [L+1][T][d] layer inputs for the cold path
+  uint16_t* hcold_d_ = nullptr;  // device alias of hcold_h_ (written by the combine)
   uint8_t* route_h_ = nullptr;   // pinned ids [L][T][k] | gates [L][T][k]
   std::vector<cudaEvent_t> h_ready_;
   std::unique_ptr<NcclApi> nccl_;

@@ -593,6 +593,7 @@ __device__ __forceinline__ void combine_store(const CombineArgs& a, float4 acc, 
     o.x = static_cast<uint32_t>(f32_to_bf16_rn(r.x)) | (static_cast<uint32_t>(f32_to_bf16_rn(r.y)) << 16);
     o.y = static_cast<uint32_t>(f32_to_bf16_rn(r.z)) | (static_cast<uint32_t>(f32_to_bf16_rn(r.w)) << 16);
     *reinterpret_cast<uint2*>(a.h_out + off) = o;
+    if (a.h_host) *reinterpret_cast<uint2*>(a.h_host + off) = o;
     if (a.hT_out) {
       // the next layer's h^T UMMA image (tensor-core K3): 4 consecutive k of
       // token t share one 8-byte run (k % 8 in {0..3} or {4..7})

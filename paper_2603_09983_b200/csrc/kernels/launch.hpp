@@ -86,6 +86,7 @@ struct CombineArgs {
   float* y_out;             // [T][d] fp32 (may be null)
   uint16_t* h_out;          // [T][d] bf16 (may be null)
   uint16_t* hT_out;         // optional h^T UMMA image of h_out (next layer's tensor-core K3 operand)
+  uint16_t* h_host;         // optional second copy of h_out in mapped host memory (cold path input)
   unsigned long long* dbg;  // optional per-CTA profiling record (K3 trace rows, slots 26-29), or null
 };
 

@@ -43,11 +43,13 @@ def _pack(w, kernel):
     return abi.pack_expert(*[torch.from_numpy(x.view(np.int16)).cuda() for x in w], kernel=kernel)
 
 
-def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel=abi.FFN_AUTO, cold=-1):
+def _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel=abi.FFN_AUTO, cold=-1, stage=None):
     cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=cache)
     kernel = abi.ffn_resolve(kernel, d, ffn)
     ctx = abi.Context(0, abi.ModelDesc(L, N, k, g, d, ffn, units, gate_mode, kernel), cfg)
     ctx.set_cold_threads(cold)
+    if stage:
+        ctx.set_cold_staging(*stage)
     arena = ctx.host_arena(L * N)
     for (l, e), w in std.items():
         arena[l * N + e] = _pack(w, kernel).cpu().numpy().view(np.uint16)
@@ -74,10 +76,28 @@ def _resident(rb, l, N):
     (2, 8, 2, 4, 4096, 128, 0, 0, 0.5, abi.FFN_TENSOR, -1),    # per-segment K3 (d > 2048) + cold path
 ])
 def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, cold):
+    _engine_steps(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, cold)
+
+
+@pytest.mark.parametrize("L,N,k,g,d,ffn,units,gate_mode,cache,kernel,stage", [
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_TENSOR, (4, 0.5)),     # grouped K3, shared units
+    (3, 16, 4, 6, 1024, 64, 1, 1, 0.25, abi.FFN_CUDACORE, (4, 0.5)),
+    (2, 32, 8, 8, 2048, 128, 0, 0, 0.5, abi.FFN_TENSOR, (16, 1.0)),    # every miss staged: no host path
+    (3, 32, 8, 8, 2048, 128, 0, 0, 0.25, abi.FFN_TENSOR, (4, 1.0)),    # ring half caps the staged share
+    (2, 8, 2, 4, 4096, 128, 0, 0, 0.5, abi.FFN_TENSOR, (2, 1.0)),      # per-segment K3 (d > 2048)
+])
+def test_staged_cold_experts_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, stage):
+    """Misses split between the host cores and the HBM staging ring: the same
+    decisions, the full Eq. 3 output, every miss run exactly once."""
+    _engine_steps(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, -1, stage)
+
+
+def _engine_steps(L, N, k, g, d, ffn, units, gate_mode, cache, kernel, cold, stage=None):
     ref_or_skip()
     rng = np.random.default_rng(L * 100 + N)
     std, shared = _experts(rng, L, N, d, ffn, units)
-    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel, cold)
+    ctx, cfg = _make_ctx(L, N, k, g, d, ffn, units, gate_mode, cache, std, shared, kernel, cold, stage)
+    n_staged = 0
     T = g + 1
     steps = 10
     gen = O.Generator(L, N, k, g, seed=1)
@@ -117,7 +137,14 @@ def test_engine_steps_match_reference_and_oracle(L, N, k, g, d, ffn, units, gate
             _, rb, _, _ = ctx.step_tables()
             n_miss = sum(1 for l in range(L) for e in range(N)
                          if e in set(ids[l].ravel()) and not (int(rb[l, e >> 5]) >> (e & 31)) & 1)
-            assert rep.cold_experts == n_miss
+            assert rep.cold_experts + rep.staged_experts == n_miss
+            if stage is None:
+                assert rep.staged_experts == 0
+            elif stage[1] == 1.0 and stage[0] // 2 >= N:
+                assert rep.cold_experts == 0
+        n_staged += rep.staged_experts
+    if stage:
+        assert n_staged > 0, "the test must exercise staged misses"
     assert np.array_equal(ctx.sched_events(), run.events)
     if cache < 1.0:
         assert total_loads > 0, "the test must exercise real expert loads"
