@@ -51,6 +51,15 @@ REASONS = {  # clocks_event_reasons bitmask (nvml)
 }
 
 
+HWB_PROFILE_NAME = "reference"
+
+
+def HWB_PROFILE(w):
+    """SchedConfig profile overrides of the selected --hwb-profile for workload w."""
+    from paper_2603_09983_b200.configs import HWB_PROFILES
+    return HWB_PROFILES[HWB_PROFILE_NAME](w)
+
+
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -82,6 +91,10 @@ def parse_args():
                          "layer's misses is copied over PCIe and run by K3 instead of on the host cores (decisions "
                          "unchanged; measured on Qwen3 @ 0.17: 0.2 -> +16%% TPS, host DRAM is the shared bound)")
     ap.add_argument("--stage-frac", type=float, default=0.2)
+    ap.add_argument("--hwb-profile", default="reference", choices=["reference", "b200"],
+                    help="HWB hardware profile: the reference's defaults (config.cpp:23-27) or constants calibrated "
+                         "to B200 (configs.b200_hwb_profile); decisions are checked against the reference run with "
+                         "the same constants where a golden fixture exists")
     ap.add_argument("--draft-window", action="store_true",
                     help="emulated draft phase: gamma x t_draft_unit (reference default 300 us/token) on the compute "
                          "stream before each verification step, expert loads overlapping it; TPS then counts "
@@ -199,7 +212,8 @@ def cpu_path_sample(w, budget_s: float, use_ref_sched: bool):
     # reference scheduler (the reference's own code) per step
     t_sched, sched_kind = 0.0, "none"
     if use_ref_sched and O.ref_available():
-        cfg = O.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=w.cache_ratio, token_budget=0)
+        cfg = O.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=w.cache_ratio, token_budget=0,
+                               **HWB_PROFILE(w))
         ids_arr = np.stack([t[1] for t in trace])
         t_sched = O.ref().ref_sim_time_ns(cfg, ids_arr.reshape(-1).astype(np.int32),
                                           accepted.astype(np.int32), n_steps) * 1e-9
@@ -250,6 +264,8 @@ def golden_path(w):
         (w.name, round(w.cache_ratio, 2)))
     if w.name == "qwen3":
         name = "qwen3_c%03d" % round(w.cache_ratio * 100)
+    if name and HWB_PROFILE_NAME != "reference":
+        name += "_" + HWB_PROFILE_NAME
     p = os.path.join(ROOT, "tests", "golden", f"sim_{name}.npz") if name else None
     return p if p and os.path.exists(p) else None
 
@@ -288,7 +304,8 @@ def run_ours(args, w, rank, world, local_rank, windows=1, label="headline", step
 
     torch.cuda.set_device(local_rank)
     L, N, k, g, d, ffn, T = w.n_layers, w.n_experts, w.top_k, w.gamma, w.d_model, w.d_ffn, w.tokens
-    cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=w.cache_ratio)
+    cfg = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=g, cache_ratio=w.cache_ratio,
+                             **HWB_PROFILE(w))
     model = w.model_desc(args.ffn_kernel)
 
     def make_ctx():
@@ -547,7 +564,9 @@ def leg_summary(r, w, args, world, hbm_peak, peak_kind):
 
 
 def main():
+    global HWB_PROFILE_NAME
     args = parse_args()
+    HWB_PROFILE_NAME = args.hwb_profile
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -572,6 +591,7 @@ def main():
                            "against the reference's golden fixture), then one K-step trace window for value, the "
                            "next K steps with K3 %%globaltimer stamps (roofline), the next with per-K3 CUDA events; "
                            "e2e on a fresh context through the same warm-up and window" % args.settle,
+                "hwb_profile": args.hwb_profile,
                 "host_arena": "expert (l, e) -> pinned image (l*N + e) %% n_images, n_images >= N + 1 (and >= 8 GiB "
                               "below a full cache): no image shared by the same expert id in consecutive layers"}
     base = {"metric": "decode TPS and expert-FFN HBM GB/s (roofline %) at 1/2/4/8 B200 vs host CPU",
@@ -627,7 +647,8 @@ def main():
                       "layers_non_ffn_ms": r["layers_other_ms"], "tokens_per_step": r["tokens"] / args.steps,
                       "ms_per_step_k3_stamps_window": r["ms_st"] / args.steps,
                       "ms_per_step_kernel_events_window": r["ms_ev"] / args.steps,
-                      "host_arena_images": r["n_images"]}
+                      "host_arena_images": r["n_images"],
+                      "k3_busy_frac_of_step": float(np.sum(r["k3_span_ms"]) / r["ms_st"]) if r["ms_st"] else None}
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_path_sample(w, args.cpu_budget_s, use_ref_sched=True)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -667,6 +688,9 @@ def main():
                   "staged_experts_per_step": rb["staged_experts"] / (nwin * K),
                   "staging": {"slots": args.stage_slots, "fraction": args.stage_frac},
                   "host_cold_ms_per_step": rb["cpu_ms_cold"] / (nwin * K),
+                  # device time inside K3 launches (globaltimer spans, stamps window) over the step time: the
+                  # rest of the step the tensor cores / HBM stream idle (host cold path, PCIe, launches)
+                  "k3_busy_frac_of_step": float(np.sum(rb["k3_span_ms"]) / rb["ms_st"]) if rb["ms_st"] else None,
                   "gpu_step_ms": rb["gpu_step_ms"], "host_arena_images": rb["n_images"],
                   "e2e_bytes": {"h2d_bytes_per_step": int(rb["h2d"]), "d2h_bytes_per_step": int(rb["d2h"])}}
         if not args.no_cpu_baseline:

@@ -73,3 +73,31 @@ CONFIGS = {
     "qwen3": WorkloadConfig("qwen3", 48, 128, 8, 8, 2048, 768, 0, 0, 0.17,
                             "Qwen3-30B-A3B shape: 128 experts top-8, cache-budget sweep 10-100%"),
 }
+
+
+# HWB hardware profile (HardwareProfile, core/include/moesim/workload_balancer.hpp:15-21)
+# calibrated to one B200 box of this pool instead of the reference's defaults
+# (core/src/config.cpp:23-27: t_cpu 100 us per token-activation, t_gpu 40 us
+# per expert pass, t_io 400 us per expert load, t_draft 300 us per token,
+# expert_bytes 25 MB). Rates measured in round 2 (profiles/bench_r2*):
+#   host cold path, 16 threads, AVX-512 BF16 over the pinned arena: 90 GB/s
+#     (Qwen3 @ 0.17: 136 missed experts x 9.44 MB in 14.2 ms per step)
+#   K3 on HBM: ~5 TB/s per resident expert pass (0.7-0.94 of the copy peak)
+#   pinned host -> HBM expert loads: 48 GB/s (46-53 measured)
+#   draft phase: 2e9-parameter bf16 stand-in at 6.99 TB/s per token
+# t_cpu is charged per token-activation by the reference; a miss with one
+# token costs a whole expert read on the host, so one expert read it is.
+B200_RATES = {"host_cold_Bps": 90e9, "k3_Bps": 5e12, "h2d_Bps": 48e9, "draft_s_per_token": 4e9 / 6.99e12}
+
+
+def b200_hwb_profile(w: WorkloadConfig) -> dict:
+    """SchedConfig profile fields for workload w on B200 (see B200_RATES)."""
+    eb = w.expert_bytes
+    r = B200_RATES
+    return {"t_cpu_unit_ns": round(eb / r["host_cold_Bps"] * 1e9), "t_gpu_unit_ns": round(eb / r["k3_Bps"] * 1e9),
+            "t_io_unit_ns": round(eb / r["h2d_Bps"] * 1e9), "t_draft_unit_ns": round(r["draft_s_per_token"] * 1e9),
+            "expert_bytes": eb}
+
+
+HWB_PROFILES = {"reference": lambda w: {}, "b200": b200_hwb_profile}
+

@@ -25,6 +25,9 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import oracle as O  # noqa: E402
 
+sys.path.insert(0, ROOT)
+from paper_2603_09983_b200.configs import CONFIGS, b200_hwb_profile  # noqa: E402  (pure Python, no library)
+
 # (name, L, N, k, gamma, cache_ratio, policy, steps)
 SIM_CASES = [
     ("tiny", 1, 8, 2, 4, 0.17, "moe_spac", 200),
@@ -42,7 +45,11 @@ SIM_CASES = [
     ("mixtral_c100", 32, 8, 2, 4, 1.00, "moe_spac", 60),   # the bench headline's budget
     ("ar_mode", 4, 32, 8, 8, 0.17, "ar_mode", 30),         # one simulated step per accepted token
     ("tiny_c100", 1, 8, 2, 4, 1.00, "moe_spac", 200),
+    ("qwen3_c017_b200", 48, 128, 8, 8, 0.17, "moe_spac", 24),  # HWB profile calibrated to B200 (configs.py)
 ]
+
+
+PROFILE_KEYS = ("t_cpu_unit_ns", "t_gpu_unit_ns", "t_io_unit_ns", "t_draft_unit_ns", "expert_bytes")
 
 
 def sim_case(name, L, N, k, g, cache, policy, steps, **extra):
@@ -50,7 +57,8 @@ def sim_case(name, L, N, k, g, cache, policy, steps, **extra):
                            token_budget=0, **extra)
     ids, acc = O.ref_trace(cfg, steps)
     run = O.ref_sim_run(cfg, ids, acc)
-    return dict(L=L, N=N, k=k, gamma=g, cache_ratio=cache, policy=O.POLICIES.index(policy),
+    prof = {key: extra[key] for key in PROFILE_KEYS if key in extra}  # non-default HWB profile, if any
+    return dict(L=L, N=N, k=k, gamma=g, cache_ratio=cache, policy=O.POLICIES.index(policy), **prof,
                 shift_period=cfg.shift_period, drift_scale=cfg.drift_scale, ids=ids, accepted=acc,
                 layer_rec=run.layer_rec, step_rec=run.step_rec, accuracy=run.accuracy, events=run.events,
                 total_time_ns=run.total_time_ns)
@@ -65,6 +73,8 @@ def main(only=None):
             continue
         name = case[0]
         extra = {"shift_period": 7, "drift_scale": 0.5} if name == "shift_regime" else {}
+        if name.endswith("_b200"):
+            extra = b200_hwb_profile(CONFIGS[name.split("_")[0]])
         d = sim_case(*case, **extra)
         np.savez_compressed(os.path.join(HERE, f"sim_{name}.npz"), **d)
         print(name, d["ids"].shape, d["events"].shape)

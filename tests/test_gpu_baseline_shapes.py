@@ -30,7 +30,7 @@ import torch
 
 import oracle as O
 from paper_2603_09983_b200 import abi
-from paper_2603_09983_b200.configs import CONFIGS, SYNTH_STD
+from paper_2603_09983_b200.configs import CONFIGS, HWB_PROFILES, SYNTH_STD
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -81,9 +81,9 @@ def _dev_view(addr, n):
     return torch.from_numpy(host).cuda()
 
 
-def _build(w, n_images, cold=-1):
+def _build(w, n_images, cold=-1, profile="reference"):
     cfg = abi.default_config(n_layers=w.n_layers, n_experts=w.n_experts, top_k=w.top_k, gamma=w.gamma,
-                             cache_ratio=w.cache_ratio)
+                             cache_ratio=w.cache_ratio, **HWB_PROFILES[profile](w))
     ctx = abi.Context(0, w.model_desc(), cfg)
     ctx.set_cold_threads(cold)
     arena = ctx.host_arena(n_images)
@@ -120,6 +120,9 @@ CASES = [
     ("sim_qwen3_c010", "qwen3", 0.10, 8, 129, {7: [5, 40]}),
     ("sim_qwen3_c050", "qwen3", 0.50, 8, 129, {7: [5, 40]}),
     ("sim_qwen3_c100", "qwen3", 1.00, 8, 129, {0: [0, 47], 7: [5, 40]}),
+    # HWB profile calibrated to B200 (configs.b200_hwb_profile; the golden is
+    # the reference Simulation run with the same constants)
+    ("sim_qwen3_c017_b200", "qwen3", 0.17, 12, 129, {11: [0, 24, 47]}),
 ]
 
 
@@ -129,7 +132,7 @@ def test_engine_at_baseline_shape(golden, name, cache, steps, n_images, ycheck):
     w = CONFIGS[name].with_(cache_ratio=cache)
     assert (int(z["L"]), int(z["N"]), int(z["k"]), int(z["gamma"]), float(z["cache_ratio"])) == \
         (w.n_layers, w.n_experts, w.top_k, w.gamma, cache)
-    ctx, arena, W = _build(w, n_images)
+    ctx, arena, W = _build(w, n_images, profile="b200" if golden.endswith("_b200") else "reference")
     L, N, k, T, d = w.n_layers, w.n_experts, w.top_k, w.tokens, w.d_model
     gen = O.Generator(L, N, k, w.gamma, seed=1)
     rng = np.random.default_rng(2)

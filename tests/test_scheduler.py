@@ -54,8 +54,12 @@ def replay(cfg, ids, accepted, shard_world=1, cap=None):
                          ids=lambda p: os.path.basename(p)[4:-4])
 def test_scheduler_matches_reference_simulation(path):
     z = np.load(path)
+    # (fixtures made with a non-default HWB profile carry its constants)
+    prof = {key: int(z[key]) for key in ("t_cpu_unit_ns", "t_gpu_unit_ns", "t_io_unit_ns", "t_draft_unit_ns",
+                                         "expert_bytes") if key in z.files}
     cfg = abi.default_config(n_layers=int(z["L"]), n_experts=int(z["N"]), top_k=int(z["k"]),
-                             gamma=int(z["gamma"]), cache_ratio=float(z["cache_ratio"]), policy=int(z["policy"]))
+                             gamma=int(z["gamma"]), cache_ratio=float(z["cache_ratio"]), policy=int(z["policy"]),
+                             **prof)
     s, recs, steps = replay(cfg, z["ids"], z["accepted"])
     assert np.array_equal(recs, z["layer_rec"][:, :, :9])
     for i, rep in enumerate(steps):
