@@ -72,11 +72,14 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, u
       : "memory");
 }
 
-// bar.sync is warp-aligned (a warp that arrives in divergent pieces is
-// counted once per piece), so reconverge the warp first.
+// Named barrier over `threads` threads. The non-.aligned form counts threads
+// individually, so a warp may arrive from divergent paths (bar.sync =
+// barrier.sync.aligned requires the whole warp to execute it convergently;
+// compute-sanitizer synccheck flagged the epilogue's drain barrier as
+// divergent with it). The warp is still reconverged first.
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   __syncwarp();
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // Programmatic dependent launch: let the next kernel in the stream start its

@@ -100,3 +100,19 @@ def test_nccl_combine_matches_loopback_bitwise():
     for c in ctxs:
         c.close()
     group.close()
+
+
+def test_nccl_library_loads_and_single_rank_comm_inits():
+    """Runs on one GPU: the engine's dlopen'ed NCCL (libnccl.so.2, the one
+    torch already mapped) exports what it binds, hands out a unique id, and
+    a one-rank communicator initialises on it — the setup path every rank of
+    `bench.py --gpus N` takes before its first all-gather."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as _dist  # noqa: F401  (maps torch's libnccl first, as under torchrun)
+    from paper_2603_09983_b200 import abi
+    torch.cuda.set_device(0)
+    uid = abi.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    ctx, _, _ = _setup(0, 1, 0, uid=uid)
+    ctx.close()
