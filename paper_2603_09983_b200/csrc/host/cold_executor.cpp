@@ -8,6 +8,7 @@
 #include <pthread.h>
 #include <sched.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -24,6 +25,20 @@ inline float bf(uint16_t b) {
 }
 
 inline float silu(float x) { return x / (1.f + std::exp(-x)); }
+
+// Spin on pred with _mm_pause for at most kSpinNs; true if pred came true.
+template <typename Pred>
+bool spin_until(Pred pred) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned i = 0;; ++i) {
+    if (pred()) return true;
+    _mm_pause();
+    if ((i & 63u) == 63u &&
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count() >
+            ColdExecutor::kSpinNs)
+      return pred();
+  }
+}
 
 }  // namespace
 
@@ -61,11 +76,8 @@ ColdExecutor::ColdExecutor(int threads, int layout, int d, int ffn, int T)
       }
       int seen = 0;
       for (;;) {
-        bool got = false;
-        for (int spin = 0; spin < kSpin && !got; ++spin) {
-          got = gen_a_.load(std::memory_order_acquire) != seen || stop_a_.load(std::memory_order_acquire);
-          if (!got) _mm_pause();
-        }
+        const bool got = spin_until(
+            [&] { return gen_a_.load(std::memory_order_acquire) != seen || stop_a_.load(std::memory_order_acquire); });
         if (!got) {
           std::unique_lock<std::mutex> lk(mu_);
           cv_.wait(lk, [&] { return stop_a_.load() || gen_a_.load() != seen; });
@@ -302,8 +314,7 @@ void ColdExecutor::run(const std::vector<ColdItem>& items, const uint16_t* h, fl
   }
   cv_.notify_all();
   work(0);
-  for (int spin = 0; spin < kSpin && pending_a_.load(std::memory_order_acquire) != 0; ++spin) _mm_pause();
-  if (pending_a_.load(std::memory_order_acquire) != 0) {
+  if (!spin_until([&] { return pending_a_.load(std::memory_order_acquire) == 0; })) {
     std::unique_lock<std::mutex> lk(mu_);
     done_cv_.wait(lk, [&] { return pending_a_.load() == 0; });
   }

@@ -27,6 +27,11 @@ struct ColdItem {
 
 class ColdExecutor {
  public:
+  // Spin this long before sleeping (bounded by the clock, not by a pause
+  // count: a pause is ~140 cycles on this pool's Xeons, so 65536 of them
+  // spun ~4 ms and kept a second context's workers off the shared cores).
+  // Long enough to bridge a layer's host gap (h_l D2H + wake-up).
+  static constexpr long long kSpinNs = 500000;
   // layout: 1 = CUDA-core image (16-row chunks), 2 = tensor-core image (64-row chunks)
   ColdExecutor(int threads, int layout, int d, int ffn, int T);
   ~ColdExecutor();
@@ -42,7 +47,6 @@ class ColdExecutor {
   void chunk(const ColdItem& it, int c, const float* hf, float* y, std::vector<float>& scratch) const;
   int layout_, d_, ffn_, T_, rows_;
   std::vector<std::thread> workers_;
-  static constexpr int kSpin = 1 << 16;  // ~100-200 us of _mm_pause before sleeping
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   std::atomic<int> gen_a_{0}, pending_a_{0};
