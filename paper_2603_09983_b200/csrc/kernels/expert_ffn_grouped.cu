@@ -54,9 +54,9 @@ constexpr int NSLOT = 32;      // ring entries in flight (mbarrier pairs)
 constexpr int TILE = k3s::TILE;  // one gate|up K-tile or down M-tile of a 64-row chunk
 constexpr int UB = k3s::UB;      // one 8-row unit (gate + up octet) of a gate|up tile, or 8 k of a down tile
 constexpr int GMAX = 16;       // units per group: up to two M = 128 gate|up tiles (8 units each)
-constexpr int HTS = 2048;      // h^T slice of one K-tile (16 tokens x 64 k)
+constexpr int HTS = 2048;      // h^T slice of one K-tile (16 tokens x 64 k); 1 KiB (8 tokens) in N = 8 mode
 constexpr int ENT_MAX = 32;    // entries one CTA may touch (one producer lane each)
-constexpr int MAX_KT = 32;     // d <= 2048
+constexpr int MAX_KT = 64;     // d <= 2048 (d <= 4096 in N = 8 mode, T <= 8)
 constexpr int D2_COL0 = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int DBG = 32;
@@ -139,6 +139,14 @@ __device__ __forceinline__ void bulk_commit_wait_all() {
 __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int d = a.d, T = a.T;
+  // N = 8 mode (d > 2048, T <= 8): MMAs over 8 token columns, so D2 takes 8
+  // TMEM columns per M-tile and fits 32 M-tiles (d = 4096) in columns
+  // 256-511; the resident h^T keeps only the first 8 token rows (1 KiB per
+  // K-tile)
+  const bool n8 = d > 2048;
+  const uint32_t hsz = n8 ? 1024u : static_cast<uint32_t>(HTS);
+  const uint32_t idesc = n8 ? tc::IDESC_N8 : tc::IDESC;
+  const int d2w = n8 ? 8 : 16;
   const int ktiles = d / 64, mtiles = d / 128;
   const long long chunk_bytes = 3LL * 64 * d * 2;
   const int upe = a.ffn / 8;
@@ -150,7 +158,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   uint8_t* aT = p;
   p += 2 * 2 * 4096;
   uint8_t* hts = p;
-  p += static_cast<size_t>(ktiles) * HTS;
+  p += static_cast<size_t>(ktiles) * hsz;
   uint8_t* ring = p;
   p += RB;
   uint8_t* zeros = p;  // the missing half of an odd group's last down K-step (finite, times a^T = 0)
@@ -242,8 +250,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       {  // one slice per lane: bulk copies issued by one thread serialise
         const uint8_t* hTb = reinterpret_cast<const uint8_t*>(a.hT);
         for (int kt = lane; kt < ktiles; kt += 32) {
-          mbar_arrive_expect_tx(&ht_full[kt], HTS);
-          bulk_g2s(hts + kt * HTS, hTb + static_cast<size_t>(kt) * HTS, HTS, &ht_full[kt], pol_h);
+          mbar_arrive_expect_tx(&ht_full[kt], hsz);
+          bulk_g2s(hts + kt * hsz, hTb + static_cast<size_t>(kt) * HTS, hsz, &ht_full[kt], pol_h);
         }
       }
       waited = true;
@@ -300,7 +308,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
                    static_cast<uint32_t>(g.n[1]) * UB, bar, pol);
       }
     };
-    GroupIt it{u0, u1, upe, gmax};
+    GroupIt it{u0, u1, upe, gmax, a.tail_absorb};
     Grp cur, prev;
     bool more = it.next(cur), has_prev = false;
     const uint8_t* cb[2];
@@ -407,7 +415,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       int ht_ok = 0;  // h^T slices [0, ht_ok) known to have landed
       const uint32_t ring_addr = smem_u32(ring), at_addr = smem_u32(aT), ht_addr = smem_u32(hts);
       const uint32_t zero_addr = smem_u32(zeros);
-      GroupIt it{u0, u1, upe, gmax};
+      GroupIt it{u0, u1, upe, gmax, a.tail_absorb};
       Grp cur, prev;
       bool more = it.next(cur), has_prev = false;
       int i = 0;
@@ -430,12 +438,12 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
             fence_after();
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
-                const uint64_t bdesc = smem_desc(ht_addr + (kt + j) * HTS, 128, 1024);
+                const uint64_t bdesc = smem_desc(ht_addr + (kt + j) * hsz, 128, 1024);
                 for (int t = 0; t < nt; ++t) {
                   const uint64_t adesc = smem_desc(ring_addr + off + j * ab + t * TILE, 128, 1024);
 #pragma unroll
                   for (int k = 0; k < 4; ++k)  // +256 B per K=16 step = +16 in the start-address field
-                    mma_bf16(d1 + 16 * t, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0);
+                    tc::mma_bf16_id(d1 + 16 * t, adesc + 16 * k, bdesc + 16 * k, (kt | j | k) != 0, idesc);
                 }
               }
               mma_commit(&empty[slot]);
@@ -463,7 +471,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
             fence_after();
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
-                const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>((mt + j) * 16);
+                const uint32_t d2 = tmem + D2_COL0 + static_cast<uint32_t>((mt + j) * d2w);
                 // K-step s2 = units 2 s2, 2 s2 + 1 (two 8-k core-matrix columns,
                 // LBO apart); an odd group's last step takes its second
                 // column from the zero buffer (a^T rows there are 0 too)
@@ -471,8 +479,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
                   const uint32_t run = ring_addr + off + j * ab + 2 * s2 * UB;
                   const uint32_t lbo = 2 * s2 + 1 < prev.nu ? UB : zero_addr - run;
                   const uint64_t adn = smem_desc(run, lbo, 128);
-                  mma_bf16(d2, adn, bhi + 32 * s2, (i == 1 && s2 == 0) ? 0u : 1u);  // +512 B of a^T per step
-                  mma_bf16(d2, adn, blo + 32 * s2, 1u);
+                  tc::mma_bf16_id(d2, adn, bhi + 32 * s2, (i == 1 && s2 == 0) ? 0u : 1u, idesc);  // +512 B of a^T per step
+                  tc::mma_bf16_id(d2, adn, blo + 32 * s2, 1u, idesc);
                 }
               }
               mma_commit(&empty[slot]);
@@ -523,7 +531,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
             if (t < T) {
-              const uint4 hv = *reinterpret_cast<const uint4*>(ht16 + kt * 1024 + (t >> 3) * 512 + j * 64 + (t & 7) * 8);
+              const uint4 hv = *reinterpret_cast<const uint4*>(ht16 + kt * (hsz / 2) + (t >> 3) * 512 + j * 64 + (t & 7) * 8);
               float h8[8];
               bf16x8_to_f32(hv, h8);
 #pragma unroll
@@ -549,7 +557,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       }
       Phase d1f[2], atf[2];
       long long w_d1f = 0, w_d2f = 0;
-      GroupIt it{u0, u1, upe, gmax};
+      GroupIt it{u0, u1, upe, gmax, a.tail_absorb};
       Grp g;
       int i = 0;
       while (it.next(g)) {
@@ -649,9 +657,9 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         for (int j = 0; j < 4; ++j)
           if (j < nm) {
             if (T <= 8)
-              tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + j) * 16), y[j]);
+              tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + j) * d2w), y[j]);
             else
-              tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + j) * 16), y[j]);
+              tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + j) * d2w), y[j]);
           }
         tc::tmem_wait_ld();
         float* r0 = stg + mt * 128 + 32 * q + lane;
@@ -692,7 +700,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 }  // namespace dev
 
 size_t ffn_tg_smem_bytes(int d, int ring_bytes) {
-  return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * dev::tg::HTS + static_cast<size_t>(ring_bytes) + dev::tg::UB +
+  const size_t hsz = d > 2048 ? 1024 : dev::tg::HTS;  // (N = 8 mode keeps 8 token rows of h^T)
+  return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * hsz + static_cast<size_t>(ring_bytes) + dev::tg::UB +
          dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 4 * 16 * 4 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
 }
 
@@ -708,7 +717,9 @@ bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid) {
 // holds the widest entry window (58 KiB: 3 or 7 units x 8 or 4 tiles, the
 // last tile read as a full 16 KiB A operand).
 int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
-  if (d > dev::tg::MAX_KT * 64 || d % 128 || T > 16) return 0;
+  // D2 (all d/128 M-tiles) in TMEM columns 256-511: 16 columns per M-tile
+  // (d <= 2048), or 8 in N = 8 mode (d <= 4096, T <= 8)
+  if (d % 128 || T > 16 || d > 4096 || (d > 2048 && T > 8)) return 0;
   const size_t fixed = ffn_tg_smem_bytes(d, 0);
   if (fixed >= smem_limit) return 0;
   const int rb = static_cast<int>(((smem_limit - fixed) / 1024) * 1024);

@@ -1024,7 +1024,11 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
     return p;
   };
   const bool tmem_ok = d <= dev::tc::TMEM_ACC_MAX_D;
-  if (accum == 4 || (accum == 0 && tmem_ok)) {
+  // the grouped kernel holds D2 for every M-tile in TMEM: d <= 2048 at
+  // N = 16, or d <= 4096 with T <= 8 tokens at N = 8 (the Mixtral shape:
+  // measured 5.44 -> 5.22 ms per step against the per-segment kernel)
+  const bool grouped_ok = tmem_ok || (d <= 4096 && T <= 8);
+  if (accum == 4 || (accum == 0 && grouped_ok)) {
     // grouped kernel (expert_ffn_grouped.cu): whole-CTA TMEM accumulator
     const int rb = ffn_tg_ring_bytes(T, d, limit_grouped);
     if (rb > 0) {

@@ -27,12 +27,14 @@ struct GroupIt {
   long long u, u1;
   int upe;    // units per entry = ffn / 8
   int gmax;   // units per group (8 or 16)
+  int absorb = 0;  // a remainder of <= absorb units joins the group before it (a second M-tile)
   __device__ __forceinline__ bool next(Grp& g) {
     if (u >= u1) return false;
     const int o = static_cast<int>(u / upe), ui = static_cast<int>(u % upe);
     // end of u's chunk, and of the chunk after it (a group has <= 2 pieces)
     const long long cend = static_cast<long long>(o) * upe + (ui / UPC + 1) * UPC;
     long long ue = u + gmax < u1 ? u + gmax : u1;
+    if (u1 - ue <= absorb) ue = u1;
     if (ue > cend + UPC) ue = cend + UPC;
     g.us = u;
     g.nu = static_cast<int>(ue - u);

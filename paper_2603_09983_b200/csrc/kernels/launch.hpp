@@ -68,6 +68,9 @@ struct FfnArgs {
   // grouped K3: units per group (8: one M = 128 gate|up tile per group
   // round; 0 / 16: up to two tiles, one round for CTAs with <= 16 units)
   int group_units;
+  // grouped K3: a last remainder of <= tail_absorb units joins the group
+  // before it as a second M-tile instead of running a round of its own
+  int tail_absorb;
 };
 
 struct CombineArgs {

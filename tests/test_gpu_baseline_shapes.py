@@ -282,6 +282,9 @@ def test_shared_gate_sigmoid_matches_oracle():
         outs[mode] = ys[0]
         ctx.close()
     assert np.linalg.norm(outs[0] - outs[1]) > 1e-2 * np.linalg.norm(outs[0])
-    with pytest.raises(abi.MoespacError) as ei:  # the gate needs the grouped K3
-        abi.Context(0, abi.ModelDesc(L, N, k, g, 4096, ffn, units, 1, kernel, 0, abi.SHARED_GATE_SIGMOID), cfg)
+    # the gate needs the grouped K3, which d = 4096 only gets at T <= 8:
+    # gamma 8 (T = 9) falls back to the per-segment kernel
+    cfg9 = abi.default_config(n_layers=L, n_experts=N, top_k=k, gamma=8, cache_ratio=1.0)
+    with pytest.raises(abi.MoespacError) as ei:
+        abi.Context(0, abi.ModelDesc(L, N, k, 8, 4096, ffn, units, 1, kernel, 0, abi.SHARED_GATE_SIGMOID), cfg9)
     assert ei.value.code == "E_INVALID"

@@ -197,6 +197,8 @@ def test_expert_ffn_tc_accumulator_modes(N, k, T, d, ffn, n_shared, gate_mode, r
     (64, 6, 9, 2048, 1408, 2, 1, 0.3),     # DeepSeek-V2-Lite shape (shared units)
     (16, 4, 16, 1024, 128, 1, 0, 0.7),     # T = 16, 2 quarters/entry chunk crossings
     (4, 4, 3, 512, 64, 0, 0, 1.0),         # every token on every expert, 1 chunk per expert
+    (8, 2, 5, 4096, 448, 0, 0, 1.0),       # d = 4096, T <= 8: N = 8 MMAs, D2 in 8 columns per M-tile
+    (8, 2, 8, 4096, 192, 1, 0, 0.7),       # d = 4096, T = 8 + shared unit
 ])
 def test_expert_ffn_grouped_grids(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, grid):
     """Grouped K3: groups of eight 8-row units cross chunk and expert
@@ -228,7 +230,8 @@ def test_expert_ffn_per_segment_grids(N, k, T, d, ffn, n_shared, gate_mode, resi
     fp64 oracle."""
     if abi.FFN_TENSOR not in _kernels(d, ffn):
         pytest.skip("shape not supported by the tensor-core kernel")
-    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 0, grid=grid)
+    # accum 1 = the per-segment kernel (auto picks the grouped one at T <= 8)
+    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 1, grid=grid)
 
 
 def _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, kernel, accum, grid=None, tol=1e-5):
