@@ -143,7 +143,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   // TMEM columns per M-tile and fits 32 M-tiles (d = 4096) in columns
   // 256-511; the resident h^T keeps only the first 8 token rows (1 KiB per
   // K-tile)
-  const bool n8 = d > 2048;
+  const bool n8 = a.tg_n8 != 0;
   const uint32_t hsz = n8 ? 1024u : static_cast<uint32_t>(HTS);
   const uint32_t idesc = n8 ? tc::IDESC_N8 : tc::IDESC;
   const int d2w = n8 ? 8 : 16;
@@ -699,8 +699,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 }  // namespace tg
 }  // namespace dev
 
-size_t ffn_tg_smem_bytes(int d, int ring_bytes) {
-  const size_t hsz = d > 2048 ? 1024 : dev::tg::HTS;  // (N = 8 mode keeps 8 token rows of h^T)
+size_t ffn_tg_smem_bytes(int T, int d, int ring_bytes) {
+  const size_t hsz = ffn_tg_n8(d, T) ? 1024 : dev::tg::HTS;  // (N = 8 mode keeps 8 token rows of h^T)
   return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * hsz + static_cast<size_t>(ring_bytes) + dev::tg::UB +
          dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 4 * 16 * 4 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
 }
@@ -720,7 +720,7 @@ int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
   // D2 (all d/128 M-tiles) in TMEM columns 256-511: 16 columns per M-tile
   // (d <= 2048), or 8 in N = 8 mode (d <= 4096, T <= 8)
   if (d % 128 || T > 16 || d > 4096 || (d > 2048 && T > 8)) return 0;
-  const size_t fixed = ffn_tg_smem_bytes(d, 0);
+  const size_t fixed = ffn_tg_smem_bytes(T, d, 0);
   if (fixed >= smem_limit) return 0;
   const int rb = static_cast<int>(((smem_limit - fixed) / 1024) * 1024);
   const int need = static_cast<int>(T) * d * 4 > 59392 ? T * d * 4 : 59392;
@@ -729,7 +729,9 @@ int ffn_tg_ring_bytes(int T, int d, size_t smem_limit) {
 
 cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl) {
   if (const cudaError_t e = smem_optin_once<dev::tg::expert_ffn_tg_kernel>(232448); e != cudaSuccess) return e;
-  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, a);
+  dev::FfnArgs b = a;
+  b.tg_n8 = ffn_tg_n8(a.d, a.T) ? 1 : 0;  // (the same rule sized its shared memory)
+  return launch_pdl(dev::tg::expert_ffn_tg_kernel, dim3(grid), dim3(dev::tg::THREADS), smem, stream, pdl, b);
 }
 
 }  // namespace moespac

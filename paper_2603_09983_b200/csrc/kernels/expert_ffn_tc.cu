@@ -1032,7 +1032,7 @@ FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum) {
     // grouped kernel (expert_ffn_grouped.cu): whole-CTA TMEM accumulator
     const int rb = ffn_tg_ring_bytes(T, d, limit_grouped);
     if (rb > 0) {
-      FfnPlan p{rb / 1024, false, ffn_tg_smem_bytes(d, rb)};
+      FfnPlan p{rb / 1024, false, ffn_tg_smem_bytes(T, d, rb)};
       p.acc_mode = dev::tc::ACC_GROUP;
       return p;
     }

@@ -1,6 +1,7 @@
 // Kernel argument blocks and host-side launcher declarations.
 #pragma once
 #include <cstddef>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -71,6 +72,7 @@ struct FfnArgs {
   // grouped K3: a last remainder of <= tail_absorb units joins the group
   // before it as a second M-tile instead of running a round of its own
   int tail_absorb;
+  int tg_n8;  // grouped K3 N = 8 mode (ffn_tg_n8(d, T), set by the launcher)
 };
 
 struct CombineArgs {
@@ -116,7 +118,18 @@ cudaError_t launch_expert_ffn(const dev::FfnArgs& a, int grid, size_t smem, cuda
 size_t ffn_tc_smem_bytes(int T, int d, int ring_bytes, int acc_mode);
 FfnPlan ffn_tc_plan(int T, int d, size_t smem_limit, int accum = 0);
 cudaError_t launch_expert_ffn_tc(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
-size_t ffn_tg_smem_bytes(int d, int ring_bytes);
+// grouped K3 N = 8 mode: needed for d > 2048 (D2 in TMEM); at d <= 2048
+// only with MOESPAC_TG_N8=1 (measured neutral there: Qwen1.5 1.036 vs 1.039
+// ms per step, tiny within noise — the freed 32 KiB of h^T do not pay)
+inline bool ffn_tg_n8_small() {
+  static const bool on = [] {
+    const char* e = std::getenv("MOESPAC_TG_N8");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+inline bool ffn_tg_n8(int d, int T) { return d > 2048 || (T <= 8 && ffn_tg_n8_small()); }
+size_t ffn_tg_smem_bytes(int T, int d, int ring_bytes);
 int ffn_tg_ring_bytes(int T, int d, size_t smem_limit);
 bool ffn_tg_grid_ok(int n_entries, int d_ffn, int grid);
 cudaError_t launch_expert_ffn_tg(const dev::FfnArgs& a, int grid, size_t smem, cudaStream_t stream, bool pdl = false);
