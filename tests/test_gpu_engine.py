@@ -330,7 +330,8 @@ def test_model_mode_needs_cold_path_off():
     (2, 0.5, abi.FFN_CUDACORE, 0, 0),
     (2, 1.0, abi.FFN_TENSOR, 0, 0),     # auto -> unit split (every expert fits)
     (3, 1.0, abi.FFN_TENSOR, -1, 2),    # unit split, grouped K3
-    (2, 1.0, abi.FFN_TENSOR, 0, 2),     # unit split with d > 2048 (per-segment K3), below
+    (2, 1.0, abi.FFN_TENSOR, 0, 2),     # unit split, d = 4096, T = 7: grouped K3 in N = 8 mode, below
+    (2, 1.0, abi.FFN_TENSOR, 1, 2),     # unit split, d = 4096, T = 9: per-segment K3, below
 ])
 def test_expert_parallel_device_path(world, cache, kernel, cold, mode):
     """Expert-parallel mode on one GPU: `world` contexts
@@ -341,8 +342,10 @@ def test_expert_parallel_device_path(world, cache, kernel, cold, mode):
     resident on any rank (+ the host cold path when on)."""
     import threading
     L, N, k, g, d, ffn, units = 2, 16, 4, 6, 1024, 128, 1
-    if (world, mode) == (2, 2) and cold == 0:
-        d = 4096  # the per-segment K3 in the unit-split mode
+    if (world, mode) == (2, 2) and cold >= 0:
+        # d = 4096 in the unit-split mode: T = 7 runs the grouped K3 at N = 8,
+        # T = 9 the per-segment K3 (cache 1.0: the cold path stays idle)
+        d, g = 4096, (6 if cold == 0 else 8)
     rng = np.random.default_rng(world * 10 + int(cache * 10))
     std, shared = _experts(rng, L, N, d, ffn, units)
     T = g + 1
