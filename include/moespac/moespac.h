@@ -459,8 +459,9 @@ moespac_status moespac_ctx_set_k3_trace(moespac_ctx* c, void* dev_buf);
  * off): after its last weight copy, each CTA prefetches into L2 the part of
  * its next-layer work that follows the next CTA's own ring fill, so HBM
  * keeps working through the launch tail and the layer handoff. Default: 128
- * KiB for the grouped K3 (d <= 2048; -2.5 to -3% step time measured), 0 for
- * the per-segment K3 (no gain on the Mixtral shape). */
+ * KiB for the grouped K3 (-2.5 to -3% step time measured at d = 2048; within
+ * noise on the Mixtral shape, 5.13 vs 5.12 ms), 0 for the per-segment K3 (no
+ * gain there). */
 moespac_status moespac_ctx_set_l2_prefetch(moespac_ctx* c, int bytes);
 /* The context's compute stream (cudaStream_t as void*) — every kernel of a
  * step runs on it, so events recorded there bracket whole steps. */
