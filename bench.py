@@ -89,8 +89,10 @@ def parse_args():
     ap.add_argument("--stage-slots", type=int, default=16,
                     help="cold-expert staging ring below a full cache (HBM images; 0 = off): --stage-frac of each "
                          "layer's misses is copied over PCIe and run by K3 instead of on the host cores (decisions "
-                         "unchanged; measured on Qwen3 @ 0.17: 0.2 -> +16%% TPS, host DRAM is the shared bound)")
-    ap.add_argument("--stage-frac", type=float, default=0.2)
+                         "unchanged; measured, median of 7 windows: Qwen3 @ 0.17 288 / 291 / 307 / 311 TPS at "
+                         "0 / 0.2 / 0.3 / 0.4, DSV2 @ 0.17 185 / 200 / 198 at 0 / 0.2 / 0.4 — host DRAM is the "
+                         "shared bound)")
+    ap.add_argument("--stage-frac", type=float, default=0.3)
     ap.add_argument("--hwb-profile", default="reference", choices=["reference", "b200"],
                     help="HWB hardware profile: the reference's defaults (config.cpp:23-27) or constants calibrated "
                          "to B200 (configs.b200_hwb_profile); decisions are checked against the reference run with "
