@@ -112,7 +112,7 @@ def main():
     segs = np.array(segs)
     for nq in sorted(set(quarters.tolist())):
         m = quarters == nq
-        rel_med = {str(j): round(float(np.median((x[m, j] - base) / 1e3)), 2) for j in (2, 3, 5, 11, 15, 17, 25, 16, 21, 4, 18, 7, 1, 19, 20)
+        rel_med = {str(j): round(float(np.median((x[m, j] - base) / 1e3)), 2) for j in (2, 3, 31, 5, 11, 15, 17, 25, 16, 21, 4, 18, 7, 1, 19, 20)
                    if (x[m, j] > 0).all()}
         print(json.dumps({"layer": lm, "units": nq, "ctas": int(m.sum()),
                           "end_us_med": round(float(np.median(ends[m])), 2),
