@@ -435,7 +435,6 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
             ++idx;
             for (; ht_ok < kt + g.m; ++ht_ok) mbar_wait(&ht_full[ht_ok], 0);
             if (i == 0 && kt == 0 && leader) stamp(a, 2);
-            if (i == 1 && kt == 0 && leader) stamp(a, 31);  // second round: first gate|up entry landed
             fence_after();
             if (leader) {
               for (int j = 0; j < g.m; ++j) {
