@@ -1,6 +1,7 @@
 // extern "C" boundary (include/moespac/moespac.h). Every entry point
 // converts C++ exceptions into moespac_status, following the reference's
 // exception classes.
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -517,6 +518,9 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     f.hT = a->hT_dev;
     f.dbg = reinterpret_cast<unsigned long long*>(a->debug_ts_dev);
     f.l2_policy = a->l2_policy;
+    // grouped-K3 profiling knobs, as the engine reads them (engine.cpp)
+    if (const char* e = std::getenv("MOESPAC_TAIL_ABSORB")) f.tail_absorb = std::atoi(e);
+    if (const char* e = std::getenv("MOESPAC_DRAIN_LATE")) f.drain_late = std::atoi(e);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_ok(kern == kFfnTensorCore ? launch_expert_ffn_tc(f, grid, plan.smem, st) : launch_expert_ffn(f, grid, plan.smem, st),
             "expert_ffn");

@@ -209,6 +209,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   if (const char* e = std::getenv("MOESPAC_FFN_ACCUM")) ffn_accum_ = std::atoi(e);
   if (const char* e = std::getenv("MOESPAC_GROUP_UNITS")) group_units_ = std::atoi(e);
   if (const char* e = std::getenv("MOESPAC_TAIL_ABSORB")) tail_absorb_ = std::atoi(e);
+  if (const char* e = std::getenv("MOESPAC_DRAIN_LATE")) drain_late_ = std::atoi(e);
   if (const char* e = std::getenv("MOESPAC_L2_PF")) l2_prefetch_ = std::atoi(e);
   const size_t smem_optin = prop.sharedMemPerBlockOptin;
   FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, smem_optin, ffn_accum_)
@@ -912,10 +913,13 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     fa.acc_mode = acc_mode_;
     fa.hT = hT[l & 1];
     fa.group_units = group_units_;
-    // (a 1-unit last round at d = 4096 is tensor-pipe bound — 256 gate|up
-    // MMAs for 196 KiB: measured -0.7% step on Mixtral when it joins the
-    // group before; neutral or worse on the d = 2048 shapes)
-    fa.tail_absorb = tail_absorb_ >= 0 ? tail_absorb_ : (d > 2048 ? 1 : 0);
+    // a 1-unit last round joins the group before it as a second M-tile: at
+    // d = 4096 it is tensor-pipe bound (256 gate|up MMAs for 196 KiB, -0.7%
+    // step on Mixtral); at d = 2048, once the D2 drain overlaps the last DN
+    // pass, it also shortens the 9-unit CTAs (same box: Qwen3 -0.4%,
+    // DeepSeek-V2-Lite -1.3%, Qwen1.5 -1.1% step)
+    fa.tail_absorb = tail_absorb_ >= 0 ? tail_absorb_ : 1;
+    fa.drain_late = drain_late_;
     if (split_) {
       fa.cta_base = rank_ * sms_;
       fa.cta_total = world_ * sms_;

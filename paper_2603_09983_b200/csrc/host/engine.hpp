@@ -202,6 +202,7 @@ class Engine {
   int ffn_accum_ = 0;
   int group_units_ = 0;  // grouped K3 units per group (MOESPAC_GROUP_UNITS profiling knob; 0 = 8)
   int tail_absorb_ = -1;  // grouped K3: remainder units joining the last group (MOESPAC_TAIL_ABSORB; -1 = per shape)
+  int drain_late_ = 0;    // grouped K3: D2 drained after the whole last DN pass (MOESPAC_DRAIN_LATE, profiling)
   const int32_t* replay_ids_ = nullptr;  // set for the duration of step_ids()
   const float* replay_gates_ = nullptr;
   uint16_t* wg_d_ = nullptr;      // [L][N][d] bf16 router weights (model mode)

@@ -60,6 +60,7 @@ constexpr int MAX_KT = 64;     // d <= 2048 (d <= 4096 in N = 8 mode, T <= 8)
 constexpr int D2_COL0 = 256;
 constexpr int TMEM_COLS = 512;
 constexpr int DBG = 32;
+constexpr int D2E = 32;        // entries of a CTA's last DN pass (<= d/128 M-tiles)
 
 // ---------------------------------------------------------------- groups
 // Work unit = 8 ffn rows of one expert; groups of <= gmax (8 or 16) units,
@@ -178,8 +179,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
   uint64_t* d1_empty = d1_full + 2;   // [2]
   uint64_t* at_full = d1_empty + 2;   // [2]
   uint64_t* at_empty = at_full + 2;   // [2]
-  uint64_t* d2_full = at_empty + 2;   // [1]
-  uint64_t* ht_full = d2_full + 1;    // [ktiles]
+  uint64_t* d2e = at_empty + 2;       // [D2E]: the last DN pass's entries, one each
+  uint64_t* ht_full = d2e + D2E;      // [ktiles]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -215,7 +216,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       mbar_init(&at_full[i], 1);
       mbar_init(&at_empty[i], 1);
     }
-    mbar_init(d2_full, 1);
+    for (int i = 0; i < D2E; ++i) mbar_init(&d2e[i], 1);
     for (int i = 0; i < ktiles; ++i) mbar_init(&ht_full[i], 1);
     fence_mbar_init();
   }
@@ -464,6 +465,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
           const uint64_t bhi = smem_desc(ahi, 256, 128), blo = smem_desc(ahi + 4096u, 256, 128);
           const Geom g = dn_geom(prev.nu, mcap);
           const uint32_t ab = static_cast<uint32_t>(prev.nu) * UB;
+          const bool last = !more;  // D2 M-tiles are final as this pass's entries complete
           for (int mt = 0; mt < mtiles; mt += g.m) {
             const uint32_t off = ring_place(head, g, RB), slot = idx % NSLOT;
             wait_acc(a, &full[slot], (idx / NSLOT) & 1u, w_full);
@@ -484,6 +486,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
                 }
               }
               mma_commit(&empty[slot]);
+              if (last) mma_commit(&d2e[mt / g.m]);
             }
             __syncwarp();
           }
@@ -497,8 +500,6 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         }
         ++i;
       }
-      if (leader) mma_commit(d2_full);
-      __syncwarp();
       if (a.dbg && leader) {
         a.dbg[blockIdx.x * DBG + 9] = static_cast<unsigned long long>(w_full);
         a.dbg[blockIdx.x * DBG + 10] = static_cast<unsigned long long>(w_at);
@@ -637,53 +638,80 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
         }
         ++i;
       }
-      // ---- drain: D2 (all M-tiles, the CTA's whole sum) -> shared memory
-      // [T][d] fp32 (the ring is idle: every entry has been consumed) -> one
-      // bulk store per token row this CTA touched
-      wait_acc(a, d2_full, 0, w_d2f);
-      if (et == 0) stamp(a, 18);
-      fence_after();
+      // ---- drain, overlapped with the last DN pass: D2 M-tiles [mt, mt + nm)
+      // are final once the pass's entry holding M-tile mt + nm - 1 has
+      // completed (the MMA warp commits each of that pass's entries to its own
+      // mbarrier), so while the pass's later entries still stream, chunks of
+      // sc M-tiles are read from TMEM, staged [T][nm * 128] fp32 in the h^T
+      // slices (dead once the last gate|up MMAs are done: every DN MMA is
+      // issued after them, two buffers) and stored, one bulk copy per touched
+      // token row. A pass of one entry (a short last group) — or two buffers
+      // not fitting in the h^T slices — drains after the whole pass instead:
+      // all M-tiles staged in the idle ring, one d * 4-byte copy per row.
       uint32_t tmask = 0;  // tokens this CTA touched
       for (int r = 0; r < n_ent; ++r) tmask |= ent_mask[r];
       const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(D2_COL0);
-      float* stg = reinterpret_cast<float*>(ring);
-      if (et == 0) stamp(a, 7);
-      // four M-tiles per tcgen05.wait::ld (mtiles is even; the drain is
-      // load-latency bound: one round trip per wait)
-      for (int mt = 0; mt < mtiles; mt += 4) {
-        uint32_t y[4][16];
-        const int nm = mtiles - mt < 4 ? mtiles - mt : 4;
+      const Geom gl = dn_geom(g.nu, mcap);  // g: the last group (GroupIt leaves it)
+      const int n_last = (mtiles + gl.m - 1) / gl.m;
+      const uint32_t hts_bytes = static_cast<uint32_t>(ktiles) * hsz;
+      int sc = 4;
+      while (sc > 1 && 2u * sc * 512u * static_cast<uint32_t>(T) > hts_bytes) sc >>= 1;
+      const bool early = !a.drain_late && n_last > 1 && 2u * sc * 512u * static_cast<uint32_t>(T) <= hts_bytes;
+      if (!early) sc = mtiles;
+      float* stg0 = reinterpret_cast<float*>(early ? hts : ring);
+      const bool issuer = q == 0 && lane < T;  // one lane per token row
+      int c = 0;
+      for (int mt = 0; mt < mtiles; mt += sc, ++c) {
+        const int nm = mtiles - mt < sc ? mtiles - mt : sc;
+        wait_acc(a, &d2e[early ? (mt + nm - 1) / gl.m : n_last - 1], 0, w_d2f);
+        if (mt == 0 && et == 0) stamp(a, 18);
+        fence_after();
+        // buffer c & 1 was last read by chunk c - 2's stores
+        if (c >= 2 && issuer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (c >= 2) named_bar_sync(2, EPI_THREADS);
+        float* s = stg0 + static_cast<size_t>(c & 1) * sc * 128 * T;
+        // four M-tiles per tcgen05.wait::ld (the loads are latency bound)
+        for (int m4 = 0; m4 < nm; m4 += 4) {
+          const int n4 = nm - m4 < 4 ? nm - m4 : 4;
+          uint32_t y[4][16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < nm) {
-            if (T <= 8)
-              tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + j) * d2w), y[j]);
-            else
-              tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + j) * d2w), y[j]);
-          }
-        tc::tmem_wait_ld();
-        float* r0 = stg + mt * 128 + 32 * q + lane;
+          for (int j = 0; j < 4; ++j)
+            if (j < n4) {
+              if (T <= 8)
+                tc::tmem_ld8_nw(tbase + static_cast<uint32_t>((mt + m4 + j) * d2w), y[j]);
+              else
+                tc::tmem_ld16_nw(tbase + static_cast<uint32_t>((mt + m4 + j) * d2w), y[j]);
+            }
+          tc::tmem_wait_ld();
+          float* r0 = s + 128 * m4 + 32 * q + lane;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < nm) {
+          for (int j = 0; j < 4; ++j)
+            if (j < n4) {
 #pragma unroll
-            for (int t = 0; t < 16; ++t)
-              if (t < T) r0[static_cast<size_t>(t) * d + 128 * j] = __uint_as_float(y[j][t]);
-          }
+              for (int t = 0; t < 16; ++t)
+                if (t < T) r0[static_cast<size_t>(t) * nm * 128 + 128 * j] = __uint_as_float(y[j][t]);
+            }
+        }
+        fence_proxy_async();
+        if (mt + nm >= mtiles) {
+          if (et == 0) stamp(a, 1);
+          // TMEM is dead past this barrier: warp 1 (also arriving) deallocates
+          // it while the last rows are stored
+          fence_before();
+          named_bar_sync(3, EPI_THREADS + 32);
+        }
+        named_bar_sync(2, EPI_THREADS);
+        if (issuer) {
+          if ((tmask >> lane) & 1u)
+            bulk_s2g(a.partial + (static_cast<long long>(b) * T + lane) * d + mt * 128,
+                     s + static_cast<size_t>(lane) * nm * 128, static_cast<uint32_t>(nm) * 512u);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
-      if (et == 0) stamp(a, 1);
-      fence_before();
-      fence_proxy_async();
-      // TMEM is dead past this barrier: warp 1 (also arriving) deallocates it
-      // while the partial rows are stored (it used to wait for CTA exit)
-      named_bar_sync(3, EPI_THREADS + 32);
       if (et == 0) stamp(a, 19);
-      if (q == 0 && lane < T) {  // one lane per token row
-        if ((tmask >> lane) & 1u)
-          bulk_s2g(a.partial + (static_cast<long long>(b) * T + lane) * d, stg + static_cast<size_t>(lane) * d,
-                   static_cast<uint32_t>(d) * 4u);
-        bulk_commit_wait_all();
-      }
+      // (the source reads only: kernel completion makes the writes visible to
+      // the dependent combine)
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       if (et == 0) stamp(a, 20);
       if (a.dbg && tid == 64) {
         a.dbg[blockIdx.x * DBG + 13] = static_cast<unsigned long long>(w_d1f);
@@ -702,7 +730,8 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
 size_t ffn_tg_smem_bytes(int T, int d, int ring_bytes) {
   const size_t hsz = ffn_tg_n8(d, T) ? 1024 : dev::tg::HTS;  // (N = 8 mode keeps 8 token rows of h^T)
   return 2 * 2 * 4096 + static_cast<size_t>(d / 64) * hsz + static_cast<size_t>(ring_bytes) + dev::tg::UB +
-         dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 4 * 16 * 4 + 8 + 8 * (2 * dev::tg::NSLOT + 9 + dev::tg::MAX_KT);
+         dev::tg::ENT_MAX * (16 * 4 + 4) + 16 + 4 * 16 * 4 + 8 +
+         8 * (2 * dev::tg::NSLOT + 8 + dev::tg::D2E + dev::tg::MAX_KT);
 }
 
 // Every CTA's range must touch <= ENT_MAX entries (one producer lane each).

@@ -73,6 +73,9 @@ struct FfnArgs {
   // before it as a second M-tile instead of running a round of its own
   int tail_absorb;
   int tg_n8;  // grouped K3 N = 8 mode (ffn_tg_n8(d, T), set by the launcher)
+  // grouped K3: drain D2 only after the whole last DN pass (profiling A/B;
+  // 0 = drain each M-tile chunk as soon as its entry completes)
+  int drain_late;
 };
 
 struct CombineArgs {

@@ -217,6 +217,27 @@ def test_expert_ffn_grouped_grids(N, k, T, d, ffn, n_shared, gate_mode, resident
     _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 4, grid=grid, tol=3e-5)
 
 
+@pytest.mark.parametrize("absorb,drain_late", [(1, 0), (2, 0), (3, 1), (0, 1)])
+@pytest.mark.parametrize("grid", [37, 148])
+@pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
+    (128, 8, 9, 2048, 768, 0, 0, 0.6),     # Qwen3 shape
+    (64, 6, 9, 2048, 1408, 2, 1, 0.3),     # DeepSeek-V2-Lite shape (shared units)
+    (8, 2, 5, 4096, 448, 0, 0, 1.0),       # N = 8 mode
+    (16, 4, 9, 128, 64, 0, 0, 1.0),        # one M-tile: the drain stages in the ring
+])
+def test_expert_ffn_grouped_group_variants(monkeypatch, N, k, T, d, ffn, n_shared, gate_mode, resident_frac, grid,
+                                           absorb, drain_late):
+    """Grouped K3 knobs: a remainder of <= absorb units joins the group before
+    it as a second M-tile; the D2 drain either follows the last DN pass's
+    entries chunk by chunk (staged in the dead h^T slices) or waits for the
+    whole pass (staged in the ring)."""
+    if abi.FFN_TENSOR not in _kernels(d, ffn):
+        pytest.skip("shape not supported by the tensor-core kernel")
+    monkeypatch.setenv("MOESPAC_TAIL_ABSORB", str(absorb))
+    monkeypatch.setenv("MOESPAC_DRAIN_LATE", str(drain_late))
+    _ffn_case(N, k, T, d, ffn, n_shared, gate_mode, resident_frac, abi.FFN_TENSOR, 4, grid=grid, tol=3e-5)
+
+
 @pytest.mark.parametrize("grid", [1, 5, 37, 148, 300])
 @pytest.mark.parametrize("N,k,T,d,ffn,n_shared,gate_mode,resident_frac", [
     (8, 2, 5, 4096, 448, 0, 0, 1.0),      # Mixtral d: chunk pieces split across CTAs at every grid
