@@ -521,6 +521,7 @@ moespac_status moespac_expert_ffn(const moespac_ffn_args* a, void* stream) {
     // grouped-K3 profiling knobs, as the engine reads them (engine.cpp)
     if (const char* e = std::getenv("MOESPAC_TAIL_ABSORB")) f.tail_absorb = std::atoi(e);
     if (const char* e = std::getenv("MOESPAC_DRAIN_LATE")) f.drain_late = std::atoi(e);
+    if (const char* e = std::getenv("MOESPAC_DRAIN_SC")) f.drain_sc = std::atoi(e);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_ok(kern == kFfnTensorCore ? launch_expert_ffn_tc(f, grid, plan.smem, st) : launch_expert_ffn(f, grid, plan.smem, st),
             "expert_ffn");

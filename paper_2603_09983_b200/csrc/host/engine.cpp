@@ -210,6 +210,7 @@ Engine::Engine(int device, const moespac_model_desc& m, const moespac_sched_conf
   if (const char* e = std::getenv("MOESPAC_GROUP_UNITS")) group_units_ = std::atoi(e);
   if (const char* e = std::getenv("MOESPAC_TAIL_ABSORB")) tail_absorb_ = std::atoi(e);
   if (const char* e = std::getenv("MOESPAC_DRAIN_LATE")) drain_late_ = std::atoi(e);
+  if (const char* e = std::getenv("MOESPAC_DRAIN_SC")) drain_sc_ = std::atoi(e);
   if (const char* e = std::getenv("MOESPAC_L2_PF")) l2_prefetch_ = std::atoi(e);
   const size_t smem_optin = prop.sharedMemPerBlockOptin;
   FfnPlan plan = kernel_ == kFfnTensorCore ? ffn_tc_plan(T_, m.d_model, smem_optin, ffn_accum_)
@@ -920,6 +921,7 @@ void Engine::step(const double* logits, bool logits_host, const uint16_t* h_in, 
     // DeepSeek-V2-Lite -1.3%, Qwen1.5 -1.1% step)
     fa.tail_absorb = tail_absorb_ >= 0 ? tail_absorb_ : 1;
     fa.drain_late = drain_late_;
+    fa.drain_sc = drain_sc_;
     if (split_) {
       fa.cta_base = rank_ * sms_;
       fa.cta_total = world_ * sms_;

@@ -203,6 +203,7 @@ class Engine {
   int group_units_ = 0;  // grouped K3 units per group (MOESPAC_GROUP_UNITS profiling knob; 0 = 8)
   int tail_absorb_ = -1;  // grouped K3: remainder units joining the last group (MOESPAC_TAIL_ABSORB; -1 = per shape)
   int drain_late_ = 0;    // grouped K3: D2 drained after the whole last DN pass (MOESPAC_DRAIN_LATE, profiling)
+  int drain_sc_ = 0;      // grouped K3: M-tiles per drain chunk (MOESPAC_DRAIN_SC, profiling; 0 = kernel default)
   const int32_t* replay_ids_ = nullptr;  // set for the duration of step_ids()
   const float* replay_gates_ = nullptr;
   uint16_t* wg_d_ = nullptr;      // [L][N][d] bf16 router weights (model mode)

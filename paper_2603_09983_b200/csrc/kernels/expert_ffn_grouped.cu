@@ -654,7 +654,7 @@ __global__ void __maxnreg__(200) expert_ffn_tg_kernel(FfnArgs a) {
       const Geom gl = dn_geom(g.nu, mcap);  // g: the last group (GroupIt leaves it)
       const int n_last = (mtiles + gl.m - 1) / gl.m;
       const uint32_t hts_bytes = static_cast<uint32_t>(ktiles) * hsz;
-      int sc = 4;
+      int sc = a.drain_sc > 0 ? a.drain_sc : 4;
       while (sc > 1 && 2u * sc * 512u * static_cast<uint32_t>(T) > hts_bytes) sc >>= 1;
       const bool early = !a.drain_late && n_last > 1 && 2u * sc * 512u * static_cast<uint32_t>(T) <= hts_bytes;
       if (!early) sc = mtiles;

@@ -76,6 +76,7 @@ struct FfnArgs {
   // grouped K3: drain D2 only after the whole last DN pass (profiling A/B;
   // 0 = drain each M-tile chunk as soon as its entry completes)
   int drain_late;
+  int drain_sc;  // grouped K3: M-tiles per drain chunk (0 = 4; halved until two fit the h^T slices)
 };
 
 struct CombineArgs {
